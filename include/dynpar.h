@@ -1,0 +1,187 @@
+/*
+ * dynpar.h — C-ABI of libdynpar.so, the B200 (sm_100a) nested-parallel hot path.
+ *
+ * The reference (arXiv 2201.02789 package `dynoptc`, pure Python) has no FFI:
+ * its operator API for this path is `dynoptc.bench` (pkg/src/dynoptc/bench/
+ * __init__.py:3-19) and every run goes through the simulator's Machine
+ * (pkg/src/dynoptc/sim/machine.py:73-184).  Each entry point below replaces
+ * one reference call site; the Python layer `paper_2201_02789_b200.bench`
+ * keeps the reference's names and calls these through ctypes.
+ *
+ *   reference call                                     -> entry point
+ *   run_config(bfs, wl, cfg)      harness.py:65-80     -> dp_bfs / dp_bfs_dev
+ *     (BFS_CDP main+visit, benchmarks.py:91-120, drive :157-168)
+ *   run_reference(bfs, wl)        harness.py:57-62     -> dp_bfs (variant=NOCDP)
+ *     (BFS_NOCDP, benchmarks.py:122-141)
+ *   run_config / run_reference for sssp                -> dp_sssp / dp_sssp_dev
+ *     (benchmarks.py:175-270)
+ *   run_config / run_reference for manylaunch          -> dp_manylaunch / _dev
+ *     (benchmarks.py:277-332)
+ *   (no reference; BASELINE.json configs 2 and 4)      -> dp_tc, dp_bt (+_dev)
+ *   transform(... threshold, cfactor, agg, group_size, agg_threshold)
+ *                                 pipeline.py:45-81    -> dp_config (policy knobs)
+ *   SimReport counters            sim/report.py:12-28  -> dp_stats
+ *   SimTrap(kind, ...)            sim/machine.py:43-50 -> negative return codes
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  `*_dev` entry points take DEVICE pointers
+ *    and a cudaStream_t passed as void* (NULL = legacy default stream); the
+ *    others take caller-owned HOST arrays and copy H2D/D2H inside the call.
+ *  - Every call is synchronous on return.  Calls are not re-entrant per
+ *    device (the library keeps one workspace per device).
+ *  - Return 0 on success, a negative DP_ERR_* code otherwise; the message is
+ *    in dp_last_error() (thread-local).
+ *  - Knob validation mirrors passes/aggregate.py:174-179 and is ALSO done in
+ *    Python before the call (ValueError there, DP_ERR_INVALID here).
+ */
+#ifndef DYNPAR_H
+#define DYNPAR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DP_ABI_VERSION 1
+
+/* aggregation granularity (passes/aggregate.py:84 GRANULARITIES, + warp) */
+#define DP_AGG_NONE 0
+#define DP_AGG_WARP 1
+#define DP_AGG_BLOCK 2
+#define DP_AGG_MULTIBLOCK 3
+#define DP_AGG_GRID 4
+
+/* program variant (Benchmark.cdp_source / nocdp_source, benchmarks.py:56-68) */
+#define DP_VARIANT_NOCDP 0
+#define DP_VARIANT_CDP 1
+
+/* how a below-threshold child grid runs inside the parent
+ * (passes/threshold.py:60-83 runs it in the parent THREAD) */
+#define DP_SERIAL_THREAD 0
+#define DP_SERIAL_WARP 1 /* B200 addition: the parent warp shares the loop */
+
+/* "always serialize" sentinel, passes/common.py:10 */
+#define DP_INF_THRESHOLD 2147483647
+
+/* error codes -> SimTrap kinds (sim/machine.py:43-50) */
+#define DP_OK 0
+#define DP_ERR_QUEUE_OVERFLOW (-1) /* "queue-overflow": pending launch pool full */
+#define DP_ERR_LAUNCH_CONFIG (-2)  /* "launch-config" */
+#define DP_ERR_CUDA (-3)           /* "cuda-error" */
+#define DP_ERR_INVALID (-4)        /* bad knob / argument (ValueError in Python) */
+#define DP_ERR_NO_DEVICE (-5)      /* no CUDA device visible */
+#define DP_ERR_ITERATIONS (-6)     /* "more levels than vertices", benchmarks.py:168 */
+
+typedef struct dp_config {
+  int32_t threshold;     /* T: child count >= T launches, else serial; 0 = pass off */
+  int32_t cfactor;       /* C: logical child blocks per physical block, >= 1 */
+  int32_t agg;           /* DP_AGG_* */
+  int32_t group_size;    /* multiblock: parent blocks per group, >= 1 */
+  int32_t agg_threshold; /* block only: < this many participants -> direct launches */
+  int32_t variant;       /* DP_VARIANT_* */
+  int32_t parent_block;  /* parent threads per block (reference BLOCK = 32) */
+  int32_t child_block;   /* child threads per block (reference launches use 32) */
+  int32_t serial_mode;   /* DP_SERIAL_* */
+  int32_t pending_launch_limit; /* cudaLimitDevRuntimePendingLaunchCount; 0 = auto */
+  int32_t reserved[6];
+} dp_config;
+
+/* SimReport (sim/report.py:12-28) counters, measured on the device */
+typedef struct dp_stats {
+  uint64_t num_launches;      /* device-side launches with grid, block > 0 */
+  uint64_t host_launches;     /* host-side launches with grid, block > 0 */
+  uint64_t blocks_scheduled;  /* sum of grid sizes over every launched grid */
+  uint64_t max_pending_depth; /* not observable on hardware: always 0 */
+  uint64_t iterations;        /* host-loop trips (BFS levels / SSSP rounds) */
+  uint64_t work_units;        /* child items executed (edges examined, ...) */
+  uint64_t bytes_alg;         /* algorithmic HBM bytes (DESIGN.md per app) */
+  double ns_device;           /* CUDA-event time of the whole run (device) */
+  double ns_host;             /* host wall time of the call, copies included */
+  double ns_kernel_max;       /* longest host-launched step (parent grid + its
+                                 children [+ grid-glue launch]), CUDA events */
+  double ns_kernel_sum;       /* sum of those step durations (no host gaps) */
+  double ns_phase[5];         /* parent, launch, agg, disagg, child (0 unless profiled) */
+  uint64_t h2d_bytes;         /* bytes copied host->device in this call */
+  uint64_t d2h_bytes;         /* bytes copied device->host in this call */
+  uint64_t kernel_launches;   /* launches of library kernels issued from the host */
+} dp_stats;
+
+/* ---- library -------------------------------------------------------------- */
+int dp_abi_version(void);
+const char* dp_last_error(void);
+int dp_device_count(void);
+/* nonzero when the library was built for sm_100a and a device is usable */
+int dp_init(int32_t device);
+
+/* ---- BFS (benchmarks.py:91-168) ------------------------------------------ */
+/* host buffers: rowptr[n+1], col[m]; out dist[n], counts[n] */
+int dp_bfs(const int32_t* rowptr, const int32_t* col, int32_t n, int64_t m,
+           int32_t src, const dp_config* cfg, int32_t* dist, int32_t* counts,
+           dp_stats* stats);
+/* device buffers; dist/counts are initialised by the call */
+int dp_bfs_dev(const int32_t* d_rowptr, const int32_t* d_col, int32_t n,
+               int64_t m, int32_t src, const dp_config* cfg, int32_t* d_dist,
+               int32_t* d_counts, void* stream, dp_stats* stats);
+
+/* ---- SSSP (benchmarks.py:175-270) ---------------------------------------- */
+int dp_sssp(const int32_t* rowptr, const int32_t* col, const int32_t* weight,
+            int32_t n, int64_t m, int32_t src, const dp_config* cfg,
+            int32_t* dist, dp_stats* stats);
+int dp_sssp_dev(const int32_t* d_rowptr, const int32_t* d_col,
+                const int32_t* d_weight, int32_t n, int64_t m, int32_t src,
+                const dp_config* cfg, int32_t* d_dist, void* stream,
+                dp_stats* stats);
+
+/* ---- manylaunch (benchmarks.py:277-332) ---------------------------------- */
+int dp_manylaunch(const int32_t* sizes, int32_t n, const dp_config* cfg,
+                  int32_t* out, int32_t* total, dp_stats* stats);
+int dp_manylaunch_dev(const int32_t* d_sizes, int32_t n, const dp_config* cfg,
+                      int32_t* d_out, int32_t* d_total, void* stream,
+                      dp_stats* stats);
+
+/* ---- triangle counting (no reference) -------------- */
+/* oriented CSR+ (u->v iff (deg u, u) < (deg v, v)), rows sorted ascending.
+ * [edge_lo, edge_hi) restricts the count to a range of oriented edges
+ * (the multi-GPU shard); pass 0, m for the whole graph. */
+int dp_tc(const int32_t* rowptr, const int32_t* col, int32_t n, int64_t m,
+          int64_t edge_lo, int64_t edge_hi, const dp_config* cfg,
+          uint64_t* triangles, dp_stats* stats);
+int dp_tc_dev(const int32_t* d_rowptr, const int32_t* d_col, int32_t n,
+              int64_t m, int64_t edge_lo, int64_t edge_hi,
+              const dp_config* cfg, uint64_t* d_triangles, void* stream,
+              dp_stats* stats);
+
+/* ---- Bezier line tessellation (no reference) ------- */
+/* cp[ncurves][3][2] float32 control points.  Outputs: ntess[ncurves] vertex
+ * counts, offsets[ncurves] start of each curve's vertices in verts, and
+ * verts[2*vert_capacity] float32 (x,y).  Offsets come from a device bump
+ * allocator (the device-side cudaMalloc of the original), so
+ * they depend on scheduling; the per-curve vertices do not.
+ * Returns DP_ERR_INVALID if the vertices do not fit vert_capacity. */
+int dp_bt(const float* cp, int32_t ncurves, int32_t max_tess, float curv_scale,
+          const dp_config* cfg, int32_t* ntess, int64_t* offsets, float* verts,
+          int64_t vert_capacity, int64_t* nverts, dp_stats* stats);
+int dp_bt_dev(const float* d_cp, int32_t ncurves, int32_t max_tess,
+              float curv_scale, const dp_config* cfg, int32_t* d_ntess,
+              int64_t* d_offsets, float* d_verts, int64_t vert_capacity,
+              int64_t* nverts, void* stream, dp_stats* stats);
+
+/* ---- host-side input generation (builder-defined, no reference) ----------- */
+/* RMAT (Graph500 a,b,c = .57,.19,.19), n = 2^scale, m = edge_factor*n edges,
+ * multi-edges and self-loops kept, CSR rows sorted ascending.  Deterministic
+ * for (scale, edge_factor, seed) on any host.  rowptr[n+1], col[m]. */
+int dp_rmat_csr(int32_t scale, int32_t edge_factor, uint64_t seed,
+                int32_t* rowptr, int32_t* col, int32_t nthreads);
+/* symmetrise, drop self-loops and duplicates, orient by (degree, id).
+ * Allocates *rowptr_plus (n+1) and *col_plus (*m_plus); free with dp_free. */
+int dp_tc_orient(const int32_t* rowptr, const int32_t* col, int32_t n,
+                 int32_t** rowptr_plus, int32_t** col_plus, int64_t* m_plus,
+                 int32_t nthreads);
+void dp_free(void* p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DYNPAR_H */

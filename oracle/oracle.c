@@ -1,0 +1,192 @@
+/*
+ * oracle.c — CPU restatement of the reference algorithms on the hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Nothing in the product package
+ * (paper_2201_02789_b200/) may import, link or call this; only tests/,
+ * __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference arm
+ * use it, and only as the checker / the timed CPU baseline.
+ *
+ * Each function restates the reference's serial (No-CDP) variant, which the
+ * reference itself uses as ground truth (bench/harness.py:57-62):
+ *   oracle_bfs         BFS_NOCDP main + _bfs_drive  bench/benchmarks.py:122-168
+ *   oracle_sssp        SSSP_NOCDP main + relax + _sssp_drive  :184-195,225-270
+ *   oracle_manylaunch  MANYLAUNCH_NOCDP main        :303-332
+ * and the builder-defined apps the reference lacks (parity unpinned by the
+ * reference):
+ *   oracle_tc          exact triangle count over a degree-oriented CSR+
+ *   oracle_bt          Bezier tessellation, fp64 vertices, fp32 counts
+ *
+ * Parallel versions (nthreads > 1) use the same atomics the reference's
+ * kernels use; outputs are schedule-invariant (benchmarks.py:10-15), so any
+ * thread count gives the same bytes.  Integer arithmetic wraps at 32 bits
+ * like the reference's (sim/compile.py:36-37, sim/machine.py:35-40).
+ */
+#include <math.h>
+#include <omp.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define UNREACHED (1 << 30) /* bench/graphs.py:29 */
+
+static int nthr(int t) { return t > 0 ? t : omp_get_max_threads(); }
+
+static inline int32_t wrap_add(int32_t a, int32_t b) {
+  return (int32_t)((uint32_t)a + (uint32_t)b);
+}
+
+/* Returns the number of host launches (levels including the final
+ * no-change pass), or -1 if more than n+1 levels were needed. */
+long oracle_bfs(const int32_t* rowptr, const int32_t* col, int32_t n,
+                int32_t src, int32_t* dist, int32_t* counts, int nthreads) {
+  const int nt = nthr(nthreads);
+  for (int32_t i = 0; i < n; ++i) {
+    dist[i] = UNREACHED;
+    counts[i] = 0;
+  }
+  dist[src] = 0;
+  for (long level = 0; level <= n; ++level) {
+    int changed = 0;
+#pragma omp parallel for num_threads(nt) schedule(dynamic, 256) reduction(| : changed)
+    for (int32_t u = 0; u < n; ++u) {
+      if (__atomic_load_n(&dist[u], __ATOMIC_RELAXED) != level) continue;
+      const int32_t start = rowptr[u];
+      const int32_t deg = rowptr[u + 1] - start;
+      for (int32_t e = 0; e < deg; ++e) {
+        const int32_t v = col[start + e];
+        __atomic_fetch_add(&counts[v], 1, __ATOMIC_RELAXED);
+        int32_t expect = UNREACHED;
+        if (__atomic_compare_exchange_n(&dist[v], &expect, (int32_t)level + 1,
+                                        0, __ATOMIC_RELAXED, __ATOMIC_RELAXED))
+          changed = 1;
+      }
+    }
+    if (!changed) return level + 1;
+  }
+  return -1;
+}
+
+/* Bellman-Ford rounds; returns rounds executed or -1 past n+1 rounds. */
+long oracle_sssp(const int32_t* rowptr, const int32_t* col,
+                 const int32_t* weight, int32_t n, int32_t src, int32_t* dist,
+                 int nthreads) {
+  const int nt = nthr(nthreads);
+  for (int32_t i = 0; i < n; ++i) dist[i] = UNREACHED;
+  dist[src] = 0;
+  for (long round = 0; round <= n; ++round) {
+    int changed = 0;
+#pragma omp parallel for num_threads(nt) schedule(dynamic, 256) reduction(| : changed)
+    for (int32_t u = 0; u < n; ++u) {
+      const int32_t du = __atomic_load_n(&dist[u], __ATOMIC_RELAXED);
+      if (!(du < UNREACHED)) continue;
+      const int32_t start = rowptr[u];
+      const int32_t deg = rowptr[u + 1] - start;
+      for (int32_t e = 0; e < deg; ++e) {
+        const int32_t v = col[start + e];
+        const int32_t alt = wrap_add(du, weight[start + e]);
+        /* relax(): CAS loop lowering dist[v] (benchmarks.py:184-195) */
+        int32_t cur = __atomic_load_n(&dist[v], __ATOMIC_RELAXED);
+        while (alt < cur) {
+          if (__atomic_compare_exchange_n(&dist[v], &cur, alt, 0,
+                                          __ATOMIC_RELAXED, __ATOMIC_RELAXED)) {
+            changed = 1;
+            break;
+          }
+        }
+      }
+    }
+    if (!changed) return round + 1;
+  }
+  return -1;
+}
+
+void oracle_manylaunch(const int32_t* sizes, int32_t n, int32_t* out,
+                       int32_t* total, int nthreads) {
+  const int nt = nthr(nthreads);
+  int32_t tot = 0;
+  memset(out, 0, sizeof(int32_t) * (size_t)n);
+#pragma omp parallel for num_threads(nt) schedule(dynamic, 256)
+  for (int32_t i = 0; i < n; ++i) {
+    const int32_t s = sizes[i];
+    int32_t acc = 0, cnt = 0;
+    for (int32_t j = 0; j < s; ++j) {
+      acc = wrap_add(acc, j + 1);
+      cnt = wrap_add(cnt, 1);
+    }
+    out[i] = acc;
+    __atomic_fetch_add(&tot, cnt, __ATOMIC_RELAXED);
+  }
+  *total = tot;
+}
+
+/* sorted-merge intersection size */
+static int64_t merge_count(const int32_t* a, int64_t na, const int32_t* b,
+                           int64_t nb) {
+  int64_t i = 0, j = 0, c = 0;
+  while (i < na && j < nb) {
+    if (a[i] < b[j]) ++i;
+    else if (a[i] > b[j]) ++j;
+    else { ++c; ++i; ++j; }
+  }
+  return c;
+}
+
+/* triangles = sum over oriented edges (u,v) in [lo,hi) of |N+(u) ∩ N+(v)| */
+uint64_t oracle_tc(const int32_t* rowptr, const int32_t* col, int32_t n,
+                   int64_t lo, int64_t hi, int nthreads) {
+  const int nt = nthr(nthreads);
+  uint64_t total = 0;
+#pragma omp parallel for num_threads(nt) schedule(dynamic, 64) reduction(+ : total)
+  for (int32_t u = 0; u < n; ++u) {
+    int64_t b = rowptr[u], e = rowptr[u + 1];
+    if (b < lo) b = lo;
+    if (e > hi) e = hi;
+    for (int64_t k = b; k < e; ++k) {
+      const int32_t v = col[k];
+      total += (uint64_t)merge_count(col + rowptr[u], rowptr[u + 1] - rowptr[u],
+                                     col + rowptr[v], rowptr[v + 1] - rowptr[v]);
+    }
+  }
+  return total;
+}
+
+/* Vertex count per curve, fp32 round-to-nearest with no contraction (built
+ * with -ffp-contract=off), identical to the device computation. */
+static int32_t tess_count(const float* p, float scale, int32_t max_tess) {
+  volatile float mx = 0.5f * (p[0] + p[4]);
+  volatile float my = 0.5f * (p[1] + p[5]);
+  volatile float dx = p[2] - mx, dy = p[3] - my;
+  volatile float lx = p[4] - p[0], ly = p[5] - p[1];
+  volatile float dxx = dx * dx, dyy = dy * dy, lxx = lx * lx, lyy = ly * ly;
+  volatile float num = sqrtf(dxx + dyy);
+  volatile float den = sqrtf(lxx + lyy);
+  volatile float q = num / den;
+  volatile float t = q * scale;
+  int32_t nt = t < (float)max_tess ? (int32_t)t : max_tess;
+  return nt < 4 ? 4 : nt;
+}
+
+/* ntess[c]; canonical offsets[c] = exclusive prefix; verts[2*V] in fp64.
+ * Returns total vertex count (call with verts == NULL to size). */
+int64_t oracle_bt(const float* cp, int32_t ncurves, int32_t max_tess,
+                  float scale, int32_t* ntess, int64_t* offsets, double* verts) {
+  int64_t acc = 0;
+  for (int32_t c = 0; c < ncurves; ++c) {
+    ntess[c] = tess_count(cp + 6 * (int64_t)c, scale, max_tess);
+    offsets[c] = acc;
+    acc += ntess[c];
+  }
+  if (!verts) return acc;
+  for (int32_t c = 0; c < ncurves; ++c) {
+    const float* p = cp + 6 * (int64_t)c;
+    const int32_t nt = ntess[c];
+    for (int32_t i = 0; i < nt; ++i) {
+      const double t = (double)i / (double)(nt - 1);
+      const double s = 1.0 - t;
+      double* o = verts + 2 * (offsets[c] + i);
+      o[0] = s * s * p[0] + 2.0 * s * t * p[2] + t * t * p[4];
+      o[1] = s * s * p[1] + 2.0 * s * t * p[3] + t * t * p[5];
+    }
+  }
+  return acc;
+}

@@ -1,0 +1,296 @@
+"""Nested-parallel benchmarks on the B200: registry and per-app runners.
+
+The reference registers each application as a ``Benchmark`` carrying
+mini-language sources for its dynamic (CDP) and serial (No-CDP) variants plus
+``prepare``/``drive`` host functions (bench/benchmarks.py:56-68, 339-347).
+Here the kernels are hand-written sm_100a CUDA (csrc/apps.cuh) behind
+libdynpar.so, so a Benchmark carries ``prepare`` (same buffers as the
+reference) and ``run`` (one call through the C-ABI, both variants).
+
+Applications
+  bfs         level-synchronous BFS, outputs dist, counts  (ref :91-168)
+  sssp        Bellman-Ford rounds, output dist             (ref :175-270)
+  manylaunch  launch-congestion microbenchmark, out, total (ref :277-332)
+  tc          triangle counting over a degree-oriented CSR+   (new, config 4)
+  bt          Bezier line tessellation                        (new, config 2)
+Outputs are written only through commutative / idempotent atomics, so they
+are schedule-invariant and must match the serial variant element-exactly
+(bt: vertex coordinates within 1e-5, see harness.verify_outputs).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Callable
+
+import numpy as np
+
+from .. import _lib
+from .graphs import (BT_CURV_SCALE, BT_MAX_TESS, UNREACHED, DatasetSpec,
+                     bezier_curves, child_sizes, edge_weights, make_graph,
+                     parse_spec, tc_orient)
+
+BLOCK = 32  # parent block size of every reference driver (benchmarks.py:44)
+
+
+@dataclass(frozen=True)
+class Workload:
+    """A dataset resolved into initial buffer contents (benchmarks.py:47-53)."""
+    spec: DatasetSpec
+    buffers: dict
+    n: int
+    payload: object
+
+
+@dataclass(frozen=True)
+class Benchmark:
+    name: str
+    outputs: tuple
+    kinds: dict
+    prepare: Callable[[DatasetSpec], Workload]
+    # run(workload, dp_config) -> (outputs: dict[str, ndarray], stats: dict)
+    run: Callable[[Workload, _lib.DpConfig], tuple]
+    # (workload, outputs, stats) -> (work units, algorithmic bytes)
+    traffic: Callable[[Workload, dict, dict], tuple]
+    description: str = ""
+
+    def workload(self, spec_text: str) -> Workload:
+        return self.prepare(parse_spec(spec_text))
+
+
+def _c32(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+def _call(fn, *args):
+    st = _lib.DpStats()
+    _lib.check(fn(*args, ctypes.byref(st)))
+    return _lib.stats_dict(st)
+
+
+# ---------------------------------------------------------------------------
+# bfs
+# ---------------------------------------------------------------------------
+
+def _bfs_prepare(spec: DatasetSpec) -> Workload:
+    g = make_graph(spec)
+    dist = np.full(g.n, UNREACHED, dtype=np.int32)
+    dist[0] = 0
+    return Workload(spec=spec, n=g.n, payload=g, buffers={
+        "rowptr": _c32(g.rowptr), "col": _c32(g.col), "dist": dist,
+        "counts": np.zeros(g.n, dtype=np.int32),
+        "changed": np.zeros(1, dtype=np.int32)})
+
+
+def _bfs_run(wl: Workload, cfg: _lib.DpConfig):
+    lib = _lib.device()
+    b = wl.buffers
+    dist = np.empty(wl.n, dtype=np.int32)
+    counts = np.empty(wl.n, dtype=np.int32)
+    st = _call(lib.dp_bfs, _lib.ptr(b["rowptr"]), _lib.ptr(b["col"]), wl.n,
+               b["col"].shape[0], 0, ctypes.byref(cfg), _lib.ptr(dist),
+               _lib.ptr(counts))
+    return {"dist": dist, "counts": counts}, st
+
+
+def bfs_traffic(n_reached: int, edges: int) -> int:
+    """16 B per examined edge (col 4, dist probe 4, counts RMW 8) + 12 B per
+    reached vertex (rowptr pair 8, dist write 4) — SURVEY §8(d) config 1."""
+    return 16 * edges + 12 * n_reached
+
+
+def _bfs_traffic(wl, out, st):
+    e_t = int(out["counts"].astype(np.int64).sum())
+    v_r = int(np.count_nonzero(out["dist"] < UNREACHED))
+    return e_t, bfs_traffic(v_r, e_t)
+
+
+# ---------------------------------------------------------------------------
+# sssp
+# ---------------------------------------------------------------------------
+
+def _sssp_prepare(spec: DatasetSpec) -> Workload:
+    g = make_graph(spec)
+    # unit weights on the hand fixture so distances equal BFS levels
+    w = (np.ones(g.m, dtype=np.int32) if spec.kind == "hand"
+         else edge_weights(g, spec.seed))
+    dist = np.full(g.n, UNREACHED, dtype=np.int32)
+    dist[0] = 0
+    return Workload(spec=spec, n=g.n, payload=(g, w), buffers={
+        "rowptr": _c32(g.rowptr), "col": _c32(g.col), "weight": _c32(w),
+        "dist": dist, "changed": np.zeros(1, dtype=np.int32)})
+
+
+def _sssp_run(wl: Workload, cfg: _lib.DpConfig):
+    lib = _lib.device()
+    b = wl.buffers
+    dist = np.empty(wl.n, dtype=np.int32)
+    st = _call(lib.dp_sssp, _lib.ptr(b["rowptr"]), _lib.ptr(b["col"]),
+               _lib.ptr(b["weight"]), wl.n, b["col"].shape[0], 0,
+               ctypes.byref(cfg), _lib.ptr(dist))
+    return {"dist": dist}, st
+
+
+def sssp_traffic(n: int, n_reached: int, edges_reached: int,
+                 rounds: int) -> int:
+    """Per round: 4 B dist scan per vertex, 8 B rowptr pair per reached
+    vertex, 12 B per relaxed edge (col, weight, dist probe)."""
+    return rounds * (4 * n + 8 * n_reached + 12 * edges_reached)
+
+
+def _sssp_traffic(wl, out, st):
+    reached = out["dist"] < UNREACHED
+    deg = np.diff(wl.buffers["rowptr"].astype(np.int64))
+    e_reach = int(deg[reached].sum())
+    return e_reach, sssp_traffic(wl.n, int(reached.sum()), e_reach,
+                                 int(st["iterations"]))
+
+
+# ---------------------------------------------------------------------------
+# manylaunch
+# ---------------------------------------------------------------------------
+
+def _manylaunch_prepare(spec: DatasetSpec) -> Workload:
+    if spec.kind != "sizes":
+        raise ValueError("manylaunch expects a sizes:<n>:seedN dataset")
+    sizes = child_sizes(spec.size, spec.seed)
+    return Workload(spec=spec, n=spec.size, payload=sizes, buffers={
+        "sizes": _c32(sizes), "out": np.zeros(spec.size, dtype=np.int32),
+        "total": np.zeros(1, dtype=np.int32)})
+
+
+def _manylaunch_run(wl: Workload, cfg: _lib.DpConfig):
+    lib = _lib.device()
+    out = np.empty(wl.n, dtype=np.int32)
+    total = np.empty(1, dtype=np.int32)
+    st = _call(lib.dp_manylaunch, _lib.ptr(wl.buffers["sizes"]), wl.n,
+               ctypes.byref(cfg), _lib.ptr(out), _lib.ptr(total))
+    return {"out": out, "total": total}, st
+
+
+def _manylaunch_traffic(wl, out, st):
+    items = int(np.clip(wl.buffers["sizes"], 0, None).astype(np.int64).sum())
+    return items, 4 * wl.n + 4 * wl.n + 4 * items  # sizes, out, out RMW/item
+
+
+# ---------------------------------------------------------------------------
+# tc
+# ---------------------------------------------------------------------------
+
+def _tc_prepare(spec: DatasetSpec) -> Workload:
+    g = make_graph(spec)
+    gp = tc_orient(g)
+    return Workload(spec=spec, n=gp.n, payload=(g, gp), buffers={
+        "rowptr": _c32(gp.rowptr), "col": _c32(gp.col),
+        "triangles": np.zeros(1, dtype=np.uint64)})
+
+
+def _tc_run(wl: Workload, cfg: _lib.DpConfig, lo: int = 0, hi: int = -1):
+    lib = _lib.device()
+    b = wl.buffers
+    m = b["col"].shape[0]
+    tri = np.zeros(1, dtype=np.uint64)
+    st = _call(lib.dp_tc, _lib.ptr(b["rowptr"]), _lib.ptr(b["col"]), wl.n, m,
+               lo, m if hi < 0 else hi, ctypes.byref(cfg), _lib.ptr(tri))
+    return {"triangles": tri}, st
+
+
+def tc_traffic(rowptr: np.ndarray, col: np.ndarray, lo: int = 0,
+               hi: int = -1) -> int:
+    """sum over oriented edges (u,v) of 4*(d+u + d+v) + 8."""
+    rp = rowptr.astype(np.int64)
+    deg = np.diff(rp)
+    hi = col.shape[0] if hi < 0 else hi
+    src = np.repeat(np.arange(deg.shape[0]), deg)[lo:hi]
+    return int(4 * (deg[src].sum() + deg[col[lo:hi]].sum()) + 8 * (hi - lo))
+
+
+def _tc_traffic(wl, out, st):
+    b = wl.buffers
+    return int(b["col"].shape[0]), tc_traffic(b["rowptr"], b["col"])
+
+
+# ---------------------------------------------------------------------------
+# bt
+# ---------------------------------------------------------------------------
+
+def _bt_prepare(spec: DatasetSpec) -> Workload:
+    if spec.kind != "curves":
+        raise ValueError("bt expects a curves:<n>:seedN dataset")
+    cp = bezier_curves(spec.size, spec.seed)
+    return Workload(spec=spec, n=spec.size, payload=cp, buffers={
+        "cp": np.ascontiguousarray(cp, dtype=np.float32),
+        "max_tess": BT_MAX_TESS, "scale": BT_CURV_SCALE})
+
+
+def canonical_vertices(verts: np.ndarray, ntess: np.ndarray,
+                       offsets: np.ndarray) -> np.ndarray:
+    """Gather the bump-allocated vertices into curve order."""
+    nt = ntess.astype(np.int64)
+    canon = np.concatenate(([0], np.cumsum(nt)[:-1])) if nt.size else nt
+    idx = (np.repeat(offsets.astype(np.int64), nt)
+           + np.arange(int(nt.sum()), dtype=np.int64)
+           - np.repeat(canon, nt))
+    return verts.reshape(-1, 2)[idx]
+
+
+def _bt_run(wl: Workload, cfg: _lib.DpConfig):
+    lib = _lib.device()
+    b = wl.buffers
+    n = wl.n
+    cap = n * int(b["max_tess"])
+    ntess = np.empty(n, dtype=np.int32)
+    offsets = np.empty(n, dtype=np.int64)
+    verts = np.empty((cap, 2), dtype=np.float32)
+    used = ctypes.c_int64()
+    st = _call(lib.dp_bt, _lib.ptr(b["cp"]), n, int(b["max_tess"]),
+               float(b["scale"]), ctypes.byref(cfg), _lib.ptr(ntess),
+               _lib.ptr(offsets), _lib.ptr(verts), cap, ctypes.byref(used))
+    return {"ntess": ntess,
+            "verts": canonical_vertices(verts[:used.value], ntess, offsets)}, st
+
+
+def bt_traffic(ncurves: int, nverts: int) -> int:
+    """24 B control points + 12 B (ntess, offset) per curve, 8 B per vertex."""
+    return 36 * ncurves + 8 * nverts
+
+
+def _bt_traffic(wl, out, st):
+    nv = int(out["ntess"].astype(np.int64).sum())
+    return wl.n, bt_traffic(wl.n, nv)
+
+
+# ---------------------------------------------------------------------------
+# registry
+# ---------------------------------------------------------------------------
+
+BENCHMARKS: dict[str, Benchmark] = {
+    "bfs": Benchmark("bfs", ("dist", "counts"), {"dist": "int",
+                                                 "counts": "int"},
+                     _bfs_prepare, _bfs_run, _bfs_traffic,
+                     "level-synchronous BFS (benchmarks.py:91-168)"),
+    "sssp": Benchmark("sssp", ("dist",), {"dist": "int"}, _sssp_prepare,
+                      _sssp_run, _sssp_traffic,
+                      "Bellman-Ford SSSP (benchmarks.py:175-270)"),
+    "manylaunch": Benchmark("manylaunch", ("out", "total"),
+                            {"out": "int", "total": "int"},
+                            _manylaunch_prepare, _manylaunch_run,
+                            _manylaunch_traffic,
+                            "launch congestion (benchmarks.py:277-332)"),
+    "tc": Benchmark("tc", ("triangles",), {"triangles": "long"}, _tc_prepare,
+                    _tc_run, _tc_traffic, "triangle counting (new)"),
+    "bt": Benchmark("bt", ("ntess", "verts"), {"ntess": "int",
+                                               "verts": "float"},
+                    _bt_prepare, _bt_run, _bt_traffic,
+                    "Bezier line tessellation (new)"),
+}
+
+
+def get_benchmark(name: str) -> Benchmark:
+    try:
+        return BENCHMARKS[name]
+    except KeyError:
+        raise ValueError(f"unknown benchmark {name!r} "
+                         f"(expected one of {', '.join(BENCHMARKS)})") \
+            from None

@@ -1,0 +1,306 @@
+// apps.cuh — per-application parent/child functors for the scheduler.
+//
+// Each App supplies
+//   Args                  16-byte-multiple POD of scalar child arguments (the
+//                         rows of the aggregation tables, aggregate.py:103-136)
+//   Acc                   per-thread accumulator flushed once per thread
+//   nparents()            parent threads per host launch
+//   parent_prologue()     once-per-grid bookkeeping (all threads call)
+//   expand(u, valid, a)   parent work; returns the child thread count
+//                         (all threads call; 0 when !valid)
+//   count(a)              child thread count recorded in a row
+//   item(a, e, acc)       child thread e's work
+//   flush(acc)            warp-collective epilogue (all 32 lanes call)
+#pragma once
+#include "common.cuh"
+
+namespace dp {
+
+// ---------------------------------------------------------------------------
+// BFS — BFS_CDP main/visit (bench/benchmarks.py:91-120)
+// ---------------------------------------------------------------------------
+struct BfsApp {
+  const int* __restrict__ rowptr;
+  const int* __restrict__ col;
+  int* dist;
+  int* counts;
+  int* changed;       // this level's flag
+  int* changed_next;  // next level's flag, cleared here
+  int n;
+  int level;
+
+  struct alignas(16) Args {
+    int start, deg, level, pad;
+  };
+  struct Acc {
+    int changed;
+  };
+
+  __device__ int nparents() const { return n; }
+  __device__ void parent_prologue() const {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *changed_next = 0;
+  }
+  // main (:105-119): u with dist[u] == level owns deg = rowptr[u+1]-rowptr[u]
+  __device__ int expand(int u, bool valid, Args& a) const {
+    if (!valid || __ldcg(dist + u) != level) return 0;
+    const int s = __ldg(rowptr + u);
+    const int d = __ldg(rowptr + u + 1) - s;
+    a = Args{s, d, level, 0};
+    return d > 0 ? d : 0;
+  }
+  __device__ static int count(const Args& a) { return a.deg; }
+  // visit (:92-103): count the edge, discover v with one CAS against
+  // UNREACHED.  The plain pre-check only skips CASes that would fail.
+  __device__ void item(const Args& a, int e, Acc& acc) const {
+    const int v = __ldg(col + a.start + e);
+    atomicAdd(counts + v, 1);
+    if (__ldcg(dist + v) == kUnreached &&
+        atomicCAS(dist + v, kUnreached, a.level + 1) == kUnreached)
+      acc.changed = 1;
+  }
+  __device__ void flush(Acc& acc) const {
+    if (__any_sync(DP_FULL, acc.changed) && lane_id() == 0) *changed = 1;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// SSSP — SSSP_CDP main/relax_edges/relax (bench/benchmarks.py:175-222)
+// ---------------------------------------------------------------------------
+struct SsspApp {
+  const int* __restrict__ rowptr;
+  const int* __restrict__ col;
+  const int* __restrict__ weight;
+  int* dist;
+  int* changed;
+  int* changed_next;
+  int n;
+  int pad;
+
+  struct alignas(16) Args {
+    int start, deg, du, pad;
+  };
+  struct Acc {
+    int changed;
+  };
+
+  __device__ int nparents() const { return n; }
+  __device__ void parent_prologue() const {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *changed_next = 0;
+  }
+  // main (:207-222): every reached u relaxes all its out-edges from its
+  // round-start distance du
+  __device__ int expand(int u, bool valid, Args& a) const {
+    if (!valid) return 0;
+    const int du = __ldcg(dist + u);
+    if (du >= kUnreached) return 0;
+    const int s = __ldg(rowptr + u);
+    const int d = __ldg(rowptr + u + 1) - s;
+    a = Args{s, d, du, 0};
+    return d > 0 ? d : 0;
+  }
+  __device__ static int count(const Args& a) { return a.deg; }
+  // relax (:184-195): the CAS loop lowers dist[v] to alt and flags the round
+  // when it succeeds; atomicMin reaches the same final value and succeeds
+  // exactly when the old value was larger.  Arithmetic wraps like the
+  // reference's 32-bit ints (sim/compile.py:36-37).
+  __device__ void item(const Args& a, int e, Acc& acc) const {
+    const int v = __ldg(col + a.start + e);
+    const int alt =
+        (int)((unsigned)a.du + (unsigned)__ldg(weight + a.start + e));
+    if (alt < __ldcg(dist + v) && atomicMin(dist + v, alt) > alt)
+      acc.changed = 1;
+  }
+  __device__ void flush(Acc& acc) const {
+    if (__any_sync(DP_FULL, acc.changed) && lane_id() == 0) *changed = 1;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// manylaunch — MANYLAUNCH_CDP main/spawn (bench/benchmarks.py:283-300)
+// ---------------------------------------------------------------------------
+struct ManyLaunchApp {
+  const int* __restrict__ sizes;
+  int* out;
+  int* total;
+  int n;
+  int pad;
+
+  struct alignas(16) Args {
+    int s, i, pad0, pad1;
+  };
+  struct Acc {
+    int cnt;
+  };
+
+  __device__ int nparents() const { return n; }
+  __device__ void parent_prologue() const {}
+  __device__ int expand(int u, bool valid, Args& a) const {
+    if (!valid) return 0;
+    const int s = __ldg(sizes + u);
+    a = Args{s, u, 0, 0};
+    return s > 0 ? s : 0;
+  }
+  __device__ static int count(const Args& a) { return a.s; }
+  // spawn (:284-290): out[i] += j + 1; total[0] += 1.  The hot total[0]
+  // increment is summed per warp in flush (one atomic per warp).
+  __device__ void item(const Args& a, int j, Acc& acc) const {
+    atomicAdd(out + a.i, j + 1);
+    acc.cnt += 1;
+  }
+  __device__ void flush(Acc& acc) const {
+    const int c = __reduce_add_sync(DP_FULL, acc.cnt);
+    if (c && lane_id() == 0) atomicAdd(total, c);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Triangle counting (no reference implementation)
+//   parent = vertex u of the degree-oriented CSR+, child item = one oriented
+//   edge (u, v) in [edge_lo, edge_hi), work = |N+(u) ∩ N+(v)|.
+// ---------------------------------------------------------------------------
+struct TcApp {
+  const int* __restrict__ rowptr;
+  const int* __restrict__ col;
+  unsigned long long* total;
+  long long edge_lo, edge_hi;
+  int n;
+  int pad;
+
+  struct alignas(16) Args {
+    int u, first, cnt, pad;  // edges [first, first + cnt) of u
+  };
+  struct Acc {
+    unsigned long long tri;
+  };
+
+  __device__ int nparents() const { return n; }
+  __device__ void parent_prologue() const {}
+  __device__ int expand(int u, bool valid, Args& a) const {
+    if (!valid) return 0;
+    long long b = __ldg(rowptr + u), e = __ldg(rowptr + u + 1);
+    if (b < edge_lo) b = edge_lo;
+    if (e > edge_hi) e = edge_hi;
+    if (e <= b) return 0;
+    a = Args{u, (int)b, (int)(e - b), 0};
+    return (int)(e - b);
+  }
+  __device__ static int count(const Args& a) { return a.cnt; }
+
+  // |A ∩ B| of two ascending lists: walk the shorter, lower_bound into the
+  // longer with a window that only moves forward.
+  __device__ static int intersect(const int* __restrict__ A, int na,
+                                  const int* __restrict__ B, int nb) {
+    if (na > nb) {
+      const int* t = A; A = B; B = t;
+      int tn = na; na = nb; nb = tn;
+    }
+    int c = 0, lo = 0;
+    for (int i = 0; i < na && lo < nb; ++i) {
+      const int x = __ldg(A + i);
+      int hi = nb;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(B + mid) < x) lo = mid + 1; else hi = mid;
+      }
+      if (lo < nb && __ldg(B + lo) == x) { ++c; ++lo; }
+    }
+    return c;
+  }
+
+  __device__ void item(const Args& a, int e, Acc& acc) const {
+    const int v = __ldg(col + a.first + e);
+    const int ub = __ldg(rowptr + a.u), ue = __ldg(rowptr + a.u + 1);
+    const int vb = __ldg(rowptr + v), ve = __ldg(rowptr + v + 1);
+    acc.tri += (unsigned long long)intersect(col + ub, ue - ub, col + vb,
+                                             ve - vb);
+  }
+  __device__ void flush(Acc& acc) const {
+    const unsigned long long s = warp_sum_u64(acc.tri);
+    if (s && lane_id() == 0) atomicAdd(total, s);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Bezier line tessellation (no reference implementation; modelled on the
+// CUDA sample cdpBezierTessellation cited by PAPER.md:433; SURVEY §8(d) cfg 2)
+//   parent = curve: curvature -> vertex count, bump-allocate its vertices
+//   (the original's device-side cudaMalloc); child item i =
+//   vertex B(i / (ntess - 1)).
+// ---------------------------------------------------------------------------
+struct BtApp {
+  const float2* __restrict__ cp;  // [ncurves][3]
+  int* ntess;
+  long long* offsets;
+  float2* verts;
+  unsigned long long* cursor;  // bump allocator
+  int* overflow;
+  long long cap;  // vertex capacity
+  int ncurves;
+  int max_tess;
+  float scale;
+  int pad;
+
+  struct alignas(16) Args {
+    int u, nt;
+    long long off;
+  };
+  struct Acc {};
+
+  __device__ int nparents() const { return ncurves; }
+  __device__ void parent_prologue() const {}
+
+  // Vertex count from curvature, fp32 with explicit round-to-nearest ops
+  // (no FMA contraction) so the CPU oracle reproduces it bit-for-bit:
+  //   curv = |P1 - (P0+P2)/2| / |P2 - P0|,  nt = clamp(int(curv*scale), 4, max)
+  __device__ static int tess_count(float2 p0, float2 p1, float2 p2,
+                                   float scale, int max_tess) {
+    const float mx = __fmul_rn(0.5f, __fadd_rn(p0.x, p2.x));
+    const float my = __fmul_rn(0.5f, __fadd_rn(p0.y, p2.y));
+    const float dx = __fsub_rn(p1.x, mx), dy = __fsub_rn(p1.y, my);
+    const float lx = __fsub_rn(p2.x, p0.x), ly = __fsub_rn(p2.y, p0.y);
+    const float num = __fsqrt_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)));
+    const float den = __fsqrt_rn(__fadd_rn(__fmul_rn(lx, lx), __fmul_rn(ly, ly)));
+    const float t = __fmul_rn(__fdiv_rn(num, den), scale);
+    int nt = t < (float)max_tess ? (int)t : max_tess;  // NaN/inf -> max
+    return nt < 4 ? 4 : nt;
+  }
+
+  __device__ int expand(int u, bool valid, Args& a) const {
+    int nt = 0;
+    if (valid) {
+      const float2 p0 = __ldg(cp + 3 * u), p1 = __ldg(cp + 3 * u + 1),
+                   p2 = __ldg(cp + 3 * u + 2);
+      nt = tess_count(p0, p1, p2, scale, max_tess);
+    }
+    // warp-aggregated bump allocation: one 64-bit atomic per warp
+    const int incl = warp_incl_scan(nt);
+    unsigned long long base = 0;
+    if (lane_id() == 31 && incl > 0) base = atomicAdd(cursor, (unsigned long long)incl);
+    base = __shfl_sync(DP_FULL, base, 31);
+    if (!valid) return 0;
+    const long long off = (long long)base + incl - nt;
+    if (off + nt > cap) {  // output pool exhausted: report, do not write
+      atomicExch(overflow, 1);
+      ntess[u] = nt;
+      offsets[u] = -1;
+      return 0;
+    }
+    ntess[u] = nt;
+    offsets[u] = off;
+    a = Args{u, nt, off};
+    return nt;
+  }
+  __device__ static int count(const Args& a) { return a.nt; }
+  __device__ void item(const Args& a, int i, Acc&) const {
+    const float2 p0 = __ldg(cp + 3 * a.u), p1 = __ldg(cp + 3 * a.u + 1),
+                 p2 = __ldg(cp + 3 * a.u + 2);
+    const float t = (float)i / (float)(a.nt - 1);
+    const float s = 1.0f - t;
+    const float w0 = s * s, w1 = 2.0f * s * t, w2 = t * t;
+    verts[a.off + i] = make_float2(w0 * p0.x + w1 * p1.x + w2 * p2.x,
+                                   w0 * p0.y + w1 * p1.y + w2 * p2.y);
+  }
+  __device__ void flush(Acc&) const {}
+};
+
+}  // namespace dp

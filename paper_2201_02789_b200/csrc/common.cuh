@@ -1,0 +1,141 @@
+// common.cuh — warp/block primitives shared by the scheduler and the apps.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define DP_FULL 0xffffffffu
+
+namespace dp {
+
+constexpr int kUnreached = 1 << 30;  // bench/graphs.py:29 UNREACHED
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+__host__ __device__ __forceinline__ int ceil_div(int a, int b) {
+  return (a + b - 1) / b;
+}
+
+__host__ __device__ __forceinline__ long long ceil_div_ll(long long a,
+                                                         long long b) {
+  return (a + b - 1) / b;
+}
+
+// inclusive warp scan (all 32 lanes must participate)
+__device__ __forceinline__ int warp_incl_scan(int x) {
+  const int lane = lane_id();
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(DP_FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  return x;
+}
+
+__device__ __forceinline__ unsigned long long warp_sum_u64(
+    unsigned long long x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(DP_FULL, x, o);
+  return x;
+}
+
+// Broadcast a 4-byte-multiple POD from lane `src` to the whole warp.
+template <class T>
+__device__ __forceinline__ T shfl_pod(const T& v, int src) {
+  static_assert(sizeof(T) % 4 == 0, "POD must be a multiple of 4 bytes");
+  T r;
+  const int* pv = reinterpret_cast<const int*>(&v);
+  int* pr = reinterpret_cast<int*>(&r);
+#pragma unroll
+  for (int i = 0; i < (int)(sizeof(T) / 4); ++i)
+    pr[i] = __shfl_sync(DP_FULL, pv[i], src);
+  return r;
+}
+
+// Block-wide exclusive scan of (participation flag, value) pairs.
+// Every thread of the block must call it (contains __syncthreads).
+struct BlockScan {
+  int rank;   // exclusive count of participants before this thread
+  int excl;   // exclusive sum of values before this thread
+  int np;     // participants in the block
+  int total;  // sum of values in the block
+};
+
+__device__ __forceinline__ BlockScan block_scan(int part, int val,
+                                                int* smem /* >= 66 ints */) {
+  const int lane = lane_id();
+  const int wid = threadIdx.x >> 5;
+  const int nw = (blockDim.x + 31) >> 5;
+  int x = val, c = part;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(DP_FULL, x, o);
+    int z = __shfl_up_sync(DP_FULL, c, o);
+    if (lane >= o) {
+      x += y;
+      c += z;
+    }
+  }
+  if (lane == 31) {
+    smem[wid] = x;
+    smem[32 + wid] = c;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    int wx = lane < nw ? smem[lane] : 0;
+    int wc = lane < nw ? smem[32 + lane] : 0;
+    int ix = warp_incl_scan(wx);
+    int ic = warp_incl_scan(wc);
+    if (lane < nw) {
+      smem[lane] = ix - wx;
+      smem[32 + lane] = ic - wc;
+    }
+    if (lane == 31) {
+      smem[64] = ix;
+      smem[65] = ic;
+    }
+  }
+  __syncthreads();
+  BlockScan s;
+  s.excl = smem[wid] + x - val;
+  s.rank = smem[32 + wid] + c - part;
+  s.total = smem[64];
+  s.np = smem[65];
+  __syncthreads();  // smem may be reused by the caller
+  return s;
+}
+
+// Device-side run counters: the SimReport launch/block counters
+// (sim/machine.py:165-247) measured on hardware.
+struct DevState {
+  unsigned long long launches;  // device-initiated non-empty launches
+  unsigned long long blocks;    // blocks of device-launched grids
+  int err;                      // first cudaError_t seen by a device launch
+  int flag[2];                  // double-buffered `changed` (levels / rounds)
+  int pad;
+};
+
+__device__ __forceinline__ void note_launch_error(DevState* ds) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) atomicCAS(&ds->err, 0, (int)e);
+}
+
+// warp-aggregated launch accounting; all 32 lanes must call
+__device__ __forceinline__ void count_launches_warp(DevState* ds, bool launched,
+                                                    int blocks) {
+  unsigned m = __ballot_sync(DP_FULL, launched);
+  if (m) {
+    int sum = __reduce_add_sync(DP_FULL, launched ? blocks : 0);
+    if (lane_id() == 0) {
+      atomicAdd(&ds->launches, (unsigned long long)__popc(m));
+      atomicAdd(&ds->blocks, (unsigned long long)sum);
+    }
+  }
+}
+
+}  // namespace dp

@@ -1,0 +1,929 @@
+// dynpar.cu — host drivers and the C-ABI of libdynpar.so (include/dynpar.h).
+//
+// The host loop of each application mirrors the reference's `drive`
+// functions (bench/benchmarks.py:157-168, 259-270, 328-332): one host launch
+// of the parent grid per level/round, then a readback of the `changed` flag.
+// What the reference's GlueRunner does around a launch (pipeline.py:99-110:
+// arm tables, grid-granularity completion hook) is done here: tables re-arm
+// on the device, and grid granularity reads the fused counter back and
+// host-launches the aggregated child (passes/common.py:144-164).
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "../../include/dynpar.h"
+#include "apps.cuh"
+#include "sched.cuh"
+
+using namespace dp;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define DP_CUDA(call)                                                        \
+  do {                                                                       \
+    cudaError_t e_ = (call);                                                 \
+    if (e_ != cudaSuccess)                                                   \
+      return fail(DP_ERR_CUDA, std::string("cuda-error: ") + #call + ": " +  \
+                                   cudaGetErrorString(e_));                  \
+  } while (0)
+
+// Per-device workspace: aggregation tables, counters, pinned readback, I/O
+// staging for the host-buffer entry points.  Grow-only.
+struct Workspace {
+  bool ready = false;
+  void* tab = nullptr;  // Args rows
+  size_t tab_bytes = 0;
+  int* scan = nullptr;
+  size_t scan_rows = 0;
+  unsigned long long* ctr = nullptr;  // per group
+  int* done = nullptr;
+  size_t groups = 0;
+  DevState* ds = nullptr;
+  DevState* h_ds = nullptr;            // pinned
+  unsigned long long* h_ctr = nullptr;  // pinned
+  unsigned long long* d_scratch = nullptr;  // TC total / BT cursor
+  int* d_flag = nullptr;                    // BT overflow
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, evk0 = nullptr, evk1 = nullptr;
+  long long pending_limit = 0;
+  // staging for host-buffer calls
+  void* io[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  size_t io_bytes[6] = {0, 0, 0, 0, 0, 0};
+};
+
+Workspace g_ws[64];
+
+int current_device(int* dev) {
+  cudaError_t e = cudaGetDevice(dev);
+  if (e != cudaSuccess)
+    return fail(DP_ERR_NO_DEVICE, std::string("no CUDA device: ") +
+                                      cudaGetErrorString(e));
+  return 0;
+}
+
+Workspace* workspace(int* rc) {
+  int dev = 0;
+  *rc = current_device(&dev);
+  if (*rc) return nullptr;
+  Workspace& w = g_ws[dev & 63];
+  if (!w.ready) {
+    cudaError_t e;
+    if ((e = cudaMalloc(&w.ds, sizeof(DevState))) != cudaSuccess ||
+        (e = cudaMallocHost(&w.h_ds, sizeof(DevState))) != cudaSuccess ||
+        (e = cudaMallocHost(&w.h_ctr, 2 * sizeof(unsigned long long))) !=
+            cudaSuccess ||
+        (e = cudaMalloc(&w.d_scratch, 2 * sizeof(unsigned long long))) !=
+            cudaSuccess ||
+        (e = cudaMalloc(&w.d_flag, sizeof(int))) != cudaSuccess ||
+        (e = cudaEventCreate(&w.ev0)) != cudaSuccess ||
+        (e = cudaEventCreate(&w.ev1)) != cudaSuccess ||
+        (e = cudaEventCreate(&w.evk0)) != cudaSuccess ||
+        (e = cudaEventCreate(&w.evk1)) != cudaSuccess) {
+      *rc = fail(DP_ERR_CUDA,
+                 std::string("workspace init: ") + cudaGetErrorString(e));
+      return nullptr;
+    }
+    w.ready = true;
+  }
+  return &w;
+}
+
+int grow(void** p, size_t* have, size_t need) {
+  if (need <= *have) return 0;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  *have = 0;
+  size_t n = std::max(need, (size_t)256);
+  cudaError_t e = cudaMalloc(p, n);
+  if (e != cudaSuccess)
+    return fail(DP_ERR_CUDA, std::string("workspace alloc of ") +
+                                 std::to_string(n) + " bytes: " +
+                                 cudaGetErrorString(e));
+  *have = n;
+  return 0;
+}
+
+int validate(const dp_config* c) {
+  if (!c) return fail(DP_ERR_INVALID, "null config");
+  if (c->variant != DP_VARIANT_NOCDP && c->variant != DP_VARIANT_CDP)
+    return fail(DP_ERR_INVALID, "unknown variant");
+  if (c->agg < DP_AGG_NONE || c->agg > DP_AGG_GRID)
+    return fail(DP_ERR_INVALID, "unknown aggregation granularity");
+  if (c->agg_threshold > 0 && c->agg != DP_AGG_BLOCK)
+    return fail(DP_ERR_INVALID,
+                "aggregation threshold requires block granularity");
+  if (c->agg == DP_AGG_MULTIBLOCK && c->group_size < 1)
+    return fail(DP_ERR_INVALID, "group size must be at least 1");
+  if (c->cfactor < 1) return fail(DP_ERR_INVALID, "cfactor must be >= 1");
+  if (c->threshold < 0) return fail(DP_ERR_INVALID, "threshold must be >= 0");
+  if (c->parent_block < 32 || c->parent_block > 1024 ||
+      c->parent_block % 32)
+    return fail(DP_ERR_INVALID,
+                "parent_block must be a multiple of 32 in [32, 1024]");
+  if (c->child_block < 32 || c->child_block > 1024 || c->child_block % 32)
+    return fail(DP_ERR_INVALID,
+                "child_block must be a multiple of 32 in [32, 1024]");
+  return 0;
+}
+
+int map_device_error(int e) {
+  if (e == (int)cudaErrorLaunchPendingCountExceeded)
+    return fail(DP_ERR_QUEUE_OVERFLOW,
+                "queue-overflow: pending launch count exceeded the device "
+                "runtime pool (raise pending_launch_limit)");
+  if (e == (int)cudaErrorInvalidConfiguration)
+    return fail(DP_ERR_LAUNCH_CONFIG, "launch-config: invalid device launch");
+  return fail(DP_ERR_CUDA, std::string("cuda-error in device launch: ") +
+                               cudaGetErrorString((cudaError_t)e));
+}
+
+// ---------------------------------------------------------------------------
+// CDP2 pending-launch pool.  Measured on B200 (profiles/cdp_probe_r01.txt):
+// a device launch beyond cudaLimitDevRuntimePendingLaunchCount does NOT fail,
+// it stalls the grid indefinitely, and each slot costs ~11 KB of HBM.  So the
+// pool is sized from an exact upper bound on the device launches one host
+// launch can issue under the chosen policy, and a run whose bound does not
+// fit the memory budget is refused up front with "queue-overflow" — the
+// reference traps the same way when its bounded FIFO overflows
+// (sim/machine.py:237-241; PAPER.md:417 raised this limit on the V100).
+// ---------------------------------------------------------------------------
+
+// parents whose child count can reach `thr`: CSR degree >= thr
+__global__ void count_deg_ge_kernel(const int* __restrict__ rowptr, int n,
+                                    int thr, unsigned long long* out) {
+  unsigned long long c = 0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    c += (__ldg(rowptr + i + 1) - __ldg(rowptr + i)) >= thr;
+  c = warp_sum_u64(c);
+  if (lane_id() == 0 && c) atomicAdd(out, c);
+}
+
+__global__ void count_val_ge_kernel(const int* __restrict__ v, int n, int thr,
+                                    unsigned long long* out) {
+  unsigned long long c = 0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    c += __ldg(v + i) >= thr;
+  c = warp_sum_u64(c);
+  if (lane_id() == 0 && c) atomicAdd(out, c);
+}
+
+int effective_threshold(const dp_config* c) {
+  return c->threshold > 1 ? c->threshold : 1;
+}
+
+// kind 0: CSR rowptr degrees, 1: per-parent values
+int count_launchers(Workspace* w, const int* data, int n, int kind, int thr,
+                    cudaStream_t s, long long* out) {
+  DP_CUDA(cudaMemsetAsync(w->d_scratch + 1, 0, sizeof(unsigned long long), s));
+  if (n > 0) {
+    const int blocks = std::min(dp::ceil_div(n, 256), 148 * 8);
+    if (kind == 0)
+      count_deg_ge_kernel<<<blocks, 256, 0, s>>>(data, n, thr,
+                                                 w->d_scratch + 1);
+    else
+      count_val_ge_kernel<<<blocks, 256, 0, s>>>(data, n, thr,
+                                                 w->d_scratch + 1);
+    DP_CUDA(cudaGetLastError());
+  }
+  DP_CUDA(cudaMemcpyAsync(w->h_ctr + 1, w->d_scratch + 1,
+                          sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                          s));
+  DP_CUDA(cudaStreamSynchronize(s));
+  *out = (long long)w->h_ctr[1];
+  return 0;
+}
+
+// Upper bound on device launches issued by ONE host launch of the parent
+// grid, given `launchers` parents that may meet the threshold.
+long long launch_bound(const dp_config* c, long long parents,
+                       long long launchers) {
+  if (c->variant != DP_VARIANT_CDP) return 0;
+  const long long warps = dp::ceil_div_ll(parents, 32);
+  const long long blocks = dp::ceil_div_ll(parents, c->parent_block);
+  switch (c->agg) {
+    case DP_AGG_NONE: return launchers;
+    case DP_AGG_WARP: return std::min(launchers, warps);
+    case DP_AGG_BLOCK:
+      if (c->agg_threshold > 0)  // direct launches below agg_threshold
+        return std::min(launchers, blocks * (long long)c->agg_threshold);
+      return std::min(launchers, blocks);
+    case DP_AGG_MULTIBLOCK:
+      return std::min(launchers, dp::ceil_div_ll(blocks, c->group_size));
+    default: return 0;  // grid: the aggregated launch is a host launch
+  }
+}
+
+constexpr long long kSlotBytes = 12 * 1024;  // measured ~11.3 KB per slot
+// Largest pool used.  The B200 driver clamps the limit to 599,186 slots
+// (cudaDeviceGetLimit readback); launching past an explicit limit below the
+// clamp fails with cudaErrorLaunchPendingCountExceeded, past the clamp it
+// stalls (profiles/cdp_probe_r01.txt).  Waves keep every host launch's
+// worst case under this.
+constexpr long long kMaxPending = 1 << 19;
+
+int ensure_pending_limit(Workspace* w, const dp_config* c, long long bound) {
+  if (c->variant != DP_VARIANT_CDP) return 0;
+  bound = std::min(bound, kMaxPending);  // larger bounds run in waves
+  long long want = bound + 64;
+  if (c->pending_launch_limit > 0) {
+    if (c->pending_launch_limit < bound)
+      return fail(DP_ERR_QUEUE_OVERFLOW,
+                  "queue-overflow: up to " + std::to_string(bound) +
+                      " pending device launches exceed pending_launch_limit " +
+                      std::to_string(c->pending_launch_limit));
+    want = std::min<long long>(c->pending_launch_limit, kMaxPending + 64);
+  }
+  want = std::max<long long>(want, 2048);
+  if (want <= w->pending_limit) return 0;  // grow-only
+  size_t freeb = 0, totb = 0;
+  DP_CUDA(cudaMemGetInfo(&freeb, &totb));
+  const long long extra = (want - w->pending_limit) * kSlotBytes;
+  if (extra > (long long)(freeb * 0.85))
+    return fail(DP_ERR_QUEUE_OVERFLOW,
+                "queue-overflow: " + std::to_string(bound) +
+                    " pending device launches need ~" +
+                    std::to_string(extra >> 20) + " MiB of launch pool, " +
+                    std::to_string(freeb >> 20) + " MiB free");
+  DP_CUDA(cudaDeviceSynchronize());
+  DP_CUDA(cudaDeviceSetLimit(cudaLimitDevRuntimePendingLaunchCount,
+                             (size_t)want));
+  size_t got = 0;
+  DP_CUDA(cudaDeviceGetLimit(&got, cudaLimitDevRuntimePendingLaunchCount));
+  w->pending_limit = (long long)got;
+  if ((long long)got < bound + 64)
+    return fail(DP_ERR_QUEUE_OVERFLOW,
+                "queue-overflow: the device runtime granted " +
+                    std::to_string(got) + " pending launches, " +
+                    std::to_string(bound) + " may be needed");
+  return 0;
+}
+
+Knobs knobs_of(const dp_config* c) {
+  Knobs k;
+  k.threshold = c->threshold;
+  k.cf = c->cfactor;
+  k.cb = c->child_block;
+  k.group = c->group_size;
+  k.agg_threshold = c->agg_threshold;
+  k.serial_warp = c->serial_mode == DP_SERIAL_WARP;
+  return k;
+}
+
+struct RunCounters {
+  unsigned long long host_launches = 0;
+  unsigned long long host_blocks = 0;
+  unsigned long long kernel_launches = 0;
+  double ms_kernel_max = 0.0;
+  double ms_kernel_sum = 0.0;
+};
+
+template <class App, int AGG, bool CDP>
+void launch_parent_inst(const App& app, int grid, int pb, const Knobs& k,
+                        const AggTables<App>& t, DevState* ds, long long base,
+                        cudaStream_t s) {
+  parent_kernel<App, AGG, CDP><<<grid, pb, 0, s>>>(app, k, t, ds, base);
+}
+
+// Parents per host launch such that the policy's worst-case number of
+// pending device launches fits the pool (see ensure_pending_limit).
+long long wave_parents(const dp_config* c, long long nparents,
+                       long long launchers) {
+  if (c->variant != DP_VARIANT_CDP) return nparents;
+  if (launch_bound(c, nparents, launchers) <= kMaxPending) return nparents;
+  long long per_launch = 1;  // parents that share one potential launch
+  switch (c->agg) {
+    case DP_AGG_WARP: per_launch = 32; break;
+    case DP_AGG_BLOCK:
+      per_launch = c->agg_threshold > 0 ? 1 : c->parent_block;
+      break;
+    case DP_AGG_MULTIBLOCK:
+      per_launch = (long long)c->parent_block * c->group_size;
+      break;
+    default: break;
+  }
+  const long long align = (long long)c->parent_block *
+                          (c->agg == DP_AGG_MULTIBLOCK ? c->group_size : 1);
+  long long w = kMaxPending * per_launch;
+  w = std::max(align, w / align * align);
+  return std::min(w, nparents);
+}
+
+// One host launch of the parent grid over parents [base, base + nparents)
+// (+ the grid-granularity glue).
+template <class App>
+int launch_wave(const App& app, long long base, long long nparents,
+                const dp_config* c, Workspace* w, cudaStream_t s,
+                RunCounters* rc) {
+  if (nparents <= 0) return 0;  // empty host launch: suppressed (machine.py:172)
+  const int pb = c->parent_block;
+  const long long grid_ll = dp::ceil_div_ll(nparents, pb);
+  if (grid_ll > 0x7fffffffLL)
+    return fail(DP_ERR_INVALID, "parent grid too large");
+  const int grid = (int)grid_ll;
+  AggTables<App> t{nullptr, nullptr, nullptr, nullptr};
+  const bool cdp = c->variant == DP_VARIANT_CDP;
+  if (cdp && c->agg != DP_AGG_NONE) {
+    const size_t rows = (size_t)grid * pb;
+    size_t groups = 1;
+    if (c->agg == DP_AGG_BLOCK) groups = grid;
+    if (c->agg == DP_AGG_MULTIBLOCK)
+      groups = dp::ceil_div_ll(grid, c->group_size);
+    int r;
+    if ((r = grow(&w->tab, &w->tab_bytes, rows * sizeof(typename App::Args))))
+      return r;
+    size_t scan_bytes = w->scan_rows * sizeof(int);
+    void* scan = w->scan;
+    if ((r = grow(&scan, &scan_bytes, rows * sizeof(int)))) return r;
+    w->scan = (int*)scan;
+    w->scan_rows = scan_bytes / sizeof(int);
+    if (groups > w->groups) {
+      if (w->ctr) cudaFree(w->ctr);
+      if (w->done) cudaFree(w->done);
+      w->ctr = nullptr;
+      w->done = nullptr;
+      w->groups = 0;
+      DP_CUDA(cudaMalloc(&w->ctr, groups * sizeof(unsigned long long)));
+      DP_CUDA(cudaMalloc(&w->done, groups * sizeof(int)));
+      DP_CUDA(cudaMemsetAsync(w->ctr, 0, groups * sizeof(unsigned long long), s));
+      DP_CUDA(cudaMemsetAsync(w->done, 0, groups * sizeof(int), s));
+      w->groups = groups;
+    }
+    t.args = (typename App::Args*)w->tab;
+    t.scan = w->scan;
+    t.ctr = w->ctr;
+    t.done = w->done;
+  }
+  const Knobs k = knobs_of(c);
+  if (!cdp) {
+    launch_parent_inst<App, kAggNone, false>(app, grid, pb, k, t, w->ds, base, s);
+  } else {
+    switch (c->agg) {
+      case DP_AGG_NONE:
+        launch_parent_inst<App, kAggNone, true>(app, grid, pb, k, t, w->ds, base, s);
+        break;
+      case DP_AGG_WARP:
+        launch_parent_inst<App, kAggWarp, true>(app, grid, pb, k, t, w->ds, base, s);
+        break;
+      case DP_AGG_BLOCK:
+        launch_parent_inst<App, kAggBlock, true>(app, grid, pb, k, t, w->ds, base, s);
+        break;
+      case DP_AGG_MULTIBLOCK:
+        launch_parent_inst<App, kAggMulti, true>(app, grid, pb, k, t, w->ds, base, s);
+        break;
+      default:
+        launch_parent_inst<App, kAggGrid, true>(app, grid, pb, k, t, w->ds, base, s);
+        break;
+    }
+  }
+  DP_CUDA(cudaGetLastError());
+  rc->host_launches += 1;
+  rc->host_blocks += grid;
+  rc->kernel_launches += 1;
+  if (cdp && c->agg == DP_AGG_GRID) {
+    // completion hook (common.py:144-164): read the fused counter, launch
+    // the aggregated child from the host, re-arm the counter
+    DP_CUDA(cudaMemcpyAsync(w->h_ctr, w->ctr, sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, s));
+    DP_CUDA(cudaStreamSynchronize(s));
+    const unsigned long long cv = w->h_ctr[0];
+    const int np = (int)(cv >> 32);
+    const int total = (int)(cv & 0xffffffffull);
+    if (total > 0) {
+      child_agg_kernel<App><<<total, c->child_block, 0, s>>>(
+          app, t.args, t.scan, np, c->cfactor);
+      DP_CUDA(cudaGetLastError());
+      rc->host_launches += 1;
+      rc->host_blocks += total;
+      rc->kernel_launches += 1;
+      DP_CUDA(cudaMemsetAsync(w->ctr, 0, sizeof(unsigned long long), s));
+    }
+  }
+  return 0;
+}
+
+// One logical host launch = one or more waves (more only when the policy's
+// pending-launch bound exceeds the pool; the reference would trap there).
+template <class App>
+int launch_parent(const App& app, long long nparents, long long launchers,
+                  const dp_config* c, Workspace* w, cudaStream_t s,
+                  RunCounters* rc) {
+  const long long wave = wave_parents(c, nparents, launchers);
+  // step time = parent grid(s) + every child they spawned (a CDP2 parent
+  // grid completes only after its children) + the grid-glue launch
+  DP_CUDA(cudaEventRecord(w->evk0, s));
+  for (long long b = 0; b < nparents; b += wave) {
+    int r = launch_wave(app, b, std::min(wave, nparents - b), c, w, s, rc);
+    if (r) return r;
+  }
+  DP_CUDA(cudaEventRecord(w->evk1, s));
+  return 0;
+}
+
+// after the stream has been synchronised
+int account_step(Workspace* w, RunCounters* rc) {
+  float ms = 0.f;
+  DP_CUDA(cudaEventElapsedTime(&ms, w->evk0, w->evk1));
+  rc->ms_kernel_sum += ms;
+  rc->ms_kernel_max = std::max<double>(rc->ms_kernel_max, ms);
+  return 0;
+}
+
+__global__ void init_dist_kernel(int* dist, int n, int src) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dist[i] = i == src ? 0 : kUnreached;
+}
+
+template <class T>
+__global__ void fill_kernel(T* p, long long n, T v) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+int begin_run(Workspace* w, cudaStream_t s) {
+  DP_CUDA(cudaMemsetAsync(w->ds, 0, sizeof(DevState), s));
+  if (w->groups) {
+    DP_CUDA(cudaMemsetAsync(w->ctr, 0, w->groups * sizeof(unsigned long long), s));
+    DP_CUDA(cudaMemsetAsync(w->done, 0, w->groups * sizeof(int), s));
+  }
+  return 0;
+}
+
+int read_state(Workspace* w, cudaStream_t s) {
+  DP_CUDA(cudaMemcpyAsync(w->h_ds, w->ds, sizeof(DevState),
+                          cudaMemcpyDeviceToHost, s));
+  DP_CUDA(cudaStreamSynchronize(s));
+  if (w->h_ds->err) return map_device_error(w->h_ds->err);
+  return 0;
+}
+
+void finish_stats(Workspace* w, const RunCounters& rc, float ms,
+                  dp_stats* st) {
+  if (!st) return;
+  st->num_launches = w->h_ds->launches;
+  st->host_launches = rc.host_launches;
+  st->blocks_scheduled = w->h_ds->blocks + rc.host_blocks;
+  st->max_pending_depth = 0;
+  st->ns_device = (double)ms * 1e6;
+  st->ns_kernel_max = rc.ms_kernel_max * 1e6;
+  st->ns_kernel_sum = rc.ms_kernel_sum * 1e6;
+  st->kernel_launches = rc.kernel_launches;
+}
+
+void clear_stats(dp_stats* st) {
+  if (st) std::memset(st, 0, sizeof(*st));
+}
+
+double now_ns() {
+  return (double)std::chrono::duration_cast<std::chrono::nanoseconds>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
+// ---------------------------------------------------------------------------
+// level/round-loop apps
+// ---------------------------------------------------------------------------
+
+template <class MakeApp>
+int iterate(Workspace* w, const dp_config* c, long long nparents,
+            long long launchers, int max_iter, cudaStream_t s, MakeApp make,
+            dp_stats* st) {
+  RunCounters rc;
+  int r;
+  if ((r = ensure_pending_limit(w, c, launch_bound(c, nparents, launchers))))
+    return r;
+  if ((r = begin_run(w, s))) return r;
+  DP_CUDA(cudaEventRecord(w->ev0, s));
+  int it = 0;
+  bool converged = false;
+  for (; it <= max_iter; ++it) {
+    auto app = make(it, w->ds);
+    if ((r = launch_parent(app, nparents, launchers, c, w, s, &rc))) return r;
+    if ((r = read_state(w, s))) return r;
+    if ((r = account_step(w, &rc))) return r;
+    if (w->h_ds->flag[it & 1] == 0) {
+      converged = true;
+      ++it;
+      break;
+    }
+  }
+  DP_CUDA(cudaEventRecord(w->ev1, s));
+  DP_CUDA(cudaEventSynchronize(w->ev1));
+  float ms = 0.f;
+  DP_CUDA(cudaEventElapsedTime(&ms, w->ev0, w->ev1));
+  if ((r = read_state(w, s))) return r;
+  finish_stats(w, rc, ms, st);
+  if (st) st->iterations = it;
+  if (!converged)
+    return fail(DP_ERR_ITERATIONS, "used more iterations than vertices");
+  return 0;
+}
+
+int bfs_dev_impl(const int32_t* rowptr, const int32_t* col, int32_t n,
+                 int32_t src, const dp_config* c, int32_t* dist,
+                 int32_t* counts, cudaStream_t s, dp_stats* st) {
+  int r;
+  if ((r = validate(c))) return r;
+  if (n < 1) return fail(DP_ERR_INVALID, "graph must have at least 1 vertex");
+  if (src < 0 || src >= n) return fail(DP_ERR_INVALID, "source out of range");
+  Workspace* w = workspace(&r);
+  if (!w) return r;
+  init_dist_kernel<<<dp::ceil_div(n, 256), 256, 0, s>>>(dist, n, src);
+  DP_CUDA(cudaMemsetAsync(counts, 0, (size_t)n * sizeof(int), s));
+  long long launchers = 0;
+  if (c->variant == DP_VARIANT_CDP &&
+      (r = count_launchers(w, rowptr, n, 0, effective_threshold(c), s,
+                           &launchers)))
+    return r;
+  // bench/benchmarks.py:157-168: one launch per level until nothing changes
+  return iterate(w, c, n, launchers, n, s,
+                 [&](int level, DevState* ds) {
+                   BfsApp a;
+                   a.rowptr = rowptr;
+                   a.col = col;
+                   a.dist = dist;
+                   a.counts = counts;
+                   a.changed = &ds->flag[level & 1];
+                   a.changed_next = &ds->flag[(level + 1) & 1];
+                   a.n = n;
+                   a.level = level;
+                   return a;
+                 },
+                 st);
+}
+
+int sssp_dev_impl(const int32_t* rowptr, const int32_t* col,
+                  const int32_t* weight, int32_t n, int32_t src,
+                  const dp_config* c, int32_t* dist, cudaStream_t s,
+                  dp_stats* st) {
+  int r;
+  if ((r = validate(c))) return r;
+  if (n < 1) return fail(DP_ERR_INVALID, "graph must have at least 1 vertex");
+  if (src < 0 || src >= n) return fail(DP_ERR_INVALID, "source out of range");
+  Workspace* w = workspace(&r);
+  if (!w) return r;
+  init_dist_kernel<<<dp::ceil_div(n, 256), 256, 0, s>>>(dist, n, src);
+  long long launchers = 0;
+  if (c->variant == DP_VARIANT_CDP &&
+      (r = count_launchers(w, rowptr, n, 0, effective_threshold(c), s,
+                           &launchers)))
+    return r;
+  // bench/benchmarks.py:259-270: rounds until a full round changes nothing
+  return iterate(w, c, n, launchers, n, s,
+                 [&](int round, DevState* ds) {
+                   SsspApp a;
+                   a.rowptr = rowptr;
+                   a.col = col;
+                   a.weight = weight;
+                   a.dist = dist;
+                   a.changed = &ds->flag[round & 1];
+                   a.changed_next = &ds->flag[(round + 1) & 1];
+                   a.n = n;
+                   a.pad = 0;
+                   return a;
+                 },
+                 st);
+}
+
+// single host launch apps
+template <class App>
+int once(Workspace* w, const dp_config* c, const App& app, long long nparents,
+         long long launchers, cudaStream_t s, dp_stats* st) {
+  RunCounters rc;
+  int r;
+  if ((r = ensure_pending_limit(w, c, launch_bound(c, nparents, launchers))))
+    return r;
+  if ((r = begin_run(w, s))) return r;
+  DP_CUDA(cudaEventRecord(w->ev0, s));
+  if ((r = launch_parent(app, nparents, launchers, c, w, s, &rc))) return r;
+  DP_CUDA(cudaEventRecord(w->ev1, s));
+  DP_CUDA(cudaEventSynchronize(w->ev1));
+  float ms = 0.f;
+  DP_CUDA(cudaEventElapsedTime(&ms, w->ev0, w->ev1));
+  if ((r = read_state(w, s))) return r;
+  if ((r = account_step(w, &rc))) return r;
+  finish_stats(w, rc, ms, st);
+  if (st) st->iterations = 1;
+  return 0;
+}
+
+int manylaunch_dev_impl(const int32_t* sizes, int32_t n, const dp_config* c,
+                        int32_t* out, int32_t* total, cudaStream_t s,
+                        dp_stats* st) {
+  int r;
+  if ((r = validate(c))) return r;
+  if (n < 0) return fail(DP_ERR_INVALID, "negative size");
+  Workspace* w = workspace(&r);
+  if (!w) return r;
+  if (n) DP_CUDA(cudaMemsetAsync(out, 0, (size_t)n * sizeof(int), s));
+  DP_CUDA(cudaMemsetAsync(total, 0, sizeof(int), s));
+  ManyLaunchApp a;
+  a.sizes = sizes;
+  a.out = out;
+  a.total = total;
+  a.n = n;
+  a.pad = 0;
+  long long launchers = 0;
+  if (c->variant == DP_VARIANT_CDP &&
+      (r = count_launchers(w, sizes, n, 1, effective_threshold(c), s,
+                           &launchers)))
+    return r;
+  return once(w, c, a, n, launchers, s, st);
+}
+
+int tc_dev_impl(const int32_t* rowptr, const int32_t* col, int32_t n,
+                int64_t m, int64_t lo, int64_t hi, const dp_config* c,
+                uint64_t* tri, cudaStream_t s, dp_stats* st) {
+  int r;
+  if ((r = validate(c))) return r;
+  if (n < 0 || m < 0) return fail(DP_ERR_INVALID, "negative size");
+  if (lo < 0) lo = 0;
+  if (hi > m) hi = m;
+  Workspace* w = workspace(&r);
+  if (!w) return r;
+  DP_CUDA(cudaMemsetAsync(tri, 0, sizeof(uint64_t), s));
+  TcApp a;
+  a.rowptr = rowptr;
+  a.col = col;
+  a.total = (unsigned long long*)tri;
+  a.edge_lo = lo;
+  a.edge_hi = hi;
+  a.n = n;
+  a.pad = 0;
+  long long launchers = 0;
+  if (c->variant == DP_VARIANT_CDP &&
+      (r = count_launchers(w, rowptr, n, 0, effective_threshold(c), s,
+                           &launchers)))
+    return r;
+  return once(w, c, a, n, launchers, s, st);
+}
+
+int bt_dev_impl(const float* cp, int32_t ncurves, int32_t max_tess,
+                float scale, const dp_config* c, int32_t* ntess,
+                int64_t* offsets, float* verts, int64_t cap, int64_t* nverts,
+                cudaStream_t s, dp_stats* st) {
+  int r;
+  if ((r = validate(c))) return r;
+  if (ncurves < 0) return fail(DP_ERR_INVALID, "negative curve count");
+  if (max_tess < 4) return fail(DP_ERR_INVALID, "max_tess must be >= 4");
+  Workspace* w = workspace(&r);
+  if (!w) return r;
+  DP_CUDA(cudaMemsetAsync(w->d_scratch, 0, sizeof(unsigned long long), s));
+  DP_CUDA(cudaMemsetAsync(w->d_flag, 0, sizeof(int), s));
+  BtApp a;
+  a.cp = (const float2*)cp;
+  a.ntess = ntess;
+  a.offsets = (long long*)offsets;
+  a.verts = (float2*)verts;
+  a.cursor = w->d_scratch;
+  a.overflow = w->d_flag;
+  a.cap = cap;
+  a.ncurves = ncurves;
+  a.max_tess = max_tess;
+  a.scale = scale;
+  a.pad = 0;
+  // every curve owns 4..max_tess vertices
+  const long long launchers = effective_threshold(c) <= max_tess ? ncurves : 0;
+  if ((r = once(w, c, a, ncurves, launchers, s, st))) return r;
+  int ovf = 0;
+  unsigned long long used = 0;
+  DP_CUDA(cudaMemcpyAsync(&used, w->d_scratch, sizeof(used),
+                          cudaMemcpyDeviceToHost, s));
+  DP_CUDA(cudaMemcpyAsync(&ovf, w->d_flag, sizeof(int), cudaMemcpyDeviceToHost,
+                          s));
+  DP_CUDA(cudaStreamSynchronize(s));
+  if (nverts) *nverts = (int64_t)used;
+  if (ovf)
+    return fail(DP_ERR_INVALID, "vertex capacity exceeded: need " +
+                                    std::to_string(used) + " vertices");
+  return 0;
+}
+
+// host-buffer staging
+int stage(Workspace* w, int slot, const void* host, size_t bytes,
+          cudaStream_t s, uint64_t* h2d) {
+  int r;
+  if ((r = grow(&w->io[slot], &w->io_bytes[slot], bytes))) return r;
+  if (host && bytes) {
+    DP_CUDA(cudaMemcpyAsync(w->io[slot], host, bytes, cudaMemcpyHostToDevice, s));
+    *h2d += bytes;
+  }
+  return 0;
+}
+
+int unstage(Workspace* w, int slot, void* host, size_t bytes, cudaStream_t s,
+            uint64_t* d2h) {
+  if (host && bytes) {
+    DP_CUDA(cudaMemcpyAsync(host, w->io[slot], bytes, cudaMemcpyDeviceToHost, s));
+    *d2h += bytes;
+  }
+  return 0;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+int dp_abi_version(void) { return DP_ABI_VERSION; }
+
+const char* dp_last_error(void) { return g_err.c_str(); }
+
+int dp_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+int dp_init(int32_t device) {
+  int n = dp_device_count();
+  if (n <= 0) return fail(DP_ERR_NO_DEVICE, "no CUDA device visible");
+  if (device < 0 || device >= n) return fail(DP_ERR_INVALID, "bad device");
+  DP_CUDA(cudaSetDevice(device));
+  cudaDeviceProp p;
+  DP_CUDA(cudaGetDeviceProperties(&p, device));
+  if (p.major != 10)
+    return fail(DP_ERR_NO_DEVICE, std::string("libdynpar is built for sm_100a; "
+                                              "device is ") + p.name);
+  int r;
+  Workspace* w = workspace(&r);
+  return w ? 0 : r;
+}
+
+#define DP_HOST_CALL_BEGIN                \
+  clear_stats(stats);                     \
+  const double t0_ = now_ns();            \
+  int r_;                                 \
+  Workspace* w_ = workspace(&r_);         \
+  if (!w_) return r_;                     \
+  cudaStream_t s_ = 0;                    \
+  uint64_t h2d_ = 0, d2h_ = 0;
+
+#define DP_HOST_CALL_END                                      \
+  DP_CUDA(cudaStreamSynchronize(s_));                         \
+  if (stats) {                                                \
+    stats->ns_host = now_ns() - t0_;                          \
+    stats->h2d_bytes = h2d_;                                  \
+    stats->d2h_bytes = d2h_;                                  \
+  }                                                           \
+  return 0;
+
+#define DP_TRY(x)       \
+  do {                  \
+    if ((r_ = (x))) return r_; \
+  } while (0)
+
+int dp_bfs(const int32_t* rowptr, const int32_t* col, int32_t n, int64_t m,
+           int32_t src, const dp_config* cfg, int32_t* dist, int32_t* counts,
+           dp_stats* stats) {
+  DP_HOST_CALL_BEGIN
+  if (n < 1 || m < 0) return fail(DP_ERR_INVALID, "bad graph size");
+  DP_TRY(stage(w_, 0, rowptr, (size_t)(n + 1) * 4, s_, &h2d_));
+  DP_TRY(stage(w_, 1, col, (size_t)m * 4, s_, &h2d_));
+  DP_TRY(stage(w_, 2, nullptr, (size_t)n * 4, s_, &h2d_));
+  DP_TRY(stage(w_, 3, nullptr, (size_t)n * 4, s_, &h2d_));
+  DP_TRY(bfs_dev_impl((int*)w_->io[0], (int*)w_->io[1], n, src, cfg,
+                      (int*)w_->io[2], (int*)w_->io[3], s_, stats));
+  DP_TRY(unstage(w_, 2, dist, (size_t)n * 4, s_, &d2h_));
+  DP_TRY(unstage(w_, 3, counts, (size_t)n * 4, s_, &d2h_));
+  DP_HOST_CALL_END
+}
+
+int dp_bfs_dev(const int32_t* d_rowptr, const int32_t* d_col, int32_t n,
+               int64_t m, int32_t src, const dp_config* cfg, int32_t* d_dist,
+               int32_t* d_counts, void* stream, dp_stats* stats) {
+  clear_stats(stats);
+  (void)m;
+  const double t0 = now_ns();
+  int r = bfs_dev_impl(d_rowptr, d_col, n, src, cfg, d_dist, d_counts,
+                       (cudaStream_t)stream, stats);
+  if (stats) stats->ns_host = now_ns() - t0;
+  return r;
+}
+
+int dp_sssp(const int32_t* rowptr, const int32_t* col, const int32_t* weight,
+            int32_t n, int64_t m, int32_t src, const dp_config* cfg,
+            int32_t* dist, dp_stats* stats) {
+  DP_HOST_CALL_BEGIN
+  if (n < 1 || m < 0) return fail(DP_ERR_INVALID, "bad graph size");
+  DP_TRY(stage(w_, 0, rowptr, (size_t)(n + 1) * 4, s_, &h2d_));
+  DP_TRY(stage(w_, 1, col, (size_t)m * 4, s_, &h2d_));
+  DP_TRY(stage(w_, 4, weight, (size_t)m * 4, s_, &h2d_));
+  DP_TRY(stage(w_, 2, nullptr, (size_t)n * 4, s_, &h2d_));
+  DP_TRY(sssp_dev_impl((int*)w_->io[0], (int*)w_->io[1], (int*)w_->io[4], n,
+                       src, cfg, (int*)w_->io[2], s_, stats));
+  DP_TRY(unstage(w_, 2, dist, (size_t)n * 4, s_, &d2h_));
+  DP_HOST_CALL_END
+}
+
+int dp_sssp_dev(const int32_t* d_rowptr, const int32_t* d_col,
+                const int32_t* d_weight, int32_t n, int64_t m, int32_t src,
+                const dp_config* cfg, int32_t* d_dist, void* stream,
+                dp_stats* stats) {
+  clear_stats(stats);
+  (void)m;
+  const double t0 = now_ns();
+  int r = sssp_dev_impl(d_rowptr, d_col, d_weight, n, src, cfg, d_dist,
+                        (cudaStream_t)stream, stats);
+  if (stats) stats->ns_host = now_ns() - t0;
+  return r;
+}
+
+int dp_manylaunch(const int32_t* sizes, int32_t n, const dp_config* cfg,
+                  int32_t* out, int32_t* total, dp_stats* stats) {
+  DP_HOST_CALL_BEGIN
+  if (n < 0) return fail(DP_ERR_INVALID, "negative size");
+  DP_TRY(stage(w_, 0, sizes, (size_t)n * 4, s_, &h2d_));
+  DP_TRY(stage(w_, 1, nullptr, (size_t)n * 4 + 4, s_, &h2d_));
+  DP_TRY(stage(w_, 2, nullptr, 4, s_, &h2d_));
+  DP_TRY(manylaunch_dev_impl((int*)w_->io[0], n, cfg, (int*)w_->io[1],
+                             (int*)w_->io[2], s_, stats));
+  DP_TRY(unstage(w_, 1, out, (size_t)n * 4, s_, &d2h_));
+  DP_TRY(unstage(w_, 2, total, 4, s_, &d2h_));
+  DP_HOST_CALL_END
+}
+
+int dp_manylaunch_dev(const int32_t* d_sizes, int32_t n, const dp_config* cfg,
+                      int32_t* d_out, int32_t* d_total, void* stream,
+                      dp_stats* stats) {
+  clear_stats(stats);
+  const double t0 = now_ns();
+  int r = manylaunch_dev_impl(d_sizes, n, cfg, d_out, d_total,
+                              (cudaStream_t)stream, stats);
+  if (stats) stats->ns_host = now_ns() - t0;
+  return r;
+}
+
+int dp_tc(const int32_t* rowptr, const int32_t* col, int32_t n, int64_t m,
+          int64_t edge_lo, int64_t edge_hi, const dp_config* cfg,
+          uint64_t* triangles, dp_stats* stats) {
+  DP_HOST_CALL_BEGIN
+  if (n < 0 || m < 0) return fail(DP_ERR_INVALID, "bad graph size");
+  DP_TRY(stage(w_, 0, rowptr, (size_t)(n + 1) * 4, s_, &h2d_));
+  DP_TRY(stage(w_, 1, col, (size_t)m * 4, s_, &h2d_));
+  DP_TRY(stage(w_, 2, nullptr, 8, s_, &h2d_));
+  DP_TRY(tc_dev_impl((int*)w_->io[0], (int*)w_->io[1], n, m, edge_lo, edge_hi,
+                     cfg, (uint64_t*)w_->io[2], s_, stats));
+  DP_TRY(unstage(w_, 2, triangles, 8, s_, &d2h_));
+  DP_HOST_CALL_END
+}
+
+int dp_tc_dev(const int32_t* d_rowptr, const int32_t* d_col, int32_t n,
+              int64_t m, int64_t edge_lo, int64_t edge_hi,
+              const dp_config* cfg, uint64_t* d_triangles, void* stream,
+              dp_stats* stats) {
+  clear_stats(stats);
+  const double t0 = now_ns();
+  int r = tc_dev_impl(d_rowptr, d_col, n, m, edge_lo, edge_hi, cfg,
+                      d_triangles, (cudaStream_t)stream, stats);
+  if (stats) stats->ns_host = now_ns() - t0;
+  return r;
+}
+
+int dp_bt(const float* cp, int32_t ncurves, int32_t max_tess, float curv_scale,
+          const dp_config* cfg, int32_t* ntess, int64_t* offsets, float* verts,
+          int64_t vert_capacity, int64_t* nverts, dp_stats* stats) {
+  DP_HOST_CALL_BEGIN
+  if (ncurves < 0 || vert_capacity < 0)
+    return fail(DP_ERR_INVALID, "bad size");
+  int64_t used = 0;
+  DP_TRY(stage(w_, 0, cp, (size_t)ncurves * 24, s_, &h2d_));
+  DP_TRY(stage(w_, 1, nullptr, (size_t)ncurves * 4, s_, &h2d_));
+  DP_TRY(stage(w_, 2, nullptr, (size_t)ncurves * 8, s_, &h2d_));
+  DP_TRY(stage(w_, 3, nullptr, (size_t)vert_capacity * 8, s_, &h2d_));
+  DP_TRY(bt_dev_impl((float*)w_->io[0], ncurves, max_tess, curv_scale, cfg,
+                     (int*)w_->io[1], (int64_t*)w_->io[2], (float*)w_->io[3],
+                     vert_capacity, &used, s_, stats));
+  if (nverts) *nverts = used;
+  DP_TRY(unstage(w_, 1, ntess, (size_t)ncurves * 4, s_, &d2h_));
+  DP_TRY(unstage(w_, 2, offsets, (size_t)ncurves * 8, s_, &d2h_));
+  DP_TRY(unstage(w_, 3, verts, (size_t)used * 8, s_, &d2h_));
+  DP_HOST_CALL_END
+}
+
+int dp_bt_dev(const float* d_cp, int32_t ncurves, int32_t max_tess,
+              float curv_scale, const dp_config* cfg, int32_t* d_ntess,
+              int64_t* d_offsets, float* d_verts, int64_t vert_capacity,
+              int64_t* nverts, void* stream, dp_stats* stats) {
+  clear_stats(stats);
+  const double t0 = now_ns();
+  int r = bt_dev_impl(d_cp, ncurves, max_tess, curv_scale, cfg, d_ntess,
+                      d_offsets, d_verts, vert_capacity, nverts,
+                      (cudaStream_t)stream, stats);
+  if (stats) stats->ns_host = now_ns() - t0;
+  return r;
+}
+
+}  // extern "C"

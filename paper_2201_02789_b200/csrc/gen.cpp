@@ -1,0 +1,167 @@
+// gen.cpp — host-side input generation for the BASELINE configs that the
+// reference has no generator for.
+//
+// RMAT: Graph500 quadrant probabilities (a, b, c, d) = (.57, .19, .19, .05),
+// n = 2^scale vertices, m = edge_factor * n directed edges, no permutation,
+// multi-edges and self-loops kept (the reference CSR keeps both too,
+// bench/graphs.py:117-128), rows sorted ascending.  Randomness is a
+// counter-based 64-bit mix of (seed, edge, level), so the graph is the same
+// for any thread count and on any host; the quadrant draw compares 32-bit
+// integers against integer thresholds (no floating point).
+#include <omp.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "../../include/dynpar.h"
+
+namespace {
+
+inline uint64_t mix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// floor(p * 2^32) for p = .57, .57+.19, .57+.19+.19
+constexpr uint64_t kA = 2448131358ull;
+constexpr uint64_t kAB = 3264175144ull;
+constexpr uint64_t kABC = 4080218931ull;
+
+inline void rmat_edge(uint64_t key, int64_t e, int scale, int32_t* src,
+                      int32_t* dst) {
+  uint32_t s = 0, d = 0;
+  uint64_t h = 0;
+  for (int l = 0; l < scale; ++l) {
+    uint32_t r;
+    if ((l & 1) == 0) {
+      h = mix64(key ^ ((uint64_t)e * 16 + (uint64_t)(l >> 1)));
+      r = (uint32_t)h;
+    } else {
+      r = (uint32_t)(h >> 32);
+    }
+    const uint32_t sb = r >= kAB;                   // quadrants c, d
+    const uint32_t db = (r >= kA && r < kAB) || r >= kABC;  // b, d
+    s = (s << 1) | sb;
+    d = (d << 1) | db;
+  }
+  *src = (int32_t)s;
+  *dst = (int32_t)d;
+}
+
+int threads_of(int32_t nthreads) {
+  return nthreads > 0 ? nthreads : omp_get_max_threads();
+}
+
+}  // namespace
+
+extern "C" {
+
+int dp_rmat_csr(int32_t scale, int32_t edge_factor, uint64_t seed,
+                int32_t* rowptr, int32_t* col, int32_t nthreads) {
+  if (scale < 1 || scale > 30 || edge_factor < 1) return DP_ERR_INVALID;
+  const int64_t n = (int64_t)1 << scale;
+  const int64_t m = (int64_t)edge_factor * n;
+  if (m > 0x7fffffffLL) return DP_ERR_INVALID;  // int32 rowptr
+  const uint64_t key = mix64(seed ^ 0x524D4154ull /* "RMAT" */);
+  const int nt = threads_of(nthreads);
+  std::vector<int32_t> cursor(n + 1, 0);
+  // pass 1: out-degrees
+#pragma omp parallel for num_threads(nt) schedule(static)
+  for (int64_t e = 0; e < m; ++e) {
+    int32_t s, d;
+    rmat_edge(key, e, scale, &s, &d);
+    __atomic_fetch_add(&cursor[s + 1], 1, __ATOMIC_RELAXED);
+  }
+  rowptr[0] = 0;
+  for (int64_t i = 0; i < n; ++i) rowptr[i + 1] = rowptr[i] + cursor[i + 1];
+  std::memcpy(cursor.data(), rowptr, sizeof(int32_t) * n);
+  // pass 2: scatter targets, then sort each row (order-independent result)
+#pragma omp parallel for num_threads(nt) schedule(static)
+  for (int64_t e = 0; e < m; ++e) {
+    int32_t s, d;
+    rmat_edge(key, e, scale, &s, &d);
+    const int32_t pos = __atomic_fetch_add(&cursor[s], 1, __ATOMIC_RELAXED);
+    col[pos] = d;
+  }
+#pragma omp parallel for num_threads(nt) schedule(dynamic, 1024)
+  for (int64_t u = 0; u < n; ++u) std::sort(col + rowptr[u], col + rowptr[u + 1]);
+  return 0;
+}
+
+int dp_tc_orient(const int32_t* rowptr, const int32_t* col, int32_t n,
+                 int32_t** rowptr_plus, int32_t** col_plus, int64_t* m_plus,
+                 int32_t nthreads) {
+  if (n < 0 || !rowptr_plus || !col_plus || !m_plus) return DP_ERR_INVALID;
+  const int nt = threads_of(nthreads);
+  // 1) symmetric adjacency without self-loops (duplicates still present)
+  std::vector<int64_t> sp(n + 1, 0);
+  std::vector<int64_t> cur(n + 1, 0);
+#pragma omp parallel for num_threads(nt) schedule(dynamic, 4096)
+  for (int64_t u = 0; u < n; ++u)
+    for (int32_t e = rowptr[u]; e < rowptr[u + 1]; ++e) {
+      const int32_t v = col[e];
+      if (v == u) continue;
+      __atomic_fetch_add(&cur[u + 1], 1, __ATOMIC_RELAXED);
+      __atomic_fetch_add(&cur[v + 1], 1, __ATOMIC_RELAXED);
+    }
+  for (int64_t i = 0; i < n; ++i) sp[i + 1] = sp[i] + cur[i + 1];
+  std::vector<int32_t> sym(sp[n]);
+  for (int64_t i = 0; i < n; ++i) cur[i] = sp[i];
+#pragma omp parallel for num_threads(nt) schedule(dynamic, 4096)
+  for (int64_t u = 0; u < n; ++u)
+    for (int32_t e = rowptr[u]; e < rowptr[u + 1]; ++e) {
+      const int32_t v = col[e];
+      if (v == u) continue;
+      sym[__atomic_fetch_add(&cur[u], 1, __ATOMIC_RELAXED)] = v;
+      sym[__atomic_fetch_add(&cur[v], 1, __ATOMIC_RELAXED)] = (int32_t)u;
+    }
+  // 2) sort + dedup each row -> simple undirected degree
+  std::vector<int32_t> deg(n, 0);
+#pragma omp parallel for num_threads(nt) schedule(dynamic, 1024)
+  for (int64_t u = 0; u < n; ++u) {
+    int32_t* b = sym.data() + sp[u];
+    int32_t* e = sym.data() + sp[u + 1];
+    std::sort(b, e);
+    deg[u] = (int32_t)(std::unique(b, e) - b);
+  }
+  // 3) orient u -> v iff (deg u, u) < (deg v, v); rows stay sorted
+  auto keep = [&](int64_t u, int32_t v) {
+    return deg[u] < deg[v] || (deg[u] == deg[v] && u < v);
+  };
+  std::vector<int64_t> op(n + 1, 0);
+#pragma omp parallel for num_threads(nt) schedule(dynamic, 4096)
+  for (int64_t u = 0; u < n; ++u) {
+    int64_t c = 0;
+    for (int64_t i = sp[u]; i < sp[u] + deg[u]; ++i) c += keep(u, sym[i]);
+    op[u + 1] = c;
+  }
+  for (int64_t i = 0; i < n; ++i) op[i + 1] += op[i];
+  if (op[n] > 0x7fffffffLL) return DP_ERR_INVALID;
+  int32_t* rp = (int32_t*)std::malloc(sizeof(int32_t) * (n + 1));
+  int32_t* cp = (int32_t*)std::malloc(sizeof(int32_t) * std::max<int64_t>(op[n], 1));
+  if (!rp || !cp) {
+    std::free(rp);
+    std::free(cp);
+    return DP_ERR_INVALID;
+  }
+  for (int64_t i = 0; i <= n; ++i) rp[i] = (int32_t)op[i];
+#pragma omp parallel for num_threads(nt) schedule(dynamic, 4096)
+  for (int64_t u = 0; u < n; ++u) {
+    int64_t o = op[u];
+    for (int64_t i = sp[u]; i < sp[u] + deg[u]; ++i)
+      if (keep(u, sym[i])) cp[o++] = sym[i];
+  }
+  *rowptr_plus = rp;
+  *col_plus = cp;
+  *m_plus = op[n];
+  return 0;
+}
+
+void dp_free(void* p) { std::free(p); }
+
+}  // extern "C"

@@ -1,0 +1,301 @@
+// sched.cuh — the policy-templated nested-launch scheduler.
+//
+// One parent thread owns one unit of irregular work (a vertex, an edge list,
+// a curve).  App::expand() returns its child count and the scalar arguments
+// the child needs; the scheduler then decides, per the paper's three
+// optimizations, how that child grid runs:
+//
+//   T  thresholding  passes/threshold.py:86-172  (guard `_threads >= T` :149)
+//      count < T  -> the child grid runs serially inside the parent
+//      (make_serial_clone :60-83), no launch.
+//   C  coarsening    passes/coarsen.py:65-144
+//      the child grid shrinks to ceil(gd / C) blocks; each physical block
+//      loops over logical blocks [bx*C, min((bx+1)*C, gDim)) (:125-135).
+//   A  aggregation   passes/aggregate.py:171-495
+//      launches are recorded into tables and one representative launches a
+//      single aggregated grid per group; each aggregated child block finds
+//      its logical grid by searching the scanned gdim table (:435-495).
+//
+// B200 re-design of the aggregation protocol (same launch/block counts and
+// outputs as the reference, different mechanics):
+//   - the per-group prefix sum is computed with warp shuffles + one shared-
+//     memory pass (block_scan) instead of thread 0's serial O(np) scan
+//     (aggregate.py:323-343);
+//   - multiblock / grid: ONE fused 64-bit atomicAdd per parent BLOCK
+//     (participants << 32 | blocks) instead of one per participant
+//     (aggregate.py:298-320); the returned old value is both the block's slot
+//     base and its block-offset base, so table rows land already scanned;
+//   - the group's ctr/done words re-arm themselves (the last block zeroes
+//     them) instead of a host memset before every launch (common.py:120-133);
+//   - disaggregation is a 32-ary warp search (4 probes for 1M rows) instead
+//     of a one-thread binary search;
+//   - warp granularity, rejected by the reference (aggregate.py:174-175), is
+//     provided.
+// Child launches are CDP2 fire-and-forget launches.
+#pragma once
+#include "common.cuh"
+
+namespace dp {
+
+enum AggKind { kAggNone = 0, kAggWarp = 1, kAggBlock = 2, kAggMulti = 3,
+               kAggGrid = 4 };
+
+struct Knobs {
+  int threshold;      // 0: pass off (every non-empty child launches)
+  int cf;             // coarsening factor >= 1
+  int cb;             // child block size (multiple of 32)
+  int group;          // multiblock group size in parent blocks
+  int agg_threshold;  // block granularity: direct launches below this
+  int serial_warp;    // 1: below-threshold children share the parent warp
+};
+
+template <class App>
+struct AggTables {
+  typename App::Args* args;  // one row per parent thread (compacted per group)
+  int* scan;                 // exclusive block-offset of each row in its group
+  unsigned long long* ctr;   // per group: participants << 32 | total blocks
+  int* done;                 // per group: parent blocks that finished recording
+};
+
+// ---------------------------------------------------------------------------
+// children
+// ---------------------------------------------------------------------------
+
+// Logical blocks [lb*cf, min(lb*cf+cf, ceil(cnt/cb))) of one child grid.
+template <class App>
+__device__ __forceinline__ void run_logical_blocks(const App& app,
+                                                   const typename App::Args& a,
+                                                   long long lb, int cf,
+                                                   typename App::Acc& acc) {
+  const int cnt = App::count(a);
+  const long long cb = blockDim.x;
+  const long long gl = ceil_div_ll(cnt, cb);
+  long long b0 = lb * cf;
+  long long b1 = b0 + cf < gl ? b0 + cf : gl;
+  for (long long b = b0; b < b1; ++b) {
+    long long e = b * cb + threadIdx.x;
+    if (e < cnt) app.item(a, (int)e, acc);
+  }
+}
+
+// Plain child: BFS `visit` etc. (benchmarks.py:92-103), coarsened.
+template <class App>
+__global__ void child_kernel(App app, typename App::Args a, int cf) {
+  typename App::Acc acc{};
+  run_logical_blocks(app, a, blockIdx.x, cf, acc);
+  app.flush(acc);
+}
+
+// Largest lo in [0, np) with scan[lo] <= p (scan[0] == 0, strictly
+// increasing).  Whole warp; 32-ary: each round probes 32 evenly spaced rows.
+__device__ __forceinline__ int warp_search(const int* __restrict__ scan, int np,
+                                           int p) {
+  const int lane = lane_id();
+  int lo = 0, hi = np;
+  while (hi - lo > 1) {
+    const int step = (hi - lo + 31) >> 5;
+    const int idx = lo + lane * step;
+    const bool ok = idx < hi && __ldcg(scan + idx) <= p;
+    const unsigned m = __ballot_sync(DP_FULL, ok);
+    const int last = 31 - __clz(m);  // lane 0 is always ok
+    lo += last * step;
+    hi = min(lo + step, hi);
+  }
+  return lo;
+}
+
+// Aggregated child (`<child>_agg`, aggregate.py:435-495): one physical block
+// = one (parent row, local physical block) pair, found once per block and
+// reused across the coarsening loop.
+template <class App>
+__global__ void child_agg_kernel(App app, const typename App::Args* tab,
+                                 const int* scan, int np, int cf) {
+  __shared__ int s_lo;
+  int lo = 0;
+  if (threadIdx.x < 32) {
+    lo = warp_search(scan, np, (int)blockIdx.x);
+    if (threadIdx.x == 0) s_lo = lo;
+  }
+  if (blockDim.x > 32) {
+    __syncthreads();
+    lo = s_lo;
+  }
+  const long long lb = (long long)blockIdx.x - __ldcg(scan + lo);
+  typename App::Args a;
+  {
+    // rows are 16-byte multiples: load with 128-bit L2 reads
+    static_assert(sizeof(a) % 16 == 0, "Args rows must be 16-byte multiples");
+    const int4* src = reinterpret_cast<const int4*>(tab + lo);
+    int4* dst = reinterpret_cast<int4*>(&a);
+#pragma unroll
+    for (int i = 0; i < (int)(sizeof(a) / 16); ++i) dst[i] = __ldcg(src + i);
+  }
+  typename App::Acc acc{};
+  run_logical_blocks(app, a, lb, cf, acc);
+  app.flush(acc);
+}
+
+// ---------------------------------------------------------------------------
+// parent
+// ---------------------------------------------------------------------------
+
+// The below-threshold arm.  Thread mode is the reference's serial clone
+// (threshold.py:60-83): the parent thread loops over every child item.
+// Warp mode lets the 32 lanes of the parent warp share each lane's loop in
+// turn (same items, same atomics, no launch).  All lanes must call.
+template <class App>
+__device__ __forceinline__ void serial_arm(const App& app,
+                                           const typename App::Args& a, int cnt,
+                                           bool mine, bool warp_mode,
+                                           typename App::Acc& acc) {
+  if (!warp_mode) {
+    if (mine)
+      for (int e = 0; e < cnt; ++e) app.item(a, e, acc);
+    return;
+  }
+  unsigned m = __ballot_sync(DP_FULL, mine && cnt > 0);
+  const int lane = lane_id();
+  while (m) {
+    const int src = __ffs(m) - 1;
+    m &= m - 1;
+    const typename App::Args b = shfl_pod(a, src);
+    const int c = __shfl_sync(DP_FULL, cnt, src);
+    for (int e = lane; e < c; e += 32) app.item(b, e, acc);
+  }
+}
+
+template <class App, int AGG, bool CDP>
+__global__ void __launch_bounds__(1024)
+    parent_kernel(App app, Knobs k, AggTables<App> t, DevState* ds,
+                  long long base) {
+  using Args = typename App::Args;
+  typename App::Acc acc{};
+  // wave-local thread index (table rows) and the parent it owns
+  const long long lu = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long u = base + lu;
+  app.parent_prologue();
+  Args a{};
+  // called by every thread (apps may use warp collectives); returns 0 when
+  // the thread owns no parent
+  const int cnt = app.expand((int)u, u < app.nparents(), a);
+
+  if constexpr (!CDP) {
+    // No-CDP variant (e.g. BFS_NOCDP, benchmarks.py:122-141): no launch code
+    serial_arm(app, a, cnt, true, k.serial_warp != 0, acc);
+    app.flush(acc);
+  } else {
+    const bool go = cnt > 0 && (k.threshold == 0 || cnt >= k.threshold);
+    serial_arm(app, a, cnt, !go, k.serial_warp != 0, acc);
+    // physical (coarsened) child grid of this parent thread
+    const int gd = go ? ceil_div(ceil_div(cnt, k.cb), k.cf) : 0;
+
+    if constexpr (AGG == kAggNone) {
+      if (gd > 0) {
+        child_kernel<App><<<gd, k.cb, 0, cudaStreamFireAndForget>>>(app, a,
+                                                                     k.cf);
+        note_launch_error(ds);
+      }
+      count_launches_warp(ds, gd > 0, gd);
+    } else if constexpr (AGG == kAggWarp) {
+      const unsigned m = __ballot_sync(DP_FULL, gd > 0);
+      if (m) {
+        const int lane = lane_id();
+        const int incl = warp_incl_scan(gd);
+        const int total = __shfl_sync(DP_FULL, incl, 31);
+        const long long row0 = lu - lane;  // one 32-row segment per warp
+        if (gd > 0) {
+          const int rank = __popc(m & lanemask_lt());
+          t.args[row0 + rank] = a;
+          t.scan[row0 + rank] = incl - gd;
+          __threadfence();
+        }
+        __syncwarp();
+        if (lane == __ffs(m) - 1) {
+          child_agg_kernel<App><<<total, k.cb, 0, cudaStreamFireAndForget>>>(
+              app, t.args + row0, t.scan + row0, __popc(m), k.cf);
+          note_launch_error(ds);
+          atomicAdd(&ds->launches, 1ull);
+          atomicAdd(&ds->blocks, (unsigned long long)total);
+        }
+      }
+    } else {
+      __shared__ int smem[66];
+      __shared__ unsigned long long s_old;
+      const BlockScan s = block_scan(gd > 0, gd, smem);
+      if constexpr (AGG == kAggBlock) {
+        if (k.agg_threshold > 0 && s.np < k.agg_threshold) {
+          // aggregate.py:376-392: too few participants -> direct launches
+          if (gd > 0) {
+            child_kernel<App><<<gd, k.cb, 0, cudaStreamFireAndForget>>>(
+                app, a, k.cf);
+            note_launch_error(ds);
+          }
+          count_launches_warp(ds, gd > 0, gd);
+        } else if (s.np > 0) {
+          const long long row0 = (long long)blockIdx.x * blockDim.x;
+          if (gd > 0) {
+            t.args[row0 + s.rank] = a;
+            t.scan[row0 + s.rank] = s.excl;
+            __threadfence();
+          }
+          __syncthreads();
+          if (threadIdx.x == 0) {
+            child_agg_kernel<App><<<s.total, k.cb, 0,
+                                    cudaStreamFireAndForget>>>(
+                app, t.args + row0, t.scan + row0, s.np, k.cf);
+            note_launch_error(ds);
+            atomicAdd(&ds->launches, 1ull);
+            atomicAdd(&ds->blocks, (unsigned long long)s.total);
+          }
+        }
+      } else {
+        // multiblock (aggregate.py:395-422) and grid (:425-429)
+        const int grp = AGG == kAggMulti ? (int)blockIdx.x / k.group : 0;
+        const long long sb =
+            AGG == kAggMulti ? (long long)grp * k.group * blockDim.x : 0;
+        if (threadIdx.x == 0)
+          s_old = s.np > 0 ? atomicAdd(&t.ctr[grp],
+                                       ((unsigned long long)s.np << 32) +
+                                           (unsigned long long)s.total)
+                           : 0ull;
+        __syncthreads();
+        if (gd > 0) {
+          const unsigned long long old = s_old;
+          const long long row = sb + (long long)(old >> 32) + s.rank;
+          t.args[row] = a;
+          t.scan[row] = (int)(old & 0xffffffffull) + s.excl;
+          __threadfence();  // publish before the done counter (:318-319)
+        }
+        if constexpr (AGG == kAggMulti) {
+          __syncthreads();
+          if (threadIdx.x == 0) {
+            const int nblk = min(k.group, (int)gridDim.x - grp * k.group);
+            const int d = atomicAdd(&t.done[grp], 1);
+            if (d == nblk - 1) {
+              __threadfence();
+              const unsigned long long c =
+                  atomicAdd(&t.ctr[grp], 0ull);  // L2-coherent read
+              t.ctr[grp] = 0;                     // re-arm for the next launch
+              t.done[grp] = 0;
+              const int np = (int)(c >> 32);
+              const int total = (int)(c & 0xffffffffull);
+              if (np > 0) {
+                child_agg_kernel<App><<<total, k.cb, 0,
+                                        cudaStreamFireAndForget>>>(
+                    app, t.args + sb, t.scan + sb, np, k.cf);
+                note_launch_error(ds);
+                atomicAdd(&ds->launches, 1ull);
+                atomicAdd(&ds->blocks, (unsigned long long)total);
+              }
+            }
+          }
+        }
+        // grid: the host glue reads ctr[0] after the parent grid completes
+        // and performs the aggregated launch (common.py:144-164)
+      }
+    }
+    app.flush(acc);
+  }
+}
+
+}  // namespace dp

@@ -1,0 +1,172 @@
+"""Host-side logic and the C-ABI boundary (no GPU needed).
+
+Mirrors the reference's own API tests (tests/test_bench.py) for everything
+that does not execute a kernel: dataset specs, knob validation with the
+reference's error messages, the sweep schema and fault isolation, the memory
+digest formula, and that libdynpar.so loads and exports every symbol the
+header declares.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import re
+
+import numpy as np
+import pytest
+
+from paper_2201_02789_b200 import _lib
+from paper_2201_02789_b200.bench import (CSV_COLUMNS, BenchConfig,
+                                         EquivalenceError, INF_THRESHOLD,
+                                         default_grid, get_benchmark, load,
+                                         parse_spec, render_csv, sweep,
+                                         verify_outputs)
+from paper_2201_02789_b200.bench.report import Report, memory_digest
+from paper_2201_02789_b200.bench.sweep import REFERENCE_COLUMNS
+
+from conftest import ROOT
+
+
+def test_library_exports_every_declared_symbol():
+    header = (ROOT / "include" / "dynpar.h").read_text()
+    declared = set(re.findall(
+        r"^(?:int|void|const char\*)\s+(dp_[a-z0-9_]+)\(", header, re.M))
+    lib = _lib.load()
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert declared == set(_lib.EXPORTED)
+    assert lib.dp_abi_version() == 1
+
+
+def test_struct_layouts_match_header():
+    # dp_config: 16 int32; dp_stats: 7 u64 + 4 f64 + 5 f64 + 3 u64
+    assert ctypes.sizeof(_lib.DpConfig) == 64
+    assert ctypes.sizeof(_lib.DpStats) == 7 * 8 + 4 * 8 + 5 * 8 + 3 * 8
+
+
+def test_no_device_fails_loudly_without_gpu():
+    try:
+        import torch
+        if torch.cuda.is_available():
+            pytest.skip("a GPU is visible")
+    except ImportError:
+        pass
+    with pytest.raises(_lib.DeviceTrap) as e:
+        _lib.device()
+    assert e.value.kind in ("no-device", "cuda-error")
+
+
+def test_parse_spec_fields():
+    s = parse_spec("powerlaw:500:seed3")
+    assert (s.kind, s.size, s.seed) == ("powerlaw", 500, 3)
+    assert parse_spec("rmat:22:seed1").size == 22
+    assert parse_spec("hand").kind == "hand"
+
+
+@pytest.mark.parametrize("bad,needle", [
+    ("zzz:10:seed1", "unknown dataset kind"),
+    ("powerlaw", "kind:size:seedN"),
+    ("powerlaw:ten:seed1", "size"),
+    ("powerlaw:10:7", "seed"),
+    ("powerlaw:0:seed1", "size"),
+    ("hand:10:seed1", "hand"),
+    ("rmat:31:seed1", "scale"),
+])
+def test_parse_spec_rejects(bad, needle):
+    with pytest.raises(ValueError, match=needle):
+        parse_spec(bad)
+
+
+@pytest.mark.parametrize("cfg,needle", [
+    (BenchConfig(agg="multiblock", agg_threshold=2),
+     "aggregation threshold requires block granularity"),
+    (BenchConfig(agg="tile"), "unknown aggregation granularity"),
+    (BenchConfig(agg="multiblock", group_size=0),
+     "group size must be at least 1"),
+    (BenchConfig(threshold=5, order="TXA"), "unknown pass step"),
+    (BenchConfig(parent_block=48), "parent_block"),
+    (BenchConfig(child_block=16), "child_block"),
+    (BenchConfig(serial="lane"), "serial mode"),
+])
+def test_knob_validation_matches_reference_errors(cfg, needle):
+    with pytest.raises(ValueError, match=needle):
+        cfg.to_c()
+
+
+def test_knob_encoding():
+    c = BenchConfig(threshold=128, cfactor=8, agg="multiblock",
+                    group_size=4).to_c()
+    assert (c.threshold, c.cfactor, c.agg, c.group_size) == (128, 8, 3, 4)
+    assert (c.parent_block, c.child_block, c.variant) == (32, 32, 1)
+    # disabled passes (pipeline.py:59-73): T<=0, C<=1, agg None
+    c = BenchConfig(threshold=-3, cfactor=0).to_c(_lib.VARIANT_NOCDP)
+    assert (c.threshold, c.cfactor, c.agg, c.variant) == (0, 1, 0, 0)
+    assert BenchConfig(threshold=INF_THRESHOLD).to_c().threshold == 2**31 - 1
+    # order without a step disables that step
+    c = BenchConfig(threshold=9, cfactor=4, agg="block", order="A").to_c()
+    assert (c.threshold, c.cfactor, c.agg) == (0, 1, 2)
+
+
+def test_default_grid_and_schema():
+    grid = default_grid()
+    assert len(grid) == 12
+    assert [c.agg for c in grid[:4]] == [None, "block", "multiblock", "grid"]
+    assert CSV_COLUMNS[:len(REFERENCE_COLUMNS)] == REFERENCE_COLUMNS
+    assert REFERENCE_COLUMNS == (
+        "bench", "dataset", "threshold", "cfactor", "agg", "group_size",
+        "agg_threshold", "num_launches", "host_launches", "blocks_scheduled",
+        "instructions", "makespan", "t_parent", "t_launch", "t_agg",
+        "t_disagg", "t_child", "error")
+
+
+def test_sweep_isolates_invalid_rows_without_device():
+    rows = sweep("manylaunch", "sizes:40:seed3",
+                 configs=[BenchConfig(agg="multiblock", agg_threshold=4)],
+                 verify=False)
+    assert "aggregation threshold requires block granularity" in \
+        rows[0]["error"]
+    assert rows[0]["makespan"] == ""
+    text = render_csv(rows)
+    assert text.splitlines()[0] == ",".join(CSV_COLUMNS)
+
+
+def test_unknown_benchmark():
+    with pytest.raises(ValueError, match="unknown benchmark"):
+        get_benchmark("mst")
+
+
+def test_memory_digest_matches_reference_formula(golden, golden_arrays):
+    rec = next(r for r in golden["reference"]
+               if r["bench"] == "bfs" and r["dataset"] == "powerlaw:150:seed2")
+    arrays = {k: golden_arrays[f"ref/bfs/powerlaw:150:seed2/{k}"]
+              for k in ("dist", "counts")}
+    assert memory_digest(arrays, {"dist": "int", "counts": "int"}) == \
+        rec["digest"]
+
+
+def _fake_report(arrays):
+    st = {k: 0 for k, _ in _lib.DpStats._fields_}
+    st["ns_phase"] = [0.0] * 5
+    return Report.from_stats(st, arrays, {k: "int" for k in arrays})
+
+
+def test_verify_outputs_names_first_divergent_element():
+    bench, wl = load("manylaunch", "sizes:20:seed2")
+    ref = _fake_report({"out": np.arange(20, dtype=np.int32),
+                        "total": np.array([7], np.int32)})
+    got = _fake_report({"out": np.arange(20, dtype=np.int32),
+                        "total": np.array([7], np.int32)})
+    verify_outputs(bench, wl, got, ref)
+    got.arrays["out"][3] += 1
+    with pytest.raises(EquivalenceError, match=r"'out'\[3\]") as exc:
+        verify_outputs(bench, wl, got, ref)
+    assert "differs from reference" in str(exc.value)
+    assert "manylaunch/sizes:20:seed2" in str(exc.value)
+
+
+def test_report_text_and_lists():
+    r = _fake_report({"dist": np.array([0, 1, 1 << 30], np.int32)})
+    assert r.buffers["dist"] == [0, 1, 1 << 30]
+    text = r.to_text(include_buffers=True)
+    assert "buffer dist = 0 1 1073741824" in text
+    assert text.splitlines()[0] == "num_launches=0"

@@ -1,0 +1,287 @@
+"""Parity of the sm_100a CUDA path against the reference (B200 only).
+
+Three routes, all through the C-ABI (libdynpar.so):
+  1. golden: outputs and memory digests recorded from dynoptc's own
+     run_reference / run_config (tests/golden), for every dataset the
+     reference's tests use plus RMAT graphs injected into the reference;
+  2. counters: num_launches / host_launches / blocks_scheduled of the
+     reference's simulator for 17 T/C/A configurations, reproduced by the
+     device counters at parent block 32 (the counter oracles of
+     tests/test_passes.py);
+  3. oracle: the CPU restatement (oracle/) on the same inputs at sizes up
+     to RMAT-22, plus size-independent properties of BFS/SSSP results.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import oracle
+from paper_2201_02789_b200 import _lib
+from paper_2201_02789_b200.bench import (BenchConfig, EquivalenceError,
+                                         INF_THRESHOLD, graphs, load,
+                                         run_benchmark, run_config,
+                                         run_reference, sweep, verify_outputs)
+from paper_2201_02789_b200.bench.benchmarks import BENCHMARKS, Workload
+from paper_2201_02789_b200.bench.graphs import DatasetSpec, UNREACHED
+
+pytestmark = pytest.mark.gpu
+
+GRAPH_SPECS = ["hand", "powerlaw:150:seed2", "road:180:seed3",
+               "powerlaw:150:seed3", "road:160:seed4", "powerlaw:120:seed5",
+               "powerlaw:2000:seed1", "road:1000:seed7"]
+SIZE_SPECS = ["sizes:100:seed4", "sizes:1024:seed1", "sizes:40:seed3",
+              "sizes:20:seed2"]
+
+# B200-only knobs that must not change any output
+B200_VARIANTS = [dict(), dict(parent_block=256), dict(child_block=128),
+                 dict(serial="warp"), dict(parent_block=128, serial="warp",
+                                           child_block=64)]
+
+
+def _cfg(d):
+    return BenchConfig(**d)
+
+
+def _golden_ref(golden, bench, spec):
+    return next(r for r in golden["reference"]
+                if r["bench"] == bench and r["dataset"] == spec)
+
+
+# ---------------------------------------------------------------------------
+# 1 + 2: golden outputs and counters from the reference
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("bench_name,spec",
+                         [("bfs", s) for s in GRAPH_SPECS]
+                         + [("sssp", s) for s in GRAPH_SPECS]
+                         + [("manylaunch", s) for s in SIZE_SPECS])
+def test_golden_digests_and_counters(bench_name, spec, golden):
+    bench, wl = load(bench_name, spec)
+    ref = _golden_ref(golden, bench_name, spec)
+    nocdp = run_reference(bench, wl)
+    assert nocdp.memory_digest == ref["digest"]
+    assert nocdp.num_launches == 0
+    rows = [r for r in golden["counters"]
+            if r["bench"] == bench_name and r["dataset"] == spec]
+    assert len(rows) == 17
+    for row in rows:
+        rep, _ = run_config(bench, wl, BenchConfig(**row["config"]))
+        assert rep.memory_digest == ref["digest"], row["config"]
+        if bench_name == "sssp":
+            continue  # rounds depend on the (real) schedule; outputs do not
+        assert (rep.num_launches, rep.host_launches, rep.blocks_scheduled) \
+            == (row["num_launches"], row["host_launches"],
+                row["blocks_scheduled"]), row["config"]
+
+
+@pytest.mark.parametrize("knobs", B200_VARIANTS)
+@pytest.mark.parametrize("policy", [
+    dict(), dict(threshold=8), dict(agg="warp"), dict(agg="block"),
+    dict(agg="multiblock", group_size=3), dict(agg="grid"),
+    dict(threshold=4, cfactor=4, agg="multiblock", group_size=2),
+    dict(cfactor=3, agg="block", agg_threshold=5),
+    dict(threshold=INF_THRESHOLD)])
+def test_b200_knobs_keep_outputs(policy, knobs, golden):
+    for bench_name, spec in (("bfs", "powerlaw:2000:seed1"),
+                             ("sssp", "powerlaw:2000:seed1"),
+                             ("manylaunch", "sizes:1024:seed1")):
+        bench, wl = load(bench_name, spec)
+        rep, _ = run_config(bench, wl, BenchConfig(**policy, **knobs))
+        assert rep.memory_digest == \
+            _golden_ref(golden, bench_name, spec)["digest"], (policy, knobs)
+
+
+def test_warp_aggregation_launch_count():
+    bench, wl = load("manylaunch", "sizes:1024:seed1")
+    sizes = wl.payload
+    rep, _ = run_config(bench, wl, BenchConfig(agg="warp"))
+    warps = {i // 32 for i in range(sizes.shape[0]) if sizes[i] > 0}
+    assert rep.num_launches == len(warps)
+    rep, _ = run_config(bench, wl, BenchConfig(threshold=32, agg="warp"))
+    warps = {i // 32 for i in range(sizes.shape[0]) if sizes[i] >= 32}
+    assert rep.num_launches == len(warps)
+
+
+def test_manylaunch_threshold_launch_count_is_large_parent_count():
+    # reference tests/test_bench.py:245-248
+    bench, wl = load("manylaunch", "sizes:1024:seed1")
+    rep, _ = run_config(bench, wl, BenchConfig(threshold=32))
+    assert rep.num_launches == int((wl.payload >= 32).sum())
+    assert rep.buffers["out"] == [s * (s + 1) // 2 for s in wl.payload.tolist()]
+
+
+def _rmat_workload(bench_name, scale, seed):
+    g = graphs.rmat_graph(scale, seed)
+    spec = DatasetSpec("rmat", scale, seed, f"rmat:{scale}:seed{seed}")
+    dist = np.full(g.n, UNREACHED, np.int32)
+    dist[0] = 0
+    bufs = {"rowptr": g.rowptr, "col": g.col, "dist": dist}
+    if bench_name == "bfs":
+        bufs["counts"] = np.zeros(g.n, np.int32)
+        payload = g
+    else:
+        w = graphs.edge_weights(g, seed)
+        bufs["weight"] = w
+        payload = (g, w)
+    return BENCHMARKS[bench_name], Workload(spec, bufs, g.n, payload)
+
+
+@pytest.mark.parametrize("bench_name,scale,seed", [
+    ("bfs", 10, 1), ("bfs", 12, 1), ("bfs", 14, 1), ("bfs", 16, 1),
+    ("sssp", 10, 1), ("sssp", 12, 2), ("sssp", 14, 1)])
+def test_rmat_golden_digests(bench_name, scale, seed, golden):
+    rec = next(r for r in golden["rmat"] if r["bench"] == bench_name
+               and r["scale"] == scale and r["seed"] == seed)
+    bench, wl = _rmat_workload(bench_name, scale, seed)
+    configs = [dict(), dict(threshold=128, agg="block"),
+               dict(threshold=128, cfactor=8, agg="multiblock", group_size=4),
+               dict(threshold=64, cfactor=4, agg="grid", parent_block=256,
+                    serial="warp")]
+    for cfg in configs:
+        rep, _ = run_config(bench, wl, BenchConfig(**cfg))
+        assert rep.memory_digest == rec["digest"], cfg
+        for row in rec.get("counters", []):
+            if row["config"] == cfg and bench_name == "bfs":
+                assert (rep.num_launches, rep.host_launches,
+                        rep.blocks_scheduled) == (
+                    row["num_launches"], row["host_launches"],
+                    row["blocks_scheduled"]), cfg
+    assert run_reference(bench, wl).memory_digest == rec["digest"]
+
+
+# ---------------------------------------------------------------------------
+# 3: oracle at full sizes + size-independent properties
+# ---------------------------------------------------------------------------
+
+def _bfs_properties(g, dist, counts):
+    """dist is a BFS labelling from 0 and counts = in-edges from reached."""
+    assert dist[0] == 0
+    src = np.repeat(np.arange(g.n), np.diff(g.rowptr))
+    reached_u = dist[src] < UNREACHED
+    du, dv = dist[src][reached_u], dist[g.col][reached_u]
+    assert np.all(dv <= du + 1)
+    # every reached vertex except the source has a parent one level up
+    has_parent = np.zeros(g.n, bool)
+    tight = dv == du + 1
+    has_parent[g.col[reached_u][tight]] = True
+    reached = dist < UNREACHED
+    assert np.all(has_parent[reached] | (np.arange(g.n)[reached] == 0))
+    np.testing.assert_array_equal(
+        counts, np.bincount(g.col[reached_u], minlength=g.n))
+
+
+@pytest.mark.parametrize("scale", [18, 22])
+def test_bfs_rmat_full_size_vs_oracle(scale):
+    bench, wl = _rmat_workload("bfs", scale, 1)
+    g = wl.payload
+    dist, counts, levels = oracle.bfs(g.rowptr, g.col, nthreads=0)
+    for cfg in (BenchConfig(threshold=128, agg="block"),
+                BenchConfig(threshold=512, cfactor=8, agg="multiblock",
+                            group_size=4, parent_block=256, serial="warp"),
+                BenchConfig(threshold=256, cfactor=4, agg="grid",
+                            parent_block=256, child_block=128)):
+        rep, _ = run_config(bench, wl, cfg)
+        np.testing.assert_array_equal(rep.arrays["dist"], dist)
+        np.testing.assert_array_equal(rep.arrays["counts"], counts)
+        assert rep.host_launches >= levels  # + grid-glue launches
+    _bfs_properties(g, dist, counts)
+
+
+@pytest.mark.parametrize("scale", [16, 22])
+def test_sssp_rmat_full_size_vs_oracle(scale):
+    bench, wl = _rmat_workload("sssp", scale, 1)
+    g, w = wl.payload
+    dist, _ = oracle.sssp(g.rowptr, g.col, w, nthreads=0)
+    for cfg in (BenchConfig(threshold=128, agg="block"),
+                BenchConfig(threshold=512, cfactor=8, agg="multiblock",
+                            group_size=4, parent_block=256, serial="warp")):
+        rep, _ = run_config(bench, wl, cfg)
+        np.testing.assert_array_equal(rep.arrays["dist"], dist)
+    # optimality certificate: no edge can still be relaxed
+    src = np.repeat(np.arange(g.n), np.diff(g.rowptr))
+    ok = dist[src] < UNREACHED
+    assert np.all(dist[g.col[ok]] <= dist[src[ok]] + w[ok])
+
+
+def test_naive_cdp_rmat16_matches():
+    bench, wl = _rmat_workload("bfs", 16, 1)
+    g = wl.payload
+    dist, counts, _ = oracle.bfs(g.rowptr, g.col, nthreads=0)
+    rep, _ = run_config(bench, wl, BenchConfig())
+    np.testing.assert_array_equal(rep.arrays["dist"], dist)
+    np.testing.assert_array_equal(rep.arrays["counts"], counts)
+    # one launch per reached vertex with out-edges (reference: 33,957 at
+    # RMAT-16 with its own generator)
+    deg = np.diff(g.rowptr)
+    assert rep.num_launches == int(((dist < UNREACHED) & (deg > 0)).sum())
+
+
+@pytest.mark.parametrize("spec", ["rmat:12:seed1", "rmat:16:seed1",
+                                  "rmat:18:seed2"])
+def test_tc_vs_oracle(spec):
+    bench, wl = load("tc", spec)
+    gp = wl.payload[1]
+    want = oracle.tc(gp.rowptr, gp.col, nthreads=0)
+    for cfg in (BenchConfig(), BenchConfig(threshold=64, agg="block"),
+                BenchConfig(threshold=256, cfactor=4, agg="grid",
+                            parent_block=256, serial="warp")):
+        rep, _ = run_config(bench, wl, cfg)
+        assert int(rep.arrays["triangles"][0]) == want, cfg
+    assert int(run_reference(bench, wl).arrays["triangles"][0]) == want
+    # edge-range shards sum to the total (multi-GPU partition)
+    m = gp.m
+    cuts = np.linspace(0, m, 4).astype(int)
+    tot = 0
+    for lo, hi in zip(cuts[:-1], cuts[1:]):
+        out, _ = bench.run(wl, BenchConfig(threshold=64, agg="block").to_c(),
+                           lo=int(lo), hi=int(hi))
+        tot += int(out["triangles"][0])
+    assert tot == want
+
+
+@pytest.mark.parametrize("cfg", [
+    BenchConfig(), BenchConfig(threshold=4096),
+    BenchConfig(cfactor=4, agg="multiblock", group_size=4),
+    BenchConfig(threshold=64, cfactor=2, agg="block", parent_block=128),
+    BenchConfig(agg="grid", child_block=64)])
+def test_bt_vs_oracle(cfg):
+    bench, wl = load("bt", "curves:25000:seed1")
+    ntess, verts = oracle.bt(wl.buffers["cp"], graphs.BT_MAX_TESS,
+                             graphs.BT_CURV_SCALE)
+    rep, _ = run_config(bench, wl, cfg)
+    np.testing.assert_array_equal(rep.arrays["ntess"], ntess)
+    got = rep.arrays["verts"].astype(np.float64)
+    assert got.shape == verts.shape
+    # tolerance from north_star: 1e-5 (coordinates are in [0, 1))
+    assert np.max(np.abs(got - verts)) <= 1e-5
+
+
+def test_run_benchmark_and_sweep_on_device():
+    rep = run_benchmark("bfs", "hand", BenchConfig(agg="block"))
+    assert rep.buffers["dist"] == list(graphs.HAND_BFS_DISTANCES)
+    rows = sweep("bfs", "hand")
+    assert len(rows) == 12 and all(r["error"] == "" for r in rows)
+    assert rows[0]["num_launches"] > rows[-1]["num_launches"] == 0
+
+
+def test_queue_overflow_fails_fast():
+    bench, wl = load("manylaunch", "sizes:1024:seed1")
+    with pytest.raises(_lib.DeviceTrap) as e:
+        run_config(bench, wl, BenchConfig(pending_launch_limit=16))
+    assert e.value.kind == "queue-overflow"
+    # the same run with aggregation fits
+    rep, _ = run_config(bench, wl, BenchConfig(agg="block",
+                                               pending_launch_limit=2048))
+    assert rep.num_launches > 0
+
+
+def test_verify_outputs_detects_corruption():
+    bench, wl = load("bfs", "powerlaw:150:seed2")
+    ref = run_reference(bench, wl)
+    got, _ = run_config(bench, wl, BenchConfig(threshold=8, agg="block"))
+    verify_outputs(bench, wl, got, ref)
+    got.arrays["counts"][5] += 1
+    with pytest.raises(EquivalenceError, match=r"'counts'\[5\]"):
+        verify_outputs(bench, wl, got, ref)

@@ -1,0 +1,291 @@
+"""The CPU oracle and the input generators, pinned to the reference.
+
+- generators: byte-identical to dynoptc.bench.graphs (golden arrays made by
+  importing the reference, tests/golden/make_golden.py);
+- oracle bfs/sssp/manylaunch: equal to dynoptc.bench.run_reference outputs
+  and memory digests, including RMAT graphs injected into the reference;
+- oracle tc/bt (no reference implementation): against independent
+  brute-force restatements here.
+"""
+
+from __future__ import annotations
+
+import heapq
+from collections import deque
+
+import numpy as np
+import pytest
+
+from oracle import oracle
+from paper_2201_02789_b200.bench import graphs
+from paper_2201_02789_b200.bench.graphs import (UNREACHED, make_graph,
+                                                parse_spec)
+from paper_2201_02789_b200.bench.report import memory_digest
+
+GRAPH_SPECS = ["hand", "powerlaw:150:seed2", "road:180:seed3",
+               "powerlaw:150:seed3", "road:160:seed4", "powerlaw:120:seed5",
+               "powerlaw:2000:seed1", "road:1000:seed7"]
+SIZE_SPECS = ["sizes:100:seed4", "sizes:1024:seed1", "sizes:40:seed3",
+              "sizes:20:seed2"]
+
+
+def _weights(spec, g):
+    s = parse_spec(spec)
+    return (np.ones(g.m, np.int32) if s.kind == "hand"
+            else graphs.edge_weights(g, s.seed))
+
+
+# ---------------------------------------------------------------------------
+# generators == reference generators
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("spec", GRAPH_SPECS)
+def test_graph_generators_match_reference(spec, golden_arrays):
+    g = make_graph(parse_spec(spec))
+    np.testing.assert_array_equal(g.rowptr, golden_arrays[f"gen/{spec}/rowptr"])
+    np.testing.assert_array_equal(g.col, golden_arrays[f"gen/{spec}/col"])
+    np.testing.assert_array_equal(
+        graphs.edge_weights(g, parse_spec(spec).seed),
+        golden_arrays[f"gen/{spec}/weights"])
+
+
+@pytest.mark.parametrize("spec", SIZE_SPECS)
+def test_child_sizes_match_reference(spec, golden_arrays):
+    s = parse_spec(spec)
+    np.testing.assert_array_equal(graphs.child_sizes(s.size, s.seed),
+                                  golden_arrays[f"gen/{spec}/sizes"])
+
+
+def test_hand_fixture():
+    g = graphs.hand_graph()
+    dist, _, _ = oracle.bfs(g.rowptr, g.col)
+    assert tuple(dist.tolist()) == graphs.HAND_BFS_DISTANCES
+
+
+# ---------------------------------------------------------------------------
+# oracle == reference run_reference (No-CDP variant on the simulator)
+# ---------------------------------------------------------------------------
+
+def _ref(golden, bench, spec):
+    return next(r for r in golden["reference"]
+                if r["bench"] == bench and r["dataset"] == spec)
+
+
+@pytest.mark.parametrize("nthreads", [1, 4])
+@pytest.mark.parametrize("spec", GRAPH_SPECS)
+def test_oracle_bfs_matches_reference(spec, nthreads, golden, golden_arrays):
+    g = make_graph(parse_spec(spec))
+    dist, counts, levels = oracle.bfs(g.rowptr, g.col, nthreads=nthreads)
+    np.testing.assert_array_equal(dist, golden_arrays[f"ref/bfs/{spec}/dist"])
+    np.testing.assert_array_equal(counts,
+                                  golden_arrays[f"ref/bfs/{spec}/counts"])
+    ref = _ref(golden, "bfs", spec)
+    assert memory_digest({"dist": dist, "counts": counts},
+                         {"dist": "int", "counts": "int"}) == ref["digest"]
+    assert levels == ref["host_launches"]  # level-synchronous: deterministic
+
+
+@pytest.mark.parametrize("nthreads", [1, 4])
+@pytest.mark.parametrize("spec", GRAPH_SPECS)
+def test_oracle_sssp_matches_reference(spec, nthreads, golden, golden_arrays):
+    g = make_graph(parse_spec(spec))
+    dist, _ = oracle.sssp(g.rowptr, g.col, _weights(spec, g),
+                          nthreads=nthreads)
+    np.testing.assert_array_equal(dist, golden_arrays[f"ref/sssp/{spec}/dist"])
+    assert memory_digest({"dist": dist}, {"dist": "int"}) == \
+        _ref(golden, "sssp", spec)["digest"]
+
+
+@pytest.mark.parametrize("spec", SIZE_SPECS)
+def test_oracle_manylaunch_matches_reference(spec, golden, golden_arrays):
+    s = parse_spec(spec)
+    out, total = oracle.manylaunch(graphs.child_sizes(s.size, s.seed), 4)
+    np.testing.assert_array_equal(out,
+                                  golden_arrays[f"ref/manylaunch/{spec}/out"])
+    np.testing.assert_array_equal(
+        total, golden_arrays[f"ref/manylaunch/{spec}/total"])
+
+
+# ---------------------------------------------------------------------------
+# python mirrors of the reference tests (tests/test_bench.py:35-74)
+# ---------------------------------------------------------------------------
+
+def python_bfs(g, src=0):
+    dist = [UNREACHED] * g.n
+    dist[src] = 0
+    q = deque([src])
+    while q:
+        u = q.popleft()
+        for v in g.neighbors(u).tolist():
+            if dist[v] == UNREACHED:
+                dist[v] = dist[u] + 1
+                q.append(v)
+    return dist
+
+
+def python_dijkstra(g, w, src=0):
+    dist = [UNREACHED] * g.n
+    dist[src] = 0
+    heap = [(0, src)]
+    rp = g.rowptr.tolist()
+    col = g.col.tolist()
+    w = w.tolist()
+    while heap:
+        d, u = heapq.heappop(heap)
+        if d > dist[u]:
+            continue
+        for e in range(rp[u], rp[u + 1]):
+            alt = d + w[e]
+            if alt < dist[col[e]]:
+                dist[col[e]] = alt
+                heapq.heappush(heap, (alt, col[e]))
+    return dist
+
+
+@pytest.mark.parametrize("spec", ["rmat:8:seed1", "rmat:10:seed3",
+                                  "powerlaw:500:seed9", "road:400:seed2"])
+def test_oracle_against_python_mirrors(spec):
+    g = make_graph(parse_spec(spec))
+    dist, counts, _ = oracle.bfs(g.rowptr, g.col, nthreads=4)
+    want = python_bfs(g)
+    assert dist.tolist() == want
+    reached = np.array(want) < UNREACHED
+    exp_counts = np.bincount(
+        g.col[np.repeat(reached, np.diff(g.rowptr))], minlength=g.n)
+    np.testing.assert_array_equal(counts, exp_counts)
+    w = _weights(spec, g)
+    sd, _ = oracle.sssp(g.rowptr, g.col, w, nthreads=4)
+    assert sd.tolist() == python_dijkstra(g, w)
+
+
+# ---------------------------------------------------------------------------
+# RMAT generator (builder-defined) and its parity through the reference
+# ---------------------------------------------------------------------------
+
+def test_rmat_generator_pinned(golden):
+    g = graphs.rmat_graph(10, 1)
+    gold = golden["rmat_generator"]
+    assert int(g.rowptr.astype(np.int64).sum()) == \
+        gold["scale10_seed1_rowptr_sum"]
+    assert int(g.col.astype(np.int64).sum()) == gold["scale10_seed1_col_sum"]
+    assert g.col[:16].tolist() == gold["scale10_seed1_col_head"]
+
+
+def test_rmat_generator_shape_and_determinism():
+    g = graphs.rmat_graph(12, 7)
+    n, m = 1 << 12, 16 << 12
+    assert g.n == n and g.m == m
+    assert g.rowptr[0] == 0 and g.rowptr[-1] == m
+    assert np.all(np.diff(g.rowptr) >= 0)
+    assert g.col.min() >= 0 and g.col.max() < n
+    rows_sorted = all(np.all(np.diff(g.neighbors(u)) >= 0)
+                      for u in range(0, n, 97))
+    assert rows_sorted
+    g2 = graphs.rmat_graph(12, 7)
+    np.testing.assert_array_equal(g.col, g2.col)
+    assert not np.array_equal(graphs.rmat_graph(12, 8).col, g.col)
+    # RMAT skew: vertex 0 is the heaviest source, (a+b)^scale of the edges
+    deg = np.diff(g.rowptr)
+    assert deg.argmax() == 0
+    assert abs(deg[0] / m - 0.76 ** 12) < 0.01
+
+
+@pytest.mark.parametrize("bench,scale,seed", [("bfs", 10, 1), ("bfs", 12, 1),
+                                              ("bfs", 14, 1), ("bfs", 16, 1),
+                                              ("sssp", 10, 1),
+                                              ("sssp", 12, 2),
+                                              ("sssp", 14, 1)])
+def test_oracle_rmat_matches_reference_digest(bench, scale, seed, golden):
+    rec = next(r for r in golden["rmat"] if r["bench"] == bench
+               and r["scale"] == scale and r["seed"] == seed)
+    g = graphs.rmat_graph(scale, seed)
+    if bench == "bfs":
+        dist, counts, levels = oracle.bfs(g.rowptr, g.col, nthreads=8)
+        arrays = {"dist": dist, "counts": counts}
+        assert levels == rec["host_launches"]
+    else:
+        dist, _ = oracle.sssp(g.rowptr, g.col, graphs.edge_weights(g, seed),
+                              nthreads=8)
+        arrays = {"dist": dist}
+    assert memory_digest(arrays, {k: "int" for k in arrays}) == rec["digest"]
+
+
+# ---------------------------------------------------------------------------
+# triangle counting (parity unpinned by the reference: brute force here)
+# ---------------------------------------------------------------------------
+
+def _simple_undirected(g):
+    src = np.repeat(np.arange(g.n), np.diff(g.rowptr))
+    dst = g.col.astype(np.int64)
+    keep = src != dst
+    a = np.concatenate([src[keep], dst[keep]])
+    b = np.concatenate([dst[keep], src[keep]])
+    key = np.unique(a * g.n + b)
+    return key // g.n, key % g.n
+
+
+def brute_triangles(g) -> int:
+    a, b = _simple_undirected(g)
+    adj = [set() for _ in range(g.n)]
+    for x, y in zip(a.tolist(), b.tolist()):
+        adj[x].add(y)
+    t = 0
+    for x in range(g.n):
+        for y in adj[x]:
+            if y > x:
+                t += sum(1 for z in adj[x] & adj[y] if z > y)
+    return t
+
+
+def test_tc_orient_matches_numpy_restatement():
+    g = graphs.rmat_graph(10, 2)
+    gp = graphs.tc_orient(g)
+    a, b = _simple_undirected(g)
+    deg = np.bincount(a, minlength=g.n)
+    keep = (deg[a] < deg[b]) | ((deg[a] == deg[b]) & (a < b))
+    a, b = a[keep], b[keep]
+    order = np.lexsort((b, a))
+    rowptr = np.concatenate(([0], np.cumsum(np.bincount(a, minlength=g.n))))
+    np.testing.assert_array_equal(gp.rowptr, rowptr)
+    np.testing.assert_array_equal(gp.col, b[order])
+    assert gp.m * 2 == len(_simple_undirected(g)[0])
+
+
+@pytest.mark.parametrize("spec", ["rmat:8:seed1", "rmat:9:seed4",
+                                  "powerlaw:300:seed2", "road:300:seed1"])
+def test_oracle_tc_matches_brute_force(spec):
+    g = make_graph(parse_spec(spec))
+    gp = graphs.tc_orient(g)
+    want = brute_triangles(g)
+    assert oracle.tc(gp.rowptr, gp.col, nthreads=1) == want
+    assert oracle.tc(gp.rowptr, gp.col, nthreads=4) == want
+    # edge-range shards add up (the multi-GPU partition)
+    cuts = np.linspace(0, gp.m, 5).astype(int)
+    assert sum(oracle.tc(gp.rowptr, gp.col, lo, hi)
+               for lo, hi in zip(cuts[:-1], cuts[1:])) == want
+
+
+# ---------------------------------------------------------------------------
+# Bezier tessellation (parity unpinned by the reference)
+# ---------------------------------------------------------------------------
+
+def test_oracle_bt_counts_and_vertices():
+    cp = graphs.bezier_curves(500, 1)
+    ntess, verts = oracle.bt(cp, graphs.BT_MAX_TESS, graphs.BT_CURV_SCALE)
+    p0, p1, p2 = (cp[:, i, :].astype(np.float32) for i in range(3))
+    mid = np.float32(0.5) * (p0 + p2)
+    d = p1 - mid
+    ln = p2 - p0
+    curv = (np.sqrt(d[:, 0] * d[:, 0] + d[:, 1] * d[:, 1])
+            / np.sqrt(ln[:, 0] * ln[:, 0] + ln[:, 1] * ln[:, 1]))
+    t = (curv * np.float32(graphs.BT_CURV_SCALE)).astype(np.float32)
+    want = np.where(t < graphs.BT_MAX_TESS,
+                    np.clip(t, 0, graphs.BT_MAX_TESS).astype(np.int32),
+                    graphs.BT_MAX_TESS)
+    np.testing.assert_array_equal(ntess, np.maximum(want, 4))
+    assert verts.shape == (int(ntess.sum()), 2)
+    # endpoints reproduce P0 and P2; all vertices inside the hull's box
+    starts = np.concatenate(([0], np.cumsum(ntess)[:-1]))
+    np.testing.assert_allclose(verts[starts], p0, atol=1e-7)
+    np.testing.assert_allclose(verts[starts + ntess - 1], p2, atol=1e-7)
+    assert verts.min() >= -1e-9 and verts.max() <= 1 + 1e-9
