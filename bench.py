@@ -1,0 +1,502 @@
+#!/usr/bin/env python
+"""Benchmark of the nested-parallel hot path (BASELINE.json) on B200.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+
+Headline workload (BASELINE.json metric "GTEPS (BFS/SSSP RMAT-22) ...",
+config "SSSP on RMAT scale-22 integer weights, threshold/coarsening/
+aggregation ... vs naive CDP and aggregation-only"): one step = one complete
+SSSP (all Bellman-Ford rounds until no change, bench/benchmarks.py:259-270 of
+the reference) from vertex 0 over RMAT-22 (n = 4,194,304, m = 67,108,864,
+weights in [1, 9]) through libdynpar's CDP2 scheduler with the tuned
+T + C + A policy.  GTEPS = E_reach / t with E_reach = sum of out-degrees of
+reached vertices (schedule-independent).  Inputs (col + weight = 512 MiB)
+exceed the 126 MB L2, so no flush is needed between steps.
+
+The line also carries: e2e (same metric through the host-buffer C-ABI call
+dp_sssp, H2D of the graph + D2H of dist inside the timed region), roofline
+of the dominant kernel (the per-round parent grid incl. its CDP2 children),
+cpu_baseline (the C oracle on the host cores), speed-ups over the naive-CDP
+and aggregation-only (KLAP-style) builds, and the other BASELINE workloads
+(BFS RMAT-22, TC RMAT-22, BT 25k curves) under "workloads".
+
+N > 1: the SSSP hot path has no partitioned implementation yet, so each rank
+runs an independent replica ("replicas"); TC is the
+partitioned workload (--workload tc).
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+SCALE = 22
+SEED = 1
+
+# tuned policies (profiles/ + DESIGN.md); parity defaults elsewhere
+BEST = {
+    "sssp": dict(threshold=1024, cfactor=8, agg="multiblock", group_size=4,
+                 parent_block=256, child_block=128, serial="warp"),
+    "bfs": dict(threshold=1024, cfactor=8, agg="multiblock", group_size=4,
+                parent_block=256, child_block=128, serial="warp"),
+    "tc": dict(threshold=64, cfactor=4, agg="multiblock", group_size=4,
+               parent_block=256, child_block=128, serial="warp"),
+    "bt": dict(threshold=256, cfactor=4, agg="multiblock", group_size=4,
+               parent_block=256, child_block=128, serial="warp"),
+}
+
+
+def peaks() -> dict:
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:  # noqa: BLE001
+        return {}
+
+
+def hbm_peak():
+    p = peaks()
+    if "hbm_gbs" in p:
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,"
+         "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:  # noqa: BLE001
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:  # noqa: BLE001
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                 "sw_power_cap")
+        for line in self.lines:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for name, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# workloads on the device (C-ABI *_dev entry points, torch for memory/streams)
+# ---------------------------------------------------------------------------
+
+def _cfg(d: dict):
+    from paper_2201_02789_b200.bench import BenchConfig
+    return BenchConfig(**d).to_c()
+
+
+class DeviceGraph:
+    """RMAT-22 CSR (+ weights) resident in HBM."""
+
+    def __init__(self, scale: int, seed: int, weights: bool):
+        import torch
+        from paper_2201_02789_b200.bench import graphs
+        self.g = graphs.rmat_graph(scale, seed)
+        self.w = graphs.edge_weights(self.g, seed) if weights else None
+        self.n, self.m = self.g.n, self.g.m
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.rowptr = torch.from_numpy(self.g.rowptr).to(dev)
+        self.col = torch.from_numpy(self.g.col).to(dev)
+        self.weight = (torch.from_numpy(self.w).to(dev)
+                       if weights else None)
+        self.dist = torch.empty(self.n, dtype=torch.int32, device=dev)
+        self.counts = torch.empty(self.n, dtype=torch.int32, device=dev)
+
+
+def run_dev(kind: str, G, cfg, stream) -> dict:
+    from paper_2201_02789_b200 import _lib
+    lib = _lib.device()
+    st = _lib.DpStats()
+    p = _lib.ptr
+    if kind == "sssp":
+        rc = lib.dp_sssp_dev(p(G.rowptr), p(G.col), p(G.weight), G.n, G.m, 0,
+                             ctypes.byref(cfg), p(G.dist), stream,
+                             ctypes.byref(st))
+    else:
+        rc = lib.dp_bfs_dev(p(G.rowptr), p(G.col), G.n, G.m, 0,
+                            ctypes.byref(cfg), p(G.dist), p(G.counts),
+                            stream, ctypes.byref(st))
+    _lib.check(rc)
+    return _lib.stats_dict(st)
+
+
+def timed_steps(fn, steps: int, warmup: int, stream_obj):
+    """W untimed steps, then K steps bracketed by sync + CUDA events on the
+    launching stream.  Returns (total ms, per-step stats list)."""
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    if torch.distributed.is_initialized():
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    out = []
+    e0.record(stream_obj)
+    for _ in range(steps):
+        out.append(fn())
+    e1.record(stream_obj)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1), out
+
+
+def graph_traffic(kind: str, G, dist: np.ndarray, rounds: int):
+    from paper_2201_02789_b200.bench.benchmarks import (bfs_traffic,
+                                                        sssp_traffic)
+    from paper_2201_02789_b200.bench.graphs import UNREACHED
+    reached = dist < UNREACHED
+    deg = np.diff(G.g.rowptr.astype(np.int64))
+    e_reach = int(deg[reached].sum())
+    if kind == "sssp":
+        return e_reach, sssp_traffic(G.n, int(reached.sum()), e_reach, rounds)
+    return e_reach, bfs_traffic(int(reached.sum()), e_reach)
+
+
+def cpu_baseline_sssp(G, threads: int) -> dict:
+    """The oracle (C restatement of SSSP_NOCDP) on the host cores over the
+    full RMAT-22 workload (a few seconds at most, so no sub-sampling)."""
+    from oracle import oracle
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        dist, rounds = oracle.sssp(G.g.rowptr, G.g.col, G.w, nthreads=threads)
+        reps += 1
+        if time.perf_counter() - t0 > 2.0 or reps >= 5:
+            break
+    dt = (time.perf_counter() - t0) / reps
+    e_reach, _ = graph_traffic("sssp", G, dist, rounds)
+    return {"value": e_reach / dt / 1e9, "unit": "GTEPS", "cores": threads,
+            "kind": "port", "seconds_per_run": dt,
+            "sample": f"full SSSP rmat-{SCALE} from vertex 0 ({rounds} rounds)"
+                      f", mean of {reps} runs, oracle/oracle.c OpenMP",
+            "dist": dist}
+
+
+def e2e_sssp(G, cfg, steps: int) -> dict:
+    """Same metric through the host-buffer C-ABI call dp_sssp: pinned host
+    inputs, H2D copies + D2H of dist inside the timed region."""
+    import torch
+    from paper_2201_02789_b200 import _lib
+    lib = _lib.device()
+    rp = torch.from_numpy(G.g.rowptr).pin_memory()
+    col = torch.from_numpy(G.g.col).pin_memory()
+    w = torch.from_numpy(G.w).pin_memory()
+    dist = torch.empty(G.n, dtype=torch.int32).pin_memory()
+    times, st = [], _lib.DpStats()
+    for i in range(steps + 1):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _lib.check(lib.dp_sssp(rp.data_ptr(), col.data_ptr(), w.data_ptr(),
+                               G.n, G.m, 0, ctypes.byref(cfg),
+                               dist.data_ptr(), ctypes.byref(st)))
+        dt = time.perf_counter() - t0
+        if i:
+            times.append(dt)
+    return {"seconds": statistics.median(times), "h2d": st.h2d_bytes,
+            "d2h": st.d2h_bytes, "dist": dist.numpy().copy()}
+
+
+def extra_workloads(stream, quick: bool) -> dict:
+    """Other BASELINE configs, measured the same way (median of runs)."""
+    import torch
+    from paper_2201_02789_b200 import _lib
+    from paper_2201_02789_b200.bench import load, run_config, BenchConfig
+    out = {}
+    lib = _lib.device()
+    # BFS RMAT-22
+    G = DeviceGraph(SCALE, SEED, weights=False)
+    cfg = _cfg(BEST["bfs"])
+    runs = [run_dev("bfs", G, cfg, stream) for _ in range(5)]
+    ms = statistics.median(r["ns_device"] for r in runs) / 1e6
+    counts = G.counts.cpu().numpy()
+    e_t = int(counts.astype(np.int64).sum())
+    e_reach, alg = graph_traffic("bfs", G, G.dist.cpu().numpy(), 0)
+    naive = run_dev("bfs", G, _cfg(dict(parent_block=32)), stream)
+    out["bfs_rmat22"] = {"gteps": e_t / ms / 1e6, "ms": ms,
+                         "levels": runs[0]["iterations"],
+                         "launches": runs[0]["num_launches"],
+                         "gbps_alg": alg / (ms * 1e6),
+                         "vs_naive_cdp": naive["ns_device"] / 1e6 / ms,
+                         "policy": BEST["bfs"]}
+    del G
+    torch.cuda.empty_cache()
+    # TC RMAT-22
+    bench, wl = load("tc", f"rmat:{SCALE}:seed{SEED}")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    rp = torch.from_numpy(wl.buffers["rowptr"]).to(dev)
+    col = torch.from_numpy(wl.buffers["col"]).to(dev)
+    tri = torch.zeros(1, dtype=torch.int64, device=dev)
+    m = int(wl.buffers["col"].shape[0])
+
+    def tc_once(c):
+        st = _lib.DpStats()
+        _lib.check(lib.dp_tc_dev(rp.data_ptr(), col.data_ptr(), wl.n, m, 0, m,
+                                 ctypes.byref(c), tri.data_ptr(), stream,
+                                 ctypes.byref(st)))
+        return _lib.stats_dict(st)
+    c = _cfg(BEST["tc"])
+    tc_once(c)
+    runs = [tc_once(c) for _ in range(5)]
+    ms = statistics.median(r["ns_device"] for r in runs) / 1e6
+    from paper_2201_02789_b200.bench.benchmarks import tc_traffic
+    alg = tc_traffic(wl.buffers["rowptr"], wl.buffers["col"])
+    out["tc_rmat22"] = {"triangles": int(tri.item()), "ms": ms,
+                        "triangles_per_s": int(tri.item()) / (ms * 1e-3),
+                        "edges_per_s": m / (ms * 1e-3),
+                        "gbps_alg": alg / (ms * 1e6), "policy": BEST["tc"]}
+    del rp, col
+    # BT 25k curves
+    bench, wl = load("bt", "curves:25000:seed1")
+    reps = []
+    for _ in range(6):
+        rep, _ = run_config(bench, wl, BenchConfig(**BEST["bt"]))
+        reps.append(rep)
+    ms = statistics.median(r.ns_device for r in reps[1:]) / 1e6
+    nv = int(reps[-1].arrays["ntess"].astype(np.int64).sum())
+    out["bt_25k"] = {"curves_per_s": 25000 / (ms * 1e-3), "ms": ms,
+                     "vertices": nv, "gbps_alg": (36 * 25000 + 8 * nv) /
+                     (ms * 1e6), "policy": BEST["bt"]}
+    return out
+
+
+# ---------------------------------------------------------------------------
+# arms
+# ---------------------------------------------------------------------------
+
+def init_dist(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and not torch.distributed.is_initialized():
+        backend = "nccl" if args.impl == "ours" else "gloo"
+        torch.distributed.init_process_group(backend)
+    if torch.cuda.is_available():
+        torch.cuda.set_device(local)
+    return world, rank, local
+
+
+def max_over_ranks(x: float) -> float:
+    import torch
+    if not torch.distributed.is_initialized():
+        return x
+    t = torch.tensor([x], dtype=torch.float64,
+                     device="cuda" if torch.distributed.get_backend() ==
+                     "nccl" else "cpu")
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
+
+
+def arm_ours(args, world, rank, local):
+    import torch
+    from paper_2201_02789_b200 import _lib
+    from oracle import oracle  # checker + cpu_baseline only
+    _lib.device()
+    stream_obj = torch.cuda.current_stream()
+    stream = ctypes.c_void_p(stream_obj.cuda_stream)
+    G = DeviceGraph(SCALE, SEED, weights=True)
+    cfg = _cfg(BEST["sssp"])
+    with ClockSampler(local) as clk:
+        total_ms, stats = timed_steps(lambda: run_dev("sssp", G, cfg, stream),
+                                      args.steps, args.warmup, stream_obj)
+    dist = G.dist.cpu().numpy()
+    rounds = int(stats[-1]["iterations"])
+    e_reach, alg_run = graph_traffic("sssp", G, dist, rounds)
+    t_max = max_over_ranks(total_ms)
+    ms_step = t_max / args.steps
+    value = world * e_reach * args.steps / (t_max * 1e-3) / 1e9
+    line = {"metric": "GTEPS (SSSP RMAT-22, T+C+A CDP2)", "value": value,
+            "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic RMAT (Graph500 a,b,c=.57,.19,.19, seed 1, "
+                    "edge factor 16), weights U[1,9]",
+            "config": {"workload": f"sssp rmat-{SCALE} from vertex 0",
+                       "n": G.n, "m": G.m, "e_reach": e_reach,
+                       "rounds": rounds, "policy": BEST["sssp"],
+                       "parallelism": "replicas" if world > 1 else "single",
+                       "l2": "inputs (col+weight 512 MiB) exceed L2; no flush"},
+            "gpu_launches": int(sum(s["kernel_launches"] + s["num_launches"]
+                                    for s in stats))}
+    if rank != 0:
+        return
+    # parity of the timed run against the oracle (checker, not measured)
+    want, _ = oracle.sssp(G.g.rowptr, G.g.col, G.w, nthreads=0)
+    line["parity"] = "bit-exact vs oracle" if np.array_equal(dist, want) \
+        else "MISMATCH"
+    # roofline: the dominant kernel = per-round parent grid incl. children
+    steps_ns = [s["ns_kernel_sum"] / max(s["iterations"], 1) for s in stats]
+    per_round = statistics.mean(steps_ns)
+    alg_round = alg_run / rounds
+    peak, peak_src = hbm_peak()
+    achieved = alg_round / per_round  # bytes/ns == GB/s
+    line["roofline"] = {"bound": "hbm", "achieved": achieved, "peak": peak,
+                        "unit": "GB/s", "frac": achieved / peak,
+                        "traffic": read_traffic(), "peak_source": peak_src,
+                        "kernel": "parent_kernel<SsspApp,multiblock> round "
+                                  "(+CDP2 children)",
+                        "alg_bytes_per_launch": alg_round,
+                        "ms_per_launch": per_round / 1e6,
+                        "share_of_step": sum(s["ns_kernel_sum"] for s in stats)
+                        / (total_ms * 1e6)}
+    line["clocks"] = clk.summary()
+    # e2e through the host-buffer C-ABI
+    e = e2e_sssp(G, cfg, max(2, min(args.steps, 5)))
+    line["e2e"] = {"value": e_reach / e["seconds"] / 1e9, "unit": "GTEPS",
+                   "h2d_bytes_per_step": int(e["h2d"]),
+                   "d2h_bytes_per_step": int(e["d2h"]),
+                   "ms_per_step": e["seconds"] * 1e3}
+    assert np.array_equal(e["dist"], want)
+    # speed-ups over the naive-CDP and aggregation-only builds (same device)
+    naive = run_dev("sssp", G, _cfg(dict()), stream)
+    aggonly = {a: run_dev("sssp", G, _cfg(dict(agg=a)), stream)
+               for a in ("warp", "block", "grid")}
+    best_agg = min(aggonly, key=lambda a: aggonly[a]["ns_device"])
+    line["vs_naive_cdp"] = naive["ns_device"] / 1e6 / ms_step
+    line["vs_agg_only"] = aggonly[best_agg]["ns_device"] / 1e6 / ms_step
+    line["baselines_ms"] = {"naive_cdp": naive["ns_device"] / 1e6,
+                            "naive_cdp_launches": naive["num_launches"],
+                            **{f"agg_only_{a}": r["ns_device"] / 1e6
+                               for a, r in aggonly.items()}}
+    cpu = cpu_baseline_sssp(G, len(os.sched_getaffinity(0)))
+    cpu.pop("dist")
+    line["cpu_baseline"] = cpu
+    if not args.quick:
+        del G
+        torch.cuda.empty_cache()
+        line["workloads"] = extra_workloads(stream, args.quick)
+    print(json.dumps(line), flush=True)
+
+
+def read_traffic():
+    """dram bytes per launch of the dominant kernel from the committed ncu
+    capture (profiles/), else null."""
+    p = ROOT / "profiles" / "traffic.json"
+    try:
+        return json.loads(p.read_text()).get("sssp_round_dram_bytes")
+    except Exception:  # noqa: BLE001
+        return None
+
+
+def arm_reference(args, world, rank, local):
+    """The reference's CPU path for this workload: the oracle port of
+    SSSP_NOCDP (oracle/oracle.c, OpenMP on every host core) — the reference
+    itself is pure Python and cannot travel to the GPU box."""
+    if rank != 0:
+        return
+    from oracle import oracle
+    from paper_2201_02789_b200.bench import graphs
+    from paper_2201_02789_b200.bench.graphs import UNREACHED
+    g = graphs.rmat_graph(SCALE, SEED)
+    w = graphs.edge_weights(g, SEED)
+    threads = len(os.sched_getaffinity(0))
+    for _ in range(args.warmup):
+        oracle.sssp(g.rowptr, g.col, w, nthreads=threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        dist, rounds = oracle.sssp(g.rowptr, g.col, w, nthreads=threads)
+    dt = (time.perf_counter() - t0) / args.steps
+    deg = np.diff(g.rowptr.astype(np.int64))
+    e_reach = int(deg[dist < UNREACHED].sum())
+    value = e_reach / dt / 1e9
+    sample = (f"full SSSP rmat-{SCALE} from vertex 0 ({rounds} rounds) per "
+              f"step, oracle/oracle.c OpenMP")
+    print(json.dumps({
+        "impl": "reference", "metric": "GTEPS (SSSP RMAT-22, T+C+A CDP2)",
+        "value": value, "unit": "GTEPS", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "int32", "data": "synthetic RMAT, weights U[1,9]",
+        "config": {"workload": f"sssp rmat-{SCALE} from vertex 0",
+                   "n": g.n, "m": g.m, "e_reach": e_reach},
+        "cpu_baseline": {"value": value, "unit": "GTEPS", "cores": threads,
+                         "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "GTEPS", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0}}), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--quick", action="store_true",
+                    help="headline only (skip the other workloads)")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    world, rank, local = init_dist(args)
+    if args.impl == "reference":
+        arm_reference(args, world, rank, local)
+    else:
+        arm_ours(args, world, rank, local)
+    import torch
+    if torch.distributed.is_initialized():
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,103 @@
+"""Multi-GPU host logic on CPU: world_size-2 gloo process groups run the
+sharding + reduction of the partitioned workloads, with the CPU oracle
+standing in for each rank's device count (the device kernels are covered by
+tests/test_gpu_parity.py, including per-range TC counts)."""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2201_02789_b200 import dist as pdist
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, fn, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        q.put((rank, fn()))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(world, fn):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(r, world, port, fn, q))
+          for r in range(world)]
+    for p in ps:
+        p.start()
+    out = dict(q.get(timeout=120) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return [out[r] for r in range(world)]
+
+
+def _tc_job():
+    from oracle import oracle
+    from paper_2201_02789_b200.bench import graphs
+    gp = graphs.tc_orient(graphs.rmat_graph(11, 3))
+    total, rng = pdist.tc_count_sharded(
+        gp.rowptr, gp.col,
+        lambda lo, hi: oracle.tc(gp.rowptr, gp.col, lo, hi))
+    return total, rng, oracle.tc(gp.rowptr, gp.col), gp.m
+
+
+def _bt_job():
+    from oracle import oracle
+    from paper_2201_02789_b200.bench import graphs
+    cp = graphs.bezier_curves(3001, 2)
+
+    def tess(lo, hi):
+        nt, v = oracle.bt(cp[lo:hi], graphs.BT_MAX_TESS, graphs.BT_CURV_SCALE)
+        return int(nt.sum()), float(v.sum())
+    nv, cs, rng = pdist.bt_sharded(cp.shape[0], tess)
+    nt, v = oracle.bt(cp, graphs.BT_MAX_TESS, graphs.BT_CURV_SCALE)
+    return nv, cs, rng, int(nt.sum()), float(v.sum())
+
+
+def test_tc_two_ranks_gloo():
+    res = _run(2, _tc_job)
+    (t0, r0, want, m), (t1, r1, _, _) = res
+    assert t0 == t1 == want
+    assert r0[0] == 0 and r0[1] == r1[0] and r1[1] == m
+
+
+def test_bt_two_ranks_gloo():
+    res = _run(2, _bt_job)
+    (nv0, cs0, r0, nv, cs), (nv1, cs1, r1, _, _) = res
+    assert nv0 == nv1 == nv
+    assert abs(cs0 - cs) < 1e-6 * max(1.0, abs(cs)) and cs0 == cs1
+    assert r0 == (0, 1500) or r0[1] == r1[0]
+
+
+@pytest.mark.parametrize("parts", [1, 2, 3, 8])
+def test_balanced_ranges_cover_and_balance(parts):
+    rng = np.random.default_rng(0)
+    cost = rng.integers(1, 100, size=10_000)
+    rs = pdist.balanced_ranges(cost, parts)
+    assert rs[0][0] == 0 and rs[-1][1] == cost.shape[0]
+    assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
+    loads = [cost[lo:hi].sum() for lo, hi in rs]
+    assert max(loads) - min(loads) <= 2 * cost.max()
+
+
+def test_tc_edge_cost():
+    rowptr = np.array([0, 2, 3, 3], np.int32)
+    col = np.array([1, 2, 2], np.int32)
+    np.testing.assert_array_equal(pdist.tc_edge_cost(rowptr, col),
+                                  [2 + 1, 2 + 0, 1 + 0])

@@ -1,0 +1,74 @@
+"""Policy sweep on the device: median device time per configuration.
+
+    python tools/tune.py sssp 22 [--quick]
+Prints one line per config: ms, rounds, launches, blocks, GTEPS.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import itertools
+import statistics
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from bench import DeviceGraph, _cfg, run_dev  # noqa: E402
+
+
+def main():
+    kind = sys.argv[1] if len(sys.argv) > 1 else "sssp"
+    scale = int(sys.argv[2]) if len(sys.argv) > 2 else 22
+    grid = sys.argv[3] if len(sys.argv) > 3 else "wide"
+    torch.cuda.set_device(0)
+    G = DeviceGraph(scale, 1, weights=(kind == "sssp"))
+    stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    deg = np.diff(G.g.rowptr.astype(np.int64))
+    configs = []
+    if grid == "wide":
+        configs.append(dict(variant="nocdp", parent_block=256))
+        configs.append(dict(variant="nocdp", parent_block=256, serial="warp"))
+        for agg in (None, "warp", "block", "grid"):
+            configs.append(dict(agg=agg))
+        for T, C, agg, pb, cb, ser in itertools.product(
+                (128, 512, 2048, 8192), (1, 8), ("block", "multiblock", "grid"),
+                (256,), (32, 128), ("thread", "warp")):
+            configs.append(dict(threshold=T, cfactor=C, agg=agg,
+                                group_size=4, parent_block=pb, child_block=cb,
+                                serial=ser))
+    else:
+        for T, C, G_, pb, cb in itertools.product(
+                (256, 1024, 4096, 16384), (2, 8, 32), (2, 8, 32), (128, 512),
+                (128, 256)):
+            configs.append(dict(threshold=T, cfactor=C, agg="multiblock",
+                                group_size=G_, parent_block=pb,
+                                child_block=cb, serial="warp"))
+    from paper_2201_02789_b200 import _lib
+    for d in configs:
+        d = dict(d)
+        variant = d.pop("variant", "cdp")
+        c = _cfg(d)
+        if variant == "nocdp":
+            c.variant = _lib.VARIANT_NOCDP
+        try:
+            runs = [run_dev(kind, G, c, stream) for _ in range(3)]
+        except Exception as e:  # noqa: BLE001
+            print(f"{variant} {d} ERROR {e}", flush=True)
+            continue
+        ms = statistics.median(r["ns_device"] for r in runs) / 1e6
+        ks = statistics.median(r["ns_kernel_sum"] for r in runs) / 1e6
+        reached = G.dist.cpu().numpy() < (1 << 30)
+        e = int(deg[reached].sum())
+        print(f"{ms:9.3f} ms  kern {ks:9.3f}  it={runs[0]['iterations']:3d} "
+              f"launches={runs[0]['num_launches']:9d} "
+              f"blocks={runs[0]['blocks_scheduled']:10d} "
+              f"GTEPS={e / ms / 1e6:7.2f}  {variant} {d}", flush=True)
+
+
+if __name__ == "__main__":
+    main()
