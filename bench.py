@@ -48,14 +48,18 @@ SEED = 1
 
 # tuned policies (profiles/ + DESIGN.md); parity defaults elsewhere
 BEST = {
-    "sssp": dict(threshold=1024, cfactor=8, agg="multiblock", group_size=4,
-                 parent_block=256, child_block=128, serial="warp"),
-    "bfs": dict(threshold=1024, cfactor=8, agg="multiblock", group_size=4,
-                parent_block=256, child_block=128, serial="warp"),
-    "tc": dict(threshold=64, cfactor=4, agg="multiblock", group_size=4,
+    # one aggregation group spanning the parent grid: the last parent block
+    # issues ONE CDP2 launch per round (tools/tune.py, profiles/tune_*)
+    "sssp": dict(threshold=1024, cfactor=32, agg="multiblock",
+                 group_size=1 << 20, parent_block=128, child_block=64,
+                 serial="warp"),
+    "bfs": dict(threshold=1024, cfactor=16, agg="multiblock",
+                group_size=1 << 20, parent_block=256, child_block=128,
+                serial="warp"),
+    "tc": dict(threshold=256, cfactor=1, agg="multiblock", group_size=1 << 20,
                parent_block=256, child_block=128, serial="warp"),
-    "bt": dict(threshold=256, cfactor=4, agg="multiblock", group_size=4,
-               parent_block=256, child_block=128, serial="warp"),
+    "bt": dict(threshold=64, cfactor=16, agg="grid", parent_block=256,
+               child_block=32, serial="warp"),
 }
 
 

@@ -21,6 +21,7 @@ PHASES = ("parent", "launch", "agg", "disagg", "child")
 
 
 def _fmt_array(a: np.ndarray) -> str:
+    a = a.ravel()
     if a.dtype.kind == "f":
         return " ".join(repr(float(v)) for v in a.tolist())
     return " ".join(map(str, a.tolist()))

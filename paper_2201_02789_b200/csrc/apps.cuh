@@ -10,11 +10,25 @@
 //                         (all threads call; 0 when !valid)
 //   count(a)              child thread count recorded in a row
 //   item(a, e, acc)       child thread e's work
+//   items<U>(args, e, ok, acc)  U independent items at once: all streaming
+//                         loads, then all probes, then all updates, so a
+//                         thread keeps U dependent chains in flight
+//   kUnroll               U used by the scheduler
 //   flush(acc)            warp-collective epilogue (all 32 lanes call)
 #pragma once
 #include "common.cuh"
 
 namespace dp {
+
+// items<U> for apps whose item is not latency-chained: plain loop
+template <int U, class App, class ArgsOf>
+__device__ __forceinline__ void items_loop(const App& app, ArgsOf args,
+                                           const int* e, const bool* ok,
+                                           typename App::Acc& acc) {
+#pragma unroll
+  for (int j = 0; j < U; ++j)
+    if (ok[j]) app.item(args(j), e[j], acc);
+}
 
 // ---------------------------------------------------------------------------
 // BFS — BFS_CDP main/visit (bench/benchmarks.py:91-120)
@@ -57,6 +71,29 @@ struct BfsApp {
     if (__ldcg(dist + v) == kUnreached &&
         atomicCAS(dist + v, kUnreached, a.level + 1) == kUnreached)
       acc.changed = 1;
+  }
+  static constexpr int kUnroll = 4;
+  template <int U, class ArgsOf>
+  __device__ __forceinline__ void items(ArgsOf args, const int* e,
+                                        const bool* ok, Acc& acc) const {
+    int v[U], d[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j)
+      v[j] = ok[j] ? __ldg(col + args(j).start + e[j]) : 0;
+    // L1-cached probe: dist only ever decreases, so a stale copy is >= the
+    // true value and can only cost a redundant (failing) CAS, never a
+    // missed discovery; RMAT hubs then hit in L1 instead of costing a 32 B
+    // L2 sector each
+#pragma unroll
+    for (int j = 0; j < U; ++j) d[j] = ok[j] ? __ldca(dist + v[j]) : 0;
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      if (!ok[j]) continue;
+      atomicAdd(counts + v[j], 1);
+      if (d[j] == kUnreached &&
+          atomicCAS(dist + v[j], kUnreached, args(j).level + 1) == kUnreached)
+        acc.changed = 1;
+    }
   }
   __device__ void flush(Acc& acc) const {
     if (__any_sync(DP_FULL, acc.changed) && lane_id() == 0) *changed = 1;
@@ -110,6 +147,27 @@ struct SsspApp {
     if (alt < __ldcg(dist + v) && atomicMin(dist + v, alt) > alt)
       acc.changed = 1;
   }
+  static constexpr int kUnroll = 4;
+  template <int U, class ArgsOf>
+  __device__ __forceinline__ void items(ArgsOf args, const int* e,
+                                        const bool* ok, Acc& acc) const {
+    int v[U], alt[U], d[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int i = ok[j] ? args(j).start + e[j] : 0;
+      v[j] = ok[j] ? __ldg(col + i) : 0;
+      alt[j] = ok[j] ? (int)((unsigned)args(j).du + (unsigned)__ldg(weight + i))
+                     : 0;
+    }
+    // L1-cached probe (stale copies are >= the true distance: a stale hit
+    // only costs a redundant atomicMin, see BfsApp::items)
+#pragma unroll
+    for (int j = 0; j < U; ++j) d[j] = ok[j] ? __ldca(dist + v[j]) : 0;
+#pragma unroll
+    for (int j = 0; j < U; ++j)
+      if (ok[j] && alt[j] < d[j] && atomicMin(dist + v[j], alt[j]) > alt[j])
+        acc.changed = 1;
+  }
   __device__ void flush(Acc& acc) const {
     if (__any_sync(DP_FULL, acc.changed) && lane_id() == 0) *changed = 1;
   }
@@ -146,6 +204,12 @@ struct ManyLaunchApp {
   __device__ void item(const Args& a, int j, Acc& acc) const {
     atomicAdd(out + a.i, j + 1);
     acc.cnt += 1;
+  }
+  static constexpr int kUnroll = 1;
+  template <int U, class ArgsOf>
+  __device__ __forceinline__ void items(ArgsOf args, const int* e,
+                                        const bool* ok, Acc& acc) const {
+    items_loop<U>(*this, args, e, ok, acc);
   }
   __device__ void flush(Acc& acc) const {
     const int c = __reduce_add_sync(DP_FULL, acc.cnt);
@@ -213,6 +277,12 @@ struct TcApp {
     const int vb = __ldg(rowptr + v), ve = __ldg(rowptr + v + 1);
     acc.tri += (unsigned long long)intersect(col + ub, ue - ub, col + vb,
                                              ve - vb);
+  }
+  static constexpr int kUnroll = 1;
+  template <int U, class ArgsOf>
+  __device__ __forceinline__ void items(ArgsOf args, const int* e,
+                                        const bool* ok, Acc& acc) const {
+    items_loop<U>(*this, args, e, ok, acc);
   }
   __device__ void flush(Acc& acc) const {
     const unsigned long long s = warp_sum_u64(acc.tri);
@@ -299,6 +369,12 @@ struct BtApp {
     const float w0 = s * s, w1 = 2.0f * s * t, w2 = t * t;
     verts[a.off + i] = make_float2(w0 * p0.x + w1 * p1.x + w2 * p2.x,
                                    w0 * p0.y + w1 * p1.y + w2 * p2.y);
+  }
+  static constexpr int kUnroll = 1;
+  template <int U, class ArgsOf>
+  __device__ __forceinline__ void items(ArgsOf args, const int* e,
+                                        const bool* ok, Acc& acc) const {
+    items_loop<U>(*this, args, e, ok, acc);
   }
   __device__ void flush(Acc&) const {}
 };

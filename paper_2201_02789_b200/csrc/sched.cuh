@@ -62,19 +62,30 @@ struct AggTables {
 // ---------------------------------------------------------------------------
 
 // Logical blocks [lb*cf, min(lb*cf+cf, ceil(cnt/cb))) of one child grid.
+// Thread t owns item b*cb + t of each logical block b; App::kUnroll logical
+// blocks are processed together so their independent load chains overlap.
 template <class App>
 __device__ __forceinline__ void run_logical_blocks(const App& app,
                                                    const typename App::Args& a,
                                                    long long lb, int cf,
                                                    typename App::Acc& acc) {
+  constexpr int U = App::kUnroll;
   const int cnt = App::count(a);
   const long long cb = blockDim.x;
   const long long gl = ceil_div_ll(cnt, cb);
-  long long b0 = lb * cf;
-  long long b1 = b0 + cf < gl ? b0 + cf : gl;
-  for (long long b = b0; b < b1; ++b) {
-    long long e = b * cb + threadIdx.x;
-    if (e < cnt) app.item(a, (int)e, acc);
+  const long long b0 = lb * cf;
+  const long long b1 = b0 + cf < gl ? b0 + cf : gl;
+  auto args = [&](int) -> const typename App::Args& { return a; };
+  for (long long b = b0; b < b1; b += U) {
+    int e[U];
+    bool ok[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const long long ee = (b + j) * cb + threadIdx.x;
+      ok[j] = b + j < b1 && ee < cnt;
+      e[j] = (int)ee;
+    }
+    app.template items<U>(args, e, ok, acc);
   }
 }
 
@@ -141,26 +152,58 @@ __global__ void child_agg_kernel(App app, const typename App::Args* tab,
 
 // The below-threshold arm.  Thread mode is the reference's serial clone
 // (threshold.py:60-83): the parent thread loops over every child item.
-// Warp mode lets the 32 lanes of the parent warp share each lane's loop in
-// turn (same items, same atomics, no launch).  All lanes must call.
+// Warp mode (B200) flattens the below-threshold items of all 32 lanes into
+// one list and processes it 32 items per step: item k belongs to the lane
+// whose inclusive count first exceeds k (5-step shuffle search), so a warp
+// with degrees {1, 1, ..., 40} takes 3 fully-populated steps instead of 40
+// one-lane steps.  Same items, same atomics, no launch.  All lanes call.
 template <class App>
 __device__ __forceinline__ void serial_arm(const App& app,
                                            const typename App::Args& a, int cnt,
                                            bool mine, bool warp_mode,
                                            typename App::Acc& acc) {
+  constexpr int U = App::kUnroll;
+  using Args = typename App::Args;
   if (!warp_mode) {
-    if (mine)
-      for (int e = 0; e < cnt; ++e) app.item(a, e, acc);
+    if (!mine) return;
+    auto args = [&](int) -> const Args& { return a; };
+    for (int e0 = 0; e0 < cnt; e0 += U) {
+      int e[U];
+      bool ok[U];
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        e[j] = e0 + j;
+        ok[j] = e0 + j < cnt;
+      }
+      app.template items<U>(args, e, ok, acc);
+    }
     return;
   }
-  unsigned m = __ballot_sync(DP_FULL, mine && cnt > 0);
+  const int c = mine && cnt > 0 ? cnt : 0;
+  const int incl = warp_incl_scan(c);
+  const int total = __shfl_sync(DP_FULL, incl, 31);
+  const int excl = incl - c;
   const int lane = lane_id();
-  while (m) {
-    const int src = __ffs(m) - 1;
-    m &= m - 1;
-    const typename App::Args b = shfl_pod(a, src);
-    const int c = __shfl_sync(DP_FULL, cnt, src);
-    for (int e = lane; e < c; e += 32) app.item(b, e, acc);
+  for (int base = 0; base < total; base += 32 * U) {
+    Args b[U];
+    int e[U];
+    bool ok[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int k = base + j * 32 + lane;
+      int owner = 0;  // lanes whose inclusive count is <= k
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {
+        const int probe = __shfl_sync(DP_FULL, incl, owner + step - 1);
+        if (probe <= k) owner += step;
+      }
+      owner = owner < 31 ? owner : 31;
+      e[j] = k - __shfl_sync(DP_FULL, excl, owner);
+      b[j] = shfl_pod(a, owner);
+      ok[j] = k < total;
+    }
+    app.template items<U>([&](int j) -> const Args& { return b[j]; }, e, ok,
+                          acc);
   }
 }
 
@@ -185,9 +228,13 @@ __global__ void __launch_bounds__(1024)
     app.flush(acc);
   } else {
     const bool go = cnt > 0 && (k.threshold == 0 || cnt >= k.threshold);
-    serial_arm(app, a, cnt, !go, k.serial_warp != 0, acc);
     // physical (coarsened) child grid of this parent thread
     const int gd = go ? ceil_div(ceil_div(cnt, k.cb), k.cf) : 0;
+    // The launch / aggregation protocol runs BEFORE the serial arm (the
+    // reference places it after the enclosing statement, aggregate.py:
+    // 244-249; both orders give the same outputs): children start while the
+    // parent is still busy, and the protocol's barriers never wait on a
+    // long serial tail.
 
     if constexpr (AGG == kAggNone) {
       if (gd > 0) {
@@ -294,6 +341,7 @@ __global__ void __launch_bounds__(1024)
         // and performs the aggregated launch (common.py:144-164)
       }
     }
+    serial_arm(app, a, cnt, !go, k.serial_warp != 0, acc);
     app.flush(acc);
   }
 }

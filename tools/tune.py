@@ -41,13 +41,42 @@ def main():
             configs.append(dict(threshold=T, cfactor=C, agg=agg,
                                 group_size=4, parent_block=pb, child_block=cb,
                                 serial=ser))
-    else:
-        for T, C, G_, pb, cb in itertools.product(
-                (256, 1024, 4096, 16384), (2, 8, 32), (2, 8, 32), (128, 512),
-                (128, 256)):
-            configs.append(dict(threshold=T, cfactor=C, agg="multiblock",
-                                group_size=G_, parent_block=pb,
-                                child_block=cb, serial="warp"))
+    elif grid == "top":
+        for T, C, agg, cb in itertools.product(
+                (512, 1024, 2048), (16, 32), ("grid", "mb-all", "mb16"),
+                (64, 128)):
+            d = dict(threshold=T, cfactor=C, parent_block=256, child_block=cb,
+                     serial="warp")
+            if agg == "grid":
+                d["agg"] = "grid"
+            elif agg == "mb-all":
+                d.update(agg="multiblock", group_size=1 << 20)
+            else:
+                d.update(agg="multiblock", group_size=16)
+            configs.append(d)
+        for pb in (128, 512):
+            configs.append(dict(threshold=1024, cfactor=32, agg="multiblock",
+                                group_size=1 << 20, parent_block=pb,
+                                child_block=64, serial="warp"))
+    elif grid == "focus":
+        configs.append(dict(variant="nocdp", parent_block=256, serial="warp"))
+        configs.append(dict(agg="grid", parent_block=256))
+        for T, C, agg, cb in itertools.product(
+                (128, 256, 512, 1024, 2048, 4096), (4, 8, 16, 32),
+                ("grid", "mb-all", "mb16"), (64, 128, 256)):
+            d = dict(threshold=T, cfactor=C, parent_block=256, child_block=cb,
+                     serial="warp")
+            if agg == "grid":
+                d["agg"] = "grid"
+            elif agg == "mb-all":
+                d.update(agg="multiblock", group_size=1 << 20)
+            else:
+                d.update(agg="multiblock", group_size=16)
+            configs.append(d)
+        for pb in (64, 128, 512, 1024):
+            configs.append(dict(threshold=512, cfactor=8, agg="grid",
+                                parent_block=pb, child_block=128,
+                                serial="warp"))
     from paper_2201_02789_b200 import _lib
     for d in configs:
         d = dict(d)
