@@ -56,8 +56,8 @@ BEST = {
     "bfs": dict(threshold=1024, cfactor=16, agg="multiblock",
                 group_size=1 << 20, parent_block=256, child_block=128,
                 serial="warp"),
-    "tc": dict(threshold=256, cfactor=1, agg="multiblock", group_size=1 << 20,
-               parent_block=256, child_block=128, serial="warp"),
+    "tc": dict(threshold=64, cfactor=4, agg="grid", parent_block=256,
+               child_block=128, serial="warp"),
     "bt": dict(threshold=64, cfactor=16, agg="grid", parent_block=256,
                child_block=32, serial="warp"),
 }

@@ -73,6 +73,7 @@ struct BfsApp {
       acc.changed = 1;
   }
   static constexpr int kUnroll = 4;
+  static constexpr bool kBlockMode = false;
   template <int U, class ArgsOf>
   __device__ __forceinline__ void items(ArgsOf args, const int* e,
                                         const bool* ok, Acc& acc) const {
@@ -148,6 +149,7 @@ struct SsspApp {
       acc.changed = 1;
   }
   static constexpr int kUnroll = 4;
+  static constexpr bool kBlockMode = false;
   template <int U, class ArgsOf>
   __device__ __forceinline__ void items(ArgsOf args, const int* e,
                                         const bool* ok, Acc& acc) const {
@@ -206,6 +208,7 @@ struct ManyLaunchApp {
     acc.cnt += 1;
   }
   static constexpr int kUnroll = 1;
+  static constexpr bool kBlockMode = false;
   template <int U, class ArgsOf>
   __device__ __forceinline__ void items(ArgsOf args, const int* e,
                                         const bool* ok, Acc& acc) const {
@@ -279,6 +282,100 @@ struct TcApp {
                                              ve - vb);
   }
   static constexpr int kUnroll = 1;
+
+  // Child blocks: N+(u) goes into a shared-memory hash set once per physical
+  // block; each warp then takes 32 edges (u, v), flattens their wedge lists
+  // N+(v) into one list (load-balanced, owner lane by shuffle search) and
+  // probes the set: coalesced reads of N+(v), O(1) lookups, no per-thread
+  // merge chains.  Lists longer than kSlots/2 fall back to per-thread merges.
+  static constexpr bool kBlockMode = true;
+  static constexpr int kSlotBits = 12;
+  static constexpr int kSlots = 1 << kSlotBits;  // 16 KB of shared memory
+
+  __device__ static unsigned hash_slot(int x, int bits) {
+    return ((unsigned)x * 2654435761u) >> (32 - bits);
+  }
+
+  __device__ void block_items(const Args& a, long long e0, long long e1,
+                              Acc& acc) const {
+    __shared__ int set[kSlots];
+    const int ub = __ldg(rowptr + a.u), ue = __ldg(rowptr + a.u + 1);
+    if (ue - ub > kSlots / 2) {
+      for (long long e = e0 + threadIdx.x; e < e1; e += blockDim.x)
+        item(a, (int)e, acc);
+      return;
+    }
+    // always the full sparse table: most probes are misses (wedges >>
+    // triangles) and a linear-probing miss costs ~1/(1-load)^2 probes; the
+    // clear is 16 stores per thread.  Measured (profiles/tune_tc_*): sizing
+    // the table to the list (load 1/2) or to 32 KB (lower occupancy) is
+    // slower.
+    const int bits = kSlotBits;
+    const unsigned mask = (1u << bits) - 1;
+    for (int i = threadIdx.x; i <= (int)mask; i += blockDim.x) set[i] = -1;
+    __syncthreads();
+    for (int i = ub + threadIdx.x; i < ue; i += blockDim.x) {
+      const int x = __ldg(col + i);
+      unsigned h = hash_slot(x, bits);
+      while (atomicCAS(&set[h], -1, x) != -1) h = (h + 1) & mask;
+    }
+    __syncthreads();
+    const int lane = lane_id();
+    const int wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    unsigned tri = 0;  // per-lane hits (<= 2^32 per block call)
+    auto hit = [&](int w) -> unsigned {
+      unsigned h = hash_slot(w, bits);
+      int key;
+      while ((key = set[h]) != -1 && key != w) h = (h + 1) & mask;
+      return key == w;
+    };
+    for (long long base = e0 + 32LL * wid; base < e1; base += 32LL * nw) {
+      const long long e = base + lane;
+      int vb = 0, dv = 0;
+      if (e < e1) {
+        const int v = __ldg(col + a.first + e);
+        vb = __ldg(rowptr + v);
+        dv = __ldg(rowptr + v + 1) - vb;
+      }
+      // long wedge lists: the whole warp walks one list at a time, four
+      // coalesced loads in flight per lane
+      unsigned big = __ballot_sync(DP_FULL, dv >= 32);
+      while (big) {
+        const int src = __ffs(big) - 1;
+        big &= big - 1;
+        const int b = __shfl_sync(DP_FULL, vb, src);
+        const int d = __shfl_sync(DP_FULL, dv, src);
+        for (int i = lane; i < d; i += 128) {
+          int w[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            w[j] = i + 32 * j < d ? __ldg(col + b + i + 32 * j) : -1;
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (w[j] >= 0) tri += hit(w[j]);
+        }
+      }
+      // short lists (< 32): flattened into one load-balanced list
+      const int ds = dv < 32 ? dv : 0;
+      const int incl = warp_incl_scan(ds);
+      const int total = __shfl_sync(DP_FULL, incl, 31);
+      const int excl = incl - ds;
+      for (int k0 = 0; k0 < total; k0 += 32) {
+        const int k = k0 + lane;
+        int owner = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+          const int probe = __shfl_sync(DP_FULL, incl, owner + step - 1);
+          if (probe <= k) owner += step;
+        }
+        owner = owner < 31 ? owner : 31;
+        const int pos = __shfl_sync(DP_FULL, vb, owner) + k -
+                        __shfl_sync(DP_FULL, excl, owner);
+        if (k < total) tri += hit(__ldg(col + pos));
+      }
+    }
+    acc.tri += tri;
+  }
   template <int U, class ArgsOf>
   __device__ __forceinline__ void items(ArgsOf args, const int* e,
                                         const bool* ok, Acc& acc) const {
@@ -371,6 +468,7 @@ struct BtApp {
                                    w0 * p0.y + w1 * p1.y + w2 * p2.y);
   }
   static constexpr int kUnroll = 1;
+  static constexpr bool kBlockMode = false;
   template <int U, class ArgsOf>
   __device__ __forceinline__ void items(ArgsOf args, const int* e,
                                         const bool* ok, Acc& acc) const {

@@ -75,6 +75,13 @@ __device__ __forceinline__ void run_logical_blocks(const App& app,
   const long long gl = ceil_div_ll(cnt, cb);
   const long long b0 = lb * cf;
   const long long b1 = b0 + cf < gl ? b0 + cf : gl;
+  if constexpr (App::kBlockMode) {
+    // block-cooperative child (shared setup amortised over the CF logical
+    // blocks, the paper's coarsening rationale): items [b0*cb, b1*cb)
+    const long long e1 = b1 * cb < cnt ? b1 * cb : cnt;
+    app.block_items(a, b0 * cb, e1, acc);
+    return;
+  }
   auto args = [&](int) -> const typename App::Args& { return a; };
   for (long long b = b0; b < b1; b += U) {
     int e[U];

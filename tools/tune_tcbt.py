@@ -15,8 +15,8 @@ spec = "rmat:22:seed1" if kind == "tc" else "curves:25000:seed1"
 bench, wl = load(kind, spec)
 configs = [dict(), dict(agg="grid", parent_block=256)]
 for T, C, agg, pb, cb in itertools.product(
-        (16, 64, 256, 1024) if kind == "tc" else (64, 256, 1024, 4096),
-        (1, 4, 16), ("grid", "mb-all", "block"), (128, 256), (32, 128)):
+        (8, 16, 32, 64, 128) if kind == "tc" else (64, 256, 1024, 4096),
+        (1, 4, 16), ("grid", "mb-all"), (128, 256), (64, 128, 256)):
     d = dict(threshold=T, cfactor=C, parent_block=pb, child_block=cb,
              serial="warp")
     if agg == "mb-all":
