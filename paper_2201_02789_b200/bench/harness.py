@@ -67,9 +67,9 @@ class BenchConfig:
                 raise ValueError("group size must be at least 1")
         for name in ("parent_block", "child_block"):
             v = getattr(self, name)
-            if v < 32 or v > 1024 or v % 32:
+            if v < 32 or v > 256 or v % 32:
                 raise ValueError(
-                    f"{name} must be a multiple of 32 in [32, 1024]")
+                    f"{name} must be a multiple of 32 in [32, 256]")
         if self.serial not in _lib.SERIAL_MODES:
             raise ValueError(f"unknown serial mode {self.serial!r}")
 

@@ -20,6 +20,10 @@
 
 namespace dp {
 
+#ifndef DP_GRAPH_UNROLL
+#define DP_GRAPH_UNROLL 4
+#endif
+
 // items<U> for apps whose item is not latency-chained: plain loop
 template <int U, class App, class ArgsOf>
 __device__ __forceinline__ void items_loop(const App& app, ArgsOf args,
@@ -72,7 +76,7 @@ struct BfsApp {
         atomicCAS(dist + v, kUnreached, a.level + 1) == kUnreached)
       acc.changed = 1;
   }
-  static constexpr int kUnroll = 4;
+  static constexpr int kUnroll = DP_GRAPH_UNROLL;
   static constexpr bool kBlockMode = false;
   template <int U, class ArgsOf>
   __device__ __forceinline__ void items(ArgsOf args, const int* e,
@@ -148,7 +152,7 @@ struct SsspApp {
     if (alt < __ldcg(dist + v) && atomicMin(dist + v, alt) > alt)
       acc.changed = 1;
   }
-  static constexpr int kUnroll = 4;
+  static constexpr int kUnroll = DP_GRAPH_UNROLL;
   static constexpr bool kBlockMode = false;
   template <int U, class ArgsOf>
   __device__ __forceinline__ void items(ArgsOf args, const int* e,

@@ -125,13 +125,13 @@ int validate(const dp_config* c) {
     return fail(DP_ERR_INVALID, "group size must be at least 1");
   if (c->cfactor < 1) return fail(DP_ERR_INVALID, "cfactor must be >= 1");
   if (c->threshold < 0) return fail(DP_ERR_INVALID, "threshold must be >= 0");
-  if (c->parent_block < 32 || c->parent_block > 1024 ||
+  if (c->parent_block < 32 || c->parent_block > 256 ||
       c->parent_block % 32)
     return fail(DP_ERR_INVALID,
-                "parent_block must be a multiple of 32 in [32, 1024]");
-  if (c->child_block < 32 || c->child_block > 1024 || c->child_block % 32)
+                "parent_block must be a multiple of 32 in [32, 256]");
+  if (c->child_block < 32 || c->child_block > 256 || c->child_block % 32)
     return fail(DP_ERR_INVALID,
-                "child_block must be a multiple of 32 in [32, 1024]");
+                "child_block must be a multiple of 32 in [32, 256]");
   return 0;
 }
 

@@ -41,6 +41,11 @@ def main():
             configs.append(dict(threshold=T, cfactor=C, agg=agg,
                                 group_size=4, parent_block=pb, child_block=cb,
                                 serial=ser))
+    elif grid == "best":
+        from bench import BEST
+        configs.append(dict(BEST[kind]))
+        d = dict(BEST[kind]); d["agg"] = "grid"; d.pop("group_size", None)
+        configs.append(d)
     elif grid == "top":
         for T, C, agg, cb in itertools.product(
                 (512, 1024, 2048), (16, 32), ("grid", "mb-all", "mb16"),
