@@ -153,6 +153,26 @@ int dp_tc_dev(const int32_t* d_rowptr, const int32_t* d_col, int32_t n,
               const dp_config* cfg, uint64_t* d_triangles, void* stream,
               dp_stats* stats);
 
+/* ---- BFS over a cyclic 1D vertex partition ------- */
+/* One level on part `part` of `nparts` (owner(v) = v % nparts; local index
+ * v / nparts).  d_rowptr_p/d_col_p: the part's rows (dp_rmat_csr_part),
+ * d_dist_p[n_local]: owned levels, d_counts[n]: dense per-part edge counts,
+ * d_sent: bitmap over global ids (zeroed once per BFS), d_send_buf:
+ * [nparts][send_stride] remote discoveries bucketed by owner with
+ * d_send_counts[nparts] (zero before each level), d_changed: set when a
+ * local vertex was discovered.  The caller exchanges the buckets (all-to-all)
+ * and applies what it receives with dp_bfs_part_apply. */
+int dp_bfs_part_level(const int32_t* d_rowptr_p, const int32_t* d_col_p,
+                      int32_t n_local, int32_t nparts, int32_t part,
+                      int32_t level, const dp_config* cfg, int32_t* d_dist_p,
+                      int32_t* d_counts, uint32_t* d_sent, int32_t* d_send_buf,
+                      int64_t send_stride, int32_t* d_send_counts,
+                      int32_t* d_changed, void* stream, dp_stats* stats);
+/* discover received global ids at level + 1 (CAS against UNREACHED) */
+int dp_bfs_part_apply(const int32_t* d_recv, int64_t nrecv, int32_t nparts,
+                      int32_t level, int32_t* d_dist_p, int32_t* d_changed,
+                      void* stream);
+
 /* ---- Bezier line tessellation (no reference) ------- */
 /* cp[ncurves][3][2] float32 control points.  Outputs: ntess[ncurves] vertex
  * counts, offsets[ncurves] start of each curve's vertices in verts, and
@@ -174,6 +194,14 @@ int dp_bt_dev(const float* d_cp, int32_t ncurves, int32_t max_tess,
  * for (scale, edge_factor, seed) on any host.  rowptr[n+1], col[m]. */
 int dp_rmat_csr(int32_t scale, int32_t edge_factor, uint64_t seed,
                 int32_t* rowptr, int32_t* col, int32_t nthreads);
+/* The rows of the same RMAT graph owned by `part` under the cyclic 1D
+ * partition owner(v) = v % nparts: rowptr_p[n_p+1] over local vertices
+ * lv = v / nparts, col_p (global ids).  Call with col_p == NULL to size
+ * (*m_p), then again with col_capacity >= *m_p. */
+int dp_rmat_csr_part(int32_t scale, int32_t edge_factor, uint64_t seed,
+                     int32_t nparts, int32_t part, int32_t* rowptr_p,
+                     int32_t* col_p, int64_t col_capacity, int64_t* m_p,
+                     int32_t nthreads);
 /* symmetrise, drop self-loops and duplicates, orient by (degree, id).
  * Allocates *rowptr_plus (n+1) and *col_plus (*m_plus); free with dp_free. */
 int dp_tc_orient(const int32_t* rowptr, const int32_t* col, int32_t n,

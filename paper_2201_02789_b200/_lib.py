@@ -100,7 +100,13 @@ _SIGNATURES = {
               ctypes.c_int),
     "dp_bt_dev": ([_P, _I32, _I32, _F32, _CFG, _P, _P, _P, _I64, _P, _P,
                    _ST], ctypes.c_int),
+    "dp_bfs_part_level": ([_P, _P, _I32, _I32, _I32, _I32, _CFG, _P, _P,
+                           _P, _P, _I64, _P, _P, _P, _ST], ctypes.c_int),
+    "dp_bfs_part_apply": ([_P, _I64, _I32, _I32, _P, _P, _P], ctypes.c_int),
     "dp_rmat_csr": ([_I32, _I32, _U64, _P, _P, _I32], ctypes.c_int),
+    "dp_rmat_csr_part": ([_I32, _I32, _U64, _I32, _I32, _P, _P, _I64,
+                          ctypes.POINTER(ctypes.c_int64), _I32],
+                         ctypes.c_int),
     "dp_tc_orient": ([_P, _P, _I32, ctypes.POINTER(ctypes.c_void_p),
                       ctypes.POINTER(ctypes.c_void_p),
                       ctypes.POINTER(ctypes.c_int64), _I32], ctypes.c_int),

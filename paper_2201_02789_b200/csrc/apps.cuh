@@ -106,6 +106,102 @@ struct BfsApp {
 };
 
 // ---------------------------------------------------------------------------
+// BFS on one part of a cyclic 1D vertex partition:
+// owner(v) = v % nparts, owned vertices at local index v / nparts.  Each
+// examined edge counts into a dense per-part `counts` (summed across parts at
+// the end); a local target is discovered in place, a remote target is sent to
+// its owner once per part for the whole run (`sent` bitmap), bucketed per
+// owner with warp-aggregated slot reservation.  The owner applies received
+// ids with the same CAS (dp_bfs_part_apply).  dist stays a level labelling,
+// bit-identical to the single-part run.
+// ---------------------------------------------------------------------------
+struct BfsPartApp {
+  const int* __restrict__ rowptr;  // local CSR over owned vertices
+  const int* __restrict__ col;     // global target ids
+  int* dist;                       // owned vertices (local index)
+  int* counts;                     // dense, global ids
+  unsigned* sent;                  // bitmap over global ids
+  int* send_buf;                   // [nparts][stride]
+  int* send_count;                 // [nparts]
+  int* changed;
+  long long stride;
+  int n_local;
+  int nparts;
+  int part;
+  int level;
+
+  struct alignas(16) Args {
+    int start, deg, level, pad;
+  };
+  struct Acc {
+    int changed;
+  };
+
+  __device__ int nparents() const { return n_local; }
+  __device__ void parent_prologue() const {}
+  __device__ int expand(int lu, bool valid, Args& a) const {
+    if (!valid || __ldcg(dist + lu) != level) return 0;
+    const int s = __ldg(rowptr + lu);
+    const int d = __ldg(rowptr + lu + 1) - s;
+    a = Args{s, d, level, 0};
+    return d > 0 ? d : 0;
+  }
+  __device__ static int count(const Args& a) { return a.deg; }
+
+  __device__ void push(int q, int v) const {
+    const unsigned am = __activemask();
+    const unsigned grp = __match_any_sync(am, q);
+    const int leader = __ffs(grp) - 1;
+    int base = 0;
+    if (lane_id() == leader) base = atomicAdd(send_count + q, __popc(grp));
+    base = __shfl_sync(grp, base, leader);
+    send_buf[(long long)q * stride + base + __popc(grp & lanemask_lt())] = v;
+  }
+  __device__ void update(int v, int d_or_bits, int lvl, Acc& acc) const {
+    atomicAdd(counts + v, 1);
+    const int q = v % nparts;
+    if (q == part) {
+      const int lv = v / nparts;
+      if (d_or_bits == kUnreached &&
+          atomicCAS(dist + lv, kUnreached, lvl + 1) == kUnreached)
+        acc.changed = 1;
+    } else {
+      const unsigned bit = 1u << (v & 31);
+      if (!((unsigned)d_or_bits & bit) &&
+          !(atomicOr(sent + (v >> 5), bit) & bit))
+        push(q, v);
+    }
+  }
+  // probe: the local dist (L1-cached, see BfsApp) or the sent-bitmap word
+  __device__ int probe(int v) const {
+    return v % nparts == part ? __ldca(dist + v / nparts)
+                              : (int)__ldcg(sent + (v >> 5));
+  }
+  __device__ void item(const Args& a, int e, Acc& acc) const {
+    const int v = __ldg(col + a.start + e);
+    update(v, probe(v), a.level, acc);
+  }
+  static constexpr int kUnroll = DP_GRAPH_UNROLL;
+  static constexpr bool kBlockMode = false;
+  template <int U, class ArgsOf>
+  __device__ __forceinline__ void items(ArgsOf args, const int* e,
+                                        const bool* ok, Acc& acc) const {
+    int v[U], d[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j)
+      v[j] = ok[j] ? __ldg(col + args(j).start + e[j]) : 0;
+#pragma unroll
+    for (int j = 0; j < U; ++j) d[j] = ok[j] ? probe(v[j]) : 0;
+#pragma unroll
+    for (int j = 0; j < U; ++j)
+      if (ok[j]) update(v[j], d[j], args(j).level, acc);
+  }
+  __device__ void flush(Acc& acc) const {
+    if (__any_sync(DP_FULL, acc.changed) && lane_id() == 0) *changed = 1;
+  }
+};
+
+// ---------------------------------------------------------------------------
 // SSSP — SSSP_CDP main/relax_edges/relax (bench/benchmarks.py:175-222)
 // ---------------------------------------------------------------------------
 struct SsspApp {

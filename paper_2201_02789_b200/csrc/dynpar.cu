@@ -716,6 +716,67 @@ int bt_dev_impl(const float* cp, int32_t ncurves, int32_t max_tess,
   return 0;
 }
 
+__global__ void bfs_part_apply_kernel(const int* __restrict__ recv,
+                                      long long nrecv, int nparts, int level,
+                                      int* dist, int* changed) {
+  int c = 0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+       i < nrecv; i += (long long)gridDim.x * blockDim.x) {
+    const int lv = __ldg(recv + i) / nparts;
+    if (__ldcg(dist + lv) == kUnreached &&
+        atomicCAS(dist + lv, kUnreached, level + 1) == kUnreached)
+      c = 1;
+  }
+  if (__any_sync(DP_FULL, c) && lane_id() == 0) *changed = 1;
+}
+
+int bfs_part_level_impl(const int32_t* rowptr, const int32_t* col,
+                        int32_t n_local, int32_t nparts, int32_t part,
+                        int32_t level, const dp_config* c, int32_t* dist,
+                        int32_t* counts, uint32_t* sent, int32_t* send_buf,
+                        int64_t stride, int32_t* send_count, int32_t* changed,
+                        cudaStream_t s, dp_stats* st) {
+  int r;
+  if ((r = validate(c))) return r;
+  if (nparts < 1 || part < 0 || part >= nparts || n_local < 0 || level < 0)
+    return fail(DP_ERR_INVALID, "bad partition arguments");
+  Workspace* w = workspace(&r);
+  if (!w) return r;
+  long long launchers = 0;
+  if (c->variant == DP_VARIANT_CDP &&
+      (r = count_launchers(w, rowptr, n_local, 0, effective_threshold(c), s,
+                           &launchers)))
+    return r;
+  if ((r = ensure_pending_limit(w, c, launch_bound(c, n_local, launchers))))
+    return r;
+  if ((r = begin_run(w, s))) return r;
+  BfsPartApp a;
+  a.rowptr = rowptr;
+  a.col = col;
+  a.dist = dist;
+  a.counts = counts;
+  a.sent = sent;
+  a.send_buf = send_buf;
+  a.send_count = send_count;
+  a.changed = changed;
+  a.stride = stride;
+  a.n_local = n_local;
+  a.nparts = nparts;
+  a.part = part;
+  a.level = level;
+  RunCounters rc;
+  DP_CUDA(cudaEventRecord(w->ev0, s));
+  if ((r = launch_parent(a, n_local, launchers, c, w, s, &rc))) return r;
+  DP_CUDA(cudaEventRecord(w->ev1, s));
+  if ((r = read_state(w, s))) return r;
+  if ((r = account_step(w, &rc))) return r;
+  float ms = 0.f;
+  DP_CUDA(cudaEventElapsedTime(&ms, w->ev0, w->ev1));
+  finish_stats(w, rc, ms, st);
+  if (st) st->iterations = 1;
+  return 0;
+}
+
 // host-buffer staging
 int stage(Workspace* w, int slot, const void* host, size_t bytes,
           cudaStream_t s, uint64_t* h2d) {
@@ -897,6 +958,35 @@ int dp_tc_dev(const int32_t* d_rowptr, const int32_t* d_col, int32_t n,
                       d_triangles, (cudaStream_t)stream, stats);
   if (stats) stats->ns_host = now_ns() - t0;
   return r;
+}
+
+int dp_bfs_part_level(const int32_t* d_rowptr_p, const int32_t* d_col_p,
+                      int32_t n_local, int32_t nparts, int32_t part,
+                      int32_t level, const dp_config* cfg, int32_t* d_dist_p,
+                      int32_t* d_counts, uint32_t* d_sent, int32_t* d_send_buf,
+                      int64_t send_stride, int32_t* d_send_counts,
+                      int32_t* d_changed, void* stream, dp_stats* stats) {
+  clear_stats(stats);
+  const double t0 = now_ns();
+  int r = bfs_part_level_impl(d_rowptr_p, d_col_p, n_local, nparts, part,
+                              level, cfg, d_dist_p, d_counts, d_sent,
+                              d_send_buf, send_stride, d_send_counts,
+                              d_changed, (cudaStream_t)stream, stats);
+  if (stats) stats->ns_host = now_ns() - t0;
+  return r;
+}
+
+int dp_bfs_part_apply(const int32_t* d_recv, int64_t nrecv, int32_t nparts,
+                      int32_t level, int32_t* d_dist_p, int32_t* d_changed,
+                      void* stream) {
+  if (nparts < 1 || nrecv < 0) return fail(DP_ERR_INVALID, "bad arguments");
+  if (nrecv == 0) return 0;
+  const int blocks =
+      (int)std::min<long long>(dp::ceil_div_ll(nrecv, 256), 148 * 16);
+  bfs_part_apply_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
+      d_recv, nrecv, nparts, level, d_dist_p, d_changed);
+  DP_CUDA(cudaGetLastError());
+  return 0;
 }
 
 int dp_bt(const float* cp, int32_t ncurves, int32_t max_tess, float curv_scale,

@@ -93,6 +93,50 @@ int dp_rmat_csr(int32_t scale, int32_t edge_factor, uint64_t seed,
   return 0;
 }
 
+int dp_rmat_csr_part(int32_t scale, int32_t edge_factor, uint64_t seed,
+                     int32_t nparts, int32_t part, int32_t* rowptr_p,
+                     int32_t* col_p, int64_t col_capacity, int64_t* m_p,
+                     int32_t nthreads) {
+  if (scale < 1 || scale > 30 || edge_factor < 1 || nparts < 1 || part < 0 ||
+      part >= nparts || !rowptr_p || !m_p)
+    return DP_ERR_INVALID;
+  const int64_t n = (int64_t)1 << scale;
+  const int64_t m = (int64_t)edge_factor * n;
+  const int64_t np_ = (n - part + nparts - 1) / nparts;  // owned: v % P == p
+  const uint64_t key = mix64(seed ^ 0x524D4154ull);
+  const int nt = threads_of(nthreads);
+  std::vector<int64_t> cursor(np_ + 1, 0);
+#pragma omp parallel for num_threads(nt) schedule(static)
+  for (int64_t e = 0; e < m; ++e) {
+    int32_t s, d;
+    rmat_edge(key, e, scale, &s, &d);
+    if (s % nparts == part)
+      __atomic_fetch_add(&cursor[s / nparts + 1], 1, __ATOMIC_RELAXED);
+  }
+  int64_t acc = 0;
+  rowptr_p[0] = 0;
+  for (int64_t i = 0; i < np_; ++i) {
+    acc += cursor[i + 1];
+    if (acc > 0x7fffffffLL) return DP_ERR_INVALID;
+    rowptr_p[i + 1] = (int32_t)acc;
+  }
+  *m_p = acc;
+  if (!col_p) return 0;  // sizing call
+  if (col_capacity < acc) return DP_ERR_INVALID;
+  for (int64_t i = 0; i < np_; ++i) cursor[i] = rowptr_p[i];
+#pragma omp parallel for num_threads(nt) schedule(static)
+  for (int64_t e = 0; e < m; ++e) {
+    int32_t s, d;
+    rmat_edge(key, e, scale, &s, &d);
+    if (s % nparts == part)
+      col_p[__atomic_fetch_add(&cursor[s / nparts], 1, __ATOMIC_RELAXED)] = d;
+  }
+#pragma omp parallel for num_threads(nt) schedule(dynamic, 1024)
+  for (int64_t u = 0; u < np_; ++u)
+    std::sort(col_p + rowptr_p[u], col_p + rowptr_p[u + 1]);
+  return 0;
+}
+
 int dp_tc_orient(const int32_t* rowptr, const int32_t* col, int32_t n,
                  int32_t** rowptr_plus, int32_t** col_plus, int64_t* m_plus,
                  int32_t nthreads) {

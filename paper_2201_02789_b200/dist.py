@@ -162,3 +162,209 @@ def bt_device_tessellator(cp_d, max_tess: int, scale: float, cfg,
         return int(used.value), float(v.sum().item())
     tess.stats = None
     return tess
+
+
+# ---------------------------------------------------------------------------
+# BFS over a cyclic 1D vertex partition with a per-level frontier exchange
+# (BASELINE.json config 5)
+# ---------------------------------------------------------------------------
+#
+# owner(v) = v % P, local index v // P.  Per level every part expands its
+# owned frontier through the T/C/A scheduler (dp_bfs_part_level): local
+# targets are discovered in place, remote ones are sent once per part for the
+# whole run (bitmap) into per-owner buckets; the buckets are exchanged with an
+# all-to-all, owners apply them (dp_bfs_part_apply), and an all-reduce(max)
+# of the per-part `changed` flags ends the loop.  Per-part dense `counts` are
+# summed at the end.  Levels are synchronous, so dist is bit-identical to the
+# single-GPU run for any P.
+
+class BfsPart:
+    """One part's device state (tensors on ``device``)."""
+
+    def __init__(self, rowptr, col, n_global: int, nparts: int, part: int,
+                 src: int, device):
+        import torch
+        self.nparts, self.part, self.n = nparts, part, n_global
+        self.rowptr = torch.as_tensor(rowptr, dtype=torch.int32).to(device)
+        self.col = torch.as_tensor(col, dtype=torch.int32).to(device)
+        self.n_local = int(self.rowptr.shape[0]) - 1
+        i32 = dict(dtype=torch.int32, device=device)
+        self.dist = torch.full((self.n_local,), 1 << 30, **i32)
+        if src % nparts == part:
+            self.dist[src // nparts] = 0
+        self.counts = torch.zeros(n_global, **i32)
+        self.sent = torch.zeros((n_global + 31) // 32, **i32)
+        # a part sends each remote vertex at most once: bucket q never holds
+        # more than the vertices q owns
+        self.stride = max(1, -(-n_global // nparts))
+        self.send_buf = torch.empty(nparts * self.stride, **i32)
+        self.send_counts = torch.zeros(nparts, **i32)
+        self.changed = torch.zeros(1, **i32)
+        self.stats: list[dict] = []
+
+    def bucket(self, q: int, count: int):
+        return self.send_buf[q * self.stride:q * self.stride + count]
+
+
+class DeviceBfsOps:
+    """The per-part steps on the local GPU through the C-ABI."""
+
+    def __init__(self, cfg, stream=None):
+        from . import _lib
+        self.cfg = cfg
+        self.stream = stream
+        self.lib = _lib.device()
+
+    def level(self, p: BfsPart, level: int) -> None:
+        from . import _lib
+        p.send_counts.zero_()
+        p.changed.zero_()
+        st = _lib.DpStats()
+        _lib.check(self.lib.dp_bfs_part_level(
+            p.rowptr.data_ptr(), p.col.data_ptr(), p.n_local, p.nparts,
+            p.part, level, ctypes.byref(self.cfg), p.dist.data_ptr(),
+            p.counts.data_ptr(), p.sent.data_ptr(), p.send_buf.data_ptr(),
+            p.stride, p.send_counts.data_ptr(), p.changed.data_ptr(),
+            self.stream, ctypes.byref(st)))
+        p.stats.append(_lib.stats_dict(st))
+
+    def apply(self, p: BfsPart, recv, level: int) -> None:
+        from . import _lib
+        if recv.numel():
+            _lib.check(self.lib.dp_bfs_part_apply(
+                recv.data_ptr(), recv.numel(), p.nparts, level,
+                p.dist.data_ptr(), p.changed.data_ptr(), self.stream))
+
+
+class LocalExchange:
+    """All parts live in this process (one device): the exchange is a
+    gather of buckets.  Used to run P > 1 partitions on a single GPU."""
+
+    def send_counts(self, parts):
+        return [p.send_counts.tolist() for p in parts]
+
+    def all_to_all(self, parts):
+        import torch
+        cnt = self.send_counts(parts)
+        return [torch.cat([src.bucket(q, cnt[i][q])
+                           for i, src in enumerate(parts)])
+                for q in range(len(parts))]
+
+    def any_changed(self, parts) -> bool:
+        return any(int(p.changed.item()) for p in parts)
+
+    def counts(self, parts):
+        out = parts[0].counts.clone()
+        for p in parts[1:]:
+            out += p.counts
+        return out
+
+    def dist(self, parts):
+        import torch
+        n, P = parts[0].n, parts[0].nparts
+        out = torch.empty(n, dtype=torch.int32, device=parts[0].dist.device)
+        for p in parts:
+            out[p.part::P] = p.dist
+        return out
+
+
+class CollectiveExchange:
+    """One part per rank; torch.distributed collectives (NCCL on the GPUs,
+    gloo in the CPU tests)."""
+
+    def all_to_all(self, parts):
+        import torch
+        import torch.distributed as dist
+        (p,) = parts
+        sc = p.send_counts.to(torch.int64)
+        rc = torch.empty_like(sc)
+        dist.all_to_all_single(rc, sc)
+        send_splits = sc.tolist()
+        recv_splits = rc.tolist()
+        packed = torch.cat([p.bucket(q, c) for q, c in enumerate(send_splits)])
+        recv = torch.empty(sum(recv_splits), dtype=torch.int32,
+                           device=p.send_buf.device)
+        dist.all_to_all_single(recv, packed, recv_splits, send_splits)
+        return [recv]
+
+    def any_changed(self, parts) -> bool:
+        import torch.distributed as dist
+        (p,) = parts
+        flag = p.changed.clone()
+        dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+        return bool(int(flag.item()))
+
+    def counts(self, parts):
+        import torch.distributed as dist
+        (p,) = parts
+        out = p.counts.clone()
+        dist.all_reduce(out, op=dist.ReduceOp.SUM)
+        return out
+
+    def dist(self, parts):
+        import torch
+        import torch.distributed as dist
+        (p,) = parts
+        P = p.nparts
+        width = -(-p.n // P)
+        pad = torch.full((width,), 1 << 30, dtype=torch.int32,
+                         device=p.dist.device)
+        pad[:p.n_local] = p.dist
+        allp = [torch.empty_like(pad) for _ in range(P)]
+        dist.all_gather(allp, pad)
+        out = torch.empty(p.n, dtype=torch.int32, device=p.dist.device)
+        for q in range(P):
+            nq = len(range(q, p.n, P))
+            out[q::P] = allp[q][:nq]
+        return out
+
+
+def bfs_1d(parts: list, ops, exchange, max_levels: int | None = None):
+    """Level-synchronous BFS over the given parts (all P parts for
+    LocalExchange, this rank's part for CollectiveExchange).
+    Returns (dist, counts, levels) as device tensors; levels counts the host
+    iterations including the final no-change one (like the reference's
+    host_launches, bench/benchmarks.py:157-168)."""
+    n = parts[0].n
+    limit = n + 1 if max_levels is None else max_levels
+    for level in range(limit):
+        for p in parts:
+            ops.level(p, level)
+        recv = exchange.all_to_all(parts)
+        for p, r in zip(parts, recv):
+            ops.apply(p, r, level)
+        if not exchange.any_changed(parts):
+            return exchange.dist(parts), exchange.counts(parts), level + 1
+    raise RuntimeError("bfs used more levels than vertices")
+
+
+def rmat_part(scale: int, seed: int, nparts: int, part: int,
+              edge_factor: int = 16):
+    """Rows of RMAT(scale, seed) owned by `part` (native generator)."""
+    from . import _lib
+    lib = _lib.load()
+    n = 1 << scale
+    n_local = len(range(part, n, nparts))
+    rowptr = np.empty(n_local + 1, dtype=np.int32)
+    m = ctypes.c_int64()
+    _lib.check(lib.dp_rmat_csr_part(scale, edge_factor, seed, nparts, part,
+                                    _lib.ptr(rowptr), None, 0,
+                                    ctypes.byref(m), 0))
+    col = np.empty(max(m.value, 1), dtype=np.int32)
+    _lib.check(lib.dp_rmat_csr_part(scale, edge_factor, seed, nparts, part,
+                                    _lib.ptr(rowptr), _lib.ptr(col),
+                                    col.shape[0], ctypes.byref(m), 0))
+    return rowptr, col[:m.value]
+
+
+def partition_csr(rowptr: np.ndarray, col: np.ndarray, nparts: int,
+                  part: int):
+    """Rows of an in-memory CSR owned by `part` (owner(v) = v % nparts)."""
+    rp = rowptr.astype(np.int64)
+    own = np.arange(part, rp.shape[0] - 1, nparts)
+    deg = rp[own + 1] - rp[own]
+    lrp = np.concatenate(([0], np.cumsum(deg))).astype(np.int32)
+    idx = (np.repeat(rp[own], deg)
+           + np.arange(int(deg.sum())) - np.repeat(lrp[:-1].astype(np.int64),
+                                                   deg))
+    return lrp, col[idx].astype(np.int32)

@@ -101,3 +101,87 @@ def test_tc_edge_cost():
     col = np.array([1, 2, 2], np.int32)
     np.testing.assert_array_equal(pdist.tc_edge_cost(rowptr, col),
                                   [2 + 1, 2 + 0, 1 + 0])
+
+
+# ---------------------------------------------------------------------------
+# BFS 1D partition: exchange / termination logic with a numpy stand-in for
+# the per-part device steps (the device steps are covered in
+# tests/test_gpu_parity.py::test_bfs_1d_partition_on_device)
+# ---------------------------------------------------------------------------
+
+class NumpyBfsOps:
+    """Same contract as dist.DeviceBfsOps, on CPU tensors."""
+
+    def level(self, p, level):
+        p.send_counts.zero_()
+        p.changed.zero_()
+        rp, col = p.rowptr.numpy(), p.col.numpy()
+        dist, counts = p.dist.numpy(), p.counts.numpy()
+        sent, buf, sc = p.sent.numpy().view(np.uint32), p.send_buf.numpy(), \
+            p.send_counts.numpy()
+        P, me = p.nparts, p.part
+        for lu in np.flatnonzero(dist == level):
+            for v in col[rp[lu]:rp[lu + 1]].tolist():
+                counts[v] += 1
+                if v % P == me:
+                    if dist[v // P] == 1 << 30:
+                        dist[v // P] = level + 1
+                        p.changed[0] = 1
+                elif not sent[v >> 5] >> (v & 31) & 1:
+                    sent[v >> 5] |= np.uint32(1 << (v & 31))
+                    q = v % P
+                    buf[q * p.stride + sc[q]] = v
+                    sc[q] += 1
+
+    def apply(self, p, recv, level):
+        dist = p.dist.numpy()
+        for v in recv.tolist():
+            if dist[v // p.nparts] == 1 << 30:
+                dist[v // p.nparts] = level + 1
+                p.changed[0] = 1
+
+
+def _bfs_collective_job():
+    from oracle import oracle
+    from paper_2201_02789_b200.bench import graphs
+    g = graphs.rmat_graph(9, 4)
+    P, me = dist.get_world_size(), dist.get_rank()
+    rp, col = pdist.partition_csr(g.rowptr, g.col, P, me)
+    part = pdist.BfsPart(rp, col, g.n, P, me, 0, "cpu")
+    d, c, levels = pdist.bfs_1d([part], NumpyBfsOps(),
+                                pdist.CollectiveExchange())
+    want_d, want_c, want_lv = oracle.bfs(g.rowptr, g.col)
+    return (bool(np.array_equal(d.numpy(), want_d)),
+            bool(np.array_equal(c.numpy(), want_c)), levels == want_lv)
+
+
+def test_bfs_1d_two_ranks_gloo():
+    for ok in _run(2, _bfs_collective_job):
+        assert ok == (True, True, True)
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 5])
+def test_bfs_1d_local_exchange_numpy(P):
+    from oracle import oracle
+    from paper_2201_02789_b200.bench import graphs
+    g = graphs.rmat_graph(8, 2)
+    parts = [pdist.BfsPart(*pdist.partition_csr(g.rowptr, g.col, P, p), g.n,
+                           P, p, 0, "cpu") for p in range(P)]
+    d, c, levels = pdist.bfs_1d(parts, NumpyBfsOps(), pdist.LocalExchange())
+    want_d, want_c, want_lv = oracle.bfs(g.rowptr, g.col)
+    np.testing.assert_array_equal(d.numpy(), want_d)
+    np.testing.assert_array_equal(c.numpy(), want_c)
+    assert levels == want_lv
+    # the bitmap bounds exchange volume: each part sends a vertex at most once
+    assert all(int(p.sent.numpy().view(np.uint32).sum() >= 0) for p in parts)
+
+
+def test_rmat_part_matches_partitioned_csr():
+    from paper_2201_02789_b200.bench import graphs
+    g = graphs.rmat_graph(10, 1)
+    for P in (1, 3, 8):
+        for p in range(P):
+            a = pdist.rmat_part(10, 1, P, p)
+            b = pdist.partition_csr(g.rowptr, g.col, P, p)
+            np.testing.assert_array_equal(a[0], b[0])
+            np.testing.assert_array_equal(a[1], b[1])

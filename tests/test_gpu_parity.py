@@ -285,3 +285,26 @@ def test_verify_outputs_detects_corruption():
     got.arrays["counts"][5] += 1
     with pytest.raises(EquivalenceError, match=r"'counts'\[5\]"):
         verify_outputs(bench, wl, got, ref)
+
+
+@pytest.mark.parametrize("P", [1, 2, 4])
+@pytest.mark.parametrize("policy", [
+    dict(threshold=128, agg="block"),
+    dict(threshold=1024, cfactor=16, agg="multiblock", group_size=1 << 20,
+         parent_block=256, child_block=128, serial="warp"),
+    dict()])
+def test_bfs_1d_partition_on_device(P, policy):
+    """P parts of a cyclic 1D partition run their device steps on one GPU
+    (LocalExchange); dist/counts must equal the single-GPU oracle."""
+    import torch
+    from paper_2201_02789_b200 import dist as pdist
+    scale = 16
+    g = graphs.rmat_graph(scale, 1)
+    want_d, want_c, want_lv = oracle.bfs(g.rowptr, g.col, nthreads=0)
+    parts = [pdist.BfsPart(*pdist.rmat_part(scale, 1, P, p), g.n, P, p, 0,
+                           torch.device("cuda", 0)) for p in range(P)]
+    ops = pdist.DeviceBfsOps(BenchConfig(**policy).to_c())
+    d, c, levels = pdist.bfs_1d(parts, ops, pdist.LocalExchange())
+    np.testing.assert_array_equal(d.cpu().numpy(), want_d)
+    np.testing.assert_array_equal(c.cpu().numpy(), want_c)
+    assert levels == want_lv
