@@ -436,6 +436,98 @@ def arm_ours(args, world, rank, local):
     print(json.dumps(line), flush=True)
 
 
+def arm_bfs26(args, world, rank, local):
+    """BASELINE config 5: BFS on RMAT-26 over a cyclic 1D vertex partition
+    (one part per rank), per-level all-to-all frontier exchange over NCCL.
+    One step = one full BFS from vertex 0.  GTEPS = examined edges / t."""
+    import torch
+    from paper_2201_02789_b200 import _lib
+    from paper_2201_02789_b200 import dist as pdist
+    _lib.device()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    scale = args.scale or 26
+    rp, col = pdist.rmat_part_device(scale, SEED, world, rank, dev)
+    part = pdist.BfsPart(rp, col, 1 << scale, world, rank, 0, dev)
+    del rp, col
+    ex = pdist.CollectiveExchange() if world > 1 else pdist.LocalExchange()
+    ops = pdist.DeviceBfsOps(_cfg(BEST["bfs"]))
+    stream_obj = torch.cuda.current_stream()
+
+    def step():
+        part.reset(0)
+        return pdist.bfs_1d([part], ops, ex)
+    with ClockSampler(local) as clk:
+        total_ms, outs = timed_steps(step, args.steps, args.warmup,
+                                     stream_obj)
+    dist_t, counts_t, levels = outs[-1]
+    e_t = int(counts_t.to(torch.int64).sum().item())
+    t_max = max_over_ranks(total_ms)
+    ms_step = t_max / args.steps
+    if rank != 0:
+        return
+    line = {"metric": f"GTEPS (BFS RMAT-{scale}, 1D partition, T+C+A CDP2)",
+            "value": e_t / (ms_step * 1e-3) / 1e9, "unit": "GTEPS",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic RMAT (Graph500, seed 1, edge factor 16)",
+            "config": {"workload": f"bfs rmat-{scale} from vertex 0",
+                       "levels": levels, "edges_examined": e_t,
+                       "policy": BEST["bfs"],
+                       "parallelism": f"1d-cyclic-partition x{world}"},
+            "clocks": clk.summary()}
+    if scale <= 22:  # the oracle check fits the host quickly
+        from oracle import oracle
+        from paper_2201_02789_b200.bench import graphs
+        g = graphs.rmat_graph(scale, SEED)
+        wd, wc, _ = oracle.bfs(g.rowptr, g.col, nthreads=0)
+        line["parity"] = ("bit-exact vs oracle"
+                          if np.array_equal(dist_t.cpu().numpy(), wd)
+                          and np.array_equal(counts_t.cpu().numpy(), wc)
+                          else "MISMATCH")
+    print(json.dumps(line), flush=True)
+
+
+def arm_tc(args, world, rank, local):
+    """BASELINE config 4: triangle counting on RMAT-22, oriented-edge ranges
+    balanced by merge work, one all_reduce(sum).  One step = one count."""
+    import torch
+    from paper_2201_02789_b200 import _lib
+    from paper_2201_02789_b200 import dist as pdist
+    from paper_2201_02789_b200.bench import load
+    _lib.device()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    bench, wl = load("tc", f"rmat:{args.scale or SCALE}:seed{SEED}")
+    rp_h, col_h = wl.buffers["rowptr"], wl.buffers["col"]
+    rp = torch.from_numpy(rp_h).to(dev)
+    col = torch.from_numpy(col_h).to(dev)
+    counter = pdist.tc_device_counter(rp, col, wl.n, int(col_h.shape[0]),
+                                      _cfg(BEST["tc"]))
+    stream_obj = torch.cuda.current_stream()
+    rng = pdist.tc_shard(rp_h, col_h)  # host-side partitioning, untimed
+    with ClockSampler(local) as clk:
+        total_ms, outs = timed_steps(
+            lambda: pdist.tc_count_range(rng, counter, dev),
+            args.steps, args.warmup, stream_obj)
+    tri = outs[-1]
+    t_max = max_over_ranks(total_ms)
+    ms_step = t_max / args.steps
+    if rank != 0:
+        return
+    print(json.dumps({
+        "metric": "triangles/s (TC RMAT-22, edge-range partition)",
+        "value": tri / (ms_step * 1e-3), "unit": "triangles/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic RMAT, symmetrised, degree-oriented",
+        "config": {"workload": "tc rmat-22", "triangles": tri,
+                   "oriented_edges": int(col_h.shape[0]),
+                   "policy": BEST["tc"],
+                   "parallelism": f"edge-range x{world}"},
+        "clocks": clk.summary()}), flush=True)
+
+
 def read_traffic():
     """dram bytes per launch of the dominant kernel from the committed ncu
     capture (profiles/), else null."""
@@ -491,6 +583,12 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--quick", action="store_true",
                     help="headline only (skip the other workloads)")
+    ap.add_argument("--workload", choices=("sssp", "bfs26", "tc"),
+                    default="sssp",
+                    help="sssp = headline (BASELINE config 3); bfs26 / tc = "
+                         "the partitioned multi-GPU configs 5 / 4")
+    ap.add_argument("--scale", type=int, default=0,
+                    help="override the RMAT scale of bfs26 / tc")
     ap.add_argument("--profile", action="store_true",
                     help="warm-up + timed steps only (for ncu passes)")
     args = ap.parse_args()
@@ -499,6 +597,10 @@ def main():
     world, rank, local = init_dist(args)
     if args.impl == "reference":
         arm_reference(args, world, rank, local)
+    elif args.workload == "bfs26":
+        arm_bfs26(args, world, rank, local)
+    elif args.workload == "tc":
+        arm_tc(args, world, rank, local)
     else:
         arm_ours(args, world, rank, local)
     import torch

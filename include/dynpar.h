@@ -202,6 +202,13 @@ int dp_rmat_csr_part(int32_t scale, int32_t edge_factor, uint64_t seed,
                      int32_t nparts, int32_t part, int32_t* rowptr_p,
                      int32_t* col_p, int64_t col_capacity, int64_t* m_p,
                      int32_t nthreads);
+/* Device-side generation of the same graph: writes one key
+ * (v / nparts) << 32 | dst per edge whose source v is owned by `part`, in
+ * arbitrary order (sort them to get the CSR rows of dp_rmat_csr_part).
+ * d_keys == NULL or capacity == 0 only counts (*count). */
+int dp_rmat_part_keys_dev(int32_t scale, int32_t edge_factor, uint64_t seed,
+                          int32_t nparts, int32_t part, uint64_t* d_keys,
+                          int64_t capacity, int64_t* count, void* stream);
 /* symmetrise, drop self-loops and duplicates, orient by (degree, id).
  * Allocates *rowptr_plus (n+1) and *col_plus (*m_plus); free with dp_free. */
 int dp_tc_orient(const int32_t* rowptr, const int32_t* col, int32_t n,

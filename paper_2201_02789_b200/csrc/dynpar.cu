@@ -777,6 +777,55 @@ int bfs_part_level_impl(const int32_t* rowptr, const int32_t* col,
   return 0;
 }
 
+// ---------------------------------------------------------------------------
+// RMAT edge generation on the device: the same counter-based hash as the host
+// generator (gen.cpp), so the CSR built from these keys is bit-identical.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long dmix64(unsigned long long z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void rmat_part_keys_kernel(unsigned long long key, long long m,
+                                      int scale, int nparts, int part,
+                                      unsigned long long* keys,
+                                      unsigned long long* cursor) {
+  const unsigned long long kA = 2448131358ull, kAB = 3264175144ull,
+                           kABC = 4080218931ull;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  // each warp takes 32 consecutive edges per trip (warp-uniform loop)
+  for (long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x -
+                     lane_id();
+       b < m; b += stride) {
+    const long long e = b + lane_id();
+    unsigned s = 0, d = 0;
+    if (e < m) {
+      unsigned long long h = 0;
+      for (int l = 0; l < scale; ++l) {
+        unsigned r;
+        if ((l & 1) == 0) {
+          h = dmix64(key ^ ((unsigned long long)e * 16 + (unsigned)(l >> 1)));
+          r = (unsigned)h;
+        } else {
+          r = (unsigned)(h >> 32);
+        }
+        s = (s << 1) | (r >= kAB);
+        d = (d << 1) | ((r >= kA && r < kAB) || r >= kABC);
+      }
+    }
+    const bool keep = e < m && (int)(s % nparts) == part;
+    const unsigned mk = __ballot_sync(DP_FULL, keep);
+    unsigned long long base = 0;
+    if (lane_id() == 0 && mk) base = atomicAdd(cursor, (unsigned long long)__popc(mk));
+    base = __shfl_sync(DP_FULL, base, 0);
+    if (keep && keys)
+      keys[base + __popc(mk & lanemask_lt())] =
+          ((unsigned long long)(s / nparts) << 32) | d;
+  }
+}
+
 // host-buffer staging
 int stage(Workspace* w, int slot, const void* host, size_t bytes,
           cudaStream_t s, uint64_t* h2d) {
@@ -986,6 +1035,39 @@ int dp_bfs_part_apply(const int32_t* d_recv, int64_t nrecv, int32_t nparts,
   bfs_part_apply_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
       d_recv, nrecv, nparts, level, d_dist_p, d_changed);
   DP_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int dp_rmat_part_keys_dev(int32_t scale, int32_t edge_factor, uint64_t seed,
+                          int32_t nparts, int32_t part, uint64_t* d_keys,
+                          int64_t capacity, int64_t* count, void* stream) {
+  if (scale < 1 || scale > 30 || edge_factor < 1 || nparts < 1 || part < 0 ||
+      part >= nparts || !count)
+    return fail(DP_ERR_INVALID, "bad rmat arguments");
+  int r;
+  Workspace* w = workspace(&r);
+  if (!w) return r;
+  cudaStream_t s = (cudaStream_t)stream;
+  const long long m = (long long)edge_factor << scale;
+  // same seed mixing as gen.cpp
+  unsigned long long z = seed ^ 0x524D4154ull;
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  const unsigned long long key = z ^ (z >> 31);
+  DP_CUDA(cudaMemsetAsync(w->d_scratch, 0, sizeof(unsigned long long), s));
+  const int blocks = 148 * 16;
+  rmat_part_keys_kernel<<<blocks, 256, 0, s>>>(
+      key, m, scale, nparts, part,
+      capacity > 0 ? (unsigned long long*)d_keys : nullptr, w->d_scratch);
+  DP_CUDA(cudaGetLastError());
+  unsigned long long got = 0;
+  DP_CUDA(cudaMemcpyAsync(&got, w->d_scratch, sizeof(got),
+                          cudaMemcpyDeviceToHost, s));
+  DP_CUDA(cudaStreamSynchronize(s));
+  *count = (int64_t)got;
+  if (capacity > 0 && (long long)got > capacity)
+    return fail(DP_ERR_INVALID, "key capacity exceeded");
   return 0;
 }
 

@@ -89,15 +89,27 @@ def allreduce_sum_f64(values: list[float], device) -> list[float]:
 # triangle counting
 # ---------------------------------------------------------------------------
 
+def tc_shard(rowptr: np.ndarray, col: np.ndarray) -> tuple[int, int]:
+    """This rank's oriented-edge range (work-balanced)."""
+    rank, world = _group()
+    return balanced_ranges(tc_edge_cost(rowptr, col), world)[rank]
+
+
+def tc_count_range(rng: tuple[int, int],
+                   count_range: Callable[[int, int], int],
+                   device="cpu") -> int:
+    """Count this rank's range, all_reduce(sum) -> the global count."""
+    local = int(count_range(*rng))
+    return allreduce_sum_i64([local], device)[0]
+
+
 def tc_count_sharded(rowptr: np.ndarray, col: np.ndarray,
                      count_range: Callable[[int, int], int],
                      device="cpu") -> tuple[int, tuple[int, int]]:
     """This rank's share of the oriented edges is counted by
     ``count_range(lo, hi)``; returns (global count, this rank's range)."""
-    rank, world = _group()
-    lo, hi = balanced_ranges(tc_edge_cost(rowptr, col), world)[rank]
-    local = int(count_range(lo, hi))
-    return allreduce_sum_i64([local], device)[0], (lo, hi)
+    rng = tc_shard(rowptr, col)
+    return tc_count_range(rng, count_range, device), rng
 
 
 def tc_device_counter(rowptr_d, col_d, n: int, m: int, cfg, stream=None):
@@ -185,8 +197,9 @@ class BfsPart:
                  src: int, device):
         import torch
         self.nparts, self.part, self.n = nparts, part, n_global
-        self.rowptr = torch.as_tensor(rowptr, dtype=torch.int32).to(device)
-        self.col = torch.as_tensor(col, dtype=torch.int32).to(device)
+        self.rowptr = torch.as_tensor(rowptr).to(device=device,
+                                                  dtype=torch.int32)
+        self.col = torch.as_tensor(col).to(device=device, dtype=torch.int32)
         self.n_local = int(self.rowptr.shape[0]) - 1
         i32 = dict(dtype=torch.int32, device=device)
         self.dist = torch.full((self.n_local,), 1 << 30, **i32)
@@ -201,6 +214,15 @@ class BfsPart:
         self.send_counts = torch.zeros(nparts, **i32)
         self.changed = torch.zeros(1, **i32)
         self.stats: list[dict] = []
+
+    def reset(self, src: int) -> None:
+        """Fresh BFS state (keeps the graph and buffers)."""
+        self.dist.fill_(1 << 30)
+        if src % self.nparts == self.part:
+            self.dist[src // self.nparts] = 0
+        self.counts.zero_()
+        self.sent.zero_()
+        self.stats = []
 
     def bucket(self, q: int, count: int):
         return self.send_buf[q * self.stride:q * self.stride + count]
@@ -355,6 +377,33 @@ def rmat_part(scale: int, seed: int, nparts: int, part: int,
                                     _lib.ptr(rowptr), _lib.ptr(col),
                                     col.shape[0], ctypes.byref(m), 0))
     return rowptr, col[:m.value]
+
+
+def rmat_part_device(scale: int, seed: int, nparts: int, part: int, device,
+                     edge_factor: int = 16, stream=None):
+    """Same rows as rmat_part, generated on the GPU: keys (local src << 32
+    | dst) from the device hash, sorted, split into (rowptr, col) tensors."""
+    import torch
+    from . import _lib
+    lib = _lib.device()
+    n = 1 << scale
+    n_local = len(range(part, n, nparts))
+    cnt = ctypes.c_int64()
+    _lib.check(lib.dp_rmat_part_keys_dev(scale, edge_factor, seed, nparts,
+                                         part, None, 0, ctypes.byref(cnt),
+                                         stream))
+    keys = torch.empty(max(cnt.value, 1), dtype=torch.int64, device=device)
+    _lib.check(lib.dp_rmat_part_keys_dev(scale, edge_factor, seed, nparts,
+                                         part, keys.data_ptr(), cnt.value,
+                                         ctypes.byref(cnt), stream))
+    keys = keys[:cnt.value]
+    keys, _ = torch.sort(keys)
+    col = (keys & 0xFFFFFFFF).to(torch.int32)
+    deg = torch.bincount(keys >> 32, minlength=n_local)
+    del keys
+    rowptr = torch.zeros(n_local + 1, dtype=torch.int64, device=device)
+    torch.cumsum(deg, 0, out=rowptr[1:])
+    return rowptr.to(torch.int32), col
 
 
 def partition_csr(rowptr: np.ndarray, col: np.ndarray, nparts: int,

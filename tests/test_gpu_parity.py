@@ -308,3 +308,15 @@ def test_bfs_1d_partition_on_device(P, policy):
     np.testing.assert_array_equal(d.cpu().numpy(), want_d)
     np.testing.assert_array_equal(c.cpu().numpy(), want_c)
     assert levels == want_lv
+
+
+@pytest.mark.parametrize("P", [1, 3])
+def test_rmat_device_generator_matches_host(P):
+    import torch
+    from paper_2201_02789_b200 import dist as pdist
+    for p in range(P):
+        rp_h, col_h = pdist.rmat_part(14, 5, P, p)
+        rp_d, col_d = pdist.rmat_part_device(14, 5, P, p,
+                                             torch.device("cuda", 0))
+        np.testing.assert_array_equal(rp_d.cpu().numpy(), rp_h)
+        np.testing.assert_array_equal(col_d.cpu().numpy(), col_h)
