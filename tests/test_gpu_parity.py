@@ -320,3 +320,131 @@ def test_rmat_device_generator_matches_host(P):
                                              torch.device("cuda", 0))
         np.testing.assert_array_equal(rp_d.cpu().numpy(), rp_h)
         np.testing.assert_array_equal(col_d.cpu().numpy(), col_h)
+
+
+# ---------------------------------------------------------------------------
+# edge cases
+# ---------------------------------------------------------------------------
+
+EDGE_POLICIES = [dict(), dict(threshold=INF_THRESHOLD), dict(agg="warp"),
+                 dict(agg="block", agg_threshold=1000),
+                 dict(threshold=1, cfactor=1000, agg="multiblock",
+                      group_size=1), dict(agg="multiblock", group_size=10**6),
+                 dict(threshold=2, cfactor=3, agg="grid", parent_block=256,
+                      child_block=64, serial="warp")]
+
+
+def _graph_workload(bench_name, rowptr, col, weight=None):
+    rowptr = np.asarray(rowptr, np.int32)
+    col = np.asarray(col, np.int32)
+    n = rowptr.shape[0] - 1
+    g = graphs.Graph(rowptr, col)
+    spec = DatasetSpec("hand", n, 0, f"custom:{n}")
+    dist = np.full(n, UNREACHED, np.int32)
+    dist[0] = 0
+    bufs = {"rowptr": rowptr, "col": col, "dist": dist,
+            "counts": np.zeros(n, np.int32)}
+    payload = g
+    if bench_name == "sssp":
+        bufs["weight"] = np.asarray(weight if weight is not None
+                                    else np.ones(col.shape[0]), np.int32)
+        payload = (g, bufs["weight"])
+    return BENCHMARKS[bench_name], Workload(spec, bufs, n, payload)
+
+
+@pytest.mark.parametrize("policy", EDGE_POLICIES)
+@pytest.mark.parametrize("rowptr,col", [
+    ([0, 0], []),                      # single vertex, no edges
+    ([0, 0, 1], [0]),                  # source without out-edges
+    ([0, 3, 3, 3], [0, 0, 0]),         # self-loop multi-edge only
+    ([0, 2, 4, 4, 4], [1, 1, 3, 3]),   # duplicates, unreachable vertex 2
+])
+def test_bfs_sssp_degenerate_graphs(rowptr, col, policy):
+    for bench_name in ("bfs", "sssp"):
+        bench, wl = _graph_workload(bench_name, rowptr, col)
+        g = wl.payload if bench_name == "bfs" else wl.payload[0]
+        want = oracle.bfs(g.rowptr, g.col)
+        rep, _ = run_config(bench, wl, BenchConfig(**policy))
+        np.testing.assert_array_equal(rep.arrays["dist"], want[0])
+        if bench_name == "bfs":
+            np.testing.assert_array_equal(rep.arrays["counts"], want[1])
+            assert rep.host_launches >= want[2]
+
+
+def test_sssp_negative_cycle_hits_iteration_limit():
+    bench, wl = _graph_workload("sssp", [0, 1, 2], [1, 0], weight=[-1, -1])
+    with pytest.raises(RuntimeError) as e:
+        run_config(bench, wl, BenchConfig(threshold=4, agg="block"))
+    assert getattr(e.value, "kind", "") == "iteration-limit"
+
+
+@pytest.mark.parametrize("policy", EDGE_POLICIES)
+def test_manylaunch_zero_negative_and_large_sizes(policy):
+    sizes = np.array([0, -5, 1, 31, 32, 33, 1024, 0, 5000, -1] * 7, np.int32)
+    spec = DatasetSpec("sizes", sizes.shape[0], 0, "custom")
+    wl = Workload(spec, {"sizes": sizes, "out": np.zeros_like(sizes),
+                         "total": np.zeros(1, np.int32)}, sizes.shape[0],
+                  sizes)
+    bench = BENCHMARKS["manylaunch"]
+    want_out, want_total = oracle.manylaunch(sizes)
+    rep, _ = run_config(bench, wl, BenchConfig(**policy))
+    np.testing.assert_array_equal(rep.arrays["out"], want_out)
+    np.testing.assert_array_equal(rep.arrays["total"], want_total)
+    ref = run_reference(bench, wl)
+    np.testing.assert_array_equal(ref.arrays["out"], want_out)
+
+
+def test_tc_empty_and_tiny():
+    bench = BENCHMARKS["tc"]
+    for rowptr, col, want in (([0] * 11, [], 0),
+                              ([0, 2, 3, 3], [1, 2, 2], 1)):
+        rowptr = np.asarray(rowptr, np.int32)
+        col = np.asarray(col, np.int32)
+        spec = DatasetSpec("rmat", 1, 0, "custom")
+        wl = Workload(spec, {"rowptr": rowptr, "col": col}, rowptr.shape[0] - 1,
+                      None)
+        for policy in EDGE_POLICIES:
+            rep, _ = run_config(bench, wl, BenchConfig(**policy))
+            assert int(rep.arrays["triangles"][0]) == want, policy
+
+
+@pytest.mark.parametrize("policy", EDGE_POLICIES)
+def test_bt_degenerate_curves(policy):
+    cp = np.zeros((5, 3, 2), np.float32)
+    cp[1] = [[0.5, 0.5], [0.9, 0.1], [0.5, 0.5]]   # P0 == P2: curvature inf
+    cp[2] = [[0.1, 0.1], [0.2, 0.2], [0.3, 0.3]]   # straight: 4 vertices
+    cp[3] = [[0.0, 0.0], [0.0, 0.0], [0.0, 0.0]]   # 0/0: NaN -> max
+    cp[4] = [[0.0, 0.0], [1.0, 1.0], [1.0, 0.0]]
+    spec = DatasetSpec("curves", 5, 0, "custom")
+    wl = Workload(spec, {"cp": cp, "max_tess": graphs.BT_MAX_TESS,
+                         "scale": graphs.BT_CURV_SCALE}, 5, cp)
+    bench = BENCHMARKS["bt"]
+    ntess, verts = oracle.bt(cp, graphs.BT_MAX_TESS, graphs.BT_CURV_SCALE)
+    rep, _ = run_config(bench, wl, BenchConfig(**policy))
+    np.testing.assert_array_equal(rep.arrays["ntess"], ntess)
+    assert ntess[1] == ntess[3] == graphs.BT_MAX_TESS and ntess[2] == 4
+    assert np.max(np.abs(rep.arrays["verts"] - verts)) <= 1e-5
+
+
+def test_bt_zero_curves():
+    cp = np.zeros((0, 3, 2), np.float32)
+    wl = Workload(DatasetSpec("curves", 1, 0, "custom"),
+                  {"cp": cp, "max_tess": graphs.BT_MAX_TESS,
+                   "scale": graphs.BT_CURV_SCALE}, 0, cp)
+    rep, _ = run_config(BENCHMARKS["bt"], wl, BenchConfig(agg="block"))
+    assert rep.arrays["ntess"].shape == (0,)
+
+
+def test_naive_cdp_waves_rmat21():
+    """~1.1 M launching parents exceed the 2^19 pending-launch cap: the
+    parent grid runs in waves (dynpar.cu wave_parents) and stays exact."""
+    bench, wl = _rmat_workload("bfs", 21, 3)
+    g = wl.payload
+    dist, counts, _ = oracle.bfs(g.rowptr, g.col, nthreads=0)
+    rep, _ = run_config(bench, wl, BenchConfig(parent_block=256))
+    np.testing.assert_array_equal(rep.arrays["dist"], dist)
+    np.testing.assert_array_equal(rep.arrays["counts"], counts)
+    deg = np.diff(g.rowptr)
+    launchers = int(((dist < UNREACHED) & (deg > 0)).sum())
+    assert rep.num_launches == launchers
+    assert launchers > (1 << 19)
