@@ -85,7 +85,12 @@ typedef struct dp_config {
   int32_t child_block;   /* child threads per block (reference launches use 32) */
   int32_t serial_mode;   /* DP_SERIAL_* */
   int32_t pending_launch_limit; /* cudaLimitDevRuntimePendingLaunchCount; 0 = auto */
-  int32_t reserved[6];
+  int32_t persistent;    /* > 0: persistent parent grid of this many blocks per
+                            SM (single-group multiblock / grid aggregation):
+                            all launches are recorded first, the serial arms
+                            run while the aggregated child uses the rest of
+                            the GPU.  0 = one parent thread per parent. */
+  int32_t reserved[5];
 } dp_config;
 
 /* SimReport (sim/report.py:12-28) counters, measured on the device */

@@ -38,7 +38,8 @@ class DpConfig(ctypes.Structure):
                 ("child_block", ctypes.c_int32),
                 ("serial_mode", ctypes.c_int32),
                 ("pending_launch_limit", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 6)]
+                ("persistent", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 5)]
 
 
 class DpStats(ctypes.Structure):

@@ -34,7 +34,9 @@ class BenchConfig:
     parent_block / child_block (threads per parent / child block; the
     reference uses 32 for both), serial ("thread": below-threshold children
     run in the parent thread as threshold.py:60-83 does; "warp": the parent
-    warp shares them), pending_launch_limit (CDP2 pool, 0 = auto)."""
+    warp shares them), pending_launch_limit (CDP2 pool, 0 = auto),
+    persistent (blocks per SM of a persistent parent grid for single-group
+    aggregation: record every launch first, then the serial arms)."""
     threshold: int = 0
     cfactor: int = 1
     agg: str | None = None
@@ -45,6 +47,7 @@ class BenchConfig:
     child_block: int = 32
     serial: str = "thread"
     pending_launch_limit: int = 0
+    persistent: int = 0
 
     def describe(self) -> str:
         return (f"threshold={self.threshold} cfactor={self.cfactor} "
@@ -70,6 +73,8 @@ class BenchConfig:
             if v < 32 or v > 256 or v % 32:
                 raise ValueError(
                     f"{name} must be a multiple of 32 in [32, 256]")
+        if not 0 <= self.persistent <= 8:
+            raise ValueError("persistent must be in [0, 8] blocks per SM")
         if self.serial not in _lib.SERIAL_MODES:
             raise ValueError(f"unknown serial mode {self.serial!r}")
 
@@ -89,6 +94,7 @@ class BenchConfig:
         c.child_block = int(self.child_block)
         c.serial_mode = _lib.SERIAL_MODES[self.serial]
         c.pending_launch_limit = int(self.pending_launch_limit)
+        c.persistent = int(self.persistent)
         if "T" not in self.order.upper():
             c.threshold = 0
         if "C" not in self.order.upper():

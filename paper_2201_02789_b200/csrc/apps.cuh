@@ -78,6 +78,7 @@ struct BfsApp {
   }
   static constexpr int kUnroll = DP_GRAPH_UNROLL;
   static constexpr bool kBlockMode = false;
+  static constexpr bool kPureExpand = true;
   template <int U, class ArgsOf>
   __device__ __forceinline__ void items(ArgsOf args, const int* e,
                                         const bool* ok, Acc& acc) const {
@@ -183,6 +184,7 @@ struct BfsPartApp {
   }
   static constexpr int kUnroll = DP_GRAPH_UNROLL;
   static constexpr bool kBlockMode = false;
+  static constexpr bool kPureExpand = true;
   template <int U, class ArgsOf>
   __device__ __forceinline__ void items(ArgsOf args, const int* e,
                                         const bool* ok, Acc& acc) const {
@@ -250,6 +252,7 @@ struct SsspApp {
   }
   static constexpr int kUnroll = DP_GRAPH_UNROLL;
   static constexpr bool kBlockMode = false;
+  static constexpr bool kPureExpand = true;
   template <int U, class ArgsOf>
   __device__ __forceinline__ void items(ArgsOf args, const int* e,
                                         const bool* ok, Acc& acc) const {
@@ -309,6 +312,7 @@ struct ManyLaunchApp {
   }
   static constexpr int kUnroll = 1;
   static constexpr bool kBlockMode = false;
+  static constexpr bool kPureExpand = true;
   template <int U, class ArgsOf>
   __device__ __forceinline__ void items(ArgsOf args, const int* e,
                                         const bool* ok, Acc& acc) const {
@@ -389,6 +393,7 @@ struct TcApp {
   // probes the set: coalesced reads of N+(v), O(1) lookups, no per-thread
   // merge chains.  Lists longer than kSlots/2 fall back to per-thread merges.
   static constexpr bool kBlockMode = true;
+  static constexpr bool kPureExpand = true;
   static constexpr int kSlotBits = 12;
   static constexpr int kSlots = 1 << kSlotBits;  // 16 KB of shared memory
 
@@ -569,6 +574,7 @@ struct BtApp {
   }
   static constexpr int kUnroll = 1;
   static constexpr bool kBlockMode = false;
+  static constexpr bool kPureExpand = false;  // bump-allocates in expand
   template <int U, class ArgsOf>
   __device__ __forceinline__ void items(ArgsOf args, const int* e,
                                         const bool* ok, Acc& acc) const {

@@ -124,6 +124,8 @@ int validate(const dp_config* c) {
   if (c->agg == DP_AGG_MULTIBLOCK && c->group_size < 1)
     return fail(DP_ERR_INVALID, "group size must be at least 1");
   if (c->cfactor < 1) return fail(DP_ERR_INVALID, "cfactor must be >= 1");
+  if (c->persistent < 0 || c->persistent > 8)
+    return fail(DP_ERR_INVALID, "persistent must be in [0, 8]");
   if (c->threshold < 0) return fail(DP_ERR_INVALID, "threshold must be >= 0");
   if (c->parent_block < 32 || c->parent_block > 256 ||
       c->parent_block % 32)
@@ -295,10 +297,31 @@ struct RunCounters {
   double ms_kernel_sum = 0.0;
 };
 
+#ifndef DP_L1_CARVEOUT
+#define DP_L1_CARVEOUT -1  // -1: driver default
+#endif
+
+// Shared-memory carve-out preference for the graph kernels: they use < 1 KB
+// of shared memory (TC's 16 KB hash is the exception), so the rest can be
+// L1 for the random dist probes.
+template <class K>
+void prefer_l1(K kernel) {
+  if (DP_L1_CARVEOUT >= 0)
+    cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         DP_L1_CARVEOUT);
+}
+
 template <class App, int AGG, bool CDP>
 void launch_parent_inst(const App& app, int grid, int pb, const Knobs& k,
                         const AggTables<App>& t, DevState* ds, long long base,
                         cudaStream_t s) {
+  static bool once = [] {
+    prefer_l1(parent_kernel<App, AGG, CDP>);
+    prefer_l1(child_kernel<App>);
+    prefer_l1(child_agg_kernel<App>);
+    return true;
+  }();
+  (void)once;
   parent_kernel<App, AGG, CDP><<<grid, pb, 0, s>>>(app, k, t, ds, base);
 }
 
@@ -372,6 +395,28 @@ int launch_wave(const App& app, long long base, long long nparents,
     t.done = w->done;
   }
   const Knobs k = knobs_of(c);
+  const bool single_group =
+      c->agg == DP_AGG_GRID ||
+      (c->agg == DP_AGG_MULTIBLOCK && (long long)c->group_size >= grid);
+  if constexpr (App::kPureExpand) {
+    if (cdp && c->persistent > 0 && single_group) {
+      int sms = 148;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+      const long long pgrid =
+          std::min<long long>(grid, (long long)sms * c->persistent);
+      if (c->agg == DP_AGG_GRID)
+        parent_persistent_kernel<App, kAggGrid><<<(int)pgrid, pb, 0, s>>>(
+            app, k, t, w->ds, base, nparents);
+      else
+        parent_persistent_kernel<App, kAggMulti><<<(int)pgrid, pb, 0, s>>>(
+            app, k, t, w->ds, base, nparents);
+      DP_CUDA(cudaGetLastError());
+      rc->host_launches += 1;
+      rc->host_blocks += pgrid;
+      rc->kernel_launches += 1;
+      goto glue;
+    }
+  }
   if (!cdp) {
     launch_parent_inst<App, kAggNone, false>(app, grid, pb, k, t, w->ds, base, s);
   } else {
@@ -397,6 +442,7 @@ int launch_wave(const App& app, long long base, long long nparents,
   rc->host_launches += 1;
   rc->host_blocks += grid;
   rc->kernel_launches += 1;
+glue:
   if (cdp && c->agg == DP_AGG_GRID) {
     // completion hook (common.py:144-164): read the fused counter, launch
     // the aggregated child from the host, re-arm the counter

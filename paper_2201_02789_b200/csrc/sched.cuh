@@ -361,4 +361,79 @@ __global__ void __launch_bounds__(256, DP_PARENT_MINB)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Persistent parent (B200): a grid of a few blocks per SM walks the parents in
+// chunks of blockDim.x twice.  Pass 1 only expands and records the launches
+// (one fused atomic per chunk into the single group); the last block to
+// finish pass 1 performs the aggregated launch (multiblock with one group)
+// or leaves it to the host glue (grid).  Pass 2 re-expands and runs the
+// serial arms, so the aggregated child overlaps with the parent's own
+// below-threshold work instead of starting after the last of ~10^4 parent
+// blocks.  Requires App::kPureExpand (expand has no side effects).
+// ---------------------------------------------------------------------------
+template <class App, int AGG>
+__global__ void __launch_bounds__(256)
+    parent_persistent_kernel(App app, Knobs k, AggTables<App> t, DevState* ds,
+                             long long base, long long nparents) {
+  static_assert(App::kPureExpand, "persistent parents re-run expand()");
+  static_assert(AGG == kAggMulti || AGG == kAggGrid, "single-group only");
+  using Args = typename App::Args;
+  __shared__ int smem[66];
+  __shared__ unsigned long long s_old;
+  app.parent_prologue();
+  const long long nchunks = ceil_div_ll(nparents, blockDim.x);
+  // pass 1: record every launch of this block's chunks
+  for (long long c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    const long long lu = c * blockDim.x + threadIdx.x;
+    Args a{};
+    const int cnt = app.expand((int)(base + lu), lu < nparents, a);
+    const bool go = cnt > 0 && (k.threshold == 0 || cnt >= k.threshold);
+    const int gd = go ? ceil_div(ceil_div(cnt, k.cb), k.cf) : 0;
+    const BlockScan s = block_scan(gd > 0, gd, smem);
+    if (threadIdx.x == 0)
+      s_old = s.np > 0 ? atomicAdd(&t.ctr[0], ((unsigned long long)s.np << 32) +
+                                                  (unsigned long long)s.total)
+                       : 0ull;
+    __syncthreads();
+    if (gd > 0) {
+      const unsigned long long old = s_old;
+      const long long row = (long long)(old >> 32) + s.rank;
+      t.args[row] = a;
+      t.scan[row] = (int)(old & 0xffffffffull) + s.excl;
+      __threadfence();
+    }
+    __syncthreads();  // s_old is rewritten by the next chunk
+  }
+  if constexpr (AGG == kAggMulti) {
+    if (threadIdx.x == 0) {
+      const int d = atomicAdd(&t.done[0], 1);
+      if (d == (int)gridDim.x - 1) {
+        __threadfence();
+        const unsigned long long c = atomicAdd(&t.ctr[0], 0ull);
+        t.ctr[0] = 0;
+        t.done[0] = 0;
+        const int np = (int)(c >> 32);
+        const int total = (int)(c & 0xffffffffull);
+        if (np > 0) {
+          child_agg_kernel<App><<<total, k.cb, 0, cudaStreamFireAndForget>>>(
+              app, t.args, t.scan, np, k.cf);
+          note_launch_error(ds);
+          atomicAdd(&ds->launches, 1ull);
+          atomicAdd(&ds->blocks, (unsigned long long)total);
+        }
+      }
+    }
+  }
+  // pass 2: the below-threshold children, serially in the parent warps
+  typename App::Acc acc{};
+  for (long long c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    const long long lu = c * blockDim.x + threadIdx.x;
+    Args a{};
+    const int cnt = app.expand((int)(base + lu), lu < nparents, a);
+    const bool go = cnt > 0 && (k.threshold == 0 || cnt >= k.threshold);
+    serial_arm(app, a, cnt, !go, k.serial_warp != 0, acc);
+  }
+  app.flush(acc);
+}
+
 }  // namespace dp

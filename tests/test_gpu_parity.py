@@ -37,7 +37,8 @@ SIZE_SPECS = ["sizes:100:seed4", "sizes:1024:seed1", "sizes:40:seed3",
 # B200-only knobs that must not change any output
 B200_VARIANTS = [dict(), dict(parent_block=256), dict(child_block=128),
                  dict(serial="warp"), dict(parent_block=128, serial="warp",
-                                           child_block=64)]
+                                           child_block=64),
+                 dict(persistent=2, parent_block=128, serial="warp")]
 
 
 def _cfg(d):
@@ -331,7 +332,10 @@ EDGE_POLICIES = [dict(), dict(threshold=INF_THRESHOLD), dict(agg="warp"),
                  dict(threshold=1, cfactor=1000, agg="multiblock",
                       group_size=1), dict(agg="multiblock", group_size=10**6),
                  dict(threshold=2, cfactor=3, agg="grid", parent_block=256,
-                      child_block=64, serial="warp")]
+                      child_block=64, serial="warp"),
+                 dict(threshold=2, agg="multiblock", group_size=1 << 20,
+                      persistent=1, serial="warp"),
+                 dict(threshold=3, agg="grid", persistent=3)]
 
 
 def _graph_workload(bench_name, rowptr, col, weight=None):

@@ -46,6 +46,18 @@ def main():
         configs.append(dict(BEST[kind]))
         d = dict(BEST[kind]); d["agg"] = "grid"; d.pop("group_size", None)
         configs.append(d)
+    elif grid == "persist":
+        from bench import BEST
+        for ps, T, C in itertools.product((0, 1, 2, 3, 4, 6), (512, 1024, 2048),
+                                          (8, 32)):
+            d = dict(BEST[kind]); d.update(persistent=ps, threshold=T,
+                                           cfactor=C, group_size=1 << 20)
+            configs.append(d)
+    elif grid == "groups":
+        from bench import BEST
+        for gs in (8, 32, 128, 512, 2048, 1 << 20):
+            d = dict(BEST[kind]); d["group_size"] = gs
+            configs.append(d)
     elif grid == "top":
         for T, C, agg, cb in itertools.product(
                 (512, 1024, 2048), (16, 32), ("grid", "mb-all", "mb16"),
