@@ -194,7 +194,28 @@ __device__ __forceinline__ void serial_arm(const App& app,
     }
     return;
   }
-  const int c = mine && cnt > 0 ? cnt : 0;
+  // lanes with >= 32 items: the whole warp walks that lane's items, U x 32
+  // at a time (no owner search)
+  unsigned big = __ballot_sync(DP_FULL, mine && cnt >= 32);
+  while (big) {
+    const int src = __ffs(big) - 1;
+    big &= big - 1;
+    const Args b = shfl_pod(a, src);
+    const int cb = __shfl_sync(DP_FULL, cnt, src);
+    auto args = [&](int) -> const Args& { return b; };
+    for (int e0 = 0; e0 < cb; e0 += 32 * U) {
+      int e[U];
+      bool ok[U];
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        e[j] = e0 + j * 32 + lane_id();
+        ok[j] = e[j] < cb;
+      }
+      app.template items<U>(args, e, ok, acc);
+    }
+  }
+  // the rest (< 32 items per lane) as one flattened, load-balanced list
+  const int c = mine && cnt > 0 && cnt < 32 ? cnt : 0;
   const int incl = warp_incl_scan(c);
   const int total = __shfl_sync(DP_FULL, incl, 31);
   const int excl = incl - c;
