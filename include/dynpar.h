@@ -90,7 +90,11 @@ typedef struct dp_config {
                             all launches are recorded first, the serial arms
                             run while the aggregated child uses the rest of
                             the GPU.  0 = one parent thread per parent. */
-  int32_t reserved[5];
+  int32_t device_loop;   /* 1: BFS levels / SSSP rounds are chained on the
+                            device (CDP2 tail launches, up to 16 per host
+                            launch) instead of one host launch + flag
+                            readback each */
+  int32_t reserved[4];
 } dp_config;
 
 /* SimReport (sim/report.py:12-28) counters, measured on the device */

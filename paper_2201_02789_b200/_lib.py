@@ -39,7 +39,8 @@ class DpConfig(ctypes.Structure):
                 ("serial_mode", ctypes.c_int32),
                 ("pending_launch_limit", ctypes.c_int32),
                 ("persistent", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 5)]
+                ("device_loop", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 4)]
 
 
 class DpStats(ctypes.Structure):

@@ -36,7 +36,9 @@ class BenchConfig:
     run in the parent thread as threshold.py:60-83 does; "warp": the parent
     warp shares them), pending_launch_limit (CDP2 pool, 0 = auto),
     persistent (blocks per SM of a persistent parent grid for single-group
-    aggregation: record every launch first, then the serial arms)."""
+    aggregation: record every launch first, then the serial arms),
+    device_loop (chain BFS levels / SSSP rounds on the device with CDP2 tail
+    launches instead of a host launch + flag readback per level)."""
     threshold: int = 0
     cfactor: int = 1
     agg: str | None = None
@@ -48,6 +50,7 @@ class BenchConfig:
     serial: str = "thread"
     pending_launch_limit: int = 0
     persistent: int = 0
+    device_loop: bool = False
 
     def describe(self) -> str:
         return (f"threshold={self.threshold} cfactor={self.cfactor} "
@@ -95,6 +98,7 @@ class BenchConfig:
         c.serial_mode = _lib.SERIAL_MODES[self.serial]
         c.pending_launch_limit = int(self.pending_launch_limit)
         c.persistent = int(self.persistent)
+        c.device_loop = int(bool(self.device_loop))
         if "T" not in self.order.upper():
             c.threshold = 0
         if "C" not in self.order.upper():

@@ -58,6 +58,14 @@ struct BfsApp {
   __device__ void parent_prologue() const {
     if (blockIdx.x == 0 && threadIdx.x == 0) *changed_next = 0;
   }
+  // the app of level r (device-side level loop)
+  __device__ BfsApp for_round(int r, int* flags) const {
+    BfsApp a = *this;
+    a.level = r;
+    a.changed = flags + (r & 1);
+    a.changed_next = flags + ((r + 1) & 1);
+    return a;
+  }
   // main (:105-119): u with dist[u] == level owns deg = rowptr[u+1]-rowptr[u]
   __device__ int expand(int u, bool valid, Args& a) const {
     if (!valid || __ldcg(dist + u) != level) return 0;
@@ -226,6 +234,12 @@ struct SsspApp {
   __device__ int nparents() const { return n; }
   __device__ void parent_prologue() const {
     if (blockIdx.x == 0 && threadIdx.x == 0) *changed_next = 0;
+  }
+  __device__ SsspApp for_round(int r, int* flags) const {
+    SsspApp a = *this;
+    a.changed = flags + (r & 1);
+    a.changed_next = flags + ((r + 1) & 1);
+    return a;
   }
   // main (:207-222): every reached u relaxes all its out-edges from its
   // round-start distance du

@@ -117,7 +117,7 @@ struct DevState {
   unsigned long long blocks;    // blocks of device-launched grids
   int err;                      // first cudaError_t seen by a device launch
   int flag[2];                  // double-buffered `changed` (levels / rounds)
-  int pad;
+  int done_round;               // device loop: round count at convergence
 };
 
 __device__ __forceinline__ void note_launch_error(DevState* ds) {

@@ -349,21 +349,11 @@ long long wave_parents(const dp_config* c, long long nparents,
   return std::min(w, nparents);
 }
 
-// One host launch of the parent grid over parents [base, base + nparents)
-// (+ the grid-granularity glue).
+// Aggregation tables for a parent grid of `grid` x `pb` threads.
 template <class App>
-int launch_wave(const App& app, long long base, long long nparents,
-                const dp_config* c, Workspace* w, cudaStream_t s,
-                RunCounters* rc) {
-  if (nparents <= 0) return 0;  // empty host launch: suppressed (machine.py:172)
-  const int pb = c->parent_block;
-  const long long grid_ll = dp::ceil_div_ll(nparents, pb);
-  if (grid_ll > 0x7fffffffLL)
-    return fail(DP_ERR_INVALID, "parent grid too large");
-  const int grid = (int)grid_ll;
-  AggTables<App> t{nullptr, nullptr, nullptr, nullptr};
-  const bool cdp = c->variant == DP_VARIANT_CDP;
-  if (cdp && c->agg != DP_AGG_NONE) {
+int prepare_tables(const dp_config* c, int grid, int pb, Workspace* w,
+                   cudaStream_t s, AggTables<App>* t) {
+  if (c->variant == DP_VARIANT_CDP && c->agg != DP_AGG_NONE) {
     const size_t rows = (size_t)grid * pb;
     size_t groups = 1;
     if (c->agg == DP_AGG_BLOCK) groups = grid;
@@ -389,11 +379,29 @@ int launch_wave(const App& app, long long base, long long nparents,
       DP_CUDA(cudaMemsetAsync(w->done, 0, groups * sizeof(int), s));
       w->groups = groups;
     }
-    t.args = (typename App::Args*)w->tab;
-    t.scan = w->scan;
-    t.ctr = w->ctr;
-    t.done = w->done;
+    t->args = (typename App::Args*)w->tab;
+    t->scan = w->scan;
+    t->ctr = w->ctr;
+    t->done = w->done;
   }
+  return 0;
+}
+
+// One host launch of the parent grid over parents [base, base + nparents)
+// (+ the grid-granularity glue).
+template <class App>
+int launch_wave(const App& app, long long base, long long nparents,
+                const dp_config* c, Workspace* w, cudaStream_t s,
+                RunCounters* rc) {
+  if (nparents <= 0) return 0;  // empty host launch: suppressed (machine.py:172)
+  const int pb = c->parent_block;
+  const long long grid_ll = dp::ceil_div_ll(nparents, pb);
+  if (grid_ll > 0x7fffffffLL)
+    return fail(DP_ERR_INVALID, "parent grid too large");
+  const int grid = (int)grid_ll;
+  AggTables<App> t{nullptr, nullptr, nullptr, nullptr};
+  const bool cdp = c->variant == DP_VARIANT_CDP;
+  if (int r = prepare_tables(c, grid, pb, w, s, &t)) return r;
   const Knobs k = knobs_of(c);
   const bool single_group =
       c->agg == DP_AGG_GRID ||
@@ -547,6 +555,54 @@ double now_ns() {
 // level/round-loop apps
 // ---------------------------------------------------------------------------
 
+// Levels/rounds chained on the device (round_controller, sched.cuh): one
+// host launch per chain of kChain rounds; the host only checks done_round.
+template <class App>
+int device_loop(Workspace* w, const dp_config* c, long long nparents,
+                int max_iter, cudaStream_t s, const App& app0,
+                RunCounters* rc, int* it, bool* converged) {
+  constexpr int kChain = 16;
+  const int pb = c->parent_block;
+  const int grid = (int)dp::ceil_div_ll(nparents, pb);
+  AggTables<App> t{nullptr, nullptr, nullptr, nullptr};
+  int r;
+  if ((r = prepare_tables(c, grid, pb, w, s, &t))) return r;
+  const Knobs k = knobs_of(c);
+  for (int first = 0; first <= max_iter; first += kChain) {
+    const int last = std::min(first + kChain - 1, max_iter);
+    switch (c->agg) {
+      case DP_AGG_NONE:
+        round_controller<App, kAggNone><<<1, 1, 0, s>>>(
+            app0, k, t, w->ds, grid, pb, first, first, last);
+        break;
+      case DP_AGG_WARP:
+        round_controller<App, kAggWarp><<<1, 1, 0, s>>>(
+            app0, k, t, w->ds, grid, pb, first, first, last);
+        break;
+      case DP_AGG_BLOCK:
+        round_controller<App, kAggBlock><<<1, 1, 0, s>>>(
+            app0, k, t, w->ds, grid, pb, first, first, last);
+        break;
+      default:
+        round_controller<App, kAggMulti><<<1, 1, 0, s>>>(
+            app0, k, t, w->ds, grid, pb, first, first, last);
+        break;
+    }
+    DP_CUDA(cudaGetLastError());
+    rc->host_launches += 1;
+    rc->host_blocks += 1;
+    rc->kernel_launches += 1;
+    if ((r = read_state(w, s))) return r;
+    if (w->h_ds->done_round > 0) {
+      *it = w->h_ds->done_round;
+      *converged = true;
+      return 0;
+    }
+    *it = last + 1;
+  }
+  return 0;
+}
+
 template <class MakeApp>
 int iterate(Workspace* w, const dp_config* c, long long nparents,
             long long launchers, int max_iter, cudaStream_t s, MakeApp make,
@@ -559,7 +615,14 @@ int iterate(Workspace* w, const dp_config* c, long long nparents,
   DP_CUDA(cudaEventRecord(w->ev0, s));
   int it = 0;
   bool converged = false;
-  for (; it <= max_iter; ++it) {
+  if (c->device_loop && c->variant == DP_VARIANT_CDP &&
+      c->agg != DP_AGG_GRID &&
+      wave_parents(c, nparents, launchers) == nparents) {
+    if ((r = device_loop(w, c, nparents, max_iter, s, make(0, w->ds), &rc,
+                         &it, &converged)))
+      return r;
+  }
+  for (; !converged && it <= max_iter; ++it) {
     auto app = make(it, w->ds);
     if ((r = launch_parent(app, nparents, launchers, c, w, s, &rc))) return r;
     if ((r = read_state(w, s))) return r;
@@ -575,6 +638,10 @@ int iterate(Workspace* w, const dp_config* c, long long nparents,
   float ms = 0.f;
   DP_CUDA(cudaEventElapsedTime(&ms, w->ev0, w->ev1));
   if ((r = read_state(w, s))) return r;
+  if (rc.ms_kernel_sum == 0.0) {  // device loop: no per-level host events
+    rc.ms_kernel_sum = ms;
+    rc.ms_kernel_max = ms;
+  }
   finish_stats(w, rc, ms, st);
   if (st) st->iterations = it;
   if (!converged)

@@ -457,4 +457,34 @@ __global__ void __launch_bounds__(256)
   app.flush(acc);
 }
 
+// ---------------------------------------------------------------------------
+// Device-side level loop (B200, CDP2 tail launches).  The host loop of the
+// reference (bench/benchmarks.py:157-168, 259-270) launches one parent grid
+// per level and reads `changed` back.  Here a one-thread controller does it:
+// round r's parent grid goes to the fire-and-forget stream, the controller of
+// round r+1 to the tail-launch stream, so it starts only after round r and
+// every grid it spawned have completed, reads the flag, and either stops or
+// continues.  A chain covers at most `last - first + 1` rounds (bounded
+// nesting); the host relaunches until done_round is set.
+// ---------------------------------------------------------------------------
+template <class App, int AGG>
+__global__ void round_controller(App app0, Knobs k, AggTables<App> t,
+                                 DevState* ds, int grid, int pb, int round,
+                                 int first, int last) {
+  if (round > 0 && round > first && ds->flag[(round - 1) & 1] == 0) {
+    ds->done_round = round;  // round - 1 changed nothing
+    return;
+  }
+  if (round > last) return;  // hand back to the host
+  const App app = app0.for_round(round, ds->flag);
+  parent_kernel<App, AGG, true><<<grid, pb, 0, cudaStreamFireAndForget>>>(
+      app, k, t, ds, 0ll);
+  note_launch_error(ds);
+  round_controller<App, AGG><<<1, 1, 0, cudaStreamTailLaunch>>>(
+      app0, k, t, ds, grid, pb, round + 1, first, last);
+  note_launch_error(ds);
+  atomicAdd(&ds->launches, 2ull);
+  atomicAdd(&ds->blocks, (unsigned long long)grid + 1);
+}
+
 }  // namespace dp

@@ -38,7 +38,8 @@ SIZE_SPECS = ["sizes:100:seed4", "sizes:1024:seed1", "sizes:40:seed3",
 B200_VARIANTS = [dict(), dict(parent_block=256), dict(child_block=128),
                  dict(serial="warp"), dict(parent_block=128, serial="warp",
                                            child_block=64),
-                 dict(persistent=2, parent_block=128, serial="warp")]
+                 dict(persistent=2, parent_block=128, serial="warp"),
+                 dict(device_loop=True, parent_block=64)]
 
 
 def _cfg(d):
@@ -335,7 +336,9 @@ EDGE_POLICIES = [dict(), dict(threshold=INF_THRESHOLD), dict(agg="warp"),
                       child_block=64, serial="warp"),
                  dict(threshold=2, agg="multiblock", group_size=1 << 20,
                       persistent=1, serial="warp"),
-                 dict(threshold=3, agg="grid", persistent=3)]
+                 dict(threshold=3, agg="grid", persistent=3),
+                 dict(threshold=2, agg="block", device_loop=True),
+                 dict(agg="multiblock", group_size=1 << 20, device_loop=True)]
 
 
 def _graph_workload(bench_name, rowptr, col, weight=None):
@@ -372,7 +375,9 @@ def test_bfs_sssp_degenerate_graphs(rowptr, col, policy):
         np.testing.assert_array_equal(rep.arrays["dist"], want[0])
         if bench_name == "bfs":
             np.testing.assert_array_equal(rep.arrays["counts"], want[1])
-            assert rep.host_launches >= want[2]
+            assert rep.iterations == want[2]
+            if not policy.get("device_loop"):
+                assert rep.host_launches >= want[2]
 
 
 def test_sssp_negative_cycle_hits_iteration_limit():
@@ -452,3 +457,20 @@ def test_naive_cdp_waves_rmat21():
     launchers = int(((dist < UNREACHED) & (deg > 0)).sum())
     assert rep.num_launches == launchers
     assert launchers > (1 << 19)
+
+
+@pytest.mark.parametrize("policy", [
+    dict(device_loop=True), dict(threshold=4, agg="block", device_loop=True),
+    dict(threshold=4, cfactor=2, agg="multiblock", group_size=1 << 20,
+         serial="warp", parent_block=128, device_loop=True)])
+def test_device_loop_many_levels(policy, golden):
+    """road graphs have long BFS chains: several 16-round device chains."""
+    for bench_name in ("bfs", "sssp"):
+        bench, wl = load(bench_name, "road:1000:seed7")
+        ref = _golden_ref(golden, bench_name, "road:1000:seed7")
+        rep, _ = run_config(bench, wl, BenchConfig(**policy))
+        assert rep.memory_digest == ref["digest"]
+        if bench_name == "bfs":
+            assert rep.iterations == ref["host_launches"] > 16
+            assert rep.host_launches == -(-rep.iterations // 16) or \
+                rep.host_launches == -(-(rep.iterations + 1) // 16)

@@ -46,6 +46,13 @@ def main():
         configs.append(dict(BEST[kind]))
         d = dict(BEST[kind]); d["agg"] = "grid"; d.pop("group_size", None)
         configs.append(d)
+    elif grid == "dloop":
+        from bench import BEST
+        for dl in (False, True):
+            d = dict(BEST[kind]); d["device_loop"] = dl
+            configs.append(d)
+            d = dict(d); d["group_size"] = 2048
+            configs.append(d)
     elif grid == "persist":
         from bench import BEST
         for ps, T, C in itertools.product((0, 1, 2, 3, 4, 6), (512, 1024, 2048),
