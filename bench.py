@@ -51,7 +51,7 @@ BEST = {
     # one aggregation group spanning the parent grid: the last parent block
     # issues ONE CDP2 launch per round (tools/tune.py, profiles/tune_*)
     "sssp": dict(threshold=1024, cfactor=32, agg="multiblock",
-                 group_size=1 << 20, parent_block=128, child_block=64,
+                 group_size=2048, parent_block=128, child_block=64,
                  serial="warp"),
     "bfs": dict(threshold=1024, cfactor=16, agg="multiblock",
                 group_size=1 << 20, parent_block=256, child_block=128,

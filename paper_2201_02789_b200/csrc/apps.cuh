@@ -23,6 +23,12 @@ namespace dp {
 #ifndef DP_GRAPH_UNROLL
 #define DP_GRAPH_UNROLL 4
 #endif
+#ifndef DP_SSSP_UNROLL
+#define DP_SSSP_UNROLL 2
+#endif
+#ifndef DP_SSSP_MINB
+#define DP_SSSP_MINB 8  // <= 32 registers: full occupancy for the latency-
+#endif                  // bound relaxations (tools/ab.sh, profiles/)
 
 // items<U> for apps whose item is not latency-chained: plain loop
 template <int U, class App, class ArgsOf>
@@ -87,6 +93,7 @@ struct BfsApp {
   static constexpr int kUnroll = DP_GRAPH_UNROLL;
   static constexpr bool kBlockMode = false;
   static constexpr bool kPureExpand = true;
+  static constexpr int kMinBlocks = 1;
   template <int U, class ArgsOf>
   __device__ __forceinline__ void items(ArgsOf args, const int* e,
                                         const bool* ok, Acc& acc) const {
@@ -193,6 +200,7 @@ struct BfsPartApp {
   static constexpr int kUnroll = DP_GRAPH_UNROLL;
   static constexpr bool kBlockMode = false;
   static constexpr bool kPureExpand = true;
+  static constexpr int kMinBlocks = 1;
   template <int U, class ArgsOf>
   __device__ __forceinline__ void items(ArgsOf args, const int* e,
                                         const bool* ok, Acc& acc) const {
@@ -264,9 +272,10 @@ struct SsspApp {
     if (alt < __ldcg(dist + v) && atomicMin(dist + v, alt) > alt)
       acc.changed = 1;
   }
-  static constexpr int kUnroll = DP_GRAPH_UNROLL;
+  static constexpr int kUnroll = DP_SSSP_UNROLL;
   static constexpr bool kBlockMode = false;
   static constexpr bool kPureExpand = true;
+  static constexpr int kMinBlocks = DP_SSSP_MINB;
   template <int U, class ArgsOf>
   __device__ __forceinline__ void items(ArgsOf args, const int* e,
                                         const bool* ok, Acc& acc) const {
@@ -327,6 +336,7 @@ struct ManyLaunchApp {
   static constexpr int kUnroll = 1;
   static constexpr bool kBlockMode = false;
   static constexpr bool kPureExpand = true;
+  static constexpr int kMinBlocks = 1;
   template <int U, class ArgsOf>
   __device__ __forceinline__ void items(ArgsOf args, const int* e,
                                         const bool* ok, Acc& acc) const {
@@ -408,6 +418,7 @@ struct TcApp {
   // merge chains.  Lists longer than kSlots/2 fall back to per-thread merges.
   static constexpr bool kBlockMode = true;
   static constexpr bool kPureExpand = true;
+  static constexpr int kMinBlocks = 1;
   static constexpr int kSlotBits = 12;
   static constexpr int kSlots = 1 << kSlotBits;  // 16 KB of shared memory
 
@@ -589,6 +600,7 @@ struct BtApp {
   static constexpr int kUnroll = 1;
   static constexpr bool kBlockMode = false;
   static constexpr bool kPureExpand = false;  // bump-allocates in expand
+  static constexpr int kMinBlocks = 1;
   template <int U, class ArgsOf>
   __device__ __forceinline__ void items(ArgsOf args, const int* e,
                                         const bool* ok, Acc& acc) const {

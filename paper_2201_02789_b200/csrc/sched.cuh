@@ -35,13 +35,6 @@
 #pragma once
 #include "common.cuh"
 
-// occupancy hints (minimum resident 256-thread blocks per SM)
-#ifndef DP_PARENT_MINB
-#define DP_PARENT_MINB 1
-#endif
-#ifndef DP_CHILD_MINB
-#define DP_CHILD_MINB 1
-#endif
 
 namespace dp {
 
@@ -106,7 +99,7 @@ __device__ __forceinline__ void run_logical_blocks(const App& app,
 
 // Plain child: BFS `visit` etc. (benchmarks.py:92-103), coarsened.
 template <class App>
-__global__ void __launch_bounds__(256, DP_CHILD_MINB) child_kernel(App app, typename App::Args a, int cf) {
+__global__ void __launch_bounds__(256, App::kMinBlocks) child_kernel(App app, typename App::Args a, int cf) {
   typename App::Acc acc{};
   run_logical_blocks(app, a, blockIdx.x, cf, acc);
   app.flush(acc);
@@ -134,7 +127,7 @@ __device__ __forceinline__ int warp_search(const int* __restrict__ scan, int np,
 // = one (parent row, local physical block) pair, found once per block and
 // reused across the coarsening loop.
 template <class App>
-__global__ void __launch_bounds__(256, DP_CHILD_MINB) child_agg_kernel(App app, const typename App::Args* tab,
+__global__ void __launch_bounds__(256, App::kMinBlocks) child_agg_kernel(App app, const typename App::Args* tab,
                                  const int* scan, int np, int cf) {
   __shared__ int s_lo;
   int lo = 0;
@@ -244,7 +237,7 @@ __device__ __forceinline__ void serial_arm(const App& app,
 }
 
 template <class App, int AGG, bool CDP>
-__global__ void __launch_bounds__(256, DP_PARENT_MINB)
+__global__ void __launch_bounds__(256, App::kMinBlocks)
     parent_kernel(App app, Knobs k, AggTables<App> t, DevState* ds,
                   long long base) {
   using Args = typename App::Args;
