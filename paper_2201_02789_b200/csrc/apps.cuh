@@ -100,7 +100,7 @@ struct BfsApp {
     int v[U], d[U];
 #pragma unroll
     for (int j = 0; j < U; ++j)
-      v[j] = ok[j] ? __ldg(col + args(j).start + e[j]) : 0;
+      v[j] = ok[j] ? ld_stream(col + args(j).start + e[j]) : 0;
     // L1-cached probe: dist only ever decreases, so a stale copy is >= the
     // true value and can only cost a redundant (failing) CAS, never a
     // missed discovery; RMAT hubs then hit in L1 instead of costing a 32 B
@@ -207,7 +207,7 @@ struct BfsPartApp {
     int v[U], d[U];
 #pragma unroll
     for (int j = 0; j < U; ++j)
-      v[j] = ok[j] ? __ldg(col + args(j).start + e[j]) : 0;
+      v[j] = ok[j] ? ld_stream(col + args(j).start + e[j]) : 0;
 #pragma unroll
     for (int j = 0; j < U; ++j) d[j] = ok[j] ? probe(v[j]) : 0;
 #pragma unroll
@@ -283,8 +283,8 @@ struct SsspApp {
 #pragma unroll
     for (int j = 0; j < U; ++j) {
       const int i = ok[j] ? args(j).start + e[j] : 0;
-      v[j] = ok[j] ? __ldg(col + i) : 0;
-      alt[j] = ok[j] ? (int)((unsigned)args(j).du + (unsigned)__ldg(weight + i))
+      v[j] = ok[j] ? ld_stream(col + i) : 0;
+      alt[j] = ok[j] ? (int)((unsigned)args(j).du + (unsigned)ld_stream(weight + i))
                      : 0;
     }
     // L1-cached probe (stale copies are >= the true distance: a stale hit

@@ -11,6 +11,24 @@ constexpr int kUnreached = 1 << 30;  // bench/graphs.py:29 UNREACHED
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
+#ifndef DP_STREAM_NO_ALLOCATE
+#define DP_STREAM_NO_ALLOCATE 1
+#endif
+
+// Streaming read of data used once per pass (CSR col / weight): read-only
+// path without allocating in L1, so L1 keeps the reused dist lines.
+__device__ __forceinline__ int ld_stream(const int* p) {
+#if DP_STREAM_NO_ALLOCATE
+  int v;
+  asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];"
+               : "=r"(v)
+               : "l"(p));
+  return v;
+#else
+  return __ldg(p);
+#endif
+}
+
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));

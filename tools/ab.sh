@@ -5,8 +5,5 @@ for lib in paper_2201_02789_b200/csrc/libdynpar.so tools/variants/*.so; do
   for k in sssp bfs; do
     echo "== $lib $k" >> $out
     DYNPAR_LIB=$lib timeout 120 python tools/tune.py $k 22 best >> $out 2>&1
-    DYNPAR_LIB=$lib timeout 120 python tools/tune.py $k 22 groups >> $out 2>&1
   done
-  echo "== $lib tc" >> $out
-  DYNPAR_LIB=$lib timeout 120 python tools/prof_tc.py rmat:22:seed1 '{"threshold":64,"cfactor":4,"agg":"grid","parent_block":256,"child_block":128,"serial":"warp"}' 3 >> $out 2>&1
 done
