@@ -115,6 +115,8 @@ typedef struct dp_stats {
   uint64_t h2d_bytes;         /* bytes copied host->device in this call */
   uint64_t d2h_bytes;         /* bytes copied device->host in this call */
   uint64_t kernel_launches;   /* launches of library kernels issued from the host */
+  double launch_lat_ns_mean;  /* device launch -> first child block start
+                                 (%globaltimer), mean over device launches */
 } dp_stats;
 
 /* ---- library -------------------------------------------------------------- */

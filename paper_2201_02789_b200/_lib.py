@@ -58,7 +58,8 @@ class DpStats(ctypes.Structure):
                 ("ns_phase", ctypes.c_double * 5),
                 ("h2d_bytes", ctypes.c_uint64),
                 ("d2h_bytes", ctypes.c_uint64),
-                ("kernel_launches", ctypes.c_uint64)]
+                ("kernel_launches", ctypes.c_uint64),
+                ("launch_lat_ns_mean", ctypes.c_double)]
 
 
 class DeviceTrap(RuntimeError):

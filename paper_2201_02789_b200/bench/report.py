@@ -60,6 +60,7 @@ class Report:
     h2d_bytes: int = 0
     d2h_bytes: int = 0
     kernel_launches: int = 0
+    launch_lat_ns: float = 0.0  # mean device-launch latency (%globaltimer)
     extra: dict = field(default_factory=dict)
     _digest: str | None = field(default=None, repr=False)
     _lists: dict | None = field(default=None, repr=False)
@@ -118,4 +119,5 @@ class Report:
                    h2d_bytes=int(st["h2d_bytes"]),
                    d2h_bytes=int(st["d2h_bytes"]),
                    kernel_launches=int(st["kernel_launches"]),
+                   launch_lat_ns=float(st.get("launch_lat_ns_mean", 0.0)),
                    extra=dict(extra))

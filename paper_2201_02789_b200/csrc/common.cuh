@@ -136,7 +136,24 @@ struct DevState {
   int err;                      // first cudaError_t seen by a device launch
   int flag[2];                  // double-buffered `changed` (levels / rounds)
   int done_round;               // device loop: round count at convergence
+  unsigned long long lat_sum;   // device launch -> first child block start, ns
+  unsigned long long lat_cnt;
 };
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// first block of a device-launched child: launch latency sample
+__device__ __forceinline__ void note_child_start(DevState* ds,
+                                                 unsigned long long ts) {
+  if (ts && blockIdx.x == 0 && threadIdx.x == 0) {
+    atomicAdd(&ds->lat_sum, globaltimer_ns() - ts);
+    atomicAdd(&ds->lat_cnt, 1ull);
+  }
+}
 
 __device__ __forceinline__ void note_launch_error(DevState* ds) {
   cudaError_t e = cudaGetLastError();

@@ -462,7 +462,7 @@ glue:
     const int total = (int)(cv & 0xffffffffull);
     if (total > 0) {
       child_agg_kernel<App><<<total, c->child_block, 0, s>>>(
-          app, t.args, t.scan, np, c->cfactor);
+          app, t.args, t.scan, np, c->cfactor, w->ds, 0ull);
       DP_CUDA(cudaGetLastError());
       rc->host_launches += 1;
       rc->host_blocks += total;
@@ -539,6 +539,9 @@ void finish_stats(Workspace* w, const RunCounters& rc, float ms,
   st->ns_kernel_max = rc.ms_kernel_max * 1e6;
   st->ns_kernel_sum = rc.ms_kernel_sum * 1e6;
   st->kernel_launches = rc.kernel_launches;
+  st->launch_lat_ns_mean =
+      w->h_ds->lat_cnt ? (double)w->h_ds->lat_sum / (double)w->h_ds->lat_cnt
+                       : 0.0;
 }
 
 void clear_stats(dp_stats* st) {

@@ -99,7 +99,9 @@ __device__ __forceinline__ void run_logical_blocks(const App& app,
 
 // Plain child: BFS `visit` etc. (benchmarks.py:92-103), coarsened.
 template <class App>
-__global__ void __launch_bounds__(256, App::kMinBlocks) child_kernel(App app, typename App::Args a, int cf) {
+__global__ void __launch_bounds__(256, App::kMinBlocks) child_kernel(App app, typename App::Args a, int cf,
+                                     DevState* ds, unsigned long long ts) {
+  note_child_start(ds, ts);
   typename App::Acc acc{};
   run_logical_blocks(app, a, blockIdx.x, cf, acc);
   app.flush(acc);
@@ -128,7 +130,9 @@ __device__ __forceinline__ int warp_search(const int* __restrict__ scan, int np,
 // reused across the coarsening loop.
 template <class App>
 __global__ void __launch_bounds__(256, App::kMinBlocks) child_agg_kernel(App app, const typename App::Args* tab,
-                                 const int* scan, int np, int cf) {
+                                 const int* scan, int np, int cf,
+                                 DevState* ds, unsigned long long ts) {
+  note_child_start(ds, ts);
   __shared__ int s_lo;
   int lo = 0;
   if (threadIdx.x < 32) {
@@ -267,8 +271,8 @@ __global__ void __launch_bounds__(256, App::kMinBlocks)
 
     if constexpr (AGG == kAggNone) {
       if (gd > 0) {
-        child_kernel<App><<<gd, k.cb, 0, cudaStreamFireAndForget>>>(app, a,
-                                                                     k.cf);
+        child_kernel<App><<<gd, k.cb, 0, cudaStreamFireAndForget>>>(
+            app, a, k.cf, ds, globaltimer_ns());
         note_launch_error(ds);
       }
       count_launches_warp(ds, gd > 0, gd);
@@ -288,7 +292,8 @@ __global__ void __launch_bounds__(256, App::kMinBlocks)
         __syncwarp();
         if (lane == __ffs(m) - 1) {
           child_agg_kernel<App><<<total, k.cb, 0, cudaStreamFireAndForget>>>(
-              app, t.args + row0, t.scan + row0, __popc(m), k.cf);
+              app, t.args + row0, t.scan + row0, __popc(m), k.cf, ds,
+              globaltimer_ns());
           note_launch_error(ds);
           atomicAdd(&ds->launches, 1ull);
           atomicAdd(&ds->blocks, (unsigned long long)total);
@@ -303,7 +308,7 @@ __global__ void __launch_bounds__(256, App::kMinBlocks)
           // aggregate.py:376-392: too few participants -> direct launches
           if (gd > 0) {
             child_kernel<App><<<gd, k.cb, 0, cudaStreamFireAndForget>>>(
-                app, a, k.cf);
+                app, a, k.cf, ds, globaltimer_ns());
             note_launch_error(ds);
           }
           count_launches_warp(ds, gd > 0, gd);
@@ -318,7 +323,8 @@ __global__ void __launch_bounds__(256, App::kMinBlocks)
           if (threadIdx.x == 0) {
             child_agg_kernel<App><<<s.total, k.cb, 0,
                                     cudaStreamFireAndForget>>>(
-                app, t.args + row0, t.scan + row0, s.np, k.cf);
+                app, t.args + row0, t.scan + row0, s.np, k.cf, ds,
+                globaltimer_ns());
             note_launch_error(ds);
             atomicAdd(&ds->launches, 1ull);
             atomicAdd(&ds->blocks, (unsigned long long)s.total);
@@ -358,7 +364,8 @@ __global__ void __launch_bounds__(256, App::kMinBlocks)
               if (np > 0) {
                 child_agg_kernel<App><<<total, k.cb, 0,
                                         cudaStreamFireAndForget>>>(
-                    app, t.args + sb, t.scan + sb, np, k.cf);
+                    app, t.args + sb, t.scan + sb, np, k.cf, ds,
+                    globaltimer_ns());
                 note_launch_error(ds);
                 atomicAdd(&ds->launches, 1ull);
                 atomicAdd(&ds->blocks, (unsigned long long)total);
@@ -430,7 +437,7 @@ __global__ void __launch_bounds__(256)
         const int total = (int)(c & 0xffffffffull);
         if (np > 0) {
           child_agg_kernel<App><<<total, k.cb, 0, cudaStreamFireAndForget>>>(
-              app, t.args, t.scan, np, k.cf);
+              app, t.args, t.scan, np, k.cf, ds, globaltimer_ns());
           note_launch_error(ds);
           atomicAdd(&ds->launches, 1ull);
           atomicAdd(&ds->blocks, (unsigned long long)total);

@@ -41,7 +41,7 @@ def test_library_exports_every_declared_symbol():
 def test_struct_layouts_match_header():
     # dp_config: 16 int32; dp_stats: 7 u64 + 4 f64 + 5 f64 + 3 u64
     assert ctypes.sizeof(_lib.DpConfig) == 64
-    assert ctypes.sizeof(_lib.DpStats) == 7 * 8 + 4 * 8 + 5 * 8 + 3 * 8
+    assert ctypes.sizeof(_lib.DpStats) == 7 * 8 + 4 * 8 + 5 * 8 + 3 * 8 + 8
 
 
 def test_no_device_fails_loudly_without_gpu():

@@ -120,7 +120,8 @@ def main():
         print(f"{ms:9.3f} ms  kern {ks:9.3f}  it={runs[0]['iterations']:3d} "
               f"launches={runs[0]['num_launches']:9d} "
               f"blocks={runs[0]['blocks_scheduled']:10d} "
-              f"GTEPS={e / ms / 1e6:7.2f}  {variant} {d}", flush=True)
+              f"GTEPS={e / ms / 1e6:7.2f} lat={runs[0]['launch_lat_ns_mean']:8.0f}ns"
+              f"  {variant} {d}", flush=True)
 
 
 if __name__ == "__main__":
