@@ -20,9 +20,9 @@ cpu_baseline (the C oracle on the host cores), speed-ups over the naive-CDP
 and aggregation-only (KLAP-style) builds, and the other BASELINE workloads
 (BFS RMAT-22, TC RMAT-22, BT 25k curves) under "workloads".
 
-N > 1: the SSSP hot path has no partitioned implementation yet, so each rank
-runs an independent replica ("replicas"); TC is the
-partitioned workload (--workload tc).
+N > 1: the same SSSP over a cyclic 1D vertex partition (one part per rank,
+per-round NCCL all-to-all of improving remote relaxations; DESIGN.md §8);
+--workload bfs26 / tc run the other partitioned configs (5 / 4).
 """
 
 from __future__ import annotations
@@ -332,7 +332,9 @@ def init_dist(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1 and not torch.distributed.is_initialized():
+    launched = world > 1 or ("MASTER_ADDR" in os.environ
+                             and "RANK" in os.environ)
+    if launched and not torch.distributed.is_initialized():
         backend = "nccl" if args.impl == "ours" else "gloo"
         torch.distributed.init_process_group(backend)
     if torch.cuda.is_available():
@@ -351,8 +353,91 @@ def max_over_ranks(x: float) -> float:
     return float(t.item())
 
 
+def arm_sssp_partitioned(args, world, rank, local):
+    """N > 1: the headline SSSP over a cyclic 1D vertex partition, one part
+    per rank, per-round NCCL all-to-all of improving remote relaxations
+    (paper_2201_02789_b200/dist.py).  Same metric: E_reach / t."""
+    import torch
+    from paper_2201_02789_b200 import _lib
+    from paper_2201_02789_b200 import dist as pdist
+    from paper_2201_02789_b200.bench import graphs
+    from paper_2201_02789_b200.bench.graphs import UNREACHED
+    _lib.device()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    g = graphs.rmat_graph(SCALE, SEED)
+    w = graphs.edge_weights(g, SEED)
+    rp_p, col_p, w_p = pdist.partition_csr(g.rowptr, g.col, world, rank, w)
+    part = pdist.SsspPart(rp_p, col_p, w_p, g.n, world, rank, 0, dev)
+    ops = pdist.DeviceSsspOps(_cfg(BEST["sssp"]))
+    ex = (pdist.CollectiveExchange() if torch.distributed.is_initialized()
+          else pdist.LocalExchange())
+    stream_obj = torch.cuda.current_stream()
+
+    def step():
+        part.reset(0)
+        return pdist.sssp_1d([part], ops, ex)
+    with ClockSampler(local) as clk:
+        total_ms, outs = timed_steps(step, args.steps, args.warmup,
+                                     stream_obj)
+    dist_t, rounds = outs[-1]
+    t_max = max_over_ranks(total_ms)
+    ms_step = t_max / args.steps
+    dist_h = dist_t.cpu().numpy()
+    deg = np.diff(g.rowptr.astype(np.int64))
+    e_reach = int(deg[dist_h < UNREACHED].sum())
+    # e2e: this rank's part copied from pinned host memory every step
+    hp = [torch.from_numpy(x).pin_memory() for x in (rp_p, col_p, w_p)]
+    out_h = torch.empty(part.n_local, dtype=torch.int32).pin_memory()
+    e2e = []
+    for i in range(3):
+        torch.cuda.synchronize()
+        if torch.distributed.is_initialized():
+            torch.distributed.barrier()
+        t0 = time.perf_counter()
+        part.rowptr.copy_(hp[0], non_blocking=True)
+        part.col.copy_(hp[1], non_blocking=True)
+        part.weight.copy_(hp[2], non_blocking=True)
+        part.reset(0)
+        pdist.sssp_1d([part], ops, ex)
+        out_h.copy_(part.dist, non_blocking=True)
+        torch.cuda.synchronize()
+        if i:
+            e2e.append(time.perf_counter() - t0)
+    e2e_s = max_over_ranks(statistics.median(e2e))
+    h2d = sum(x.numel() * 4 for x in hp)
+    if rank != 0:
+        return
+    from oracle import oracle
+    want, _ = oracle.sssp(g.rowptr, g.col, w, nthreads=0)
+    print(json.dumps({
+        "metric": "GTEPS (SSSP RMAT-22, T+C+A CDP2)",
+        "value": e_reach * args.steps / (t_max * 1e-3) / 1e9,
+        "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "int32",
+        "data": "synthetic RMAT (Graph500 a,b,c=.57,.19,.19, seed 1, "
+                "edge factor 16), weights U[1,9]",
+        "config": {"workload": f"sssp rmat-{SCALE} from vertex 0",
+                   "n": g.n, "m": g.m, "e_reach": e_reach, "rounds": rounds,
+                   "policy": BEST["sssp"],
+                   "parallelism": f"1d-cyclic-partition x{world}",
+                   "l2": "inputs exceed L2; no flush"},
+        "parity": "bit-exact vs oracle" if np.array_equal(dist_h, want)
+        else "MISMATCH",
+        "e2e": {"value": e_reach / e2e_s / 1e9, "unit": "GTEPS",
+                "h2d_bytes_per_step": h2d * world,
+                "d2h_bytes_per_step": g.n * 4,
+                "ms_per_step": e2e_s * 1e3},
+        "gpu_launches": int(sum(s["kernel_launches"] + s["num_launches"]
+                                for s in part.stats)) * args.steps,
+        "clocks": clk.summary()}), flush=True)
+
+
 def arm_ours(args, world, rank, local):
     import torch
+    if world > 1 or args.partitioned:
+        return arm_sssp_partitioned(args, world, rank, local)
     from paper_2201_02789_b200 import _lib
     from oracle import oracle  # checker + cpu_baseline only
     _lib.device()
@@ -376,7 +461,7 @@ def arm_ours(args, world, rank, local):
             "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+            "scaling": "strong", "vs_baseline": None, "dtype": "int32",
             "data": "synthetic RMAT (Graph500 a,b,c=.57,.19,.19, seed 1, "
                     "edge factor 16), weights U[1,9]",
             "config": {"workload": f"sssp rmat-{SCALE} from vertex 0",
@@ -449,7 +534,8 @@ def arm_bfs26(args, world, rank, local):
     rp, col = pdist.rmat_part_device(scale, SEED, world, rank, dev)
     part = pdist.BfsPart(rp, col, 1 << scale, world, rank, 0, dev)
     del rp, col
-    ex = pdist.CollectiveExchange() if world > 1 else pdist.LocalExchange()
+    ex = (pdist.CollectiveExchange() if torch.distributed.is_initialized()
+          else pdist.LocalExchange())
     ops = pdist.DeviceBfsOps(_cfg(BEST["bfs"]))
     stream_obj = torch.cuda.current_stream()
 
@@ -565,7 +651,7 @@ def arm_reference(args, world, rank, local):
         "impl": "reference", "metric": "GTEPS (SSSP RMAT-22, T+C+A CDP2)",
         "value": value, "unit": "GTEPS", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "int32", "data": "synthetic RMAT, weights U[1,9]",
         "config": {"workload": f"sssp rmat-{SCALE} from vertex 0",
                    "n": g.n, "m": g.m, "e_reach": e_reach},
@@ -589,6 +675,9 @@ def main():
                          "the partitioned multi-GPU configs 5 / 4")
     ap.add_argument("--scale", type=int, default=0,
                     help="override the RMAT scale of bfs26 / tc")
+    ap.add_argument("--partitioned", action="store_true",
+                    help="run the headline through the 1D-partitioned path "
+                         "even at N=1 (exercises the collective code)")
     ap.add_argument("--profile", action="store_true",
                     help="warm-up + timed steps only (for ncu passes)")
     args = ap.parse_args()

@@ -184,6 +184,23 @@ int dp_bfs_part_apply(const int32_t* d_recv, int64_t nrecv, int32_t nparts,
                       int32_t level, int32_t* d_dist_p, int32_t* d_changed,
                       void* stream);
 
+/* ---- SSSP over the cyclic 1D vertex partition --------------------------- */
+/* One Bellman-Ford round on part `part`: owned dist[n_local] lowered in
+ * place; a remote relaxation (v, alt) is appended to owner(v)'s bucket as
+ * (uint64)v << 32 | alt when it strictly lowers d_best[v] (dense, global ids,
+ * UNREACHED-initialised once per SSSP).  Bucket q starts at d_send_off[q]
+ * and must hold the part's edges into owner q; d_send_counts[nparts] and
+ * d_changed are zeroed by the caller before each round. */
+int dp_sssp_part_round(const int32_t* d_rowptr_p, const int32_t* d_col_p,
+                       const int32_t* d_weight_p, int32_t n_local,
+                       int32_t nparts, int32_t part, const dp_config* cfg,
+                       int32_t* d_dist_p, int32_t* d_best, uint64_t* d_send_buf,
+                       const int64_t* d_send_off, int32_t* d_send_counts,
+                       int32_t* d_changed, void* stream, dp_stats* stats);
+/* lower owned dist by received (v << 32 | alt) pairs (atomicMin) */
+int dp_sssp_part_apply(const uint64_t* d_recv, int64_t nrecv, int32_t nparts,
+                       int32_t* d_dist_p, int32_t* d_changed, void* stream);
+
 /* ---- Bezier line tessellation (no reference) ------- */
 /* cp[ncurves][3][2] float32 control points.  Outputs: ntess[ncurves] vertex
  * counts, offsets[ncurves] start of each curve's vertices in verts, and

@@ -220,6 +220,98 @@ struct BfsPartApp {
 };
 
 // ---------------------------------------------------------------------------
+// SSSP on one part of the cyclic 1D partition.  Local relaxations lower the
+// owned dist in place; a remote relaxation (v, alt) is sent to owner(v) only
+// if it strictly improves this part's best-sent value best[v] (atomicMin),
+// so a part never re-sends a value that cannot lower dist[v].  Buckets hold
+// packed (v << 32 | alt) pairs at per-owner offsets sized by the part's
+// edges into each owner (one push per edge per round at most).
+// ---------------------------------------------------------------------------
+struct SsspPartApp {
+  const int* __restrict__ rowptr;
+  const int* __restrict__ col;
+  const int* __restrict__ weight;
+  int* dist;  // owned (local index)
+  int* best;  // dense, global ids: best value sent per remote vertex
+  unsigned long long* send_buf;
+  const long long* send_off;  // [nparts] bucket bases
+  int* send_count;            // [nparts]
+  int* changed;
+  int n_local;
+  int nparts;
+  int part;
+  int pad;
+
+  struct alignas(16) Args {
+    int start, deg, du, pad;
+  };
+  struct Acc {
+    int changed;
+  };
+
+  __device__ int nparents() const { return n_local; }
+  __device__ void parent_prologue() const {}
+  __device__ int expand(int lu, bool valid, Args& a) const {
+    if (!valid) return 0;
+    const int du = __ldcg(dist + lu);
+    if (du >= kUnreached) return 0;
+    const int s = __ldg(rowptr + lu);
+    const int d = __ldg(rowptr + lu + 1) - s;
+    a = Args{s, d, du, 0};
+    return d > 0 ? d : 0;
+  }
+  __device__ static int count(const Args& a) { return a.deg; }
+  __device__ void push(int q, int v, int alt) const {
+    const unsigned am = __activemask();
+    const unsigned grp = __match_any_sync(am, q);
+    const int leader = __ffs(grp) - 1;
+    int base = 0;
+    if (lane_id() == leader) base = atomicAdd(send_count + q, __popc(grp));
+    base = __shfl_sync(grp, base, leader);
+    send_buf[send_off[q] + base + __popc(grp & lanemask_lt())] =
+        ((unsigned long long)(unsigned)v << 32) | (unsigned)alt;
+  }
+  __device__ void relax(int v, int alt, Acc& acc) const {
+    const int q = v % nparts;
+    if (q == part) {
+      const int lv = v / nparts;
+      if (alt < __ldca(dist + lv) && atomicMin(dist + lv, alt) > alt)
+        acc.changed = 1;
+    } else if (alt < __ldca(best + v) && atomicMin(best + v, alt) > alt) {
+      push(q, v, alt);
+    }
+  }
+  __device__ void item(const Args& a, int e, Acc& acc) const {
+    relax(ld_stream(col + a.start + e),
+          (int)((unsigned)a.du + (unsigned)ld_stream(weight + a.start + e)),
+          acc);
+  }
+  static constexpr int kUnroll = DP_SSSP_UNROLL;
+  static constexpr bool kBlockMode = false;
+  static constexpr bool kPureExpand = true;
+  static constexpr int kMinBlocks = 1;
+  template <int U, class ArgsOf>
+  __device__ __forceinline__ void items(ArgsOf args, const int* e,
+                                        const bool* ok, Acc& acc) const {
+    int v[U], alt[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int i = ok[j] ? args(j).start + e[j] : 0;
+      v[j] = ok[j] ? ld_stream(col + i) : 0;
+      alt[j] = ok[j] ? (int)((unsigned)args(j).du +
+                             (unsigned)ld_stream(weight + i))
+                     : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j)
+      if (ok[j]) relax(v[j], alt[j], acc);
+  }
+  __device__ void flush(Acc& acc) const {
+    if (__any_sync(DP_FULL, acc.changed) && lane_id() == 0) *changed = 1;
+  }
+};
+
+// ---------------------------------------------------------------------------
 // SSSP — SSSP_CDP main/relax_edges/relax (bench/benchmarks.py:175-222)
 // ---------------------------------------------------------------------------
 struct SsspApp {

@@ -184,9 +184,20 @@ int effective_threshold(const dp_config* c) {
   return c->threshold > 1 ? c->threshold : 1;
 }
 
-// kind 0: CSR rowptr degrees, 1: per-parent values
-int count_launchers(Workspace* w, const int* data, int n, int kind, int thr,
-                    cudaStream_t s, long long* out) {
+long long launch_bound(const dp_config* c, long long parents,
+                       long long launchers);
+
+// kind 0: CSR rowptr degrees, 1: per-parent values.  Skipped (returns the
+// parent count) when the policy's structural bound -- warps, blocks or
+// groups -- already keeps the pool small, so aggregated runs pay no extra
+// kernel + sync for pool sizing.
+int count_launchers(Workspace* w, const dp_config* c, const int* data, int n,
+                    int kind, cudaStream_t s, long long* out) {
+  if (launch_bound(c, n, n) <= (1 << 16)) {
+    *out = n;
+    return 0;
+  }
+  const int thr = effective_threshold(c);
   DP_CUDA(cudaMemsetAsync(w->d_scratch + 1, 0, sizeof(unsigned long long), s));
   if (n > 0) {
     const int blocks = std::min(dp::ceil_div(n, 256), 148 * 8);
@@ -665,8 +676,7 @@ int bfs_dev_impl(const int32_t* rowptr, const int32_t* col, int32_t n,
   DP_CUDA(cudaMemsetAsync(counts, 0, (size_t)n * sizeof(int), s));
   long long launchers = 0;
   if (c->variant == DP_VARIANT_CDP &&
-      (r = count_launchers(w, rowptr, n, 0, effective_threshold(c), s,
-                           &launchers)))
+      (r = count_launchers(w, c, rowptr, n, 0, s, &launchers)))
     return r;
   // bench/benchmarks.py:157-168: one launch per level until nothing changes
   return iterate(w, c, n, launchers, n, s,
@@ -698,8 +708,7 @@ int sssp_dev_impl(const int32_t* rowptr, const int32_t* col,
   init_dist_kernel<<<dp::ceil_div(n, 256), 256, 0, s>>>(dist, n, src);
   long long launchers = 0;
   if (c->variant == DP_VARIANT_CDP &&
-      (r = count_launchers(w, rowptr, n, 0, effective_threshold(c), s,
-                           &launchers)))
+      (r = count_launchers(w, c, rowptr, n, 0, s, &launchers)))
     return r;
   // bench/benchmarks.py:259-270: rounds until a full round changes nothing
   return iterate(w, c, n, launchers, n, s,
@@ -758,8 +767,7 @@ int manylaunch_dev_impl(const int32_t* sizes, int32_t n, const dp_config* c,
   a.pad = 0;
   long long launchers = 0;
   if (c->variant == DP_VARIANT_CDP &&
-      (r = count_launchers(w, sizes, n, 1, effective_threshold(c), s,
-                           &launchers)))
+      (r = count_launchers(w, c, sizes, n, 1, s, &launchers)))
     return r;
   return once(w, c, a, n, launchers, s, st);
 }
@@ -785,8 +793,7 @@ int tc_dev_impl(const int32_t* rowptr, const int32_t* col, int32_t n,
   a.pad = 0;
   long long launchers = 0;
   if (c->variant == DP_VARIANT_CDP &&
-      (r = count_launchers(w, rowptr, n, 0, effective_threshold(c), s,
-                           &launchers)))
+      (r = count_launchers(w, c, rowptr, n, 0, s, &launchers)))
     return r;
   return once(w, c, a, n, launchers, s, st);
 }
@@ -860,8 +867,7 @@ int bfs_part_level_impl(const int32_t* rowptr, const int32_t* col,
   if (!w) return r;
   long long launchers = 0;
   if (c->variant == DP_VARIANT_CDP &&
-      (r = count_launchers(w, rowptr, n_local, 0, effective_threshold(c), s,
-                           &launchers)))
+      (r = count_launchers(w, c, rowptr, n_local, 0, s, &launchers)))
     return r;
   if ((r = ensure_pending_limit(w, c, launch_bound(c, n_local, launchers))))
     return r;
@@ -880,6 +886,66 @@ int bfs_part_level_impl(const int32_t* rowptr, const int32_t* col,
   a.nparts = nparts;
   a.part = part;
   a.level = level;
+  RunCounters rc;
+  DP_CUDA(cudaEventRecord(w->ev0, s));
+  if ((r = launch_parent(a, n_local, launchers, c, w, s, &rc))) return r;
+  DP_CUDA(cudaEventRecord(w->ev1, s));
+  if ((r = read_state(w, s))) return r;
+  if ((r = account_step(w, &rc))) return r;
+  float ms = 0.f;
+  DP_CUDA(cudaEventElapsedTime(&ms, w->ev0, w->ev1));
+  finish_stats(w, rc, ms, st);
+  if (st) st->iterations = 1;
+  return 0;
+}
+
+__global__ void sssp_part_apply_kernel(const unsigned long long* __restrict__ recv,
+                                       long long nrecv, int nparts, int* dist,
+                                       int* changed) {
+  int c = 0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+       i < nrecv; i += (long long)gridDim.x * blockDim.x) {
+    const unsigned long long p = __ldg(recv + i);
+    const int lv = (int)(p >> 32) / nparts;
+    const int alt = (int)(unsigned)(p & 0xffffffffull);
+    if (alt < __ldcg(dist + lv) && atomicMin(dist + lv, alt) > alt) c = 1;
+  }
+  if (__any_sync(DP_FULL, c) && lane_id() == 0) *changed = 1;
+}
+
+int sssp_part_round_impl(const int32_t* rowptr, const int32_t* col,
+                         const int32_t* weight, int32_t n_local,
+                         int32_t nparts, int32_t part, const dp_config* c,
+                         int32_t* dist, int32_t* best, uint64_t* send_buf,
+                         const int64_t* send_off, int32_t* send_count,
+                         int32_t* changed, cudaStream_t s, dp_stats* st) {
+  int r;
+  if ((r = validate(c))) return r;
+  if (nparts < 1 || part < 0 || part >= nparts || n_local < 0)
+    return fail(DP_ERR_INVALID, "bad partition arguments");
+  Workspace* w = workspace(&r);
+  if (!w) return r;
+  long long launchers = 0;
+  if (c->variant == DP_VARIANT_CDP &&
+      (r = count_launchers(w, c, rowptr, n_local, 0, s, &launchers)))
+    return r;
+  if ((r = ensure_pending_limit(w, c, launch_bound(c, n_local, launchers))))
+    return r;
+  if ((r = begin_run(w, s))) return r;
+  SsspPartApp a;
+  a.rowptr = rowptr;
+  a.col = col;
+  a.weight = weight;
+  a.dist = dist;
+  a.best = best;
+  a.send_buf = (unsigned long long*)send_buf;
+  a.send_off = (const long long*)send_off;
+  a.send_count = send_count;
+  a.changed = changed;
+  a.n_local = n_local;
+  a.nparts = nparts;
+  a.part = part;
+  a.pad = 0;
   RunCounters rc;
   DP_CUDA(cudaEventRecord(w->ev0, s));
   if ((r = launch_parent(a, n_local, launchers, c, w, s, &rc))) return r;
@@ -1150,6 +1216,34 @@ int dp_bfs_part_apply(const int32_t* d_recv, int64_t nrecv, int32_t nparts,
       (int)std::min<long long>(dp::ceil_div_ll(nrecv, 256), 148 * 16);
   bfs_part_apply_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
       d_recv, nrecv, nparts, level, d_dist_p, d_changed);
+  DP_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int dp_sssp_part_round(const int32_t* d_rowptr_p, const int32_t* d_col_p,
+                       const int32_t* d_weight_p, int32_t n_local,
+                       int32_t nparts, int32_t part, const dp_config* cfg,
+                       int32_t* d_dist_p, int32_t* d_best, uint64_t* d_send_buf,
+                       const int64_t* d_send_off, int32_t* d_send_counts,
+                       int32_t* d_changed, void* stream, dp_stats* stats) {
+  clear_stats(stats);
+  const double t0 = now_ns();
+  int r = sssp_part_round_impl(d_rowptr_p, d_col_p, d_weight_p, n_local,
+                               nparts, part, cfg, d_dist_p, d_best, d_send_buf,
+                               d_send_off, d_send_counts, d_changed,
+                               (cudaStream_t)stream, stats);
+  if (stats) stats->ns_host = now_ns() - t0;
+  return r;
+}
+
+int dp_sssp_part_apply(const uint64_t* d_recv, int64_t nrecv, int32_t nparts,
+                       int32_t* d_dist_p, int32_t* d_changed, void* stream) {
+  if (nparts < 1 || nrecv < 0) return fail(DP_ERR_INVALID, "bad arguments");
+  if (nrecv == 0) return 0;
+  const int blocks =
+      (int)std::min<long long>(dp::ceil_div_ll(nrecv, 256), 148 * 16);
+  sssp_part_apply_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
+      (const unsigned long long*)d_recv, nrecv, nparts, d_dist_p, d_changed);
   DP_CUDA(cudaGetLastError());
   return 0;
 }

@@ -304,7 +304,7 @@ class CollectiveExchange:
         send_splits = sc.tolist()
         recv_splits = rc.tolist()
         packed = torch.cat([p.bucket(q, c) for q, c in enumerate(send_splits)])
-        recv = torch.empty(sum(recv_splits), dtype=torch.int32,
+        recv = torch.empty(sum(recv_splits), dtype=p.send_buf.dtype,
                            device=p.send_buf.device)
         dist.all_to_all_single(recv, packed, recv_splits, send_splits)
         return [recv]
@@ -407,8 +407,9 @@ def rmat_part_device(scale: int, seed: int, nparts: int, part: int, device,
 
 
 def partition_csr(rowptr: np.ndarray, col: np.ndarray, nparts: int,
-                  part: int):
-    """Rows of an in-memory CSR owned by `part` (owner(v) = v % nparts)."""
+                  part: int, weight: np.ndarray | None = None):
+    """Rows of an in-memory CSR owned by `part` (owner(v) = v % nparts):
+    (rowptr_p, col_p) or, with `weight`, (rowptr_p, col_p, weight_p)."""
     rp = rowptr.astype(np.int64)
     own = np.arange(part, rp.shape[0] - 1, nparts)
     deg = rp[own + 1] - rp[own]
@@ -416,4 +417,102 @@ def partition_csr(rowptr: np.ndarray, col: np.ndarray, nparts: int,
     idx = (np.repeat(rp[own], deg)
            + np.arange(int(deg.sum())) - np.repeat(lrp[:-1].astype(np.int64),
                                                    deg))
-    return lrp, col[idx].astype(np.int32)
+    if weight is None:
+        return lrp, col[idx].astype(np.int32)
+    return lrp, col[idx].astype(np.int32), weight[idx].astype(np.int32)
+
+
+# ---------------------------------------------------------------------------
+# SSSP over the same 1D partition (SURVEY §8(e) row SSSP): per round each part
+# relaxes its reached vertices' edges (dp_sssp_part_round); remote
+# relaxations that strictly improve the part's best-sent value go to the
+# owner as packed (v << 32 | alt) pairs, owners apply them with atomicMin
+# (dp_sssp_part_apply); rounds end when no part changed anything.  dist is
+# the exact shortest-path vector, identical to the single-GPU run.
+# ---------------------------------------------------------------------------
+
+class SsspPart:
+    """One part's device state for the partitioned SSSP."""
+
+    def __init__(self, rowptr, col, weight, n_global: int, nparts: int,
+                 part: int, src: int, device):
+        import torch
+        self.nparts, self.part, self.n = nparts, part, n_global
+        self.rowptr = torch.as_tensor(rowptr).to(device=device,
+                                                  dtype=torch.int32)
+        self.col = torch.as_tensor(col).to(device=device, dtype=torch.int32)
+        self.weight = torch.as_tensor(weight).to(device=device,
+                                                  dtype=torch.int32)
+        self.n_local = int(self.rowptr.shape[0]) - 1
+        i32 = dict(dtype=torch.int32, device=device)
+        self.dist = torch.empty(self.n_local, **i32)
+        self.best = torch.empty(n_global, **i32)
+        # bucket q holds at most this part's edges into owner q per round
+        owners = torch.remainder(self.col.to(torch.int64), nparts)
+        cap = torch.bincount(owners, minlength=nparts).cpu()
+        cap[part] = 0
+        self.cap = cap.tolist()
+        off = np.concatenate(([0], np.cumsum(self.cap)[:-1]))
+        self.off_list = [int(x) for x in off]
+        self.send_off = torch.as_tensor(off, dtype=torch.int64, device=device)
+        self.send_buf = torch.empty(max(1, int(sum(self.cap))),
+                                    dtype=torch.int64, device=device)
+        self.send_counts = torch.zeros(nparts, **i32)
+        self.changed = torch.zeros(1, **i32)
+        self.stats: list[dict] = []
+        self.reset(src)
+
+    def reset(self, src: int) -> None:
+        self.dist.fill_(1 << 30)
+        if src % self.nparts == self.part:
+            self.dist[src // self.nparts] = 0
+        self.best.fill_(1 << 30)
+        self.stats = []
+
+    def bucket(self, q: int, count: int):
+        return self.send_buf[self.off_list[q]:self.off_list[q] + count]
+
+
+class DeviceSsspOps:
+    """The per-part SSSP steps on the local GPU through the C-ABI."""
+
+    def __init__(self, cfg, stream=None):
+        from . import _lib
+        self.cfg = cfg
+        self.stream = stream
+        self.lib = _lib.device()
+
+    def level(self, p: SsspPart, rnd: int) -> None:
+        from . import _lib
+        p.send_counts.zero_()
+        p.changed.zero_()
+        st = _lib.DpStats()
+        _lib.check(self.lib.dp_sssp_part_round(
+            p.rowptr.data_ptr(), p.col.data_ptr(), p.weight.data_ptr(),
+            p.n_local, p.nparts, p.part, ctypes.byref(self.cfg),
+            p.dist.data_ptr(), p.best.data_ptr(), p.send_buf.data_ptr(),
+            p.send_off.data_ptr(), p.send_counts.data_ptr(),
+            p.changed.data_ptr(), self.stream, ctypes.byref(st)))
+        p.stats.append(_lib.stats_dict(st))
+
+    def apply(self, p: SsspPart, recv, rnd: int) -> None:
+        from . import _lib
+        if recv.numel():
+            _lib.check(self.lib.dp_sssp_part_apply(
+                recv.data_ptr(), recv.numel(), p.nparts, p.dist.data_ptr(),
+                p.changed.data_ptr(), self.stream))
+
+
+def sssp_1d(parts: list, ops, exchange, max_rounds: int | None = None):
+    """Bellman-Ford rounds over the given parts.  Returns (dist, rounds)."""
+    n = parts[0].n
+    limit = n + 1 if max_rounds is None else max_rounds
+    for rnd in range(limit):
+        for p in parts:
+            ops.level(p, rnd)
+        recv = exchange.all_to_all(parts)
+        for p, r in zip(parts, recv):
+            ops.apply(p, r, rnd)
+        if not exchange.any_changed(parts):
+            return exchange.dist(parts), rnd + 1
+    raise RuntimeError("sssp used more rounds than vertices")

@@ -185,3 +185,70 @@ def test_rmat_part_matches_partitioned_csr():
             b = pdist.partition_csr(g.rowptr, g.col, P, p)
             np.testing.assert_array_equal(a[0], b[0])
             np.testing.assert_array_equal(a[1], b[1])
+
+
+class NumpySsspOps:
+    """Same contract as dist.DeviceSsspOps, on CPU tensors."""
+
+    def level(self, p, rnd):
+        p.send_counts.zero_()
+        p.changed.zero_()
+        rp, col, w = p.rowptr.numpy(), p.col.numpy(), p.weight.numpy()
+        dist, best = p.dist.numpy(), p.best.numpy()
+        buf, sc = p.send_buf.numpy(), p.send_counts.numpy()
+        P, me = p.nparts, p.part
+        for lu in np.flatnonzero(dist < 1 << 30):
+            du = int(dist[lu])
+            for e in range(rp[lu], rp[lu + 1]):
+                v, alt = int(col[e]), du + int(w[e])
+                if v % P == me:
+                    if alt < dist[v // P]:
+                        dist[v // P] = alt
+                        p.changed[0] = 1
+                elif alt < best[v]:
+                    best[v] = alt
+                    q = v % P
+                    buf[p.off_list[q] + sc[q]] = (v << 32) | alt
+                    sc[q] += 1
+
+    def apply(self, p, recv, rnd):
+        dist = p.dist.numpy()
+        for x in recv.tolist():
+            v, alt = x >> 32, x & 0xFFFFFFFF
+            if alt < dist[v // p.nparts]:
+                dist[v // p.nparts] = alt
+                p.changed[0] = 1
+
+
+def _sssp_parts(g, w, P, device="cpu"):
+    return [pdist.SsspPart(*pdist.partition_csr(g.rowptr, g.col, P, p, w),
+                           g.n, P, p, 0, device) for p in range(P)]
+
+
+@pytest.mark.parametrize("P", [1, 2, 3])
+def test_sssp_1d_local_exchange_numpy(P):
+    from oracle import oracle
+    from paper_2201_02789_b200.bench import graphs
+    g = graphs.rmat_graph(8, 3)
+    w = graphs.edge_weights(g, 3)
+    d, rounds = pdist.sssp_1d(_sssp_parts(g, w, P), NumpySsspOps(),
+                              pdist.LocalExchange())
+    want, _ = oracle.sssp(g.rowptr, g.col, w)
+    np.testing.assert_array_equal(d.numpy(), want)
+
+
+def _sssp_collective_job():
+    from oracle import oracle
+    from paper_2201_02789_b200.bench import graphs
+    g = graphs.rmat_graph(9, 5)
+    w = graphs.edge_weights(g, 5)
+    P, me = dist.get_world_size(), dist.get_rank()
+    part = pdist.SsspPart(*pdist.partition_csr(g.rowptr, g.col, P, me, w),
+                          g.n, P, me, 0, "cpu")
+    d, _ = pdist.sssp_1d([part], NumpySsspOps(), pdist.CollectiveExchange())
+    want, _ = oracle.sssp(g.rowptr, g.col, w)
+    return bool(np.array_equal(d.numpy(), want))
+
+
+def test_sssp_1d_two_ranks_gloo():
+    assert _run(2, _sssp_collective_job) == [True, True]

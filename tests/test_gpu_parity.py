@@ -474,3 +474,28 @@ def test_device_loop_many_levels(policy, golden):
             assert rep.iterations == ref["host_launches"] > 16
             assert rep.host_launches == -(-rep.iterations // 16) or \
                 rep.host_launches == -(-(rep.iterations + 1) // 16)
+
+
+@pytest.mark.parametrize("P", [1, 2, 4])
+@pytest.mark.parametrize("policy", [
+    dict(threshold=128, agg="block"),
+    dict(threshold=1024, cfactor=32, agg="multiblock", group_size=2048,
+         parent_block=128, child_block=64, serial="warp"),
+    dict()])
+def test_sssp_1d_partition_on_device(P, policy):
+    import torch
+    from paper_2201_02789_b200 import dist as pdist
+    g = graphs.rmat_graph(16, 2)
+    w = graphs.edge_weights(g, 2)
+    want, _ = oracle.sssp(g.rowptr, g.col, w, nthreads=0)
+    parts = [pdist.SsspPart(*pdist.partition_csr(g.rowptr, g.col, P, p, w),
+                            g.n, P, p, 0, torch.device("cuda", 0))
+             for p in range(P)]
+    ops = pdist.DeviceSsspOps(BenchConfig(**policy).to_c())
+    d, rounds = pdist.sssp_1d(parts, ops, pdist.LocalExchange())
+    np.testing.assert_array_equal(d.cpu().numpy(), want)
+    # a second run on the same parts after reset gives the same answer
+    for p in parts:
+        p.reset(0)
+    d2, _ = pdist.sssp_1d(parts, ops, pdist.LocalExchange())
+    np.testing.assert_array_equal(d2.cpu().numpy(), want)
