@@ -117,7 +117,11 @@ struct BfsApp {
     }
   }
   __device__ void flush(Acc& acc) const {
-    if (__any_sync(DP_FULL, acc.changed) && lane_id() == 0) *changed = 1;
+    // read before write: after the first success the flag line is only
+    // read (shared), not re-written by every succeeding warp
+    if (__any_sync(DP_FULL, acc.changed) && lane_id() == 0 &&
+        __ldcg(changed) == 0)
+      *changed = 1;
   }
 };
 
@@ -215,7 +219,11 @@ struct BfsPartApp {
       if (ok[j]) update(v[j], d[j], args(j).level, acc);
   }
   __device__ void flush(Acc& acc) const {
-    if (__any_sync(DP_FULL, acc.changed) && lane_id() == 0) *changed = 1;
+    // read before write: after the first success the flag line is only
+    // read (shared), not re-written by every succeeding warp
+    if (__any_sync(DP_FULL, acc.changed) && lane_id() == 0 &&
+        __ldcg(changed) == 0)
+      *changed = 1;
   }
 };
 
@@ -307,7 +315,11 @@ struct SsspPartApp {
       if (ok[j]) relax(v[j], alt[j], acc);
   }
   __device__ void flush(Acc& acc) const {
-    if (__any_sync(DP_FULL, acc.changed) && lane_id() == 0) *changed = 1;
+    // read before write: after the first success the flag line is only
+    // read (shared), not re-written by every succeeding warp
+    if (__any_sync(DP_FULL, acc.changed) && lane_id() == 0 &&
+        __ldcg(changed) == 0)
+      *changed = 1;
   }
 };
 
@@ -389,7 +401,11 @@ struct SsspApp {
         acc.changed = 1;
   }
   __device__ void flush(Acc& acc) const {
-    if (__any_sync(DP_FULL, acc.changed) && lane_id() == 0) *changed = 1;
+    // read before write: after the first success the flag line is only
+    // read (shared), not re-written by every succeeding warp
+    if (__any_sync(DP_FULL, acc.changed) && lane_id() == 0 &&
+        __ldcg(changed) == 0)
+      *changed = 1;
   }
 };
 
