@@ -23,6 +23,9 @@ namespace dp {
 #ifndef DP_GRAPH_UNROLL
 #define DP_GRAPH_UNROLL 4
 #endif
+#ifndef DP_MERGE_COUNTS
+#define DP_MERGE_COUNTS 1
+#endif
 #ifndef DP_SSSP_UNROLL
 #define DP_SSSP_UNROLL 2
 #endif
@@ -90,6 +93,17 @@ struct BfsApp {
         atomicCAS(dist + v, kUnreached, a.level + 1) == kUnreached)
       acc.changed = 1;
   }
+  // counts[v] += 1 with lanes that hit the same v merged into one atomic:
+  // RMAT hub destinations otherwise serialise at one L2 slice
+  __device__ __forceinline__ void count_edge(int v) const {
+#if DP_MERGE_COUNTS
+    const unsigned am = __activemask();
+    const unsigned grp = __match_any_sync(am, v);
+    if (lane_id() == __ffs(grp) - 1) atomicAdd(counts + v, __popc(grp));
+#else
+    atomicAdd(counts + v, 1);
+#endif
+  }
   static constexpr int kUnroll = DP_GRAPH_UNROLL;
   static constexpr bool kBlockMode = false;
   static constexpr bool kPureExpand = true;
@@ -110,7 +124,7 @@ struct BfsApp {
 #pragma unroll
     for (int j = 0; j < U; ++j) {
       if (!ok[j]) continue;
-      atomicAdd(counts + v[j], 1);
+      count_edge(v[j]);
       if (d[j] == kUnreached &&
           atomicCAS(dist + v[j], kUnreached, args(j).level + 1) == kUnreached)
         acc.changed = 1;
