@@ -123,7 +123,9 @@ typedef struct dp_stats {
 int dp_abi_version(void);
 const char* dp_last_error(void);
 int dp_device_count(void);
-/* nonzero when the library was built for sm_100a and a device is usable */
+/* Select `device` (sm_100) for every later call from any host thread (one
+ * device per process: the library's CUDA runtime is linked statically, so
+ * its current device is independent of the caller's).  0 on success. */
 int dp_init(int32_t device);
 
 /* ---- BFS (benchmarks.py:91-168) ------------------------------------------ */

@@ -62,7 +62,18 @@ struct Workspace {
 
 Workspace g_ws[64];
 
+// The device chosen by dp_init.  libdynpar links the CUDA runtime statically,
+// so its current device is independent of the caller's runtime (e.g.
+// PyTorch's) and per host thread: every entry point re-selects it.
+int g_device = -1;
+
 int current_device(int* dev) {
+  if (g_device >= 0) {
+    cudaError_t e = cudaSetDevice(g_device);
+    if (e != cudaSuccess)
+      return fail(DP_ERR_NO_DEVICE, std::string("cudaSetDevice: ") +
+                                        cudaGetErrorString(e));
+  }
   cudaError_t e = cudaGetDevice(dev);
   if (e != cudaSuccess)
     return fail(DP_ERR_NO_DEVICE, std::string("no CUDA device: ") +
@@ -419,8 +430,9 @@ int launch_wave(const App& app, long long base, long long nparents,
       (c->agg == DP_AGG_MULTIBLOCK && (long long)c->group_size >= grid);
   if constexpr (App::kPureExpand) {
     if (cdp && c->persistent > 0 && single_group) {
-      int sms = 148;
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+      int sms = 148, dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       const long long pgrid =
           std::min<long long>(grid, (long long)sms * c->persistent);
       if (c->agg == DP_AGG_GRID)
@@ -1051,6 +1063,7 @@ int dp_init(int32_t device) {
   if (n <= 0) return fail(DP_ERR_NO_DEVICE, "no CUDA device visible");
   if (device < 0 || device >= n) return fail(DP_ERR_INVALID, "bad device");
   DP_CUDA(cudaSetDevice(device));
+  g_device = device;
   cudaDeviceProp p;
   DP_CUDA(cudaGetDeviceProperties(&p, device));
   if (p.major != 10)
