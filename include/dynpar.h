@@ -166,6 +166,16 @@ int dp_tc_dev(const int32_t* d_rowptr, const int32_t* d_col, int32_t n,
               const dp_config* cfg, uint64_t* d_triangles, void* stream,
               dp_stats* stats);
 
+/* ---- graph colouring (north-star app, no reference) -------- */
+/* Jones-Plassmann with priority key(v) = (hash32(v), v) over a symmetric
+ * simple CSR (dp_symmetrize): color[n] equals the sequential greedy colouring
+ * in decreasing priority order.  stats->iterations = rounds. */
+int dp_gc(const int32_t* rowptr, const int32_t* col, int32_t n, int64_t m,
+          const dp_config* cfg, int32_t* color, dp_stats* stats);
+int dp_gc_dev(const int32_t* d_rowptr, const int32_t* d_col, int32_t n,
+              int64_t m, const dp_config* cfg, int32_t* d_color, void* stream,
+              dp_stats* stats);
+
 /* ---- BFS over a cyclic 1D vertex partition ------- */
 /* One level on part `part` of `nparts` (owner(v) = v % nparts; local index
  * v / nparts).  d_rowptr_p/d_col_p: the part's rows (dp_rmat_csr_part),
@@ -244,6 +254,10 @@ int dp_rmat_part_keys_dev(int32_t scale, int32_t edge_factor, uint64_t seed,
 int dp_tc_orient(const int32_t* rowptr, const int32_t* col, int32_t n,
                  int32_t** rowptr_plus, int32_t** col_plus, int64_t* m_plus,
                  int32_t nthreads);
+/* symmetrise, drop self-loops and duplicates (both directions kept). */
+int dp_symmetrize(const int32_t* rowptr, const int32_t* col, int32_t n,
+                  int32_t** rowptr_s, int32_t** col_s, int64_t* m_s,
+                  int32_t nthreads);
 void dp_free(void* p);
 
 #ifdef __cplusplus

@@ -15,6 +15,7 @@
  * reference):
  *   oracle_tc          exact triangle count over a degree-oriented CSR+
  *   oracle_bt          Bezier tessellation, fp64 vertices, fp32 counts
+ *   oracle_gc          greedy colouring in Jones-Plassmann priority order
  *
  * Parallel versions (nthreads > 1) use the same atomics the reference's
  * kernels use; outputs are schedule-invariant (benchmarks.py:10-15), so any
@@ -189,4 +190,59 @@ int64_t oracle_bt(const float* cp, int32_t ncurves, int32_t max_tess,
     }
   }
   return acc;
+}
+
+/* ---- graph colouring (north-star app; no reference implementation) ------
+ * Sequential greedy colouring in decreasing priority key(v) = (hash32(v), v):
+ * each vertex takes the smallest colour unused by its already-coloured (=
+ * higher-priority) neighbours.  Independent restatement of what the
+ * Jones-Plassmann rounds on the device must produce. */
+static uint64_t gc_key(int32_t v) {
+  uint32_t x = (uint32_t)v * 0x9E3779B1u;
+  x ^= x >> 16;
+  x *= 0x85EBCA6Bu;
+  x ^= x >> 13;
+  x *= 0xC2B2AE35u;
+  x ^= x >> 16;
+  return ((uint64_t)x << 32) | (uint32_t)v;
+}
+
+static int gc_cmp_desc(const void* a, const void* b) {
+  const uint64_t ka = *(const uint64_t*)a, kb = *(const uint64_t*)b;
+  return ka < kb ? 1 : (ka > kb ? -1 : 0);
+}
+
+/* returns the number of colours used, or -1 on allocation failure */
+int32_t oracle_gc(const int32_t* rowptr, const int32_t* col, int32_t n,
+                  int32_t* color) {
+  uint64_t* keys = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)(n ? n : 1));
+  int32_t maxdeg = 0;
+  for (int32_t u = 0; u < n; ++u) {
+    keys[u] = gc_key(u);
+    color[u] = -1;
+    if (rowptr[u + 1] - rowptr[u] > maxdeg) maxdeg = rowptr[u + 1] - rowptr[u];
+  }
+  int32_t* stamp = (int32_t*)calloc((size_t)maxdeg + 2, sizeof(int32_t));
+  if (!keys || !stamp) {
+    free(keys);
+    free(stamp);
+    return -1;
+  }
+  qsort(keys, (size_t)n, sizeof(uint64_t), gc_cmp_desc);
+  int32_t ncolors = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    const int32_t u = (int32_t)(keys[i] & 0xffffffffu);
+    const int32_t deg = rowptr[u + 1] - rowptr[u];
+    for (int32_t e = rowptr[u]; e < rowptr[u + 1]; ++e) {
+      const int32_t c = color[col[e]];
+      if (c >= 0 && c <= deg) stamp[c] = i + 1;
+    }
+    int32_t c = 0;
+    while (stamp[c] == i + 1) ++c;
+    color[u] = c;
+    if (c + 1 > ncolors) ncolors = c + 1;
+  }
+  free(keys);
+  free(stamp);
+  return ncolors;
 }

@@ -119,6 +119,11 @@ _SIGNATURES = {
     "dp_tc_orient": ([_P, _P, _I32, ctypes.POINTER(ctypes.c_void_p),
                       ctypes.POINTER(ctypes.c_void_p),
                       ctypes.POINTER(ctypes.c_int64), _I32], ctypes.c_int),
+    "dp_gc": ([_P, _P, _I32, _I64, _CFG, _P, _ST], ctypes.c_int),
+    "dp_gc_dev": ([_P, _P, _I32, _I64, _CFG, _P, _P, _ST], ctypes.c_int),
+    "dp_symmetrize": ([_P, _P, _I32, ctypes.POINTER(ctypes.c_void_p),
+                       ctypes.POINTER(ctypes.c_void_p),
+                       ctypes.POINTER(ctypes.c_int64), _I32], ctypes.c_int),
     "dp_free": ([_P], None),
 }
 

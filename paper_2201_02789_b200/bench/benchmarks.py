@@ -29,7 +29,7 @@ import numpy as np
 from .. import _lib
 from .graphs import (BT_CURV_SCALE, BT_MAX_TESS, UNREACHED, DatasetSpec,
                      bezier_curves, child_sizes, edge_weights, make_graph,
-                     parse_spec, tc_orient)
+                     parse_spec, symmetrize, tc_orient)
 
 BLOCK = 32  # parent block size of every reference driver (benchmarks.py:44)
 
@@ -212,6 +212,34 @@ def _tc_traffic(wl, out, st):
 
 
 # ---------------------------------------------------------------------------
+# gc (graph colouring; north-star app without reference code)
+# ---------------------------------------------------------------------------
+
+def _gc_prepare(spec: DatasetSpec) -> Workload:
+    g = symmetrize(make_graph(spec))
+    return Workload(spec=spec, n=g.n, payload=g, buffers={
+        "rowptr": _c32(g.rowptr), "col": _c32(g.col),
+        "color": np.full(g.n, -1, dtype=np.int32)})
+
+
+def _gc_run(wl: Workload, cfg: _lib.DpConfig):
+    lib = _lib.device()
+    b = wl.buffers
+    color = np.empty(max(wl.n, 1), dtype=np.int32)
+    st = _call(lib.dp_gc, _lib.ptr(b["rowptr"]), _lib.ptr(b["col"]), wl.n,
+               b["col"].shape[0], ctypes.byref(cfg), _lib.ptr(color))
+    return {"color": color[:wl.n]}, st
+
+
+def _gc_traffic(wl, out, st):
+    """per round: every uncoloured vertex scans its neighbours' colours (the
+    max test) -> bound by rounds x (8 n + 8 m); reported as 4 B col + 4 B
+    colour per scanned edge on the first round + 8 B per vertex per round"""
+    m = int(wl.buffers["col"].shape[0])
+    return wl.n, 8 * m + 8 * wl.n * int(st["iterations"])
+
+
+# ---------------------------------------------------------------------------
 # bt
 # ---------------------------------------------------------------------------
 
@@ -280,6 +308,9 @@ BENCHMARKS: dict[str, Benchmark] = {
                             "launch congestion (benchmarks.py:277-332)"),
     "tc": Benchmark("tc", ("triangles",), {"triangles": "long"}, _tc_prepare,
                     _tc_run, _tc_traffic, "triangle counting (new)"),
+    "gc": Benchmark("gc", ("color",), {"color": "int"}, _gc_prepare,
+                    _gc_run, _gc_traffic,
+                    "Jones-Plassmann graph colouring (new)"),
     "bt": Benchmark("bt", ("ntess", "verts"), {"ntess": "int",
                                                "verts": "float"},
                     _bt_prepare, _bt_run, _bt_traffic,

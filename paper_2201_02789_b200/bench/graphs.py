@@ -232,6 +232,31 @@ def tc_orient(graph: Graph) -> Graph:
     return Graph(rowptr, col)
 
 
+def symmetrize(graph: Graph) -> Graph:
+    """Undirected simple graph: both directions of every non-loop edge,
+    duplicates dropped, rows ascending (graph colouring input)."""
+    from .. import _lib
+    import ctypes
+    lib = _lib.load()
+    rp = ctypes.c_void_p()
+    cp = ctypes.c_void_p()
+    mp = ctypes.c_int64()
+    _lib.check(lib.dp_symmetrize(_lib.ptr(graph.rowptr), _lib.ptr(graph.col),
+                                 graph.n, ctypes.byref(rp), ctypes.byref(cp),
+                                 ctypes.byref(mp), 0))
+    try:
+        n, m = graph.n, mp.value
+        rowptr = np.ctypeslib.as_array(
+            ctypes.cast(rp, ctypes.POINTER(ctypes.c_int32)), (n + 1,)).copy()
+        col = (np.ctypeslib.as_array(
+            ctypes.cast(cp, ctypes.POINTER(ctypes.c_int32)), (m,)).copy()
+            if m else np.zeros(0, dtype=np.int32))
+    finally:
+        lib.dp_free(rp)
+        lib.dp_free(cp)
+    return Graph(rowptr, col)
+
+
 # ---------------------------------------------------------------------------
 # Bezier tessellation input
 # ---------------------------------------------------------------------------

@@ -471,6 +471,111 @@ struct ManyLaunchApp {
 };
 
 // ---------------------------------------------------------------------------
+// Graph coloring (north-star app; no reference implementation).  Jones-
+// Plassmann with a deterministic priority key(v) = (hash(v), v): a vertex is
+// coloured in the round in which it outranks all its uncoloured neighbours,
+// with the smallest colour unused by its (then all coloured) higher-priority
+// neighbours — exactly the sequential greedy colouring in priority order,
+// whatever the schedule.  Per round: GcMaxApp (parent = uncoloured vertex,
+// child item = neighbour: "does it outrank me and is it still uncoloured?"),
+// GcGatherApp (parents that are local maxima mark their neighbours' colours
+// in a deg+1-bit bitmap at bit offset rowptr[u] + u), then a flat mex pass.
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ unsigned long long gc_key(int v) {
+  unsigned x = (unsigned)v * 0x9E3779B1u;
+  x ^= x >> 16;
+  x *= 0x85EBCA6Bu;
+  x ^= x >> 13;
+  x *= 0xC2B2AE35u;
+  x ^= x >> 16;
+  return ((unsigned long long)x << 32) | (unsigned)v;
+}
+
+struct GcMaxApp {
+  const int* __restrict__ rowptr;
+  const int* __restrict__ col;
+  const int* color;  // -1: uncoloured
+  int* notmax;       // set when an uncoloured neighbour outranks the vertex
+  int n;
+  int pad;
+
+  struct alignas(16) Args {
+    int start, deg, u, pad;
+  };
+  struct Acc {};
+
+  __device__ int nparents() const { return n; }
+  __device__ void parent_prologue() const {}
+  __device__ int expand(int u, bool valid, Args& a) const {
+    if (!valid || __ldcg(color + u) >= 0) return 0;
+    const int s = __ldg(rowptr + u);
+    const int d = __ldg(rowptr + u + 1) - s;
+    a = Args{s, d, u, 0};
+    return d > 0 ? d : 0;
+  }
+  __device__ static int count(const Args& a) { return a.deg; }
+  __device__ void item(const Args& a, int e, Acc&) const {
+    const int w = ld_stream(col + a.start + e);
+    if (__ldcg(color + w) < 0 && gc_key(w) > gc_key(a.u) &&
+        __ldcg(notmax + a.u) == 0)
+      notmax[a.u] = 1;
+  }
+  static constexpr int kUnroll = 1;
+  static constexpr bool kBlockMode = false;
+  static constexpr bool kPureExpand = true;
+  static constexpr int kMinBlocks = 1;
+  template <int U, class ArgsOf>
+  __device__ __forceinline__ void items(ArgsOf args, const int* e,
+                                        const bool* ok, Acc& acc) const {
+    items_loop<U>(*this, args, e, ok, acc);
+  }
+  __device__ void flush(Acc&) const {}
+};
+
+struct GcGatherApp {
+  const int* __restrict__ rowptr;
+  const int* __restrict__ col;
+  const int* color;
+  const int* notmax;
+  unsigned* used;  // bit rowptr[u] + u + c: colour c taken by a neighbour
+  int n;
+  int pad;
+
+  struct alignas(16) Args {
+    int start, deg, u, pad;
+  };
+  struct Acc {};
+
+  __device__ int nparents() const { return n; }
+  __device__ void parent_prologue() const {}
+  __device__ int expand(int u, bool valid, Args& a) const {
+    if (!valid || __ldcg(color + u) >= 0 || __ldcg(notmax + u)) return 0;
+    const int s = __ldg(rowptr + u);
+    const int d = __ldg(rowptr + u + 1) - s;
+    a = Args{s, d, u, 0};
+    return d > 0 ? d : 0;
+  }
+  __device__ static int count(const Args& a) { return a.deg; }
+  __device__ void item(const Args& a, int e, Acc&) const {
+    const int c = __ldcg(color + ld_stream(col + a.start + e));
+    if (c >= 0 && c <= a.deg) {
+      const long long bit = (long long)a.start + a.u + c;
+      atomicOr(used + (bit >> 5), 1u << (bit & 31));
+    }
+  }
+  static constexpr int kUnroll = 1;
+  static constexpr bool kBlockMode = false;
+  static constexpr bool kPureExpand = true;
+  static constexpr int kMinBlocks = 1;
+  template <int U, class ArgsOf>
+  __device__ __forceinline__ void items(ArgsOf args, const int* e,
+                                        const bool* ok, Acc& acc) const {
+    items_loop<U>(*this, args, e, ok, acc);
+  }
+  __device__ void flush(Acc&) const {}
+};
+
+// ---------------------------------------------------------------------------
 // Triangle counting (no reference implementation)
 //   parent = vertex u of the degree-oriented CSR+, child item = one oriented
 //   edge (u, v) in [edge_lo, edge_hi), work = |N+(u) ∩ N+(v)|.

@@ -739,6 +739,117 @@ int sssp_dev_impl(const int32_t* rowptr, const int32_t* col,
                  st);
 }
 
+// mex pass of a colouring round: local maxima take the smallest colour not
+// marked in their bitmap [rowptr[u] + u, rowptr[u] + u + deg]; the others
+// clear their notmax flag for the next round.  Counts vertices coloured.
+__global__ void gc_finalize_kernel(const int* __restrict__ rowptr, int n,
+                                   int* color, int* notmax,
+                                   const unsigned* __restrict__ used,
+                                   unsigned long long* colored) {
+  unsigned long long c = 0;
+  for (long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x; u < n;
+       u += (long long)gridDim.x * blockDim.x) {
+    if (color[u] >= 0) continue;
+    if (notmax[u]) {
+      notmax[u] = 0;
+      continue;
+    }
+    const long long b0 = (long long)rowptr[u] + u;
+    const long long b1 = (long long)rowptr[u + 1] + u + 1;  // deg + 1 bits
+    long long bit = b0;
+    int mex = -1;
+    while (bit < b1) {
+      const long long wi = bit >> 5;
+      unsigned free_bits = ~__ldcg(used + wi);
+      free_bits &= ~0u << (bit & 31);  // bits before the range
+      const long long wend = (wi + 1) << 5;
+      if (wend > b1) free_bits &= (1u << (b1 & 31)) - 1;  // bits after
+      if (free_bits) {
+        mex = (int)((wi << 5) + __ffs(free_bits) - 1 - b0);
+        break;
+      }
+      bit = wend;
+    }
+    color[u] = mex;  // always found: deg neighbours use at most deg colours
+    ++c;
+  }
+  c = warp_sum_u64(c);
+  if (lane_id() == 0 && c) atomicAdd(colored, c);
+}
+
+int gc_dev_impl(const int32_t* rowptr, const int32_t* col, int32_t n,
+                int64_t m, const dp_config* c, int32_t* color,
+                cudaStream_t s, dp_stats* st) {
+  int r;
+  if ((r = validate(c))) return r;
+  if (n < 0 || m < 0) return fail(DP_ERR_INVALID, "bad graph size");
+  Workspace* w = workspace(&r);
+  if (!w) return r;
+  const size_t words = (size_t)((m + n + 31) / 32) + 1;
+  if ((r = grow(&w->io[5], &w->io_bytes[5],
+                words * sizeof(unsigned) + (size_t)n * sizeof(int))))
+    return r;
+  unsigned* used = (unsigned*)w->io[5];
+  int* notmax = (int*)(used + words);
+  DP_CUDA(cudaMemsetAsync(used, 0, words * sizeof(unsigned), s));
+  DP_CUDA(cudaMemsetAsync(notmax, 0, (size_t)n * sizeof(int), s));
+  if (n) DP_CUDA(cudaMemsetAsync(color, 0xff, (size_t)n * sizeof(int), s));
+  long long launchers = 0;
+  if (c->variant == DP_VARIANT_CDP &&
+      (r = count_launchers(w, c, rowptr, n, 0, s, &launchers)))
+    return r;
+  if ((r = ensure_pending_limit(w, c, launch_bound(c, n, launchers))))
+    return r;
+  if ((r = begin_run(w, s))) return r;
+  RunCounters rc;
+  DP_CUDA(cudaEventRecord(w->ev0, s));
+  long long remaining = n;
+  int rounds = 0;
+  const int fin_blocks = std::max(1, std::min(dp::ceil_div(n, 256), 148 * 8));
+  while (remaining > 0) {
+    GcMaxApp a0;
+    a0.rowptr = rowptr;
+    a0.col = col;
+    a0.color = color;
+    a0.notmax = notmax;
+    a0.n = n;
+    a0.pad = 0;
+    if ((r = launch_parent(a0, n, launchers, c, w, s, &rc))) return r;
+    GcGatherApp a1;
+    a1.rowptr = rowptr;
+    a1.col = col;
+    a1.color = color;
+    a1.notmax = notmax;
+    a1.used = used;
+    a1.n = n;
+    a1.pad = 0;
+    if ((r = launch_parent(a1, n, launchers, c, w, s, &rc))) return r;
+    DP_CUDA(cudaMemsetAsync(w->d_scratch + 1, 0, sizeof(unsigned long long),
+                            s));
+    gc_finalize_kernel<<<fin_blocks, 256, 0, s>>>(rowptr, n, color, notmax,
+                                                  used, w->d_scratch + 1);
+    DP_CUDA(cudaGetLastError());
+    rc.kernel_launches += 1;
+    DP_CUDA(cudaMemcpyAsync(w->h_ctr + 1, w->d_scratch + 1,
+                            sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                            s));
+    if ((r = read_state(w, s))) return r;
+    const long long got = (long long)w->h_ctr[1];
+    if (got <= 0) return fail(DP_ERR_ITERATIONS, "colouring made no progress");
+    remaining -= got;
+    ++rounds;
+  }
+  DP_CUDA(cudaEventRecord(w->ev1, s));
+  DP_CUDA(cudaEventSynchronize(w->ev1));
+  float ms = 0.f;
+  DP_CUDA(cudaEventElapsedTime(&ms, w->ev0, w->ev1));
+  if ((r = read_state(w, s))) return r;
+  rc.ms_kernel_sum = rc.ms_kernel_max = ms;  // three launches per round
+  finish_stats(w, rc, ms, st);
+  if (st) st->iterations = rounds;
+  return 0;
+}
+
 // single host launch apps
 template <class App>
 int once(Workspace* w, const dp_config* c, const App& app, long long nparents,
@@ -1200,6 +1311,30 @@ int dp_tc_dev(const int32_t* d_rowptr, const int32_t* d_col, int32_t n,
   const double t0 = now_ns();
   int r = tc_dev_impl(d_rowptr, d_col, n, m, edge_lo, edge_hi, cfg,
                       d_triangles, (cudaStream_t)stream, stats);
+  if (stats) stats->ns_host = now_ns() - t0;
+  return r;
+}
+
+int dp_gc(const int32_t* rowptr, const int32_t* col, int32_t n, int64_t m,
+          const dp_config* cfg, int32_t* color, dp_stats* stats) {
+  DP_HOST_CALL_BEGIN
+  if (n < 0 || m < 0) return fail(DP_ERR_INVALID, "bad graph size");
+  DP_TRY(stage(w_, 0, rowptr, (size_t)(n + 1) * 4, s_, &h2d_));
+  DP_TRY(stage(w_, 1, col, (size_t)m * 4, s_, &h2d_));
+  DP_TRY(stage(w_, 2, nullptr, (size_t)n * 4 + 4, s_, &h2d_));
+  DP_TRY(gc_dev_impl((int*)w_->io[0], (int*)w_->io[1], n, m, cfg,
+                     (int*)w_->io[2], s_, stats));
+  DP_TRY(unstage(w_, 2, color, (size_t)n * 4, s_, &d2h_));
+  DP_HOST_CALL_END
+}
+
+int dp_gc_dev(const int32_t* d_rowptr, const int32_t* d_col, int32_t n,
+              int64_t m, const dp_config* cfg, int32_t* d_color, void* stream,
+              dp_stats* stats) {
+  clear_stats(stats);
+  const double t0 = now_ns();
+  int r = gc_dev_impl(d_rowptr, d_col, n, m, cfg, d_color,
+                      (cudaStream_t)stream, stats);
   if (stats) stats->ns_host = now_ns() - t0;
   return r;
 }

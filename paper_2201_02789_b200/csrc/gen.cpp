@@ -206,6 +206,60 @@ int dp_tc_orient(const int32_t* rowptr, const int32_t* col, int32_t n,
   return 0;
 }
 
+int dp_symmetrize(const int32_t* rowptr, const int32_t* col, int32_t n,
+                  int32_t** rowptr_s, int32_t** col_s, int64_t* m_s,
+                  int32_t nthreads) {
+  if (n < 0 || !rowptr_s || !col_s || !m_s) return DP_ERR_INVALID;
+  const int nt = threads_of(nthreads);
+  std::vector<int64_t> cur(n + 1, 0);
+#pragma omp parallel for num_threads(nt) schedule(dynamic, 4096)
+  for (int64_t u = 0; u < n; ++u)
+    for (int32_t e = rowptr[u]; e < rowptr[u + 1]; ++e) {
+      const int32_t v = col[e];
+      if (v == u) continue;
+      __atomic_fetch_add(&cur[u + 1], 1, __ATOMIC_RELAXED);
+      __atomic_fetch_add(&cur[v + 1], 1, __ATOMIC_RELAXED);
+    }
+  std::vector<int64_t> sp(n + 1, 0);
+  for (int64_t i = 0; i < n; ++i) sp[i + 1] = sp[i] + cur[i + 1];
+  std::vector<int32_t> sym(std::max<int64_t>(sp[n], 1));
+  for (int64_t i = 0; i < n; ++i) cur[i] = sp[i];
+#pragma omp parallel for num_threads(nt) schedule(dynamic, 4096)
+  for (int64_t u = 0; u < n; ++u)
+    for (int32_t e = rowptr[u]; e < rowptr[u + 1]; ++e) {
+      const int32_t v = col[e];
+      if (v == u) continue;
+      sym[__atomic_fetch_add(&cur[u], 1, __ATOMIC_RELAXED)] = v;
+      sym[__atomic_fetch_add(&cur[v], 1, __ATOMIC_RELAXED)] = (int32_t)u;
+    }
+  std::vector<int64_t> deg(n + 1, 0);
+#pragma omp parallel for num_threads(nt) schedule(dynamic, 1024)
+  for (int64_t u = 0; u < n; ++u) {
+    int32_t* b = sym.data() + sp[u];
+    int32_t* e = sym.data() + sp[u + 1];
+    std::sort(b, e);
+    deg[u + 1] = std::unique(b, e) - b;
+  }
+  for (int64_t i = 0; i < n; ++i) deg[i + 1] += deg[i];
+  if (deg[n] > 0x7fffffffLL) return DP_ERR_INVALID;
+  int32_t* rp = (int32_t*)std::malloc(sizeof(int32_t) * (n + 1));
+  int32_t* cp = (int32_t*)std::malloc(sizeof(int32_t) * std::max<int64_t>(deg[n], 1));
+  if (!rp || !cp) {
+    std::free(rp);
+    std::free(cp);
+    return DP_ERR_INVALID;
+  }
+  for (int64_t i = 0; i <= n; ++i) rp[i] = (int32_t)deg[i];
+#pragma omp parallel for num_threads(nt) schedule(dynamic, 4096)
+  for (int64_t u = 0; u < n; ++u)
+    std::memcpy(cp + deg[u], sym.data() + sp[u],
+                sizeof(int32_t) * (deg[u + 1] - deg[u]));
+  *rowptr_s = rp;
+  *col_s = cp;
+  *m_s = deg[n];
+  return 0;
+}
+
 void dp_free(void* p) { std::free(p); }
 
 }  // extern "C"

@@ -499,3 +499,21 @@ def test_sssp_1d_partition_on_device(P, policy):
         p.reset(0)
     d2, _ = pdist.sssp_1d(parts, ops, pdist.LocalExchange())
     np.testing.assert_array_equal(d2.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("spec", ["hand", "powerlaw:2000:seed1",
+                                  "road:1000:seed7", "rmat:12:seed1",
+                                  "rmat:18:seed2"])
+def test_gc_vs_oracle(spec):
+    bench, wl = load("gc", spec)
+    want, k = oracle.gc(wl.buffers["rowptr"], wl.buffers["col"])
+    for policy in (dict(), dict(threshold=INF_THRESHOLD),
+                   dict(threshold=64, agg="block"),
+                   dict(threshold=256, cfactor=8, agg="multiblock",
+                        group_size=1 << 20, parent_block=256,
+                        child_block=128, serial="warp"),
+                   dict(threshold=32, agg="grid", serial="warp")):
+        rep, _ = run_config(bench, wl, BenchConfig(**policy))
+        np.testing.assert_array_equal(rep.arrays["color"], want)
+    np.testing.assert_array_equal(run_reference(bench, wl).arrays["color"],
+                                  want)

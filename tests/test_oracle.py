@@ -289,3 +289,45 @@ def test_oracle_bt_counts_and_vertices():
     np.testing.assert_allclose(verts[starts], p0, atol=1e-7)
     np.testing.assert_allclose(verts[starts + ntess - 1], p2, atol=1e-7)
     assert verts.min() >= -1e-9 and verts.max() <= 1 + 1e-9
+
+
+# ---------------------------------------------------------------------------
+# graph colouring (no reference implementation: brute-force checks here)
+# ---------------------------------------------------------------------------
+
+def _py_gc_key(v):
+    x = (v * 0x9E3779B1) & 0xFFFFFFFF
+    x ^= x >> 16
+    x = (x * 0x85EBCA6B) & 0xFFFFFFFF
+    x ^= x >> 13
+    x = (x * 0xC2B2AE35) & 0xFFFFFFFF
+    x ^= x >> 16
+    return (x << 32) | v
+
+
+@pytest.mark.parametrize("spec", ["hand", "rmat:9:seed1", "powerlaw:400:seed2",
+                                  "road:500:seed3"])
+def test_oracle_gc_is_priority_greedy_and_proper(spec):
+    g = graphs.symmetrize(make_graph(parse_spec(spec)))
+    color, k = oracle.gc(g.rowptr, g.col)
+    src = np.repeat(np.arange(g.n), np.diff(g.rowptr))
+    assert np.all(color[src] != color[g.col])          # proper
+    assert color.max() + 1 == k
+    want = [-1] * g.n                                   # greedy mirror
+    for u in sorted(range(g.n), key=_py_gc_key, reverse=True):
+        used = {want[w] for w in g.neighbors(u).tolist() if want[w] >= 0}
+        c = 0
+        while c in used:
+            c += 1
+        want[u] = c
+    assert color.tolist() == want
+
+
+def test_symmetrize_matches_numpy():
+    g = graphs.rmat_graph(10, 4)
+    s = graphs.symmetrize(g)
+    a, b = _simple_undirected(g)
+    order = np.lexsort((b, a))
+    np.testing.assert_array_equal(s.col, b[order])
+    np.testing.assert_array_equal(
+        s.rowptr, np.concatenate(([0], np.cumsum(np.bincount(a, minlength=g.n)))))
