@@ -501,19 +501,28 @@ def test_sssp_1d_partition_on_device(P, policy):
     np.testing.assert_array_equal(d2.cpu().numpy(), want)
 
 
+GC_FAST = (dict(threshold=64, agg="block"),
+           dict(threshold=256, cfactor=8, agg="multiblock", group_size=1 << 20,
+                parent_block=256, child_block=128, serial="warp"),
+           dict(threshold=32, agg="grid", serial="warp"))
+
+
 @pytest.mark.parametrize("spec", ["hand", "powerlaw:2000:seed1",
-                                  "road:1000:seed7", "rmat:12:seed1",
-                                  "rmat:18:seed2"])
+                                  "road:1000:seed7", "rmat:12:seed1"])
 def test_gc_vs_oracle(spec):
     bench, wl = load("gc", spec)
     want, k = oracle.gc(wl.buffers["rowptr"], wl.buffers["col"])
-    for policy in (dict(), dict(threshold=INF_THRESHOLD),
-                   dict(threshold=64, agg="block"),
-                   dict(threshold=256, cfactor=8, agg="multiblock",
-                        group_size=1 << 20, parent_block=256,
-                        child_block=128, serial="warp"),
-                   dict(threshold=32, agg="grid", serial="warp")):
+    for policy in (dict(), dict(threshold=INF_THRESHOLD)) + GC_FAST:
         rep, _ = run_config(bench, wl, BenchConfig(**policy))
         np.testing.assert_array_equal(rep.arrays["color"], want)
     np.testing.assert_array_equal(run_reference(bench, wl).arrays["color"],
                                   want)
+
+
+def test_gc_rmat18_vs_oracle():
+    bench, wl = load("gc", "rmat:18:seed2")
+    want, k = oracle.gc(wl.buffers["rowptr"], wl.buffers["col"])
+    for policy in GC_FAST:
+        rep, _ = run_config(bench, wl, BenchConfig(**policy))
+        np.testing.assert_array_equal(rep.arrays["color"], want)
+        assert int(rep.arrays["color"].max()) + 1 == k
