@@ -1,0 +1,46 @@
+"""Small runs of every app under several policies, checked against the
+oracle; meant to run under compute-sanitizer (memcheck / racecheck /
+synccheck) -- the stand-in for the reference's fence/publication checker
+(sim/machine.py:543-649)."""
+import sys
+from pathlib import Path
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import numpy as np
+from oracle import oracle
+from paper_2201_02789_b200.bench import BenchConfig, graphs, load, run_config
+
+POLICIES = [dict(), dict(agg="warp"), dict(threshold=4, agg="block"),
+            dict(threshold=2, cfactor=2, agg="multiblock", group_size=2),
+            dict(threshold=2, agg="grid", serial="warp", parent_block=64),
+            dict(agg="block", agg_threshold=3, child_block=64),
+            dict(threshold=8, cfactor=4, agg="multiblock", group_size=1 << 20,
+                 serial="warp", parent_block=128)]
+fails = 0
+for app, spec in (("bfs", "powerlaw:300:seed2"), ("sssp", "powerlaw:300:seed3"),
+                  ("manylaunch", "sizes:200:seed1"), ("tc", "rmat:8:seed1"),
+                  ("bt", "curves:300:seed1"), ("gc", "powerlaw:300:seed1")):
+    bench, wl = load(app, spec)
+    b = wl.buffers
+    if app == "bfs":
+        want = {"dist": oracle.bfs(b["rowptr"], b["col"])[0]}
+    elif app == "sssp":
+        want = {"dist": oracle.sssp(b["rowptr"], b["col"], b["weight"])[0]}
+    elif app == "manylaunch":
+        want = {"out": oracle.manylaunch(b["sizes"])[0]}
+    elif app == "tc":
+        want = {"triangles": np.array([oracle.tc(b["rowptr"], b["col"])],
+                                      np.uint64)}
+    elif app == "bt":
+        want = {"ntess": oracle.bt(b["cp"], graphs.BT_MAX_TESS,
+                                   graphs.BT_CURV_SCALE)[0]}
+    else:
+        want = {"color": oracle.gc(b["rowptr"], b["col"])[0]}
+    for pol in POLICIES:
+        rep, _ = run_config(bench, wl, BenchConfig(**pol))
+        for k, v in want.items():
+            if not np.array_equal(rep.arrays[k], v):
+                fails += 1
+                print("MISMATCH", app, k, pol, flush=True)
+    print("ok", app, flush=True)
+print("FAILS", fails)
+sys.exit(1 if fails else 0)
