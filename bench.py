@@ -273,6 +273,24 @@ def extra_workloads(stream, quick: bool) -> dict:
     from paper_2201_02789_b200.bench import load, run_config, BenchConfig
     out = {}
     lib = _lib.device()
+    # BASELINE config 1: BFS RMAT-16, T=128, block aggregation, the
+    # reference's launch shapes (parent and child blocks of 32)
+    G16 = DeviceGraph(16, SEED, weights=False)
+    c1 = dict(threshold=128, agg="block")
+    runs = [run_dev("bfs", G16, _cfg(c1), stream) for _ in range(6)][1:]
+    ms = statistics.median(r["ns_device"] for r in runs) / 1e6
+    e16 = int(G16.counts.to(torch.int64).sum().item())
+    naive16 = run_dev("bfs", G16, _cfg(dict()), stream)
+    out["config1_bfs_rmat16_t128_block"] = {
+        "gteps": e16 / ms / 1e6, "ms": ms, "levels": runs[0]["iterations"],
+        "device_launches": runs[0]["num_launches"],
+        "blocks_scheduled": runs[0]["blocks_scheduled"],
+        "launch_lat_us": runs[0]["launch_lat_ns_mean"] / 1e3,
+        "vs_naive_cdp": naive16["ns_device"] / 1e6 / ms,
+        "naive_cdp_launches": naive16["num_launches"],
+        "reference_python_cpu_s": 3.08,  # BASELINE.md §2 (own RMAT, 1 core)
+        "policy": c1}
+    del G16
     # BFS RMAT-22
     G = DeviceGraph(SCALE, SEED, weights=False)
     cfg = _cfg(BEST["bfs"])
@@ -326,6 +344,16 @@ def extra_workloads(stream, quick: bool) -> dict:
     out["bt_25k"] = {"curves_per_s": 25000 / (ms * 1e-3), "ms": ms,
                      "vertices": nv, "gbps_alg": (36 * 25000 + 8 * nv) /
                      (ms * 1e6), "policy": BEST["bt"]}
+    # BASELINE config 2 as written: coarsening + multi-block aggregation
+    c2 = dict(threshold=64, cfactor=16, agg="multiblock", group_size=4,
+              parent_block=256, child_block=32, serial="warp")
+    reps = [run_config(bench, wl, BenchConfig(**c2))[0] for _ in range(6)]
+    ms2 = statistics.median(r.ns_device for r in reps[1:]) / 1e6
+    naive = run_config(bench, wl, BenchConfig())[0]
+    out["config2_bt_25k_c_multiblock"] = {
+        "curves_per_s": 25000 / (ms2 * 1e-3), "ms": ms2,
+        "device_launches": reps[-1].num_launches,
+        "vs_naive_cdp": naive.ns_device / 1e6 / ms2, "policy": c2}
     return out
 
 

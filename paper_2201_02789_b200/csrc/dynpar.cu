@@ -55,6 +55,15 @@ struct Workspace {
   int* d_flag = nullptr;                    // BT overflow
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evk0 = nullptr, evk1 = nullptr;
   long long pending_limit = 0;
+  // mapped (zero-copy) readback of DevState for the per-level host loop
+  struct Signal {
+    DevState ds;
+    unsigned seq;
+    unsigned pad;
+  };
+  Signal* h_sig = nullptr;  // host view (mapped pinned)
+  Signal* d_sig = nullptr;  // device view of the same memory
+  unsigned seq = 0;
   // staging for host-buffer calls
   void* io[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   size_t io_bytes[6] = {0, 0, 0, 0, 0, 0};
@@ -98,7 +107,10 @@ Workspace* workspace(int* rc) {
         (e = cudaEventCreate(&w.ev0)) != cudaSuccess ||
         (e = cudaEventCreate(&w.ev1)) != cudaSuccess ||
         (e = cudaEventCreate(&w.evk0)) != cudaSuccess ||
-        (e = cudaEventCreate(&w.evk1)) != cudaSuccess) {
+        (e = cudaEventCreate(&w.evk1)) != cudaSuccess ||
+        (e = cudaHostAlloc(&w.h_sig, sizeof(Workspace::Signal),
+                           cudaHostAllocMapped)) != cudaSuccess ||
+        (e = cudaHostGetDevicePointer(&w.d_sig, w.h_sig, 0)) != cudaSuccess) {
       *rc = fail(DP_ERR_CUDA,
                  std::string("workspace init: ") + cudaGetErrorString(e));
       return nullptr;
@@ -543,6 +555,39 @@ int begin_run(Workspace* w, cudaStream_t s) {
   return 0;
 }
 
+__global__ void signal_kernel(const DevState* ds, Workspace::Signal* sig,
+                              unsigned seq) {
+  sig->ds = *ds;
+  __threadfence_system();
+  *(volatile unsigned*)&sig->seq = seq;
+}
+
+// Same result as read_state, lower latency: a one-thread kernel queued after
+// the level's work publishes DevState into mapped host memory and the host
+// spins on the sequence number (no cudaMemcpyAsync + stream synchronise).
+int read_state_fast(Workspace* w, cudaStream_t s) {
+  const unsigned seq = ++w->seq;
+  signal_kernel<<<1, 1, 0, s>>>(w->ds, w->d_sig, seq);
+  DP_CUDA(cudaGetLastError());
+  volatile unsigned* flag = &w->h_sig->seq;
+  for (unsigned spin = 1; *flag != seq; ++spin) {
+    if ((spin & 1023) == 0) {
+      const cudaError_t e = cudaStreamQuery(s);
+      if (e != cudaSuccess && e != cudaErrorNotReady)
+        return fail(DP_ERR_CUDA, std::string("cuda-error: ") +
+                                     cudaGetErrorString(e));
+      if (e == cudaSuccess && *flag != seq) break;  // drained: re-check below
+    }
+  }
+  __atomic_thread_fence(__ATOMIC_ACQUIRE);
+  if (w->h_sig->seq != seq) {  // stream drained without the signal: fall back
+    DP_CUDA(cudaStreamSynchronize(s));
+  }
+  std::memcpy((void*)w->h_ds, (const void*)&w->h_sig->ds, sizeof(DevState));
+  if (w->h_ds->err) return map_device_error(w->h_ds->err);
+  return 0;
+}
+
 int read_state(Workspace* w, cudaStream_t s) {
   DP_CUDA(cudaMemcpyAsync(w->h_ds, w->ds, sizeof(DevState),
                           cudaMemcpyDeviceToHost, s));
@@ -651,7 +696,7 @@ int iterate(Workspace* w, const dp_config* c, long long nparents,
   for (; !converged && it <= max_iter; ++it) {
     auto app = make(it, w->ds);
     if ((r = launch_parent(app, nparents, launchers, c, w, s, &rc))) return r;
-    if ((r = read_state(w, s))) return r;
+    if ((r = read_state_fast(w, s))) return r;
     if ((r = account_step(w, &rc))) return r;
     if (w->h_ds->flag[it & 1] == 0) {
       converged = true;
@@ -1013,7 +1058,7 @@ int bfs_part_level_impl(const int32_t* rowptr, const int32_t* col,
   DP_CUDA(cudaEventRecord(w->ev0, s));
   if ((r = launch_parent(a, n_local, launchers, c, w, s, &rc))) return r;
   DP_CUDA(cudaEventRecord(w->ev1, s));
-  if ((r = read_state(w, s))) return r;
+  if ((r = read_state_fast(w, s))) return r;
   if ((r = account_step(w, &rc))) return r;
   float ms = 0.f;
   DP_CUDA(cudaEventElapsedTime(&ms, w->ev0, w->ev1));
@@ -1073,7 +1118,7 @@ int sssp_part_round_impl(const int32_t* rowptr, const int32_t* col,
   DP_CUDA(cudaEventRecord(w->ev0, s));
   if ((r = launch_parent(a, n_local, launchers, c, w, s, &rc))) return r;
   DP_CUDA(cudaEventRecord(w->ev1, s));
-  if ((r = read_state(w, s))) return r;
+  if ((r = read_state_fast(w, s))) return r;
   if ((r = account_step(w, &rc))) return r;
   float ms = 0.f;
   DP_CUDA(cudaEventElapsedTime(&ms, w->ev0, w->ev1));
