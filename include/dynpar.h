@@ -176,6 +176,25 @@ int dp_gc_dev(const int32_t* d_rowptr, const int32_t* d_col, int32_t n,
               int64_t m, const dp_config* cfg, int32_t* d_color, void* stream,
               dp_stats* stats);
 
+/* ---- minimum spanning forest: MSTF / MSTV (no reference) */
+/* Boruvka rounds over a symmetric simple CSR (dp_symmetrize) with symmetric
+ * weights and eid[e] = the canonical slot of slot e's undirected edge
+ * (min(e, mirror[e]), dp_edge_mirror).  Edges are ordered by (weight, eid),
+ * so the forest is unique (= Kruskal in that order).  cfg_find drives the
+ * nested find kernel (MSTF), cfg_verify the nested verify kernel (MSTV;
+ * NULL = cfg_find).  Out: in_mst[m] = 1 at the canonical slot of every forest
+ * edge, *total_weight, *nedges.  stats->iterations = find rounds. */
+int dp_mst(const int32_t* rowptr, const int32_t* col, const int32_t* weight,
+           const int32_t* eid, int32_t n, int64_t m, const dp_config* cfg_find,
+           const dp_config* cfg_verify, uint8_t* in_mst, int64_t* total_weight,
+           int64_t* nedges, dp_stats* stats);
+int dp_mst_dev(const int32_t* d_rowptr, const int32_t* d_col,
+               const int32_t* d_weight, const int32_t* d_eid, int32_t n,
+               int64_t m, const dp_config* cfg_find,
+               const dp_config* cfg_verify, uint8_t* d_in_mst,
+               int64_t* total_weight, int64_t* nedges, void* stream,
+               dp_stats* stats);
+
 /* ---- BFS over a cyclic 1D vertex partition ------- */
 /* One level on part `part` of `nparts` (owner(v) = v % nparts; local index
  * v / nparts).  d_rowptr_p/d_col_p: the part's rows (dp_rmat_csr_part),
@@ -258,6 +277,10 @@ int dp_tc_orient(const int32_t* rowptr, const int32_t* col, int32_t n,
 int dp_symmetrize(const int32_t* rowptr, const int32_t* col, int32_t n,
                   int32_t** rowptr_s, int32_t** col_s, int64_t* m_s,
                   int32_t nthreads);
+/* symmetric CSR, sorted rows, no duplicates: mirror[e] = slot of the reverse
+ * edge.  DP_ERR_INVALID if a reverse edge is missing. */
+int dp_edge_mirror(const int32_t* rowptr, const int32_t* col, int32_t n,
+                   int32_t* mirror, int32_t nthreads);
 void dp_free(void* p);
 
 #ifdef __cplusplus

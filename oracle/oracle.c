@@ -16,6 +16,7 @@
  *   oracle_tc          exact triangle count over a degree-oriented CSR+
  *   oracle_bt          Bezier tessellation, fp64 vertices, fp32 counts
  *   oracle_gc          greedy colouring in Jones-Plassmann priority order
+ *   oracle_mst         Kruskal minimum spanning forest in (weight, eid) order
  *
  * Parallel versions (nthreads > 1) use the same atomics the reference's
  * kernels use; outputs are schedule-invariant (benchmarks.py:10-15), so any
@@ -245,4 +246,69 @@ int32_t oracle_gc(const int32_t* rowptr, const int32_t* col, int32_t n,
   free(keys);
   free(stamp);
   return ncolors;
+}
+
+/* ---- minimum spanning forest: MSTF / MSTV (no reference
+ * implementation) ------------------------------------------------------------
+ * Kruskal over the canonical slots (eid[e] == e) in increasing key =
+ * (weight, eid) with a union-find: under that strict total order the minimum
+ * spanning forest is unique, so it must equal the device's Boruvka forest
+ * edge for edge.  in_mst[m] gets 1 at each forest edge's canonical slot.
+ * Returns the number of forest edges (-1 on allocation failure). */
+static uint64_t mst_key(int32_t w, int32_t e) {
+  return ((uint64_t)((uint32_t)w ^ 0x80000000u) << 32) | (uint32_t)e;
+}
+
+static int u64_cmp(const void* a, const void* b) {
+  const uint64_t ka = *(const uint64_t*)a, kb = *(const uint64_t*)b;
+  return ka < kb ? -1 : (ka > kb ? 1 : 0);
+}
+
+static int32_t uf_find(int32_t* parent, int32_t x) {
+  while (parent[x] != x) {
+    parent[x] = parent[parent[x]];
+    x = parent[x];
+  }
+  return x;
+}
+
+int64_t oracle_mst(const int32_t* rowptr, const int32_t* col,
+                   const int32_t* weight, const int32_t* eid, int32_t n,
+                   int64_t m, uint8_t* in_mst, int64_t* total_weight) {
+  int64_t k = 0;
+  for (int64_t e = 0; e < m; ++e) k += eid[e] == e;
+  uint64_t* keys = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)(k ? k : 1));
+  int32_t* src = (int32_t*)malloc(sizeof(int32_t) * (size_t)(m ? m : 1));
+  int32_t* parent = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));
+  if (!keys || !src || !parent) {
+    free(keys);
+    free(src);
+    free(parent);
+    return -1;
+  }
+  for (int32_t u = 0; u < n; ++u) {
+    parent[u] = u;
+    for (int32_t e = rowptr[u]; e < rowptr[u + 1]; ++e) src[e] = u;
+  }
+  k = 0;
+  for (int64_t e = 0; e < m; ++e) {
+    in_mst[e] = 0;
+    if (eid[e] == e) keys[k++] = mst_key(weight[e], (int32_t)e);
+  }
+  qsort(keys, (size_t)k, sizeof(uint64_t), u64_cmp);
+  int64_t nedges = 0, total = 0;
+  for (int64_t i = 0; i < k; ++i) {
+    const int32_t e = (int32_t)(keys[i] & 0xffffffffu);
+    const int32_t a = uf_find(parent, src[e]), b = uf_find(parent, col[e]);
+    if (a == b) continue;
+    parent[a < b ? b : a] = a < b ? a : b;
+    in_mst[e] = 1;
+    total += weight[e];
+    ++nedges;
+  }
+  *total_weight = total;
+  free(keys);
+  free(src);
+  free(parent);
+  return nedges;
 }

@@ -124,6 +124,13 @@ _SIGNATURES = {
     "dp_symmetrize": ([_P, _P, _I32, ctypes.POINTER(ctypes.c_void_p),
                        ctypes.POINTER(ctypes.c_void_p),
                        ctypes.POINTER(ctypes.c_int64), _I32], ctypes.c_int),
+    "dp_mst": ([_P, _P, _P, _P, _I32, _I64, _CFG, _CFG, _P,
+                ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64),
+                _ST], ctypes.c_int),
+    "dp_mst_dev": ([_P, _P, _P, _P, _I32, _I64, _CFG, _CFG, _P,
+                    ctypes.POINTER(ctypes.c_int64),
+                    ctypes.POINTER(ctypes.c_int64), _P, _ST], ctypes.c_int),
+    "dp_edge_mirror": ([_P, _P, _I32, _P, _I32], ctypes.c_int),
     "dp_free": ([_P], None),
 }
 

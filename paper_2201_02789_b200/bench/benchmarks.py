@@ -12,6 +12,9 @@ Applications
   sssp        Bellman-Ford rounds, output dist             (ref :175-270)
   manylaunch  launch-congestion microbenchmark, out, total (ref :277-332)
   tc          triangle counting over a degree-oriented CSR+   (new, config 4)
+  gc          Jones-Plassmann graph colouring                 (new, north star)
+  mstf, mstv  Boruvka minimum spanning forest; the policy drives the find
+              (mstf) or the verify (mstv) kernel          (new)
   bt          Bezier line tessellation                        (new, config 2)
 Outputs are written only through commutative / idempotent atomics, so they
 are schedule-invariant and must match the serial variant element-exactly
@@ -29,7 +32,7 @@ import numpy as np
 from .. import _lib
 from .graphs import (BT_CURV_SCALE, BT_MAX_TESS, UNREACHED, DatasetSpec,
                      bezier_curves, child_sizes, edge_weights, make_graph,
-                     parse_spec, symmetrize, tc_orient)
+                     mst_inputs, parse_spec, symmetrize, tc_orient)
 
 BLOCK = 32  # parent block size of every reference driver (benchmarks.py:44)
 
@@ -240,6 +243,62 @@ def _gc_traffic(wl, out, st):
 
 
 # ---------------------------------------------------------------------------
+# mstf / mstv (Boruvka minimum spanning forest, no
+# reference code).  Both run the whole forest computation; the BenchConfig
+# policy drives the nested find kernel (mstf) or the nested verify kernel
+# (mstv) and the other kernel runs its serial (No-CDP) form, so each row
+# measures one kernel's transformation as the paper's Table I does.
+# ---------------------------------------------------------------------------
+
+def _mst_prepare(spec: DatasetSpec) -> Workload:
+    g, w, eid = mst_inputs(make_graph(spec), spec.seed)
+    return Workload(spec=spec, n=g.n, payload=g, buffers={
+        "rowptr": _c32(g.rowptr), "col": _c32(g.col), "weight": w,
+        "eid": eid})
+
+
+def _nocdp_copy(cfg: _lib.DpConfig) -> _lib.DpConfig:
+    c = _lib.DpConfig.from_buffer_copy(cfg)
+    c.variant = _lib.VARIANT_NOCDP
+    return c
+
+
+def _mst_run_with(wl: Workload, cfg_find, cfg_verify):
+    lib = _lib.device()
+    b = wl.buffers
+    m = int(b["col"].shape[0])
+    in_mst = np.zeros(max(m, 1), dtype=np.uint8)
+    total = ctypes.c_int64()
+    nedges = ctypes.c_int64()
+    st = _call(lib.dp_mst, _lib.ptr(b["rowptr"]), _lib.ptr(b["col"]),
+               _lib.ptr(b["weight"]), _lib.ptr(b["eid"]), wl.n, m,
+               ctypes.byref(cfg_find), ctypes.byref(cfg_verify),
+               _lib.ptr(in_mst), ctypes.byref(total), ctypes.byref(nedges))
+    return {"in_mst": in_mst[:m],
+            "weight": np.array([total.value, nedges.value], dtype=np.int64)}, st
+
+
+def _mstf_run(wl: Workload, cfg: _lib.DpConfig):
+    return _mst_run_with(wl, cfg, _nocdp_copy(cfg))
+
+
+def _mstv_run(wl: Workload, cfg: _lib.DpConfig):
+    return _mst_run_with(wl, _nocdp_copy(cfg), cfg)
+
+
+def mst_traffic(n: int, m: int, rounds: int) -> int:
+    """Per find round: 8 B per vertex (rowptr, comp) + 8 B per edge slot
+    (col, comp[v] probe); the (weight, eid) reads of cross edges and the
+    verify pass come on top (schedule/graph dependent, not counted)."""
+    return rounds * (8 * n + 8 * m)
+
+
+def _mst_traffic(wl, out, st):
+    m = int(wl.buffers["col"].shape[0])
+    return m, mst_traffic(wl.n, m, int(st["iterations"]))
+
+
+# ---------------------------------------------------------------------------
 # bt
 # ---------------------------------------------------------------------------
 
@@ -311,6 +370,14 @@ BENCHMARKS: dict[str, Benchmark] = {
     "gc": Benchmark("gc", ("color",), {"color": "int"}, _gc_prepare,
                     _gc_run, _gc_traffic,
                     "Jones-Plassmann graph colouring (new)"),
+    "mstf": Benchmark("mstf", ("in_mst", "weight"), {"in_mst": "int",
+                                                     "weight": "long"},
+                      _mst_prepare, _mstf_run, _mst_traffic,
+                      "Boruvka MST, policy on the find kernel (new)"),
+    "mstv": Benchmark("mstv", ("in_mst", "weight"), {"in_mst": "int",
+                                                     "weight": "long"},
+                      _mst_prepare, _mstv_run, _mst_traffic,
+                      "Boruvka MST, policy on the verify kernel (new)"),
     "bt": Benchmark("bt", ("ntess", "verts"), {"ntess": "int",
                                                "verts": "float"},
                     _bt_prepare, _bt_run, _bt_traffic,

@@ -257,6 +257,30 @@ def symmetrize(graph: Graph) -> Graph:
     return Graph(rowptr, col)
 
 
+def edge_mirror(graph: Graph) -> np.ndarray:
+    """mirror[e] = slot of the reverse edge of slot e (symmetric simple CSR
+    with sorted rows, e.g. from ``symmetrize``)."""
+    from .. import _lib
+    mirror = np.empty(max(graph.m, 1), dtype=np.int32)
+    _lib.check(_lib.load().dp_edge_mirror(_lib.ptr(graph.rowptr),
+                                          _lib.ptr(graph.col), graph.n,
+                                          _lib.ptr(mirror), 0))
+    return mirror[:graph.m]
+
+
+def mst_inputs(graph: Graph, seed: int) -> tuple:
+    """MST input (MSTF / MSTV): the symmetric simple graph,
+    symmetric weights and canonical edge ids.  eid[e] = min(e, mirror[e]) is
+    the slot of the (min, max) copy of the undirected edge; its weight is the
+    reference rule's draw at that slot (graphs.py:184-187, [1, 9]), shared by
+    both copies.  Returns (graph, weight int32[m], eid int32[m])."""
+    g = symmetrize(graph)
+    eid = np.minimum(np.arange(g.m, dtype=np.int32), edge_mirror(g))
+    w = edge_weights(g, seed)[eid] if g.m else np.zeros(0, dtype=np.int32)
+    return g, np.ascontiguousarray(w, dtype=np.int32), \
+        np.ascontiguousarray(eid, dtype=np.int32)
+
+
 # ---------------------------------------------------------------------------
 # Bezier tessellation input
 # ---------------------------------------------------------------------------

@@ -836,4 +836,152 @@ struct BtApp {
   __device__ void flush(Acc&) const {}
 };
 
+// ---------------------------------------------------------------------------
+// Minimum spanning forest, Boruvka rounds — the paper's MSTF (find) and MSTV
+// (verify) kernels (from the LonestarGPU / KLAP suite; no
+// reference code).  Input: symmetric simple CSR, symmetric weights, and per
+// slot the canonical undirected edge id eid (the slot of its (min,max) copy).
+// Edges are totally ordered by key = (weight, eid), so the forest is unique
+// and equals Kruskal's in that order (oracle_mst) whatever the schedule.
+//   comp[v]   component root of v (fully compressed between rounds)
+//   cmin[c]   min key leaving component c (atomicMin), kNoEdge if none
+// MSTF: parent = vertex, child item = out-edge: a cross-component edge lowers
+// cmin[comp u].  MSTV: parent = the go-ahead vertex of its component (the
+// endpoint of the edge cmin names: the canonical slot lies in its row, or it
+// is that slot's target), child item = out-edge: the slot whose eid realises
+// the minimum marks the forest edge and records the partner component
+// (LonestarGPU verify_min_elem).  Hook + pointer jumping are flat kernels in
+// dynpar.cu.
+// ---------------------------------------------------------------------------
+constexpr unsigned long long kNoEdge = ~0ull;
+
+// order-preserving map of a signed weight into the high half of the key
+__host__ __device__ __forceinline__ unsigned long long mst_key(int w, int eid) {
+  return ((unsigned long long)((unsigned)w ^ 0x80000000u) << 32) |
+         (unsigned)eid;
+}
+
+struct MstFindApp {
+  const int* __restrict__ rowptr;
+  const int* __restrict__ col;
+  const int* __restrict__ weight;
+  const int* __restrict__ eid;
+  const int* __restrict__ comp;  // read-only during the kernel
+  unsigned long long* cmin;
+  int* changed;  // some cross-component edge exists
+  int n;
+  int pad;
+
+  struct alignas(16) Args {
+    int start, deg, cu, pad;
+  };
+  struct Acc {
+    int changed;
+  };
+
+  __device__ int nparents() const { return n; }
+  __device__ void parent_prologue() const {}
+  __device__ int expand(int u, bool valid, Args& a) const {
+    if (!valid) return 0;
+    const int s = __ldg(rowptr + u);
+    const int d = __ldg(rowptr + u + 1) - s;
+    if (d <= 0) return 0;
+    a = Args{s, d, __ldg(comp + u), 0};
+    return d;
+  }
+  __device__ static int count(const Args& a) { return a.deg; }
+  __device__ __forceinline__ void offer(int cu, unsigned long long k,
+                                        Acc& acc) const {
+    acc.changed = 1;
+    // cmin only decreases during the kernel: the plain L2 pre-check skips
+    // atomics that cannot succeed
+    if (k < __ldcg(cmin + cu)) atomicMin(cmin + cu, k);
+  }
+  __device__ void item(const Args& a, int e, Acc& acc) const {
+    const int i = a.start + e;
+    const int v = ld_stream(col + i);
+    if (__ldg(comp + v) != a.cu)
+      offer(a.cu, mst_key(ld_stream(weight + i), ld_stream(eid + i)), acc);
+  }
+  static constexpr int kUnroll = 4;
+  static constexpr bool kBlockMode = false;
+  static constexpr bool kPureExpand = true;
+  static constexpr int kMinBlocks = 1;
+  template <int U, class ArgsOf>
+  __device__ __forceinline__ void items(ArgsOf args, const int* e,
+                                        const bool* ok, Acc& acc) const {
+    int v[U], c[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j)
+      v[j] = ok[j] ? ld_stream(col + args(j).start + e[j]) : 0;
+#pragma unroll
+    for (int j = 0; j < U; ++j) c[j] = ok[j] ? __ldg(comp + v[j]) : 0;
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      if (!ok[j] || c[j] == args(j).cu) continue;
+      const int i = args(j).start + e[j];
+      offer(args(j).cu,
+            mst_key(ld_stream(weight + i), ld_stream(eid + i)), acc);
+    }
+  }
+  __device__ void flush(Acc& acc) const {
+    if (__any_sync(DP_FULL, acc.changed) && lane_id() == 0 &&
+        __ldcg(changed) == 0)
+      *changed = 1;
+  }
+};
+
+struct MstVerifyApp {
+  const int* __restrict__ rowptr;
+  const int* __restrict__ col;
+  const int* __restrict__ eid;
+  const int* __restrict__ comp;
+  const unsigned long long* __restrict__ cmin;
+  unsigned char* in_mst;  // [m], set at the canonical slot
+  int* partner;           // [n] per component root: the other component
+  int n;
+  int pad;
+
+  struct alignas(16) Args {
+    int start, deg, cu, want;  // want = eid of the component's min edge
+  };
+  struct Acc {};
+
+  __device__ int nparents() const { return n; }
+  __device__ void parent_prologue() const {}
+  __device__ int expand(int u, bool valid, Args& a) const {
+    if (!valid) return 0;
+    const int cu = __ldg(comp + u);
+    const unsigned long long k = __ldcg(cmin + cu);
+    if (k == kNoEdge) return 0;
+    const int want = (int)(unsigned)(k & 0xffffffffull);
+    const int s = __ldg(rowptr + u);
+    const int d = __ldg(rowptr + u + 1) - s;
+    // u is an endpoint of the chosen edge: its smaller endpoint owns the
+    // canonical slot, the larger one is that slot's target.  The endpoint in
+    // the other component is checked against that component's minimum.
+    if (!((want >= s && want < s + d) || __ldg(col + want) == u)) return 0;
+    a = Args{s, d, cu, want};
+    return d > 0 ? d : 0;
+  }
+  __device__ static int count(const Args& a) { return a.deg; }
+  __device__ void item(const Args& a, int e, Acc&) const {
+    const int i = a.start + e;
+    if (ld_stream(eid + i) == a.want) {  // unique: one slot per component
+      in_mst[a.want] = 1;
+      partner[a.cu] = __ldg(comp + __ldg(col + i));
+    }
+  }
+  static constexpr int kUnroll = 4;
+  static constexpr bool kBlockMode = false;
+  static constexpr bool kPureExpand = true;
+  static constexpr int kMinBlocks = 1;
+  template <int U, class ArgsOf>
+  __device__ __forceinline__ void items(ArgsOf args, const int* e,
+                                        const bool* ok, Acc& acc) const {
+    items_loop<U>(*this, args, e, ok, acc);
+  }
+  __device__ void flush(Acc&) const {}
+};
+
 }  // namespace dp

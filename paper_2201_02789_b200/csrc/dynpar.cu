@@ -895,6 +895,167 @@ int gc_dev_impl(const int32_t* rowptr, const int32_t* col, int32_t n,
   return 0;
 }
 
+// ---------------------------------------------------------------------------
+// MST (Boruvka): per round MSTF (nested find) -> flag readback -> MSTV (nested
+// verify) -> hook -> pointer jumping.  Under the strict (weight, eid) order
+// the chosen edges form a forest whose only cycles are mutual pairs.
+// ---------------------------------------------------------------------------
+__global__ void mst_init_kernel(int n, int* comp, unsigned long long* cmin) {
+  for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (long long)gridDim.x * blockDim.x) {
+    comp[v] = (int)v;
+    cmin[v] = kNoEdge;
+  }
+}
+
+// Roots with a chosen edge attach to their partner component; of a mutual
+// pair the smaller root stays.  Each chosen edge's weight is counted once.
+__global__ void mst_hook_kernel(int n, int* comp,
+                                const unsigned long long* __restrict__ cmin,
+                                const int* __restrict__ partner,
+                                unsigned long long* sums /* [wsum, edges] */) {
+  long long w = 0, c = 0;
+  for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (long long)gridDim.x * blockDim.x) {
+    if (comp[v] != v) continue;  // only thread v writes a root's comp
+    const unsigned long long k = cmin[v];
+    if (k == kNoEdge) continue;
+    const int p = partner[v];
+    const bool mutual = cmin[p] == k;
+    if (!mutual || v < p) {
+      w += (long long)(int)((unsigned)(k >> 32) ^ 0x80000000u);
+      c += 1;
+    }
+    if (!mutual || v > p) comp[v] = p;
+  }
+  w = (long long)warp_sum_u64((unsigned long long)w);
+  c = (long long)warp_sum_u64((unsigned long long)c);
+  if (lane_id() == 0 && c) {
+    atomicAdd(sums, (unsigned long long)w);
+    atomicAdd(sums + 1, (unsigned long long)c);
+  }
+}
+
+// New roots after hooking, in two passes.  Pass 1 (path halving) re-points
+// each visited node at its grandparent so concurrent walkers shorten each
+// other's paths; it can leave a node at a non-root ancestor (a halving step
+// that read the old parent may land after the node's owner stored the root).
+// Pass 2 walks read-only and stores only roots, which are fixed during the
+// pass, so every vertex ends at its root; it also re-arms the minima.
+__global__ void mst_halve_kernel(int n, int* comp) {
+  for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (long long)gridDim.x * blockDim.x) {
+    int x = (int)v;
+    for (;;) {
+      const int p = __ldcg(comp + x);
+      const int pp = __ldcg(comp + p);
+      if (p == pp) break;
+      __stcg(comp + x, pp);
+      x = pp;
+    }
+  }
+}
+
+__global__ void mst_root_kernel(int n, int* comp, unsigned long long* cmin) {
+  for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (long long)gridDim.x * blockDim.x) {
+    int x = __ldcg(comp + v);
+    for (int p; (p = __ldcg(comp + x)) != x;) x = p;
+    __stcg(comp + v, x);
+    cmin[v] = kNoEdge;
+  }
+}
+
+int mst_dev_impl(const int32_t* rowptr, const int32_t* col,
+                 const int32_t* weight, const int32_t* eid, int32_t n,
+                 int64_t m, const dp_config* cf, const dp_config* cv,
+                 uint8_t* in_mst, int64_t* total_weight, int64_t* nedges,
+                 cudaStream_t s, dp_stats* st) {
+  int r;
+  if (!cv) cv = cf;
+  if ((r = validate(cf)) || (r = validate(cv))) return r;
+  if (n < 0 || m < 0) return fail(DP_ERR_INVALID, "bad graph size");
+  Workspace* w = workspace(&r);
+  if (!w) return r;
+  // cmin[n] | comp[n] | partner[n]
+  const size_t nn = (size_t)std::max(n, 1);
+  if ((r = grow(&w->io[5], &w->io_bytes[5], nn * (8 + 4 + 4)))) return r;
+  unsigned long long* cmin = (unsigned long long*)w->io[5];
+  int* comp = (int*)(cmin + nn);
+  int* partner = comp + nn;
+  unsigned long long* sums = w->d_scratch;  // [0] weight, [1] edges
+  const int blocks = std::max(1, std::min(dp::ceil_div(std::max(n, 1), 256),
+                                          148 * 8));
+  mst_init_kernel<<<blocks, 256, 0, s>>>(n, comp, cmin);
+  DP_CUDA(cudaGetLastError());
+  if (m) DP_CUDA(cudaMemsetAsync(in_mst, 0, (size_t)m, s));
+  long long lf = 0, lv = 0;
+  if (cf->variant == DP_VARIANT_CDP &&
+      (r = count_launchers(w, cf, rowptr, n, 0, s, &lf)))
+    return r;
+  if (cv->variant == DP_VARIANT_CDP &&
+      (r = count_launchers(w, cv, rowptr, n, 0, s, &lv)))
+    return r;
+  if ((r = ensure_pending_limit(
+           w, cf->variant == DP_VARIANT_CDP ? cf : cv,
+           std::max(launch_bound(cf, n, lf), launch_bound(cv, n, lv)))))
+    return r;
+  // after count_launchers, which uses d_scratch[1]
+  DP_CUDA(cudaMemsetAsync(sums, 0, 2 * sizeof(unsigned long long), s));
+  if ((r = begin_run(w, s))) return r;
+  RunCounters rc;
+  DP_CUDA(cudaEventRecord(w->ev0, s));
+  int rounds = 0;
+  for (;; ++rounds) {
+    if (rounds > 64)  // components at least halve every round
+      return fail(DP_ERR_ITERATIONS, "Boruvka did not converge");
+    DP_CUDA(cudaMemsetAsync(&w->ds->flag[0], 0, sizeof(int), s));
+    MstFindApp fa;
+    fa.rowptr = rowptr;
+    fa.col = col;
+    fa.weight = weight;
+    fa.eid = eid;
+    fa.comp = comp;
+    fa.cmin = cmin;
+    fa.changed = &w->ds->flag[0];
+    fa.n = n;
+    fa.pad = 0;
+    if ((r = launch_parent(fa, n, lf, cf, w, s, &rc))) return r;
+    if ((r = read_state_fast(w, s))) return r;
+    if (w->h_ds->flag[0] == 0) break;  // no edge leaves any component
+    MstVerifyApp va;
+    va.rowptr = rowptr;
+    va.col = col;
+    va.eid = eid;
+    va.comp = comp;
+    va.cmin = cmin;
+    va.in_mst = in_mst;
+    va.partner = partner;
+    va.n = n;
+    va.pad = 0;
+    if ((r = launch_parent(va, n, lv, cv, w, s, &rc))) return r;
+    mst_hook_kernel<<<blocks, 256, 0, s>>>(n, comp, cmin, partner, sums);
+    mst_halve_kernel<<<blocks, 256, 0, s>>>(n, comp);
+    mst_root_kernel<<<blocks, 256, 0, s>>>(n, comp, cmin);
+    DP_CUDA(cudaGetLastError());
+    rc.kernel_launches += 3;
+  }
+  DP_CUDA(cudaEventRecord(w->ev1, s));
+  DP_CUDA(cudaEventSynchronize(w->ev1));
+  float ms = 0.f;
+  DP_CUDA(cudaEventElapsedTime(&ms, w->ev0, w->ev1));
+  if ((r = read_state(w, s))) return r;
+  unsigned long long h[2] = {0, 0};
+  DP_CUDA(cudaMemcpyAsync(h, sums, sizeof(h), cudaMemcpyDeviceToHost, s));
+  DP_CUDA(cudaStreamSynchronize(s));
+  if (total_weight) *total_weight = (int64_t)h[0];
+  if (nedges) *nedges = (int64_t)h[1];
+  rc.ms_kernel_sum = rc.ms_kernel_max = ms;
+  finish_stats(w, rc, ms, st);
+  if (st) st->iterations = rounds + 1;  // + the final find that saw no edge
+  return 0;
+}
+
 // single host launch apps
 template <class App>
 int once(Workspace* w, const dp_config* c, const App& app, long long nparents,
@@ -1380,6 +1541,39 @@ int dp_gc_dev(const int32_t* d_rowptr, const int32_t* d_col, int32_t n,
   const double t0 = now_ns();
   int r = gc_dev_impl(d_rowptr, d_col, n, m, cfg, d_color,
                       (cudaStream_t)stream, stats);
+  if (stats) stats->ns_host = now_ns() - t0;
+  return r;
+}
+
+int dp_mst(const int32_t* rowptr, const int32_t* col, const int32_t* weight,
+           const int32_t* eid, int32_t n, int64_t m, const dp_config* cfg_find,
+           const dp_config* cfg_verify, uint8_t* in_mst, int64_t* total_weight,
+           int64_t* nedges, dp_stats* stats) {
+  DP_HOST_CALL_BEGIN
+  if (n < 0 || m < 0) return fail(DP_ERR_INVALID, "bad graph size");
+  DP_TRY(stage(w_, 0, rowptr, (size_t)(n + 1) * 4, s_, &h2d_));
+  DP_TRY(stage(w_, 1, col, (size_t)m * 4, s_, &h2d_));
+  DP_TRY(stage(w_, 4, weight, (size_t)m * 4, s_, &h2d_));
+  DP_TRY(stage(w_, 2, eid, (size_t)m * 4, s_, &h2d_));
+  DP_TRY(stage(w_, 3, nullptr, (size_t)m + 1, s_, &h2d_));
+  DP_TRY(mst_dev_impl((int*)w_->io[0], (int*)w_->io[1], (int*)w_->io[4],
+                      (int*)w_->io[2], n, m, cfg_find, cfg_verify,
+                      (uint8_t*)w_->io[3], total_weight, nedges, s_, stats));
+  DP_TRY(unstage(w_, 3, in_mst, (size_t)m, s_, &d2h_));
+  DP_HOST_CALL_END
+}
+
+int dp_mst_dev(const int32_t* d_rowptr, const int32_t* d_col,
+               const int32_t* d_weight, const int32_t* d_eid, int32_t n,
+               int64_t m, const dp_config* cfg_find,
+               const dp_config* cfg_verify, uint8_t* d_in_mst,
+               int64_t* total_weight, int64_t* nedges, void* stream,
+               dp_stats* stats) {
+  clear_stats(stats);
+  const double t0 = now_ns();
+  int r = mst_dev_impl(d_rowptr, d_col, d_weight, d_eid, n, m, cfg_find,
+                       cfg_verify, d_in_mst, total_weight, nedges,
+                       (cudaStream_t)stream, stats);
   if (stats) stats->ns_host = now_ns() - t0;
   return r;
 }

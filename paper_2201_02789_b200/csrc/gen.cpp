@@ -260,6 +260,31 @@ int dp_symmetrize(const int32_t* rowptr, const int32_t* col, int32_t n,
   return 0;
 }
 
+// For a symmetric CSR with sorted rows and no duplicates: mirror[e] = the
+// slot of (v, u) for the slot e of (u, v).  Returns DP_ERR_INVALID if some
+// reverse edge is missing (the graph is not symmetric).
+int dp_edge_mirror(const int32_t* rowptr, const int32_t* col, int32_t n,
+                   int32_t* mirror, int32_t nthreads) {
+  if (n < 0 || !mirror) return DP_ERR_INVALID;
+  const int nt = threads_of(nthreads);
+  int bad = 0;
+#pragma omp parallel for num_threads(nt) schedule(dynamic, 4096) reduction(| : bad)
+  for (int64_t u = 0; u < n; ++u)
+    for (int32_t e = rowptr[u]; e < rowptr[u + 1]; ++e) {
+      const int32_t v = col[e];
+      const int32_t* b = col + rowptr[v];
+      const int32_t* f = col + rowptr[v + 1];
+      const int32_t* p = std::lower_bound(b, f, (int32_t)u);
+      if (p == f || *p != u) {
+        bad = 1;
+        mirror[e] = -1;
+      } else {
+        mirror[e] = (int32_t)(p - col);
+      }
+    }
+  return bad ? DP_ERR_INVALID : 0;
+}
+
 void dp_free(void* p) { std::free(p); }
 
 }  // extern "C"

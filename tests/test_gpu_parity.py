@@ -526,3 +526,47 @@ def test_gc_rmat18_vs_oracle():
         rep, _ = run_config(bench, wl, BenchConfig(**policy))
         np.testing.assert_array_equal(rep.arrays["color"], want)
         assert int(rep.arrays["color"].max()) + 1 == k
+
+
+MST_POLICIES = (dict(), dict(threshold=INF_THRESHOLD), dict(agg="warp"),
+                dict(threshold=32, agg="block"),
+                dict(threshold=64, cfactor=4, agg="multiblock", group_size=4,
+                     serial="warp"),
+                dict(threshold=256, cfactor=8, agg="multiblock",
+                     group_size=1 << 20, parent_block=256, child_block=128,
+                     serial="warp"),
+                dict(threshold=32, agg="grid", serial="warp"))
+
+
+def _mst_want(wl):
+    b = wl.buffers
+    return oracle.mst(b["rowptr"], b["col"], b["weight"], b["eid"])
+
+
+@pytest.mark.parametrize("bench_name", ["mstf", "mstv"])
+@pytest.mark.parametrize("spec", ["hand", "powerlaw:2000:seed1",
+                                  "road:1000:seed7", "rmat:12:seed1"])
+def test_mst_vs_oracle(bench_name, spec):
+    bench, wl = load(bench_name, spec)
+    in_mst, total, k = _mst_want(wl)
+    for policy in MST_POLICIES:
+        rep, _ = run_config(bench, wl, BenchConfig(**policy))
+        np.testing.assert_array_equal(rep.arrays["in_mst"], in_mst)
+        assert rep.arrays["weight"].tolist() == [total, k]
+    ref = run_reference(bench, wl)
+    np.testing.assert_array_equal(ref.arrays["in_mst"], in_mst)
+    assert ref.arrays["weight"].tolist() == [total, k]
+
+
+def test_mst_rmat18_and_long_chains_vs_oracle():
+    # rmat: one giant component + isolated vertices; road:20000: long hook
+    # chains (pointer jumping depth)
+    for spec in ("rmat:18:seed2", "road:20000:seed1"):
+        for name in ("mstf", "mstv"):
+            bench, wl = load(name, spec)
+            in_mst, total, k = _mst_want(wl)
+            for policy in MST_POLICIES[3:]:
+                rep, _ = run_config(bench, wl, BenchConfig(**policy))
+                np.testing.assert_array_equal(rep.arrays["in_mst"], in_mst)
+                assert rep.arrays["weight"].tolist() == [total, k]
+                assert rep.iterations <= 64

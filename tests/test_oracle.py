@@ -331,3 +331,64 @@ def test_symmetrize_matches_numpy():
     np.testing.assert_array_equal(s.col, b[order])
     np.testing.assert_array_equal(
         s.rowptr, np.concatenate(([0], np.cumsum(np.bincount(a, minlength=g.n)))))
+
+
+# ---------------------------------------------------------------------------
+# minimum spanning forest (MSTF / MSTV; no reference implementation): the
+# Kruskal oracle against scipy's MST weight and a pure-Python Kruskal
+# ---------------------------------------------------------------------------
+
+MST_SPECS = ["hand", "rmat:9:seed1", "powerlaw:400:seed2", "road:500:seed3",
+             "powerlaw:2000:seed1"]
+
+
+@pytest.mark.parametrize("spec", MST_SPECS)
+def test_mst_inputs_are_symmetric_and_canonical(spec):
+    s = parse_spec(spec)
+    g, w, eid = graphs.mst_inputs(make_graph(s), s.seed)
+    mirror = graphs.edge_mirror(g)
+    src = np.repeat(np.arange(g.n), np.diff(g.rowptr))
+    np.testing.assert_array_equal(src[mirror], g.col)       # reverse slot
+    np.testing.assert_array_equal(g.col[mirror], src)
+    np.testing.assert_array_equal(eid, np.minimum(np.arange(g.m), mirror))
+    np.testing.assert_array_equal(w, w[mirror])              # symmetric
+    assert w.min() >= 1 and w.max() <= 9
+    assert np.all(src[eid] < g.col[eid])                     # (min, max) copy
+
+
+@pytest.mark.parametrize("spec", MST_SPECS)
+def test_oracle_mst_weight_matches_scipy(spec):
+    from scipy.sparse import csr_matrix
+    from scipy.sparse.csgraph import connected_components, minimum_spanning_tree
+    s = parse_spec(spec)
+    g, w, eid = graphs.mst_inputs(make_graph(s), s.seed)
+    in_mst, total, k = oracle.mst(g.rowptr, g.col, w, eid)
+    a = csr_matrix((w.astype(np.float64), g.col, g.rowptr), shape=(g.n, g.n))
+    assert total == int(minimum_spanning_tree(a).sum())
+    ncomp, _ = connected_components(a, directed=False)
+    assert k == g.n - ncomp == int(in_mst.sum())
+    assert total == int(w[in_mst.astype(bool)].sum())
+    assert np.all(eid[in_mst.astype(bool)] == np.flatnonzero(in_mst))
+
+
+@pytest.mark.parametrize("spec", ["hand", "powerlaw:150:seed2",
+                                  "road:180:seed3", "rmat:7:seed2"])
+def test_oracle_mst_is_kruskal_in_key_order(spec):
+    s = parse_spec(spec)
+    g, w, eid = graphs.mst_inputs(make_graph(s), s.seed)
+    in_mst, _, _ = oracle.mst(g.rowptr, g.col, w, eid)
+    src = np.repeat(np.arange(g.n), np.diff(g.rowptr))
+    parent = list(range(g.n))
+
+    def find(x):
+        while parent[x] != x:
+            x = parent[x]
+        return x
+    want = np.zeros(g.m, np.uint8)
+    for e in sorted((e for e in range(g.m) if eid[e] == e),
+                    key=lambda e: (int(w[e]), e)):
+        a, b = find(int(src[e])), find(int(g.col[e]))
+        if a != b:
+            parent[max(a, b)] = min(a, b)
+            want[e] = 1
+    np.testing.assert_array_equal(in_mst, want)
