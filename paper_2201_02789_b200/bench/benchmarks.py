@@ -246,9 +246,15 @@ def _gc_traffic(wl, out, st):
 # mstf / mstv (Boruvka minimum spanning forest, no
 # reference code).  Both run the whole forest computation; the BenchConfig
 # policy drives the nested find kernel (mstf) or the nested verify kernel
-# (mstv) and the other kernel runs its serial (No-CDP) form, so each row
-# measures one kernel's transformation as the paper's Table I does.
+# (mstv), as the paper's Table I rows do.  The other kernel runs a fixed
+# policy (MST_OTHER_POLICY) so it does not mask the measured one: its No-CDP
+# form would leave a hub's whole edge list to one warp (round 0: 12 ms of a
+# 16 ms RMAT-22 run, profiles/).  run_reference runs both kernels No-CDP.
 # ---------------------------------------------------------------------------
+
+MST_OTHER_POLICY = dict(threshold=1024, cfactor=16, agg="multiblock",
+                        group_size=1 << 20, parent_block=256, child_block=128,
+                        serial="warp")
 
 def _mst_prepare(spec: DatasetSpec) -> Workload:
     g, w, eid = mst_inputs(make_graph(spec), spec.seed)
@@ -257,10 +263,14 @@ def _mst_prepare(spec: DatasetSpec) -> Workload:
         "eid": eid})
 
 
-def _nocdp_copy(cfg: _lib.DpConfig) -> _lib.DpConfig:
-    c = _lib.DpConfig.from_buffer_copy(cfg)
-    c.variant = _lib.VARIANT_NOCDP
-    return c
+def _other_cfg(cfg: _lib.DpConfig) -> _lib.DpConfig:
+    """The fixed policy of the kernel the row does not measure (No-CDP when
+    the measured kernel is No-CDP, i.e. under run_reference)."""
+    if cfg.variant == _lib.VARIANT_NOCDP:
+        c = _lib.DpConfig.from_buffer_copy(cfg)
+        return c
+    from .harness import BenchConfig
+    return BenchConfig(**MST_OTHER_POLICY).to_c(_lib.VARIANT_CDP)
 
 
 def _mst_run_with(wl: Workload, cfg_find, cfg_verify):
@@ -279,11 +289,11 @@ def _mst_run_with(wl: Workload, cfg_find, cfg_verify):
 
 
 def _mstf_run(wl: Workload, cfg: _lib.DpConfig):
-    return _mst_run_with(wl, cfg, _nocdp_copy(cfg))
+    return _mst_run_with(wl, cfg, _other_cfg(cfg))
 
 
 def _mstv_run(wl: Workload, cfg: _lib.DpConfig):
-    return _mst_run_with(wl, _nocdp_copy(cfg), cfg)
+    return _mst_run_with(wl, _other_cfg(cfg), cfg)
 
 
 def mst_traffic(n: int, m: int, rounds: int) -> int:

@@ -2,7 +2,7 @@ import time, numpy as np, sys
 sys.path.insert(0, '.')
 from paper_2201_02789_b200.bench import load, run_config, run_reference, BenchConfig, INF_THRESHOLD
 from oracle import oracle
-for spec in ["rmat:20:seed1", "rmat:22:seed1"]:
+for spec in sys.argv[1:] or ["rmat:22:seed1"]:
     t=time.time(); bench, wl = load("mstf", spec); print(spec, "prep s", round(time.time()-t,1), "m", wl.buffers["col"].shape[0], flush=True)
     b=wl.buffers
     t=time.time(); want=oracle.mst(b["rowptr"], b["col"], b["weight"], b["eid"]); print("oracle s", round(time.time()-t,1), want[1:], flush=True)
