@@ -195,6 +195,28 @@ int dp_mst_dev(const int32_t* d_rowptr, const int32_t* d_col,
                int64_t* total_weight, int64_t* nedges, void* stream,
                dp_stats* stats);
 
+/* ---- survey propagation on random k-SAT (no reference) ----- */
+/* Clause a owns edges [a*k, (a+1)*k): lits[e] = var << 1 | negated.
+ * occ_row[nvars+1] / occ[nclauses*k]: each variable's edges (variable-major
+ * CSR).  eta0[nclauses*k]: initial surveys.  Synchronous sweeps (nested
+ * variable->occurrence product kernel, nested clause->literal survey kernel)
+ * until max |eta' - eta| <= eps or max_sweeps.  Out: eta (final surveys),
+ * wpos/wneg[nvars] variable biases W+ / W-, *sweeps, *delta (last max
+ * change).  fp64 arithmetic and surveys, fp32 biases; the per-variable
+ * product order is schedule-dependent, so results equal the CPU oracle
+ * within a tolerance. */
+int dp_sp(const int32_t* lits, int32_t k, int32_t nclauses,
+          const int32_t* occ_row, const int32_t* occ, int32_t nvars,
+          const double* eta0, int32_t max_sweeps, float eps,
+          const dp_config* cfg, double* eta, float* wpos, float* wneg,
+          int32_t* sweeps, float* delta, dp_stats* stats);
+/* device buffers; d_eta holds eta0 on entry and the final surveys on return */
+int dp_sp_dev(const int32_t* d_lits, int32_t k, int32_t nclauses,
+              const int32_t* d_occ_row, const int32_t* d_occ, int32_t nvars,
+              int32_t max_sweeps, float eps, const dp_config* cfg,
+              double* d_eta, float* d_wpos, float* d_wneg, int32_t* sweeps,
+              float* delta, void* stream, dp_stats* stats);
+
 /* ---- BFS over a cyclic 1D vertex partition ------- */
 /* One level on part `part` of `nparts` (owner(v) = v % nparts; local index
  * v / nparts).  d_rowptr_p/d_col_p: the part's rows (dp_rmat_csr_part),

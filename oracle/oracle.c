@@ -17,6 +17,7 @@
  *   oracle_bt          Bezier tessellation, fp64 vertices, fp32 counts
  *   oracle_gc          greedy colouring in Jones-Plassmann priority order
  *   oracle_mst         Kruskal minimum spanning forest in (weight, eid) order
+ *   oracle_sp          survey propagation sweeps on a k-SAT factor graph
  *
  * Parallel versions (nthreads > 1) use the same atomics the reference's
  * kernels use; outputs are schedule-invariant (benchmarks.py:10-15), so any
@@ -311,4 +312,110 @@ int64_t oracle_mst(const int32_t* rowptr, const int32_t* col,
   free(src);
   free(parent);
   return nedges;
+}
+
+/* ---- survey propagation on random k-SAT (no reference
+ * implementation) -------------------------------------------------------------
+ * Synchronous sweeps in the Braunstein-Mezard-Zecchina form: per variable the
+ * products P_s = prod (1 - eta) over its positive / negative occurrences
+ * (zero factors counted apart), then per edge (a, i)
+ *   eta'[a,i] = prod_{j in a, j != i} Pu / (Pu + Ps + P0),
+ *   S = P_s(j) / (1 - eta[a,j]), U = P_-s(j), Pu = (1-U)S, Ps = (1-S)U, P0 = SU.
+ * fp64 arithmetic and surveys (no contraction: -ffp-contract=off), products
+ * in ascending occurrence order.  Stops when max |eta' - eta| <= eps or after
+ * max_sweeps; then the biases W+ / W- of every variable.  Returns sweeps. */
+typedef struct {
+  double p[2];
+  int32_t z[2];
+} sp_prod;
+
+static void sp_var_pass(int32_t nvars, const int32_t* occ_row,
+                        const int32_t* occ, const int32_t* lits,
+                        const double* eta, sp_prod* prod) {
+  for (int32_t i = 0; i < nvars; ++i) {
+    sp_prod q = {{1.0, 1.0}, {0, 0}};
+    for (int32_t t = occ_row[i]; t < occ_row[i + 1]; ++t) {
+      const int32_t e = occ[t];
+      const int neg = lits[e] & 1;
+      const double f = 1.0 - eta[e];
+      if (f == 0.0)
+        q.z[neg] += 1;
+      else
+        q.p[neg] *= f;
+    }
+    prod[i] = q;
+  }
+}
+
+static double sp_ratio(const sp_prod* q, int neg, double eta_e) {
+  const double f = 1.0 - eta_e;
+  double S;
+  if (f == 0.0)
+    S = q->z[neg] - 1 == 0 ? q->p[neg] : 0.0;
+  else
+    S = q->z[neg] == 0 ? q->p[neg] / f : 0.0;
+  const double U = q->z[neg ^ 1] == 0 ? q->p[neg ^ 1] : 0.0;
+  const double pu = (1.0 - U) * S;
+  const double ps = (1.0 - S) * U;
+  const double p0 = S * U;
+  const double den = (pu + ps) + p0;
+  return den > 0.0 ? pu / den : 0.0;
+}
+
+/* double -> float rounded towards +inf (the device's __double2float_ru) */
+static float sp_f32_up(double x) {
+  float f = (float)x;
+  if ((double)f < x) f = nextafterf(f, INFINITY);
+  return f;
+}
+
+int32_t oracle_sp(const int32_t* lits, int32_t k, int32_t nclauses,
+                  const int32_t* occ_row, const int32_t* occ, int32_t nvars,
+                  const double* eta0, int32_t max_sweeps, float eps,
+                  double* eta, float* wpos, float* wneg, float* last_delta) {
+  const int64_t ne = (int64_t)nclauses * k;
+  sp_prod* prod = (sp_prod*)malloc(sizeof(sp_prod) * (size_t)(nvars ? nvars : 1));
+  double* nxt = (double*)malloc(sizeof(double) * (size_t)(ne ? ne : 1));
+  if (!prod || !nxt) {
+    free(prod);
+    free(nxt);
+    return -1;
+  }
+  memcpy(eta, eta0, sizeof(double) * (size_t)ne);
+  int32_t sweeps = 0;
+  float delta = 0.f;
+  while (sweeps < max_sweeps) {
+    sp_var_pass(nvars, occ_row, occ, lits, eta, prod);
+    delta = 0.f;
+    for (int32_t a = 0; a < nclauses; ++a) {
+      const int64_t base = (int64_t)a * k;
+      for (int32_t t = 0; t < k; ++t) {
+        double v = 1.0;
+        for (int32_t j = 0; j < k; ++j) {
+          if (j == t) continue;
+          const int32_t l = lits[base + j];
+          v *= sp_ratio(&prod[l >> 1], l & 1, eta[base + j]);
+        }
+        const float d = sp_f32_up(fabs(v - eta[base + t]));
+        if (d > delta) delta = d;
+        nxt[base + t] = v;
+      }
+    }
+    memcpy(eta, nxt, sizeof(double) * (size_t)ne);
+    ++sweeps;
+    if (delta <= eps) break;
+  }
+  sp_var_pass(nvars, occ_row, occ, lits, eta, prod);
+  for (int32_t i = 0; i < nvars; ++i) {
+    const double pp = prod[i].z[0] == 0 ? prod[i].p[0] : 0.0;
+    const double pn = prod[i].z[1] == 0 ? prod[i].p[1] : 0.0;
+    const double ip = (1.0 - pp) * pn, in = (1.0 - pn) * pp, i0 = pp * pn;
+    const double den = (ip + in) + i0;
+    wpos[i] = den > 0.0 ? (float)(ip / den) : 0.f;
+    wneg[i] = den > 0.0 ? (float)(in / den) : 0.f;
+  }
+  if (last_delta) *last_delta = delta;
+  free(prod);
+  free(nxt);
+  return sweeps;
 }

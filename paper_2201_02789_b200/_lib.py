@@ -131,6 +131,12 @@ _SIGNATURES = {
                     ctypes.POINTER(ctypes.c_int64),
                     ctypes.POINTER(ctypes.c_int64), _P, _ST], ctypes.c_int),
     "dp_edge_mirror": ([_P, _P, _I32, _P, _I32], ctypes.c_int),
+    "dp_sp": ([_P, _I32, _I32, _P, _P, _I32, _P, _I32, _F32, _CFG, _P, _P,
+               _P, ctypes.POINTER(ctypes.c_int32),
+               ctypes.POINTER(ctypes.c_float), _ST], ctypes.c_int),
+    "dp_sp_dev": ([_P, _I32, _I32, _P, _P, _I32, _I32, _F32, _CFG, _P, _P,
+                   _P, ctypes.POINTER(ctypes.c_int32),
+                   ctypes.POINTER(ctypes.c_float), _P, _ST], ctypes.c_int),
     "dp_free": ([_P], None),
 }
 

@@ -15,6 +15,7 @@ Applications
   gc          Jones-Plassmann graph colouring                 (new, north star)
   mstf, mstv  Boruvka minimum spanning forest; the policy drives the find
               (mstf) or the verify (mstv) kernel          (new)
+  sp          survey propagation sweeps on random k-SAT  (new)
   bt          Bezier line tessellation                        (new, config 2)
 Outputs are written only through commutative / idempotent atomics, so they
 are schedule-invariant and must match the serial variant element-exactly
@@ -31,8 +32,9 @@ import numpy as np
 
 from .. import _lib
 from .graphs import (BT_CURV_SCALE, BT_MAX_TESS, UNREACHED, DatasetSpec,
-                     bezier_curves, child_sizes, edge_weights, make_graph,
-                     mst_inputs, parse_spec, symmetrize, tc_orient)
+                     bezier_curves, child_sizes, edge_weights, make_formula,
+                     make_graph, mst_inputs, parse_spec, sp_initial_surveys,
+                     symmetrize, tc_orient)
 
 BLOCK = 32  # parent block size of every reference driver (benchmarks.py:44)
 
@@ -57,6 +59,8 @@ class Benchmark:
     # (workload, outputs, stats) -> (work units, algorithmic bytes)
     traffic: Callable[[Workload, dict, dict], tuple]
     description: str = ""
+    # floating-point outputs: |got - ref| <= atol + rtol * |ref|
+    tol: tuple = (0.0, 1e-5)
 
     def workload(self, spec_text: str) -> Workload:
         return self.prepare(parse_spec(spec_text))
@@ -309,6 +313,62 @@ def _mst_traffic(wl, out, st):
 
 
 # ---------------------------------------------------------------------------
+# sp (survey propagation on random k-SAT, no reference code)
+# ---------------------------------------------------------------------------
+
+SP_MAX_SWEEPS = 100   # per run; the paper's benchmark iterates to convergence
+SP_EPS = 1e-3         # max |eta' - eta| that stops the sweeps
+# north star: messages within 1e-5 relative; surveys far below 1e-2 are
+# compared absolutely (their relative error is set by cancellation in 1 - U)
+SP_RTOL, SP_ATOL = 1e-5, 1e-7
+
+
+def _sp_prepare(spec: DatasetSpec) -> Workload:
+    f = make_formula(spec)
+    return Workload(spec=spec, n=f.nvars, payload=f, buffers={
+        "lits": f.lits, "occ_row": f.occ_row, "occ": f.occ,
+        "eta0": sp_initial_surveys(f, spec.seed), "k": f.k,
+        "max_sweeps": SP_MAX_SWEEPS, "eps": SP_EPS})
+
+
+def _sp_run(wl: Workload, cfg: _lib.DpConfig):
+    lib = _lib.device()
+    b = wl.buffers
+    f = wl.payload
+    ne = int(b["lits"].shape[0])
+    eta = np.empty(max(ne, 1), dtype=np.float64)
+    wpos = np.empty(max(f.nvars, 1), dtype=np.float32)
+    wneg = np.empty(max(f.nvars, 1), dtype=np.float32)
+    sweeps = ctypes.c_int32()
+    delta = ctypes.c_float()
+    st = _call(lib.dp_sp, _lib.ptr(b["lits"]), f.k, f.nclauses,
+               _lib.ptr(b["occ_row"]), _lib.ptr(b["occ"]), f.nvars,
+               _lib.ptr(b["eta0"]), int(b["max_sweeps"]), float(b["eps"]),
+               ctypes.byref(cfg), _lib.ptr(eta), _lib.ptr(wpos),
+               _lib.ptr(wneg), ctypes.byref(sweeps), ctypes.byref(delta))
+    st["sp_delta"] = float(delta.value)
+    return {"eta": eta[:ne], "wpos": wpos[:f.nvars],
+            "wneg": wneg[:f.nvars]}, st
+
+
+def sp_traffic(nvars: int, nedges: int, k: int, sweeps: int) -> int:
+    """Per sweep: variable pass 24 B per variable (occ_row pair, product
+    reset) + 24 B per occurrence (occ, lit, eta 8, 8 B product update);
+    clause pass per edge 16 B (eta' write, eta read) + (k-1) x (lit 4 +
+    eta 8 + product 24) reads.  The final bias pass adds one variable pass."""
+    var = 24 * nvars + 24 * nedges
+    clause = nedges * (16 + (k - 1) * 36)
+    return sweeps * (var + clause) + var + 8 * nvars
+
+
+def _sp_traffic(wl, out, st):
+    f = wl.payload
+    ne = int(f.lits.shape[0])
+    sweeps = int(st["iterations"])
+    return ne * sweeps, sp_traffic(f.nvars, ne, f.k, sweeps)
+
+
+# ---------------------------------------------------------------------------
 # bt
 # ---------------------------------------------------------------------------
 
@@ -388,6 +448,11 @@ BENCHMARKS: dict[str, Benchmark] = {
                                                      "weight": "long"},
                       _mst_prepare, _mstv_run, _mst_traffic,
                       "Boruvka MST, policy on the verify kernel (new)"),
+    "sp": Benchmark("sp", ("eta", "wpos", "wneg"),
+                    {"eta": "float", "wpos": "float", "wneg": "float"},
+                    _sp_prepare, _sp_run, _sp_traffic,
+                    "survey propagation on random k-SAT (new)",
+                    tol=(SP_RTOL, SP_ATOL)),
     "bt": Benchmark("bt", ("ntess", "verts"), {"ntess": "int",
                                                "verts": "float"},
                     _bt_prepare, _bt_run, _bt_traffic,

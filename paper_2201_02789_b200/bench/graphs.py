@@ -13,6 +13,8 @@ spec           contents                                           reference
 ``sizes:N``    child-grid sizes, 90% in [0,31], 10% in [256,1024]  :194-201
 ``rmat:S``     RMAT scale S, edge factor 16 (new: BASELINE.json)   --
 ``curves:N``   N quadratic Bezier curves (new: BASELINE.json)      --
+``ksat3:N``    random 3-SAT, N variables, 4.2 N clauses (SP)       --
+``ksat5:N``    random 5-SAT, N variables, 20 N clauses (SP)        --
 =============  =================================================  ==========
 
 Streams: every generator draws from ``default_rng(SeedSequence([stream_id,
@@ -31,13 +33,15 @@ import numpy as np
 UNREACHED = 1 << 30  # distance sentinel (graphs.py:29)
 
 GRAPH_KINDS = ("hand", "powerlaw", "road", "rmat")
-DATASET_KINDS = GRAPH_KINDS + ("sizes", "curves")
+SAT_KINDS = {"ksat3": (3, 4.2), "ksat5": (5, 20.0)}  # (k, clause ratio)
+DATASET_KINDS = GRAPH_KINDS + ("sizes", "curves") + tuple(SAT_KINDS)
 
 RMAT_EDGE_FACTOR = 16  # Graph500 / BASELINE.json configs
 BT_MAX_TESS = 2048     # T2048-C64
 BT_CURV_SCALE = 64.0
 
-_STREAM = {"powerlaw": 1, "road": 2, "weights": 3, "sizes": 4, "curves": 5}
+_STREAM = {"powerlaw": 1, "road": 2, "weights": 3, "sizes": 4, "curves": 5,
+           "sat": 6, "sat_eta": 7}
 
 
 def _rng(stream: str, *keys: int) -> np.random.Generator:
@@ -288,3 +292,58 @@ def mst_inputs(graph: Graph, seed: int) -> tuple:
 def bezier_curves(n: int, seed: int) -> np.ndarray:
     """float32[n, 3, 2] control points, U[0,1)^2."""
     return _rng("curves", n, seed).random((n, 3, 2), dtype=np.float32)
+
+
+# ---------------------------------------------------------------------------
+# survey propagation input: random k-SAT (the paper's RAND-3 / 5-SAT sets,
+# PAPER.md:436; generator builder-defined)
+# ---------------------------------------------------------------------------
+
+@dataclass(frozen=True, eq=False)
+class Formula:
+    """k-SAT factor graph.  Clause a owns edges [a*k, (a+1)*k) with
+    ``lits[e] = var << 1 | negated``; ``occ_row``/``occ`` list each
+    variable's edges in ascending edge order (variable-major CSR)."""
+    k: int
+    nvars: int
+    lits: np.ndarray
+    occ_row: np.ndarray
+    occ: np.ndarray
+
+    @property
+    def nclauses(self) -> int:
+        return int(self.lits.shape[0]) // self.k
+
+
+def random_ksat(nvars: int, k: int, ratio: float, seed: int) -> Formula:
+    """round(ratio * nvars) clauses of k distinct variables each, uniform
+    signs; stream ``sat`` keyed by (nvars, k, seed)."""
+    if nvars < k:
+        raise ValueError(f"a {k}-SAT formula needs at least {k} variables")
+    rng = _rng("sat", nvars, k, seed)
+    m = int(round(ratio * nvars))
+    var = rng.integers(0, nvars, size=(m, k), dtype=np.int64)
+    while True:  # redraw clauses that repeat a variable
+        srt = np.sort(var, axis=1)
+        bad = np.flatnonzero((srt[:, 1:] == srt[:, :-1]).any(axis=1))
+        if bad.size == 0:
+            break
+        var[bad] = rng.integers(0, nvars, size=(bad.size, k), dtype=np.int64)
+    neg = rng.integers(0, 2, size=(m, k), dtype=np.int64)
+    lits = ((var << 1) | neg).reshape(-1).astype(np.int32)
+    v = var.reshape(-1)
+    occ = np.argsort(v, kind="stable").astype(np.int32)
+    occ_row = np.concatenate(([0], np.cumsum(np.bincount(v, minlength=nvars))))
+    return Formula(k, nvars, lits, occ_row.astype(np.int32), occ)
+
+
+def sp_initial_surveys(f: Formula, seed: int) -> np.ndarray:
+    """eta0 ~ U[0, 1) per edge, float64 (stream ``sat_eta``)."""
+    return _rng("sat_eta", f.nvars, f.k, seed).random(f.lits.shape[0])
+
+
+def make_formula(spec: DatasetSpec) -> Formula:
+    if spec.kind not in SAT_KINDS:
+        raise ValueError(f"dataset kind {spec.kind!r} is not a k-SAT formula")
+    k, ratio = SAT_KINDS[spec.kind]
+    return random_ksat(spec.size, k, ratio, spec.seed)

@@ -198,8 +198,9 @@ def run_config(bench: Benchmark, wl: Workload, cfg: BenchConfig, cost=None,
 def verify_outputs(bench: Benchmark, wl: Workload, got: Report, ref: Report,
                    label: str = "") -> None:
     """Raise EquivalenceError at the first divergent output element
-    (harness.py:83-96).  Floating-point outputs (bt vertices) compare within
-    BT_ABS_TOL; everything else bit-exactly."""
+    (harness.py:83-96).  Floating-point outputs compare within the
+    benchmark's tolerance (bt vertices: BT_ABS_TOL absolute; sp surveys:
+    1e-5 relative); everything else bit-exactly."""
     for name in bench.outputs:
         g = np.asarray(got.arrays[name])
         r = np.asarray(ref.arrays[name])
@@ -208,7 +209,8 @@ def verify_outputs(bench: Benchmark, wl: Workload, got: Report, ref: Report,
                 f"{bench.name}/{wl.spec.text}{label}: buffer '{name}' has "
                 f"{g.shape[0]} elements, reference has {r.shape[0]}")
         if g.dtype.kind == "f" or r.dtype.kind == "f":
-            bad = ~np.isclose(g, r, rtol=0.0, atol=BT_ABS_TOL)
+            rtol, atol = bench.tol
+            bad = ~np.isclose(g, r, rtol=rtol, atol=atol)
             if bad.ndim > 1:
                 bad = bad.any(axis=tuple(range(1, bad.ndim)))
         else:

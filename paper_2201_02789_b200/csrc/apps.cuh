@@ -984,4 +984,207 @@ struct MstVerifyApp {
   __device__ void flush(Acc&) const {}
 };
 
+// ---------------------------------------------------------------------------
+// Survey propagation on random k-SAT — the paper's SP (from the
+// LonestarGPU / KLAP suite; no reference code).  Factor graph: clause a owns
+// edges e in [a*k, (a+1)*k), lit[e] = var << 1 | negated; the variable-major
+// CSR (occ_row, occ) lists each variable's edges.  One synchronous sweep of
+// the surveys eta (Braunstein, Mezard, Zecchina 2005):
+//   SpVarApp    parent = variable i, child item = occurrence e of i:
+//               P_s(i) *= (1 - eta[e]) for the occurrence's sign s, zero
+//               factors counted apart (so one factor can be divided out)
+//   SpClauseApp parent = clause a, child item = edge (a, i):
+//               eta'[a, i] = prod_{j in a, j != i} Pu_j / (Pu_j + Ps_j + P0_j)
+//               with S = P_s(j) / (1 - eta[a, j]) (a excluded), U = P_-s(j):
+//               Pu = (1-U) S, Ps = (1-S) U, P0 = S U.
+// Arithmetic and storage in fp64 (explicit round-to-nearest ops, no FMA
+// contraction, as the CPU oracle does).  The product order of P_s depends on
+// the schedule, so results match the oracle within a tolerance, not
+// bit-exactly (tests state it).  fp64 storage matters: the first sweeps
+// amplify perturbations ~1e6-fold (a 1-ulp fp32 change of eta0 moves 5-SAT
+// surveys by 0.08 after 10 sweeps), so fp32 rounding flips would not stay
+// within tolerance; fp64 order effects (~1e-16) do.
+// ---------------------------------------------------------------------------
+struct SpVarProd {
+  double p[2];  // product of the non-zero (1 - eta) factors, per sign
+  int z[2];     // zero factors, per sign
+};
+
+__device__ __forceinline__ void atomic_mul_f64(double* addr, double f) {
+  unsigned long long* a = reinterpret_cast<unsigned long long*>(addr);
+  unsigned long long old = __ldcg(a), assumed;
+  do {
+    assumed = old;
+    old = atomicCAS(a, assumed,
+                    __double_as_longlong(__dmul_rn(__longlong_as_double(assumed), f)));
+  } while (old != assumed);
+}
+
+struct SpVarApp {
+  const int* __restrict__ occ_row;
+  const int* __restrict__ occ;
+  const int* __restrict__ lit;
+  const double* __restrict__ eta;
+  SpVarProd* prod;
+  int nvars;
+  int pad;
+
+  struct alignas(16) Args {
+    int start, deg, i, pad;
+  };
+  // run-length partial product of the variable this thread is working on:
+  // committed when the thread moves to another variable, and in flush()
+  // merged across the lanes of the warp holding the same variable, so a
+  // variable costs ~one CAS per sign per warp instead of one per occurrence
+  // (5-SAT: ~100 occurrences per variable hitting two words)
+  struct Acc {
+    int has, var;
+    int z[2];
+    double p[2];
+  };
+
+  __device__ int nparents() const { return nvars; }
+  __device__ void parent_prologue() const {}
+  __device__ int expand(int i, bool valid, Args& a) const {
+    if (!valid) return 0;
+    const int s = __ldg(occ_row + i);
+    const int d = __ldg(occ_row + i + 1) - s;
+    a = Args{s, d, i, 0};
+    return d > 0 ? d : 0;
+  }
+  __device__ static int count(const Args& a) { return a.deg; }
+  __device__ void commit(int var, const double* p, const int* z) const {
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      if (p[s] != 1.0) atomic_mul_f64(&prod[var].p[s], p[s]);
+      if (z[s]) atomicAdd(&prod[var].z[s], z[s]);
+    }
+  }
+  __device__ void item(const Args& a, int t, Acc& acc) const {
+    const int e = ld_stream(occ + a.start + t);
+    const int neg = __ldg(lit + e) & 1;
+    const double f = __dsub_rn(1.0, __ldg(eta + e));
+    if (acc.has && acc.var != a.i) {
+      commit(acc.var, acc.p, acc.z);
+      acc.has = 0;
+    }
+    if (!acc.has) {
+      acc.has = 1;
+      acc.var = a.i;
+      acc.p[0] = acc.p[1] = 1.0;
+      acc.z[0] = acc.z[1] = 0;
+    }
+    if (f == 0.0)
+      acc.z[neg] += 1;
+    else
+      acc.p[neg] = __dmul_rn(acc.p[neg], f);
+  }
+  static constexpr int kUnroll = 1;
+  static constexpr bool kBlockMode = false;
+  static constexpr bool kPureExpand = true;
+  static constexpr int kMinBlocks = 1;
+  template <int U, class ArgsOf>
+  __device__ __forceinline__ void items(ArgsOf args, const int* e,
+                                        const bool* ok, Acc& acc) const {
+    items_loop<U>(*this, args, e, ok, acc);
+  }
+  __device__ void flush(Acc& acc) const {
+    const int key = acc.has ? acc.var : -1;
+    const unsigned grp = __match_any_sync(DP_FULL, key);
+    const int leader = __ffs(grp) - 1;
+    double p0 = 1.0, p1 = 1.0;
+    int z0 = 0, z1 = 0;
+    for (unsigned m = grp; m; m &= m - 1) {  // same trip count in the group
+      const int src = __ffs(m) - 1;
+      p0 = __dmul_rn(p0, __shfl_sync(grp, acc.p[0], src));
+      p1 = __dmul_rn(p1, __shfl_sync(grp, acc.p[1], src));
+      z0 += __shfl_sync(grp, acc.z[0], src);
+      z1 += __shfl_sync(grp, acc.z[1], src);
+    }
+    if (key >= 0 && lane_id() == leader) {
+      const double p[2] = {p0, p1};
+      const int z[2] = {z0, z1};
+      commit(key, p, z);
+    }
+  }
+};
+
+// the survey a variable's occurrence e contributes towards its clause:
+// Pu / (Pu + Ps + P0) (0 when all three vanish)
+__device__ __forceinline__ double sp_ratio(const SpVarProd& q, int neg,
+                                           double eta_e) {
+  const double f = __dsub_rn(1.0, eta_e);
+  double S;  // same-sign product with this clause divided out
+  if (f == 0.0)
+    S = q.z[neg] - 1 == 0 ? q.p[neg] : 0.0;
+  else
+    S = q.z[neg] == 0 ? __ddiv_rn(q.p[neg], f) : 0.0;
+  const double U = q.z[neg ^ 1] == 0 ? q.p[neg ^ 1] : 0.0;
+  const double pu = __dmul_rn(__dsub_rn(1.0, U), S);
+  const double ps = __dmul_rn(__dsub_rn(1.0, S), U);
+  const double p0 = __dmul_rn(S, U);
+  const double den = __dadd_rn(__dadd_rn(pu, ps), p0);
+  return den > 0.0 ? __ddiv_rn(pu, den) : 0.0;
+}
+
+struct SpClauseApp {
+  const int* __restrict__ lit;
+  const double* __restrict__ eta;  // previous sweep
+  const SpVarProd* __restrict__ prod;
+  double* eta_next;
+  unsigned* max_delta;  // float bits of max |eta' - eta| (rounded up)
+  int nclauses;
+  int k;
+
+  struct alignas(16) Args {
+    int a, k, pad0, pad1;
+  };
+  struct Acc {
+    float delta;
+  };
+
+  __device__ int nparents() const { return nclauses; }
+  __device__ void parent_prologue() const {}
+  __device__ int expand(int a, bool valid, Args& r) const {
+    if (!valid) return 0;
+    r = Args{a, k, 0, 0};
+    return k;
+  }
+  __device__ static int count(const Args& r) { return r.k; }
+  __device__ void item(const Args& r, int t, Acc& acc) const {
+    const long long base = (long long)r.a * r.k;
+    double v = 1.0;
+    for (int j = 0; j < r.k; ++j) {  // fixed order: the oracle's
+      if (j == t) continue;
+      const int l = __ldg(lit + base + j);
+      SpVarProd q;
+      q.p[0] = __ldcg(&prod[l >> 1].p[0]);
+      q.p[1] = __ldcg(&prod[l >> 1].p[1]);
+      q.z[0] = __ldcg(&prod[l >> 1].z[0]);
+      q.z[1] = __ldcg(&prod[l >> 1].z[1]);
+      v = __dmul_rn(v, sp_ratio(q, l & 1, __ldg(eta + base + j)));
+    }
+    const float d = __double2float_ru(fabs(__dsub_rn(v, __ldg(eta + base + t))));
+    acc.delta = fmaxf(acc.delta, d);
+    eta_next[base + t] = v;
+  }
+  static constexpr int kUnroll = 1;
+  static constexpr bool kBlockMode = false;
+  static constexpr bool kPureExpand = true;
+  static constexpr int kMinBlocks = 1;
+  template <int U, class ArgsOf>
+  __device__ __forceinline__ void items(ArgsOf args, const int* e,
+                                        const bool* ok, Acc& acc) const {
+    items_loop<U>(*this, args, e, ok, acc);
+  }
+  __device__ void flush(Acc& acc) const {
+    float d = acc.delta;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) d = fmaxf(d, __shfl_xor_sync(DP_FULL, d, o));
+    if (lane_id() == 0 && d > 0.f &&
+        __float_as_uint(d) > __ldcg(max_delta))
+      atomicMax(max_delta, __float_as_uint(d));
+  }
+};
+
 }  // namespace dp

@@ -1056,6 +1056,130 @@ int mst_dev_impl(const int32_t* rowptr, const int32_t* col,
   return 0;
 }
 
+// ---------------------------------------------------------------------------
+// Survey propagation: sweeps of (reset products -> SpVarApp -> SpClauseApp)
+// until max |eta' - eta| <= eps or max_sweeps, then the variable biases.
+// ---------------------------------------------------------------------------
+__global__ void sp_reset_kernel(int n, SpVarProd* prod) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    SpVarProd q;
+    q.p[0] = q.p[1] = 1.0;
+    q.z[0] = q.z[1] = 0;
+    prod[i] = q;
+  }
+}
+
+// W+ = Pi+ / (Pi+ + Pi- + Pi0), W- likewise, with P+ / P- the products of
+// (1 - eta) over the positive / negative occurrences:
+// Pi+ = (1 - P+) P-, Pi- = (1 - P-) P+, Pi0 = P+ P-.
+__global__ void sp_bias_kernel(int n, const SpVarProd* __restrict__ prod,
+                               float* wpos, float* wneg) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const SpVarProd q = prod[i];
+    const double pp = q.z[0] == 0 ? q.p[0] : 0.0;
+    const double pn = q.z[1] == 0 ? q.p[1] : 0.0;
+    const double ip = __dmul_rn(__dsub_rn(1.0, pp), pn);
+    const double in = __dmul_rn(__dsub_rn(1.0, pn), pp);
+    const double i0 = __dmul_rn(pp, pn);
+    const double den = __dadd_rn(__dadd_rn(ip, in), i0);
+    wpos[i] = den > 0.0 ? __double2float_rn(__ddiv_rn(ip, den)) : 0.f;
+    wneg[i] = den > 0.0 ? __double2float_rn(__ddiv_rn(in, den)) : 0.f;
+  }
+}
+
+int sp_dev_impl(const int32_t* lits, int32_t k, int32_t nclauses,
+                const int32_t* occ_row, const int32_t* occ, int32_t nvars,
+                int32_t max_sweeps, float eps, const dp_config* c,
+                double* eta, float* wpos, float* wneg, int32_t* sweeps_done,
+                float* last_delta, cudaStream_t s, dp_stats* st) {
+  int r;
+  if ((r = validate(c))) return r;
+  if (k < 1 || k > 32 || nclauses < 0 || nvars < 0 || max_sweeps < 0)
+    return fail(DP_ERR_INVALID, "bad formula size");
+  Workspace* w = workspace(&r);
+  if (!w) return r;
+  const long long ne = (long long)nclauses * k;
+  // prod[nvars] | eta scratch[ne]
+  const size_t nv = (size_t)std::max(nvars, 1);
+  if ((r = grow(&w->io[5], &w->io_bytes[5],
+                nv * sizeof(SpVarProd) + (size_t)std::max(ne, 1LL) * 8)))
+    return r;
+  SpVarProd* prod = (SpVarProd*)w->io[5];
+  double* eta_b = (double*)(prod + nv);
+  long long lv = 0;
+  if (c->variant == DP_VARIANT_CDP &&
+      (r = count_launchers(w, c, occ_row, nvars, 0, s, &lv)))
+    return r;
+  // clause children (k each) launch when k >= T
+  const long long lc = effective_threshold(c) <= k ? nclauses : 0;
+  if ((r = ensure_pending_limit(w, c,
+                                std::max(launch_bound(c, nvars, lv),
+                                         launch_bound(c, nclauses, lc)))))
+    return r;
+  if ((r = begin_run(w, s))) return r;
+  const int vb = std::max(1, std::min(dp::ceil_div(std::max(nvars, 1), 256),
+                                      148 * 8));
+  RunCounters rc;
+  DP_CUDA(cudaEventRecord(w->ev0, s));
+  double* cur = eta;
+  double* nxt = eta_b;
+  int sweeps = 0;
+  float delta = 0.f;
+  auto var_pass = [&](const double* e) -> int {
+    sp_reset_kernel<<<vb, 256, 0, s>>>(nvars, prod);
+    DP_CUDA(cudaGetLastError());
+    rc.kernel_launches += 1;
+    SpVarApp va;
+    va.occ_row = occ_row;
+    va.occ = occ;
+    va.lit = lits;
+    va.eta = e;
+    va.prod = prod;
+    va.nvars = nvars;
+    va.pad = 0;
+    return launch_parent(va, nvars, lv, c, w, s, &rc);
+  };
+  while (sweeps < max_sweeps) {
+    if ((r = var_pass(cur))) return r;
+    DP_CUDA(cudaMemsetAsync(&w->ds->flag[0], 0, sizeof(int), s));
+    SpClauseApp ca;
+    ca.lit = lits;
+    ca.eta = cur;
+    ca.prod = prod;
+    ca.eta_next = nxt;
+    ca.max_delta = (unsigned*)&w->ds->flag[0];
+    ca.nclauses = nclauses;
+    ca.k = k;
+    if ((r = launch_parent(ca, nclauses, lc, c, w, s, &rc))) return r;
+    if ((r = read_state_fast(w, s))) return r;
+    std::swap(cur, nxt);
+    ++sweeps;
+    std::memcpy(&delta, &w->h_ds->flag[0], sizeof(float));
+    if (delta <= eps) break;
+  }
+  // biases from the final surveys
+  if ((r = var_pass(cur))) return r;
+  sp_bias_kernel<<<vb, 256, 0, s>>>(nvars, prod, wpos, wneg);
+  DP_CUDA(cudaGetLastError());
+  rc.kernel_launches += 1;
+  if (cur != eta && ne)
+    DP_CUDA(cudaMemcpyAsync(eta, cur, (size_t)ne * 8,
+                            cudaMemcpyDeviceToDevice, s));
+  DP_CUDA(cudaEventRecord(w->ev1, s));
+  DP_CUDA(cudaEventSynchronize(w->ev1));
+  float ms = 0.f;
+  DP_CUDA(cudaEventElapsedTime(&ms, w->ev0, w->ev1));
+  if ((r = read_state(w, s))) return r;
+  rc.ms_kernel_sum = rc.ms_kernel_max = ms;
+  finish_stats(w, rc, ms, st);
+  if (st) st->iterations = sweeps;
+  if (sweeps_done) *sweeps_done = sweeps;
+  if (last_delta) *last_delta = delta;
+  return 0;
+}
+
 // single host launch apps
 template <class App>
 int once(Workspace* w, const dp_config* c, const App& app, long long nparents,
@@ -1574,6 +1698,51 @@ int dp_mst_dev(const int32_t* d_rowptr, const int32_t* d_col,
   int r = mst_dev_impl(d_rowptr, d_col, d_weight, d_eid, n, m, cfg_find,
                        cfg_verify, d_in_mst, total_weight, nedges,
                        (cudaStream_t)stream, stats);
+  if (stats) stats->ns_host = now_ns() - t0;
+  return r;
+}
+
+int dp_sp(const int32_t* lits, int32_t k, int32_t nclauses,
+          const int32_t* occ_row, const int32_t* occ, int32_t nvars,
+          const double* eta0, int32_t max_sweeps, float eps,
+          const dp_config* cfg, double* eta, float* wpos, float* wneg,
+          int32_t* sweeps, float* delta, dp_stats* stats) {
+  DP_HOST_CALL_BEGIN
+  if (k < 1 || nclauses < 0 || nvars < 0)
+    return fail(DP_ERR_INVALID, "bad formula size");
+  const size_t ne = (size_t)nclauses * (size_t)k;
+  DP_TRY(stage(w_, 0, lits, ne * 4, s_, &h2d_));
+  DP_TRY(stage(w_, 1, occ_row, (size_t)(nvars + 1) * 4, s_, &h2d_));
+  DP_TRY(stage(w_, 2, occ, ne * 4, s_, &h2d_));
+  DP_TRY(stage(w_, 3, eta0, ne * 8, s_, &h2d_));
+  DP_TRY(stage(w_, 4, nullptr, (size_t)nvars * 8 + 8, s_, &h2d_));
+  float* d_wpos = (float*)w_->io[4];
+  float* d_wneg = d_wpos + nvars;
+  DP_TRY(sp_dev_impl((int*)w_->io[0], k, nclauses, (int*)w_->io[1],
+                     (int*)w_->io[2], nvars, max_sweeps, eps, cfg,
+                     (double*)w_->io[3], d_wpos, d_wneg, sweeps, delta, s_,
+                     stats));
+  DP_TRY(unstage(w_, 3, eta, ne * 8, s_, &d2h_));
+  if (wpos && nvars)
+    DP_CUDA(cudaMemcpyAsync(wpos, d_wpos, (size_t)nvars * 4,
+                            cudaMemcpyDeviceToHost, s_));
+  if (wneg && nvars)
+    DP_CUDA(cudaMemcpyAsync(wneg, d_wneg, (size_t)nvars * 4,
+                            cudaMemcpyDeviceToHost, s_));
+  d2h_ += (uint64_t)nvars * 8;
+  DP_HOST_CALL_END
+}
+
+int dp_sp_dev(const int32_t* d_lits, int32_t k, int32_t nclauses,
+              const int32_t* d_occ_row, const int32_t* d_occ, int32_t nvars,
+              int32_t max_sweeps, float eps, const dp_config* cfg,
+              double* d_eta, float* d_wpos, float* d_wneg, int32_t* sweeps,
+              float* delta, void* stream, dp_stats* stats) {
+  clear_stats(stats);
+  const double t0 = now_ns();
+  int r = sp_dev_impl(d_lits, k, nclauses, d_occ_row, d_occ, nvars,
+                      max_sweeps, eps, cfg, d_eta, d_wpos, d_wneg, sweeps,
+                      delta, (cudaStream_t)stream, stats);
   if (stats) stats->ns_host = now_ns() - t0;
   return r;
 }

@@ -570,3 +570,45 @@ def test_mst_rmat18_and_long_chains_vs_oracle():
                 np.testing.assert_array_equal(rep.arrays["in_mst"], in_mst)
                 assert rep.arrays["weight"].tolist() == [total, k]
                 assert rep.iterations <= 64
+
+
+SP_POLICIES = (dict(), dict(threshold=INF_THRESHOLD), dict(agg="warp"),
+               dict(threshold=16, agg="block"),
+               dict(threshold=32, cfactor=4, agg="multiblock", group_size=8,
+                    serial="warp"),
+               dict(threshold=8, agg="grid", serial="warp",
+                    parent_block=128, child_block=64))
+
+
+def _sp_close(got, want):
+    # surveys: 1e-5 relative (north star), 1e-7 absolute for tiny surveys;
+    # biases are fp32
+    np.testing.assert_allclose(got["eta"], want[0], rtol=1e-5, atol=1e-7)
+    np.testing.assert_allclose(got["wpos"], want[1], rtol=1e-5, atol=1e-6)
+    np.testing.assert_allclose(got["wneg"], want[2], rtol=1e-5, atol=1e-6)
+
+
+@pytest.mark.parametrize("spec", ["ksat3:2000:seed1", "ksat5:1000:seed2",
+                                  "ksat3:30000:seed3"])
+def test_sp_vs_oracle_fixed_sweeps(spec):
+    bench, wl = load("sp", spec)
+    b = dict(wl.buffers, max_sweeps=25, eps=0.0)
+    wl = Workload(wl.spec, b, wl.n, wl.payload)
+    want = oracle.sp(wl.payload, b["eta0"], 25, 0.0)
+    for policy in SP_POLICIES:
+        rep, _ = run_config(bench, wl, BenchConfig(**policy))
+        assert rep.iterations == 25
+        _sp_close(rep.arrays, want)
+    _sp_close(run_reference(bench, wl).arrays, want)
+
+
+def test_sp_converges_like_oracle():
+    bench, wl = load("sp", "ksat3:20000:seed1")
+    want = oracle.sp(wl.payload, wl.buffers["eta0"],
+                     wl.buffers["max_sweeps"], wl.buffers["eps"])
+    rep, _ = run_config(bench, wl, BenchConfig(threshold=32, agg="grid",
+                                               serial="warp"))
+    assert rep.iterations == want[3]
+    _sp_close(rep.arrays, want)
+    run_benchmark("sp", "ksat5:800:seed1", BenchConfig(threshold=64,
+                                                       agg="block"))

@@ -392,3 +392,74 @@ def test_oracle_mst_is_kruskal_in_key_order(spec):
             parent[max(a, b)] = min(a, b)
             want[e] = 1
     np.testing.assert_array_equal(in_mst, want)
+
+
+# ---------------------------------------------------------------------------
+# survey propagation (no reference implementation): the oracle against the
+# textbook update written with explicit clause sets (no division trick)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("spec", ["ksat3:60:seed1", "ksat5:40:seed2"])
+def test_ksat_formula_invariants(spec):
+    f = graphs.make_formula(parse_spec(spec))
+    k, ratio = graphs.SAT_KINDS[parse_spec(spec).kind]
+    assert f.k == k and f.nclauses == round(ratio * f.nvars)
+    var = (f.lits >> 1).reshape(-1, k)
+    assert all(len(set(r)) == k for r in var.tolist())     # distinct vars
+    assert var.min() >= 0 and var.max() < f.nvars
+    for i in range(f.nvars):                               # occurrence CSR
+        occ = f.occ[f.occ_row[i]:f.occ_row[i + 1]]
+        np.testing.assert_array_equal(occ, np.flatnonzero(var.reshape(-1) == i))
+
+
+def _py_sp(f, eta0, sweeps):
+    """Braunstein-Mezard-Zecchina SP, synchronous, straight from the sets."""
+    k = f.k
+    var = (f.lits >> 1).tolist()
+    neg = (f.lits & 1).tolist()
+    eta = list(map(float, eta0))
+    occ = [f.occ[f.occ_row[i]:f.occ_row[i + 1]].tolist()
+           for i in range(f.nvars)]
+    for _ in range(sweeps):
+        new = [0.0] * len(eta)
+        for a in range(f.nclauses):
+            for t in range(k):
+                v = 1.0
+                for j in range(k):
+                    if j == t:
+                        continue
+                    e = a * k + j
+                    x = var[e]
+                    same = [b for b in occ[x] if b != e and neg[b] == neg[e]]
+                    opp = [b for b in occ[x] if neg[b] != neg[e]]
+                    S = float(np.prod([1 - eta[b] for b in same]))
+                    U = float(np.prod([1 - eta[b] for b in opp]))
+                    pu, ps, p0 = (1 - U) * S, (1 - S) * U, S * U
+                    den = pu + ps + p0
+                    v *= pu / den if den > 0 else 0.0
+                new[a * k + t] = v
+        eta = new
+    return np.array(eta)
+
+
+@pytest.mark.parametrize("spec", ["ksat3:60:seed1", "ksat5:40:seed2",
+                                  "ksat3:200:seed3"])
+def test_oracle_sp_matches_textbook_update(spec):
+    s = parse_spec(spec)
+    f = graphs.make_formula(s)
+    eta0 = graphs.sp_initial_surveys(f, s.seed)
+    for sweeps in (1, 3, 8):
+        got = oracle.sp(f, eta0, sweeps, 0.0)
+        assert got[3] == sweeps
+        np.testing.assert_allclose(got[0], _py_sp(f, eta0, sweeps),
+                                   rtol=1e-9, atol=1e-12)
+
+
+def test_oracle_sp_biases_and_convergence():
+    s = parse_spec("ksat3:2000:seed1")
+    f = graphs.make_formula(s)
+    eta, wpos, wneg, sweeps, delta = oracle.sp(
+        f, graphs.sp_initial_surveys(f, s.seed), 200, 1e-3)
+    assert sweeps < 200 and delta <= 1e-3        # converged
+    assert np.all((eta >= 0) & (eta <= 1))
+    assert np.all((wpos >= 0) & (wneg >= 0) & (wpos + wneg <= 1 + 1e-6))
