@@ -60,6 +60,14 @@ BEST = {
                child_block=128, serial="warp"),
     "bt": dict(threshold=64, cfactor=16, agg="grid", parent_block=256,
                child_block=32, serial="warp"),
+    # MSTF (find) row; the verify kernel runs MST_OTHER_POLICY
+    "mstf": dict(threshold=1024, cfactor=16, agg="multiblock",
+                 group_size=1 << 20, parent_block=256, child_block=128,
+                 serial="warp"),
+    # tools/tune_sp.py (profiles/tune_sp_r01.txt): children run in the
+    # parent thread below T, one aggregated launch per pass above it
+    "sp": dict(threshold=128, cfactor=4, agg="multiblock", group_size=1 << 20,
+               parent_block=128, child_block=128, serial="thread"),
 }
 
 
@@ -354,6 +362,41 @@ def extra_workloads(stream, quick: bool) -> dict:
         "curves_per_s": 25000 / (ms2 * 1e-3), "ms": ms2,
         "device_launches": reps[-1].num_launches,
         "vs_naive_cdp": naive.ns_device / 1e6 / ms2, "policy": c2}
+    if quick:
+        return out
+    from paper_2201_02789_b200.bench import run_reference
+    from paper_2201_02789_b200.bench.benchmarks import Workload
+
+    def med(bench, wl, pol, k=4):
+        reps = [run_config(bench, wl, BenchConfig(**pol))[0]
+                for _ in range(k)]
+        return statistics.median(r.ns_device for r in reps[1:]) / 1e6, reps[-1]
+    # MST (MSTF row) on the symmetrised RMAT-22
+    bench, wl = load("mstf", f"rmat:{SCALE}:seed{SEED}")
+    ms, rep = med(bench, wl, BEST["mstf"])
+    naive_ms, _ = med(bench, wl, dict(), k=1 + 1)
+    ref = run_reference(bench, wl)
+    m = int(wl.buffers["col"].shape[0])
+    out["mst_rmat22"] = {
+        "ms": ms, "edge_slots": m, "edges_per_s": m / (ms * 1e-3),
+        "forest_weight": int(rep.arrays["weight"][0]),
+        "forest_edges": int(rep.arrays["weight"][1]),
+        "rounds": rep.iterations, "vs_naive_cdp": naive_ms / ms,
+        "vs_nocdp": ref.ns_device / 1e6 / ms, "policy": BEST["mstf"]}
+    del wl
+    # SP: 20 synchronous sweeps of random 5-SAT
+    bench, wl = load("sp", "ksat5:200000:seed1")
+    wl = Workload(wl.spec, dict(wl.buffers, max_sweeps=20, eps=0.0), wl.n,
+                  wl.payload)
+    ms, rep = med(bench, wl, BEST["sp"])
+    grid_ms, _ = med(bench, wl, dict(agg="grid"), k=2)
+    ref = run_reference(bench, wl)
+    ne = int(wl.buffers["lits"].shape[0])
+    out["sp_ksat5_200k"] = {
+        "ms": ms, "sweeps": rep.iterations, "edges": ne,
+        "edge_updates_per_s": ne * rep.iterations / (ms * 1e-3),
+        "vs_agg_only_grid": grid_ms / ms,
+        "vs_nocdp": ref.ns_device / 1e6 / ms, "policy": BEST["sp"]}
     return out
 
 

@@ -352,13 +352,16 @@ def _sp_run(wl: Workload, cfg: _lib.DpConfig):
 
 
 def sp_traffic(nvars: int, nedges: int, k: int, sweeps: int) -> int:
-    """Per sweep: variable pass 24 B per variable (occ_row pair, product
-    reset) + 24 B per occurrence (occ, lit, eta 8, 8 B product update);
-    clause pass per edge 16 B (eta' write, eta read) + (k-1) x (lit 4 +
-    eta 8 + product 24) reads.  The final bias pass adds one variable pass."""
-    var = 24 * nvars + 24 * nedges
-    clause = nedges * (16 + (k - 1) * 36)
-    return sweeps * (var + clause) + var + 8 * nvars
+    """Per sweep (csrc/apps.cuh SpVarApp / SpRatioApp / SpClauseApp):
+    variable pass 32 B per variable (occ_row pair, product write) + 12 B per
+    occurrence (packed occurrence 4, eta 8); ratio pass 28 B per edge (lit,
+    eta, ratio write) + 24 B of products per variable; clause pass 24 B per
+    edge (its ratio, eta, eta' write).  The final bias pass adds one variable
+    pass and 8 B of biases per variable; packing the occurrences 12 B/edge."""
+    var = 32 * nvars + 12 * nedges
+    ratio = 24 * nvars + 28 * nedges
+    clause = 24 * nedges
+    return sweeps * (var + ratio + clause) + var + 8 * nvars + 12 * nedges
 
 
 def _sp_traffic(wl, out, st):

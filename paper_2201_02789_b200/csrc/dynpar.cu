@@ -1070,6 +1070,16 @@ __global__ void sp_reset_kernel(int n, SpVarProd* prod) {
   }
 }
 
+// occs[t] = occ[t] << 1 | negated (the variable side reads signs in order)
+__global__ void sp_pack_kernel(long long ne, const int* __restrict__ occ,
+                               const int* __restrict__ lits, int* occs) {
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < ne;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int e = occ[t];
+    occs[t] = (e << 1) | (lits[e] & 1);
+  }
+}
+
 // W+ = Pi+ / (Pi+ + Pi- + Pi0), W- likewise, with P+ / P- the products of
 // (1 - eta) over the positive / negative occurrences:
 // Pi+ = (1 - P+) P-, Pi- = (1 - P-) P+, Pi0 = P+ P-.
@@ -1101,13 +1111,17 @@ int sp_dev_impl(const int32_t* lits, int32_t k, int32_t nclauses,
   Workspace* w = workspace(&r);
   if (!w) return r;
   const long long ne = (long long)nclauses * k;
-  // prod[nvars] | eta scratch[ne]
+  if (ne >= (1LL << 30)) return fail(DP_ERR_INVALID, "too many edges");
+  // prod[nvars] | eta scratch[ne] | ratio[ne] | occs[ne]
   const size_t nv = (size_t)std::max(nvars, 1);
+  const size_t nes = (size_t)std::max(ne, 1LL);
   if ((r = grow(&w->io[5], &w->io_bytes[5],
-                nv * sizeof(SpVarProd) + (size_t)std::max(ne, 1LL) * 8)))
+                nv * sizeof(SpVarProd) + nes * (8 + 8 + 4))))
     return r;
   SpVarProd* prod = (SpVarProd*)w->io[5];
   double* eta_b = (double*)(prod + nv);
+  double* ratio = eta_b + nes;
+  int* occs = (int*)(ratio + nes);
   long long lv = 0;
   if (c->variant == DP_VARIANT_CDP &&
       (r = count_launchers(w, c, occ_row, nvars, 0, s, &lv)))
@@ -1123,6 +1137,13 @@ int sp_dev_impl(const int32_t* lits, int32_t k, int32_t nclauses,
                                       148 * 8));
   RunCounters rc;
   DP_CUDA(cudaEventRecord(w->ev0, s));
+  if (ne) {
+    sp_pack_kernel<<<(int)std::min<long long>(dp::ceil_div_ll(ne, 256),
+                                              148 * 8),
+                     256, 0, s>>>(ne, occ, lits, occs);
+    DP_CUDA(cudaGetLastError());
+    rc.kernel_launches += 1;
+  }
   double* cur = eta;
   double* nxt = eta_b;
   int sweeps = 0;
@@ -1133,8 +1154,7 @@ int sp_dev_impl(const int32_t* lits, int32_t k, int32_t nclauses,
     rc.kernel_launches += 1;
     SpVarApp va;
     va.occ_row = occ_row;
-    va.occ = occ;
-    va.lit = lits;
+    va.occs = occs;
     va.eta = e;
     va.prod = prod;
     va.nvars = nvars;
@@ -1143,11 +1163,18 @@ int sp_dev_impl(const int32_t* lits, int32_t k, int32_t nclauses,
   };
   while (sweeps < max_sweeps) {
     if ((r = var_pass(cur))) return r;
+    SpRatioApp ra;
+    ra.lit = lits;
+    ra.eta = cur;
+    ra.prod = prod;
+    ra.ratio = ratio;
+    ra.nclauses = nclauses;
+    ra.k = k;
+    if ((r = launch_parent(ra, nclauses, lc, c, w, s, &rc))) return r;
     DP_CUDA(cudaMemsetAsync(&w->ds->flag[0], 0, sizeof(int), s));
     SpClauseApp ca;
-    ca.lit = lits;
+    ca.ratio = ratio;
     ca.eta = cur;
-    ca.prod = prod;
     ca.eta_next = nxt;
     ca.max_delta = (unsigned*)&w->ds->flag[0];
     ca.nclauses = nclauses;

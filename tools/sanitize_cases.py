@@ -1,4 +1,4 @@
-"""Small runs of every app under several policies, checked against the
+"""Small runs of every app (9 apps x 7 policies) under several policies, checked against the
 oracle; meant to run under compute-sanitizer (memcheck / racecheck /
 synccheck) -- the stand-in for the reference's fence/publication checker
 (sim/machine.py:543-649)."""
@@ -18,7 +18,9 @@ POLICIES = [dict(), dict(agg="warp"), dict(threshold=4, agg="block"),
 fails = 0
 for app, spec in (("bfs", "powerlaw:300:seed2"), ("sssp", "powerlaw:300:seed3"),
                   ("manylaunch", "sizes:200:seed1"), ("tc", "rmat:8:seed1"),
-                  ("bt", "curves:300:seed1"), ("gc", "powerlaw:300:seed1")):
+                  ("bt", "curves:300:seed1"), ("gc", "powerlaw:300:seed1"),
+                  ("mstf", "powerlaw:300:seed1"), ("mstv", "road:300:seed2"),
+                  ("sp", "ksat3:300:seed1")):
     bench, wl = load(app, spec)
     b = wl.buffers
     if app == "bfs":
@@ -33,12 +35,20 @@ for app, spec in (("bfs", "powerlaw:300:seed2"), ("sssp", "powerlaw:300:seed3"),
     elif app == "bt":
         want = {"ntess": oracle.bt(b["cp"], graphs.BT_MAX_TESS,
                                    graphs.BT_CURV_SCALE)[0]}
-    else:
+    elif app == "gc":
         want = {"color": oracle.gc(b["rowptr"], b["col"])[0]}
+    elif app in ("mstf", "mstv"):
+        want = {"in_mst": oracle.mst(b["rowptr"], b["col"], b["weight"],
+                                     b["eid"])[0]}
+    else:
+        want = {"eta": oracle.sp(wl.payload, b["eta0"], b["max_sweeps"],
+                                 b["eps"])[0]}
     for pol in POLICIES:
         rep, _ = run_config(bench, wl, BenchConfig(**pol))
         for k, v in want.items():
-            if not np.array_equal(rep.arrays[k], v):
+            same = (np.allclose(rep.arrays[k], v, rtol=1e-5, atol=1e-7)
+                    if v.dtype.kind == "f" else np.array_equal(rep.arrays[k], v))
+            if not same:
                 fails += 1
                 print("MISMATCH", app, k, pol, flush=True)
     print("ok", app, flush=True)
