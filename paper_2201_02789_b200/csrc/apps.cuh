@@ -847,10 +847,11 @@ struct BtApp {
 //   cmin[c]   min key leaving component c (atomicMin), kNoEdge if none
 // MSTF: parent = vertex, child item = out-edge: a cross-component edge lowers
 // cmin[comp u].  MSTV: parent = the go-ahead vertex of its component (the
-// endpoint of the edge cmin names: the canonical slot lies in its row, or it
-// is that slot's target), child item = out-edge: the slot whose eid realises
-// the minimum marks the forest edge and records the partner component
-// (LonestarGPU verify_min_elem).  Hook + pointer jumping are flat kernels in
+// endpoint of the edge cmin names).  If it is the smaller endpoint, the
+// canonical slot lies in its own row and it marks the edge directly; the
+// larger endpoint expands its row (child item = out-edge) to find the slot
+// whose eid realises the minimum, marks the forest edge and records the
+// partner component (LonestarGPU verify_min_elem).  Hook + pointer jumping are flat kernels in
 // dynpar.cu.
 // ---------------------------------------------------------------------------
 constexpr unsigned long long kNoEdge = ~0ull;
@@ -960,7 +961,15 @@ struct MstVerifyApp {
     // u is an endpoint of the chosen edge: its smaller endpoint owns the
     // canonical slot, the larger one is that slot's target.  The endpoint in
     // the other component is checked against that component's minimum.
-    if (!((want >= s && want < s + d) || __ldg(col + want) == u)) return 0;
+    if (want >= s && want < s + d) {
+      // the smaller endpoint owns the canonical slot: nothing to search
+      // (idempotent stores, so a re-run of expand is harmless)
+      in_mst[want] = 1;
+      partner[cu] = __ldg(comp + __ldg(col + want));
+      return 0;
+    }
+    // the larger endpoint scans its row for the mirror slot
+    if (__ldg(col + want) != u) return 0;
     a = Args{s, d, cu, want};
     return d > 0 ? d : 0;
   }
