@@ -94,7 +94,13 @@ typedef struct dp_config {
                             device (CDP2 tail launches, up to 16 per host
                             launch) instead of one host launch + flag
                             readback each */
-  int32_t reserved[4];
+  int32_t frontier;      /* SSSP only, 1: a reached vertex relaxes its edges
+                            only when its distance changed since it last did
+                            (work-efficient rounds; same final distances,
+                            fewer relaxations).  0 = every reached vertex
+                            every round, as SSSP_CDP main does
+                            (benchmarks.py:207-222) */
+  int32_t reserved[3];
 } dp_config;
 
 /* SimReport (sim/report.py:12-28) counters, measured on the device */

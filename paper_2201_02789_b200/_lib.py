@@ -40,7 +40,8 @@ class DpConfig(ctypes.Structure):
                 ("pending_launch_limit", ctypes.c_int32),
                 ("persistent", ctypes.c_int32),
                 ("device_loop", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 4)]
+                ("frontier", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 3)]
 
 
 class DpStats(ctypes.Structure):

@@ -38,7 +38,9 @@ class BenchConfig:
     persistent (blocks per SM of a persistent parent grid for single-group
     aggregation: record every launch first, then the serial arms),
     device_loop (chain BFS levels / SSSP rounds on the device with CDP2 tail
-    launches instead of a host launch + flag readback per level)."""
+    launches instead of a host launch + flag readback per level), frontier
+    (SSSP: a vertex relaxes only when its distance changed since its last
+    relaxation; same distances, fewer relaxations)."""
     threshold: int = 0
     cfactor: int = 1
     agg: str | None = None
@@ -51,6 +53,7 @@ class BenchConfig:
     pending_launch_limit: int = 0
     persistent: int = 0
     device_loop: bool = False
+    frontier: bool = False
 
     def describe(self) -> str:
         return (f"threshold={self.threshold} cfactor={self.cfactor} "
@@ -99,6 +102,7 @@ class BenchConfig:
         c.pending_launch_limit = int(self.pending_launch_limit)
         c.persistent = int(self.persistent)
         c.device_loop = int(bool(self.device_loop))
+        c.frontier = int(bool(self.frontier))
         if "T" not in self.order.upper():
             c.threshold = 0
         if "C" not in self.order.upper():

@@ -347,6 +347,7 @@ struct SsspApp {
   int* dist;
   int* changed;
   int* changed_next;
+  int* last;  // frontier mode: distance of u's last relaxation (else null)
   int n;
   int pad;
 
@@ -373,6 +374,14 @@ struct SsspApp {
     if (!valid) return 0;
     const int du = __ldcg(dist + u);
     if (du >= kUnreached) return 0;
+    if (last) {
+      // frontier mode: edges relaxed from du already cannot lower anything
+      // again; a vertex lowered later in this round (after this read)
+      // differs from last[u] next round and relaxes then, and a round
+      // without any lowering leaves every vertex at dist == last
+      if (__ldcg(last + u) == du) return 0;
+      last[u] = du;
+    }
     const int s = __ldg(rowptr + u);
     const int d = __ldg(rowptr + u + 1) - s;
     a = Args{s, d, du, 0};
@@ -392,6 +401,8 @@ struct SsspApp {
   }
   static constexpr int kUnroll = DP_SSSP_UNROLL;
   static constexpr bool kBlockMode = false;
+  // frontier mode writes last[] in expand: the host never pairs it with the
+  // persistent parent (which re-runs expand)
   static constexpr bool kPureExpand = true;
   static constexpr int kMinBlocks = DP_SSSP_MINB;
   template <int U, class ArgsOf>

@@ -441,7 +441,7 @@ int launch_wave(const App& app, long long base, long long nparents,
       c->agg == DP_AGG_GRID ||
       (c->agg == DP_AGG_MULTIBLOCK && (long long)c->group_size >= grid);
   if constexpr (App::kPureExpand) {
-    if (cdp && c->persistent > 0 && single_group) {
+    if (cdp && c->persistent > 0 && single_group && !c->frontier) {
       int sms = 148, dev = 0;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -763,6 +763,13 @@ int sssp_dev_impl(const int32_t* rowptr, const int32_t* col,
   Workspace* w = workspace(&r);
   if (!w) return r;
   init_dist_kernel<<<dp::ceil_div(n, 256), 256, 0, s>>>(dist, n, src);
+  int* last = nullptr;
+  if (c->frontier) {
+    if ((r = grow(&w->io[5], &w->io_bytes[5], (size_t)n * sizeof(int))))
+      return r;
+    last = (int*)w->io[5];
+    fill_kernel<int><<<dp::ceil_div(n, 256), 256, 0, s>>>(last, n, kUnreached);
+  }
   long long launchers = 0;
   if (c->variant == DP_VARIANT_CDP &&
       (r = count_launchers(w, c, rowptr, n, 0, s, &launchers)))
@@ -777,6 +784,7 @@ int sssp_dev_impl(const int32_t* rowptr, const int32_t* col,
                    a.dist = dist;
                    a.changed = &ds->flag[round & 1];
                    a.changed_next = &ds->flag[(round + 1) & 1];
+                   a.last = last;
                    a.n = n;
                    a.pad = 0;
                    return a;

@@ -612,3 +612,32 @@ def test_sp_converges_like_oracle():
     _sp_close(rep.arrays, want)
     run_benchmark("sp", "ksat5:800:seed1", BenchConfig(threshold=64,
                                                        agg="block"))
+
+
+@pytest.mark.parametrize("spec", GRAPH_SPECS + ["rmat:14:seed1"])
+def test_sssp_frontier_mode_same_distances(spec):
+    """B200 work-efficient rounds (frontier=True): identical distances."""
+    bench, wl = load("sssp", spec)
+    b = wl.buffers
+    want, _ = oracle.sssp(b["rowptr"], b["col"], b["weight"], nthreads=0)
+    for policy in (dict(), dict(threshold=INF_THRESHOLD, serial="warp"),
+                   dict(threshold=64, cfactor=4, agg="multiblock",
+                        group_size=1 << 20, serial="warp"),
+                   dict(threshold=32, agg="grid"),
+                   dict(device_loop=True, parent_block=64),
+                   dict(persistent=2, agg="grid", parent_block=128)):
+        rep, _ = run_config(bench, wl, BenchConfig(frontier=True, **policy))
+        np.testing.assert_array_equal(rep.arrays["dist"], want)
+
+
+def test_sssp_frontier_rmat22_fewer_relaxations():
+    bench, wl = load("sssp", "rmat:20:seed1")
+    b = wl.buffers
+    want, _ = oracle.sssp(b["rowptr"], b["col"], b["weight"], nthreads=0)
+    pol = dict(threshold=1024, cfactor=32, agg="multiblock", group_size=2048,
+               parent_block=128, child_block=64, serial="warp")
+    full, _ = run_config(bench, wl, BenchConfig(**pol))
+    fr, _ = run_config(bench, wl, BenchConfig(frontier=True, **pol))
+    np.testing.assert_array_equal(fr.arrays["dist"], want)
+    np.testing.assert_array_equal(full.arrays["dist"], want)
+    assert fr.ns_device < full.ns_device
