@@ -641,3 +641,59 @@ def test_sssp_frontier_rmat22_fewer_relaxations():
     np.testing.assert_array_equal(fr.arrays["dist"], want)
     np.testing.assert_array_equal(full.arrays["dist"], want)
     assert fr.ns_device < full.ns_device
+
+
+def _mst_workload(name, rowptr, col, weight):
+    """A custom symmetric simple graph as an mstf / mstv workload."""
+    g = graphs.Graph(np.asarray(rowptr, np.int32), np.asarray(col, np.int32))
+    eid = np.minimum(np.arange(g.m, dtype=np.int32), graphs.edge_mirror(g))
+    w = np.asarray(weight, np.int32)[eid] if g.m else np.zeros(0, np.int32)
+    spec = DatasetSpec("hand", g.n, 0, f"custom:{g.n}")
+    return BENCHMARKS[name], Workload(spec, {
+        "rowptr": g.rowptr, "col": g.col, "weight": np.ascontiguousarray(w),
+        "eid": np.ascontiguousarray(eid)}, g.n, g)
+
+
+@pytest.mark.parametrize("policy", EDGE_POLICIES)
+@pytest.mark.parametrize("rowptr,col,weight", [
+    ([0, 0], [], []),                                  # one vertex
+    ([0, 0, 0, 0], [], []),                            # no edges at all
+    ([0, 1, 2], [1, 0], [5, 5]),                       # one edge
+    ([0, 2, 4, 6], [1, 2, 0, 2, 0, 1], [3] * 6),       # triangle, all ties
+    ([0, 1, 2, 3, 4], [1, 0, 3, 2], [-7, -7, 2**31 - 1, 2**31 - 1]),
+    # two components, extreme signed weights
+])
+def test_mst_degenerate_graphs(rowptr, col, weight, policy):
+    for name in ("mstf", "mstv"):
+        bench, wl = _mst_workload(name, rowptr, col, weight)
+        b = wl.buffers
+        want = oracle.mst(b["rowptr"], b["col"], b["weight"], b["eid"])
+        rep, _ = run_config(bench, wl, BenchConfig(**policy))
+        np.testing.assert_array_equal(rep.arrays["in_mst"], want[0])
+        assert rep.arrays["weight"].tolist() == [want[1], want[2]]
+
+
+def test_sp_edge_cases():
+    """One clause; zero and one surveys (the zero-factor bookkeeping);
+    max_sweeps = 0 leaves eta0 and only computes biases."""
+    bench = BENCHMARKS["sp"]
+    for spec_text, eta_fill in (("ksat3:3:seed1", None),
+                                ("ksat3:50:seed2", 1.0),
+                                ("ksat5:60:seed3", 0.0),
+                                ("ksat3:40:seed4", "mixed")):
+        _, wl = load("sp", spec_text)
+        eta0 = wl.buffers["eta0"].copy()
+        if eta_fill == "mixed":
+            eta0[::3] = 1.0
+            eta0[1::5] = 0.0
+        elif eta_fill is not None:
+            eta0[:] = eta_fill
+        for sweeps in (0, 1, 7):
+            b = dict(wl.buffers, eta0=eta0, max_sweeps=sweeps, eps=0.0)
+            w2 = Workload(wl.spec, b, wl.n, wl.payload)
+            want = oracle.sp(wl.payload, eta0, sweeps, 0.0)
+            for policy in EDGE_POLICIES[:4]:
+                rep, _ = run_config(bench, w2, BenchConfig(**policy))
+                # eps = 0 still stops at an exact fixed point (delta == 0)
+                assert rep.iterations == want[3] <= sweeps
+                _sp_close(rep.arrays, want)
