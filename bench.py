@@ -46,12 +46,13 @@ import numpy as np  # noqa: E402
 SCALE = 22
 SEED = 1
 
-# tuned policies (profiles/ + DESIGN.md); parity defaults elsewhere
+# tuned policies (profiles/ + DESIGN.md); parity defaults elsewhere.
+# sssp: profiles/tune_sssp_cf_r01.txt (T x C x child block x group size)
 BEST = {
     # one aggregation group spanning the parent grid: the last parent block
     # issues ONE CDP2 launch per round (tools/tune.py, profiles/tune_*)
-    "sssp": dict(threshold=1024, cfactor=32, agg="multiblock",
-                 group_size=2048, parent_block=128, child_block=64,
+    "sssp": dict(threshold=1024, cfactor=16, agg="multiblock",
+                 group_size=1 << 20, parent_block=128, child_block=128,
                  serial="warp"),
     "bfs": dict(threshold=1024, cfactor=16, agg="multiblock",
                 group_size=1 << 20, parent_block=256, child_block=128,
@@ -69,6 +70,12 @@ BEST = {
     "sp": dict(threshold=128, cfactor=4, agg="multiblock", group_size=1 << 20,
                parent_block=128, child_block=128, serial="thread"),
 }
+
+
+# SSSP with the B200 `frontier` knob (profiles/tune_sssp_frontier_r01.txt)
+FRONTIER_POLICY = dict(threshold=1024, cfactor=8, agg="multiblock",
+                       group_size=2048, parent_block=128, child_block=128,
+                       serial="warp", frontier=True)
 
 
 def peaks() -> dict:
@@ -596,7 +603,7 @@ def arm_ours(args, world, rank, local):
     # B200 work-efficient rounds (frontier knob): a vertex relaxes only when
     # its distance changed since its last relaxation.  Same distances; not
     # the headline, which keeps SSSP_CDP's every-reached-vertex rounds.
-    fcfg = _cfg(dict(BEST["sssp"], frontier=True))
+    fcfg = _cfg(FRONTIER_POLICY)
     f_ms, f_stats = timed_steps(lambda: run_dev("sssp", G, fcfg, stream),
                                 args.steps, args.warmup, stream_obj)
     f_ms = max_over_ranks(f_ms) / args.steps
@@ -606,7 +613,7 @@ def arm_ours(args, world, rank, local):
         "ms_per_step": f_ms, "rounds": int(f_stats[-1]["iterations"]),
         "speedup_vs_headline": ms_step / f_ms,
         "parity": "bit-exact vs oracle" if np.array_equal(fdist, want)
-        else "MISMATCH", "policy": dict(BEST["sssp"], frontier=True)}
+        else "MISMATCH", "policy": FRONTIER_POLICY}
     if not args.quick:
         del G
         torch.cuda.empty_cache()

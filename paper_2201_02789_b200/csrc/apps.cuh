@@ -348,8 +348,14 @@ struct SsspApp {
   int* changed;
   int* changed_next;
   int* last;  // frontier mode: distance of u's last relaxation (else null)
+  // host-buffer calls: edge slots arrive in 2^shift-slot chunks while the
+  // rounds run (null when the graph is resident); deferred parents set
+  // *skipped so the loop cannot stop before they have relaxed
+  const int* arrived;
+  int* skipped;
+  int* skipped_next;
   int n;
-  int pad;
+  int shift;
 
   struct alignas(16) Args {
     int start, deg, du, pad;
@@ -360,7 +366,10 @@ struct SsspApp {
 
   __device__ int nparents() const { return n; }
   __device__ void parent_prologue() const {
-    if (blockIdx.x == 0 && threadIdx.x == 0) *changed_next = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      *changed_next = 0;
+      if (arrived) *skipped_next = 0;
+    }
   }
   __device__ SsspApp for_round(int r, int* flags) const {
     SsspApp a = *this;
@@ -374,6 +383,15 @@ struct SsspApp {
     if (!valid) return 0;
     const int du = __ldcg(dist + u);
     if (du >= kUnreached) return 0;
+    const int s = __ldg(rowptr + u);
+    const int d = __ldg(rowptr + u + 1) - s;
+    if (d <= 0) return 0;
+    if (arrived && ((s + d - 1) >> shift) >= arrived_chunks(arrived)) {
+      // edges still in flight: relax in a later round (the outputs are
+      // the unique shortest distances whatever the relaxation order)
+      if (__ldcg(skipped) == 0) *skipped = 1;
+      return 0;
+    }
     if (last) {
       // frontier mode: edges relaxed from du already cannot lower anything
       // again; a vertex lowered later in this round (after this read)
@@ -382,10 +400,8 @@ struct SsspApp {
       if (__ldcg(last + u) == du) return 0;
       last[u] = du;
     }
-    const int s = __ldg(rowptr + u);
-    const int d = __ldg(rowptr + u + 1) - s;
     a = Args{s, d, du, 0};
-    return d > 0 ? d : 0;
+    return d;
   }
   __device__ static int count(const Args& a) { return a.deg; }
   // relax (:184-195): the CAS loop lowers dist[v] to alt and flags the round

@@ -138,7 +138,18 @@ struct DevState {
   int done_round;               // device loop: round count at convergence
   unsigned long long lat_sum;   // device launch -> first child block start, ns
   unsigned long long lat_cnt;
+  int skipped[2];  // per round (double-buffered like flag): a parent whose
+                   // edges had not arrived yet was deferred (host-buffer
+                   // calls that overlap the H2D copy with the rounds)
 };
+
+// Chunks of the edge arrays copied so far (monotone counter written by the
+// copy stream); a parent may read edge slots [0, arrived << shift).
+__device__ __forceinline__ int arrived_chunks(const int* arrived) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(arrived));
+  return v;
+}
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
   unsigned long long t;

@@ -697,3 +697,23 @@ def test_sp_edge_cases():
                 # eps = 0 still stops at an exact fixed point (delta == 0)
                 assert rep.iterations == want[3] <= sweeps
                 _sp_close(rep.arrays, want)
+
+
+@pytest.mark.parametrize("spec", ["powerlaw:2000:seed1", "road:1000:seed7",
+                                  "rmat:14:seed1"])
+def test_sssp_host_call_overlaps_copy_in_chunks(spec, monkeypatch):
+    """dp_sssp streams col / weight in chunks while the rounds run (parents
+    whose edges are in flight are deferred): tiny chunks force many
+    deferrals; distances stay exact in both round modes."""
+    bench, wl = load("sssp", spec)
+    b = wl.buffers
+    want, _ = oracle.sssp(b["rowptr"], b["col"], b["weight"], nthreads=0)
+    for shift in ("4", "8", "30"):
+        monkeypatch.setenv("DP_COPY_CHUNK_SHIFT", shift)
+        for policy in (dict(), dict(threshold=64, cfactor=4, agg="multiblock",
+                                    group_size=1 << 20, serial="warp"),
+                       dict(threshold=32, agg="grid", frontier=True)):
+            rep, _ = run_config(bench, wl, BenchConfig(**policy))
+            np.testing.assert_array_equal(rep.arrays["dist"], want)
+        ref = run_reference(bench, wl)
+        np.testing.assert_array_equal(ref.arrays["dist"], want)

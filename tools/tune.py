@@ -101,6 +101,14 @@ def main():
             configs.append(dict(threshold=512, cfactor=8, agg="grid",
                                 parent_block=pb, child_block=128,
                                 serial="warp"))
+    elif grid in ("cf", "frontier"):
+        for T, C, cb, gs in itertools.product(
+                (512, 1024, 2048), (4, 8, 16, 32), (64, 128),
+                (512, 2048, 1 << 20)):
+            configs.append(dict(threshold=T, cfactor=C, agg="multiblock",
+                                group_size=gs, parent_block=128,
+                                child_block=cb, serial="warp",
+                                frontier=grid == "frontier"))
     from paper_2201_02789_b200 import _lib
     for d in configs:
         d = dict(d)
