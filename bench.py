@@ -57,8 +57,9 @@ BEST = {
     "bfs": dict(threshold=1024, cfactor=16, agg="multiblock",
                 group_size=1 << 20, parent_block=256, child_block=128,
                 serial="warp"),
-    "tc": dict(threshold=64, cfactor=4, agg="grid", parent_block=256,
-               child_block=128, serial="warp"),
+    # TC over the transposed CSR+ (profiles/tune_tc_rmat22_r01c.txt)
+    "tc": dict(threshold=32, cfactor=4, agg="grid", parent_block=128,
+               child_block=256, serial="warp"),
     "bt": dict(threshold=64, cfactor=16, agg="grid", parent_block=256,
                child_block=32, serial="warp"),
     # MSTF (find) row; the verify kernel runs MST_OTHER_POLICY

@@ -604,19 +604,25 @@ struct GcGatherApp {
 
 // ---------------------------------------------------------------------------
 // Triangle counting (no reference implementation)
-//   parent = vertex u of the degree-oriented CSR+, child item = one oriented
-//   edge (u, v) in [edge_lo, edge_hi), work = |N+(u) ∩ N+(v)|.
+//   Input: the degree-oriented CSR+ (out-lists N+, ascending).  The call
+//   builds its transpose on the device (in-lists N-, restricted to the
+//   oriented-edge range [edge_lo, edge_hi) of a shard).
+//   parent = vertex v, child item = in-edge (u, v), work = |N+(u) ∩ N+(v)|.
+//   Probing N+(u) into a set of N+(v) (built once per child block) costs
+//   sum_u d+(u)^2 probes; the forward form, N+(v) into a set of N+(u), costs
+//   sum_v d-(v) d+(v): 14.5 G vs 28.9 G on RMAT-22.
 // ---------------------------------------------------------------------------
 struct TcApp {
-  const int* __restrict__ rowptr;
+  const int* __restrict__ rowptr;     // CSR+ (out)
   const int* __restrict__ col;
+  const int* __restrict__ in_rowptr;  // transpose (in), shard edges only
+  const int* __restrict__ in_src;
   unsigned long long* total;
-  long long edge_lo, edge_hi;
   int n;
   int pad;
 
   struct alignas(16) Args {
-    int u, first, cnt, pad;  // edges [first, first + cnt) of u
+    int v, first, cnt, pad;  // in-edges [first, first + cnt) of v
   };
   struct Acc {
     unsigned long long tri;
@@ -624,14 +630,12 @@ struct TcApp {
 
   __device__ int nparents() const { return n; }
   __device__ void parent_prologue() const {}
-  __device__ int expand(int u, bool valid, Args& a) const {
+  __device__ int expand(int v, bool valid, Args& a) const {
     if (!valid) return 0;
-    long long b = __ldg(rowptr + u), e = __ldg(rowptr + u + 1);
-    if (b < edge_lo) b = edge_lo;
-    if (e > edge_hi) e = edge_hi;
-    if (e <= b) return 0;
-    a = Args{u, (int)b, (int)(e - b), 0};
-    return (int)(e - b);
+    const int b = __ldg(in_rowptr + v), e = __ldg(in_rowptr + v + 1);
+    if (e <= b || __ldg(rowptr + v + 1) == __ldg(rowptr + v)) return 0;
+    a = Args{v, b, e - b, 0};
+    return e - b;
   }
   __device__ static int count(const Args& a) { return a.cnt; }
 
@@ -657,18 +661,18 @@ struct TcApp {
   }
 
   __device__ void item(const Args& a, int e, Acc& acc) const {
-    const int v = __ldg(col + a.first + e);
-    const int ub = __ldg(rowptr + a.u), ue = __ldg(rowptr + a.u + 1);
-    const int vb = __ldg(rowptr + v), ve = __ldg(rowptr + v + 1);
+    const int u = __ldg(in_src + a.first + e);
+    const int ub = __ldg(rowptr + u), ue = __ldg(rowptr + u + 1);
+    const int vb = __ldg(rowptr + a.v), ve = __ldg(rowptr + a.v + 1);
     acc.tri += (unsigned long long)intersect(col + ub, ue - ub, col + vb,
                                              ve - vb);
   }
   static constexpr int kUnroll = 1;
 
-  // Child blocks: N+(u) goes into a shared-memory hash set once per physical
-  // block; each warp then takes 32 edges (u, v), flattens their wedge lists
-  // N+(v) into one list (load-balanced, owner lane by shuffle search) and
-  // probes the set: coalesced reads of N+(v), O(1) lookups, no per-thread
+  // Child blocks: N+(v) goes into a shared-memory hash set once per physical
+  // block; each warp then takes 32 in-edges (u, v), flattens their lists
+  // N+(u) into one list (load-balanced, owner lane by shuffle search) and
+  // probes the set: coalesced reads of N+(u), O(1) lookups, no per-thread
   // merge chains.  Lists longer than kSlots/2 fall back to per-thread merges.
   static constexpr bool kBlockMode = true;
   static constexpr bool kPureExpand = true;
@@ -683,8 +687,8 @@ struct TcApp {
   __device__ void block_items(const Args& a, long long e0, long long e1,
                               Acc& acc) const {
     __shared__ int set[kSlots];
-    const int ub = __ldg(rowptr + a.u), ue = __ldg(rowptr + a.u + 1);
-    if (ue - ub > kSlots / 2) {
+    const int vb = __ldg(rowptr + a.v), ve = __ldg(rowptr + a.v + 1);
+    if (ve - vb > kSlots / 2) {
       for (long long e = e0 + threadIdx.x; e < e1; e += blockDim.x)
         item(a, (int)e, acc);
       return;
@@ -698,7 +702,7 @@ struct TcApp {
     const unsigned mask = (1u << bits) - 1;
     for (int i = threadIdx.x; i <= (int)mask; i += blockDim.x) set[i] = -1;
     __syncthreads();
-    for (int i = ub + threadIdx.x; i < ue; i += blockDim.x) {
+    for (int i = vb + threadIdx.x; i < ve; i += blockDim.x) {
       const int x = __ldg(col + i);
       unsigned h = hash_slot(x, bits);
       while (atomicCAS(&set[h], -1, x) != -1) h = (h + 1) & mask;
@@ -715,20 +719,20 @@ struct TcApp {
     };
     for (long long base = e0 + 32LL * wid; base < e1; base += 32LL * nw) {
       const long long e = base + lane;
-      int vb = 0, dv = 0;
+      int ub = 0, du = 0;
       if (e < e1) {
-        const int v = __ldg(col + a.first + e);
-        vb = __ldg(rowptr + v);
-        dv = __ldg(rowptr + v + 1) - vb;
+        const int u = __ldg(in_src + a.first + e);
+        ub = __ldg(rowptr + u);
+        du = __ldg(rowptr + u + 1) - ub;
       }
-      // long wedge lists: the whole warp walks one list at a time, four
+      // long lists: the whole warp walks one list at a time, four
       // coalesced loads in flight per lane
-      unsigned big = __ballot_sync(DP_FULL, dv >= 32);
+      unsigned big = __ballot_sync(DP_FULL, du >= 32);
       while (big) {
         const int src = __ffs(big) - 1;
         big &= big - 1;
-        const int b = __shfl_sync(DP_FULL, vb, src);
-        const int d = __shfl_sync(DP_FULL, dv, src);
+        const int b = __shfl_sync(DP_FULL, ub, src);
+        const int d = __shfl_sync(DP_FULL, du, src);
         for (int i = lane; i < d; i += 128) {
           int w[4];
 #pragma unroll
@@ -740,7 +744,7 @@ struct TcApp {
         }
       }
       // short lists (< 32): flattened into one load-balanced list
-      const int ds = dv < 32 ? dv : 0;
+      const int ds = du < 32 ? du : 0;
       const int incl = warp_incl_scan(ds);
       const int total = __shfl_sync(DP_FULL, incl, 31);
       const int excl = incl - ds;
@@ -753,7 +757,7 @@ struct TcApp {
           if (probe <= k) owner += step;
         }
         owner = owner < 31 ? owner : 31;
-        const int pos = __shfl_sync(DP_FULL, vb, owner) + k -
+        const int pos = __shfl_sync(DP_FULL, ub, owner) + k -
                         __shfl_sync(DP_FULL, excl, owner);
         if (k < total) tri += hit(__ldg(col + pos));
       }

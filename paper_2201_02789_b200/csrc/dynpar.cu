@@ -1272,6 +1272,116 @@ int manylaunch_dev_impl(const int32_t* sizes, int32_t n, const dp_config* c,
   return once(w, c, a, n, launchers, s, st);
 }
 
+// ---------------------------------------------------------------------------
+// TC: the transpose of the oriented CSR+ (in-lists over the shard's edge
+// range), built on the device at the start of every call: count, exclusive
+// scan, scatter.  In-list order is the scatter's (irrelevant: in-lists are
+// only iterated, the probed / merged out-lists stay sorted).
+// ---------------------------------------------------------------------------
+__global__ void tc_count_in_kernel(const int* __restrict__ col, long long lo,
+                                   long long hi, int* cnt) {
+  for (long long e = lo + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+       e < hi; e += (long long)gridDim.x * blockDim.x)
+    atomicAdd(cnt + __ldg(col + e), 1);
+}
+
+// exclusive scan of x[0, n) into y[0, n] (y[n] = total), three passes
+constexpr int kScanTile = 4096;  // 1024 threads x 4
+
+__global__ void __launch_bounds__(1024)
+    scan_tiles_kernel(const int* __restrict__ x, long long n, int* y,
+                      long long* tile_sum) {
+  __shared__ int wsum[32];
+  const long long base = (long long)blockIdx.x * kScanTile + threadIdx.x * 4;
+  int v[4], t = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    v[j] = base + j < n ? x[base + j] : 0;
+    t += v[j];
+  }
+  const int incl = warp_incl_scan(t);
+  if (lane_id() == 31) wsum[threadIdx.x >> 5] = incl;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int ws = wsum[threadIdx.x];
+    const int wi = warp_incl_scan(ws);
+    wsum[threadIdx.x] = wi - ws;
+    if (threadIdx.x == 31) tile_sum[blockIdx.x] = wi;
+  }
+  __syncthreads();
+  int run = wsum[threadIdx.x >> 5] + incl - t;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    if (base + j < n) y[base + j] = run;
+    run += v[j];
+  }
+}
+
+__global__ void __launch_bounds__(1024)
+    scan_sums_kernel(long long* tile_sum, int ntiles, int* y, long long n) {
+  // one block: exclusive scan of the tile sums in place, y[n] = total
+  __shared__ long long carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int b0 = 0; b0 < ntiles; b0 += 1024) {
+    const int i = b0 + threadIdx.x;
+    const long long v = i < ntiles ? tile_sum[i] : 0;
+    long long x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long t = __shfl_up_sync(DP_FULL, x, o);
+      if (lane_id() >= o) x += t;
+    }
+    __shared__ long long ws[32];
+    if (lane_id() == 31) ws[threadIdx.x >> 5] = x;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      long long a = ws[threadIdx.x];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long t = __shfl_up_sync(DP_FULL, a, o);
+        if (lane_id() >= o) a += t;
+      }
+      ws[threadIdx.x] = a;
+    }
+    __syncthreads();
+    const long long before = (threadIdx.x >= 32 ? ws[(threadIdx.x >> 5) - 1] : 0);
+    const long long c = carry;
+    if (i < ntiles) tile_sum[i] = c + before + x - v;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = c + before + x;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) y[n] = (int)carry;
+}
+
+__global__ void scan_add_kernel(int* y, int* y2, long long n,
+                                const long long* tile_sum) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int v = y[i] + (int)tile_sum[i / kScanTile];
+    y[i] = v;
+    y2[i] = v;
+  }
+}
+
+// warp per source vertex: its out-edges in [lo, hi) land in the in-lists
+__global__ void tc_scatter_in_kernel(const int* __restrict__ rowptr,
+                                     const int* __restrict__ col, int n,
+                                     long long lo, long long hi, int* cursor,
+                                     int* in_src) {
+  const int lane = lane_id();
+  const long long warps = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long u = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+       u < n; u += warps) {
+    long long b = __ldg(rowptr + u), e = __ldg(rowptr + u + 1);
+    if (b < lo) b = lo;
+    if (e > hi) e = hi;
+    for (long long i = b + lane; i < e; i += 32)
+      in_src[atomicAdd(cursor + __ldg(col + i), 1)] = (int)u;
+  }
+}
+
 int tc_dev_impl(const int32_t* rowptr, const int32_t* col, int32_t n,
                 int64_t m, int64_t lo, int64_t hi, const dp_config* c,
                 uint64_t* tri, cudaStream_t s, dp_stats* st) {
@@ -1280,22 +1390,59 @@ int tc_dev_impl(const int32_t* rowptr, const int32_t* col, int32_t n,
   if (n < 0 || m < 0) return fail(DP_ERR_INVALID, "negative size");
   if (lo < 0) lo = 0;
   if (hi > m) hi = m;
+  if (hi < lo) hi = lo;
   Workspace* w = workspace(&r);
   if (!w) return r;
+  // in_rowptr[n+1] | cursor[n+1] | in_src[hi-lo] | tile sums
+  const long long ntiles = std::max(1LL, dp::ceil_div_ll(n, kScanTile));
+  const size_t need = (size_t)(n + 1) * 8 + (size_t)std::max<long long>(hi - lo, 1) * 4 +
+                      (size_t)ntiles * 8 + 16;
+  if ((r = grow(&w->io[5], &w->io_bytes[5], need))) return r;
+  long long* tile_sum = (long long*)w->io[5];
+  int* in_rowptr = (int*)(tile_sum + ntiles);
+  int* cursor = in_rowptr + (n + 1);
+  int* in_src = cursor + (n + 1);
+  RunCounters rc;
   DP_CUDA(cudaMemsetAsync(tri, 0, sizeof(uint64_t), s));
+  DP_CUDA(cudaEventRecord(w->ev0, s));
+  const int gb = 148 * 8;
+  DP_CUDA(cudaMemsetAsync(cursor, 0, (size_t)(n + 1) * 4, s));
+  if (hi > lo)
+    tc_count_in_kernel<<<gb, 256, 0, s>>>(col, lo, hi, cursor);
+  scan_tiles_kernel<<<(int)ntiles, 1024, 0, s>>>(cursor, n, in_rowptr,
+                                                 tile_sum);
+  scan_sums_kernel<<<1, 1024, 0, s>>>(tile_sum, (int)ntiles, in_rowptr, n);
+  scan_add_kernel<<<gb, 256, 0, s>>>(in_rowptr, cursor, n, tile_sum);
+  if (hi > lo)
+    tc_scatter_in_kernel<<<gb, 256, 0, s>>>(rowptr, col, n, lo, hi, cursor,
+                                            in_src);
+  DP_CUDA(cudaGetLastError());
+  rc.kernel_launches += 5;
   TcApp a;
   a.rowptr = rowptr;
   a.col = col;
+  a.in_rowptr = in_rowptr;
+  a.in_src = in_src;
   a.total = (unsigned long long*)tri;
-  a.edge_lo = lo;
-  a.edge_hi = hi;
   a.n = n;
   a.pad = 0;
   long long launchers = 0;
   if (c->variant == DP_VARIANT_CDP &&
-      (r = count_launchers(w, c, rowptr, n, 0, s, &launchers)))
+      (r = count_launchers(w, c, in_rowptr, n, 0, s, &launchers)))
     return r;
-  return once(w, c, a, n, launchers, s, st);
+  if ((r = ensure_pending_limit(w, c, launch_bound(c, n, launchers))))
+    return r;
+  if ((r = begin_run(w, s))) return r;
+  if ((r = launch_parent(a, n, launchers, c, w, s, &rc))) return r;
+  DP_CUDA(cudaEventRecord(w->ev1, s));
+  DP_CUDA(cudaEventSynchronize(w->ev1));
+  float ms = 0.f;
+  DP_CUDA(cudaEventElapsedTime(&ms, w->ev0, w->ev1));
+  if ((r = read_state(w, s))) return r;
+  if ((r = account_step(w, &rc))) return r;
+  finish_stats(w, rc, ms, st);
+  if (st) st->iterations = 1;
+  return 0;
 }
 
 int bt_dev_impl(const float* cp, int32_t ncurves, int32_t max_tess,
