@@ -29,10 +29,12 @@ import numpy as np
 # ---------------------------------------------------------------------------
 
 def tc_edge_cost(rowptr: np.ndarray, col: np.ndarray) -> np.ndarray:
-    """Work of each oriented edge (u, v): d+(u) + d+(v) list elements."""
+    """Work of each oriented edge (u, v) in the transposed counter
+    (csrc/apps.cuh TcApp): the d+(u) elements of N+(u) probed into v's set,
+    plus one unit for the edge itself (set setup is amortised per block)."""
     deg = np.diff(rowptr.astype(np.int64))
     src = np.repeat(np.arange(deg.shape[0]), deg)
-    return deg[src] + deg[col.astype(np.int64)]
+    return deg[src] + 1
 
 
 def balanced_ranges(cost: np.ndarray, parts: int) -> list[tuple[int, int]]:

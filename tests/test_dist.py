@@ -100,7 +100,7 @@ def test_tc_edge_cost():
     rowptr = np.array([0, 2, 3, 3], np.int32)
     col = np.array([1, 2, 2], np.int32)
     np.testing.assert_array_equal(pdist.tc_edge_cost(rowptr, col),
-                                  [2 + 1, 2 + 0, 1 + 0])
+                                  [2 + 1, 2 + 1, 1 + 1])
 
 
 # ---------------------------------------------------------------------------
