@@ -500,13 +500,21 @@ struct ManyLaunchApp {
 // ---------------------------------------------------------------------------
 // Graph coloring (north-star app; no reference implementation).  Jones-
 // Plassmann with a deterministic priority key(v) = (hash(v), v): a vertex is
-// coloured in the round in which it outranks all its uncoloured neighbours,
-// with the smallest colour unused by its (then all coloured) higher-priority
-// neighbours — exactly the sequential greedy colouring in priority order,
-// whatever the schedule.  Per round: GcMaxApp (parent = uncoloured vertex,
-// child item = neighbour: "does it outrank me and is it still uncoloured?"),
-// GcGatherApp (parents that are local maxima mark their neighbours' colours
-// in a deg+1-bit bitmap at bit offset rowptr[u] + u), then a flat mex pass.
+// coloured once all its higher-priority neighbours are, with the smallest
+// colour they do not use — exactly the sequential greedy colouring in
+// priority order, whatever the schedule.  Counter form: wait[u] = number of
+// still-uncoloured higher-priority neighbours; rounds run over a worklist of
+// ready vertices (wait == 0), so every vertex scans its neighbours a
+// constant number of times (O(m) total) instead of once per round.  The
+// worklist length lives on the device (parents beyond it exit), so rounds
+// are queued without a host readback each:
+//   GcCountApp   parent = vertex, child = neighbour: wait[u] += key(w) > key(u)
+//   GcGatherApp  parent = ready vertex, child = neighbour: a higher-priority
+//                neighbour's colour c is marked in u's (deg+1)-bit bitmap at
+//                bit offset rowptr[u] + u + c  (then a flat mex pass)
+//   GcNotifyApp  parent = vertex coloured this round, child = neighbour: a
+//                lower-priority neighbour's wait drops; at 0 it joins the
+//                next round's worklist
 // ---------------------------------------------------------------------------
 __host__ __device__ __forceinline__ unsigned long long gc_key(int v) {
   unsigned x = (unsigned)v * 0x9E3779B1u;
@@ -518,23 +526,73 @@ __host__ __device__ __forceinline__ unsigned long long gc_key(int v) {
   return ((unsigned long long)x << 32) | (unsigned)v;
 }
 
-struct GcMaxApp {
+struct GcCountApp {
   const int* __restrict__ rowptr;
   const int* __restrict__ col;
-  const int* color;  // -1: uncoloured
-  int* notmax;       // set when an uncoloured neighbour outranks the vertex
+  int* wait;
   int n;
   int pad;
 
   struct alignas(16) Args {
     int start, deg, u, pad;
   };
-  struct Acc {};
+  // run-length count of the vertex this thread works on (one atomic per
+  // vertex per thread instead of one per edge)
+  struct Acc {
+    int u, c;
+  };
 
   __device__ int nparents() const { return n; }
   __device__ void parent_prologue() const {}
   __device__ int expand(int u, bool valid, Args& a) const {
-    if (!valid || __ldcg(color + u) >= 0) return 0;
+    if (!valid) return 0;
+    const int s = __ldg(rowptr + u);
+    const int d = __ldg(rowptr + u + 1) - s;
+    a = Args{s, d, u, 0};
+    return d > 0 ? d : 0;
+  }
+  __device__ static int count(const Args& a) { return a.deg; }
+  __device__ void item(const Args& a, int e, Acc& acc) const {
+    const int w = ld_stream(col + a.start + e);
+    if (acc.c && acc.u != a.u) {
+      atomicAdd(wait + acc.u, acc.c);
+      acc.c = 0;
+    }
+    acc.u = a.u;
+    acc.c += gc_key(w) > gc_key(a.u);
+  }
+  static constexpr int kUnroll = 1;
+  static constexpr bool kBlockMode = false;
+  static constexpr bool kPureExpand = true;
+  static constexpr int kMinBlocks = 1;
+  template <int U, class ArgsOf>
+  __device__ __forceinline__ void items(ArgsOf args, const int* e,
+                                        const bool* ok, Acc& acc) const {
+    items_loop<U>(*this, args, e, ok, acc);
+  }
+  __device__ void flush(Acc& acc) const {
+    if (acc.c) atomicAdd(wait + acc.u, acc.c);
+  }
+};
+
+struct GcGatherApp {
+  const int* __restrict__ rowptr;
+  const int* __restrict__ col;
+  const int* __restrict__ ready;  // this round's worklist
+  const int* nready;              // its length (on the device)
+  const int* color;
+  unsigned* used;  // bit rowptr[u] + u + c: colour c taken by a neighbour
+
+  struct alignas(16) Args {
+    int start, deg, u, pad;
+  };
+  struct Acc {};
+
+  __device__ int nparents() const { return __ldcg(nready); }
+  __device__ void parent_prologue() const {}
+  __device__ int expand(int i, bool valid, Args& a) const {
+    if (!valid) return 0;
+    const int u = __ldcg(ready + i);
     const int s = __ldg(rowptr + u);
     const int d = __ldg(rowptr + u + 1) - s;
     a = Args{s, d, u, 0};
@@ -543,9 +601,12 @@ struct GcMaxApp {
   __device__ static int count(const Args& a) { return a.deg; }
   __device__ void item(const Args& a, int e, Acc&) const {
     const int w = ld_stream(col + a.start + e);
-    if (__ldcg(color + w) < 0 && gc_key(w) > gc_key(a.u) &&
-        __ldcg(notmax + a.u) == 0)
-      notmax[a.u] = 1;
+    if (gc_key(w) < gc_key(a.u)) return;  // lower priority: not coloured yet
+    const int c = __ldcg(color + w);
+    if (c >= 0 && c <= a.deg) {
+      const long long bit = (long long)a.start + a.u + c;
+      atomicOr(used + (bit >> 5), 1u << (bit & 31));
+    }
   }
   static constexpr int kUnroll = 1;
   static constexpr bool kBlockMode = false;
@@ -559,24 +620,25 @@ struct GcMaxApp {
   __device__ void flush(Acc&) const {}
 };
 
-struct GcGatherApp {
+struct GcNotifyApp {
   const int* __restrict__ rowptr;
   const int* __restrict__ col;
-  const int* color;
-  const int* notmax;
-  unsigned* used;  // bit rowptr[u] + u + c: colour c taken by a neighbour
-  int n;
-  int pad;
+  const int* __restrict__ ready;  // vertices coloured this round
+  const int* nready;
+  int* wait;
+  int* next;        // next round's worklist
+  int* next_count;
 
   struct alignas(16) Args {
     int start, deg, u, pad;
   };
   struct Acc {};
 
-  __device__ int nparents() const { return n; }
+  __device__ int nparents() const { return __ldcg(nready); }
   __device__ void parent_prologue() const {}
-  __device__ int expand(int u, bool valid, Args& a) const {
-    if (!valid || __ldcg(color + u) >= 0 || __ldcg(notmax + u)) return 0;
+  __device__ int expand(int i, bool valid, Args& a) const {
+    if (!valid) return 0;
+    const int u = __ldcg(ready + i);
     const int s = __ldg(rowptr + u);
     const int d = __ldg(rowptr + u + 1) - s;
     a = Args{s, d, u, 0};
@@ -584,11 +646,17 @@ struct GcGatherApp {
   }
   __device__ static int count(const Args& a) { return a.deg; }
   __device__ void item(const Args& a, int e, Acc&) const {
-    const int c = __ldcg(color + ld_stream(col + a.start + e));
-    if (c >= 0 && c <= a.deg) {
-      const long long bit = (long long)a.start + a.u + c;
-      atomicOr(used + (bit >> 5), 1u << (bit & 31));
-    }
+    const int w = ld_stream(col + a.start + e);
+    const bool last = gc_key(w) < gc_key(a.u) && atomicSub(wait + w, 1) == 1;
+    // warp-aggregated append of the vertices that just became ready
+    const unsigned am = __activemask();
+    const unsigned m = __ballot_sync(am, last);
+    if (!m) return;
+    const int leader = __ffs(m) - 1;
+    int base = 0;
+    if (lane_id() == leader) base = atomicAdd(next_count, __popc(m));
+    base = __shfl_sync(am, base, leader);
+    if (last) next[base + __popc(m & lanemask_lt())] = w;
   }
   static constexpr int kUnroll = 1;
   static constexpr bool kBlockMode = false;

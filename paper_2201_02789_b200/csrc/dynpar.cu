@@ -818,21 +818,38 @@ int sssp_dev_impl(const int32_t* rowptr, const int32_t* col,
                  st, arr);
 }
 
-// mex pass of a colouring round: local maxima take the smallest colour not
-// marked in their bitmap [rowptr[u] + u, rowptr[u] + u + deg]; the others
-// clear their notmax flag for the next round.  Counts vertices coloured.
-__global__ void gc_finalize_kernel(const int* __restrict__ rowptr, int n,
-                                   int* color, int* notmax,
-                                   const unsigned* __restrict__ used,
-                                   unsigned long long* colored) {
-  unsigned long long c = 0;
-  for (long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x; u < n;
-       u += (long long)gridDim.x * blockDim.x) {
-    if (color[u] >= 0) continue;
-    if (notmax[u]) {
-      notmax[u] = 0;
-      continue;
-    }
+// Vertices whose wait count is 0 after the count pass: the first worklist.
+__global__ void gc_seed_kernel(const int* __restrict__ wait, int n, int* list,
+                               int* count) {
+  for (long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x -
+                     lane_id();
+       b < n; b += (long long)gridDim.x * blockDim.x) {
+    const long long u = b + lane_id();
+    const bool ready = u < n && __ldg(wait + u) == 0;
+    const unsigned m = __ballot_sync(DP_FULL, ready);
+    int base = 0;
+    if (lane_id() == 0 && m) base = atomicAdd(count, __popc(m));
+    base = __shfl_sync(DP_FULL, base, 0);
+    if (ready) list[base + __popc(m & lanemask_lt())] = (int)u;
+  }
+}
+
+// mex pass of a colouring round: each ready vertex takes the smallest colour
+// not marked in its bitmap [rowptr[u] + u, rowptr[u] + u + deg].  Thread 0
+// also counts the round if it was not empty and clears the next round's
+// worklist length.
+__global__ void gc_mex_kernel(const int* __restrict__ rowptr,
+                              const int* __restrict__ list, const int* count,
+                              int* next_count, int* rounds, int* color,
+                              const unsigned* __restrict__ used) {
+  const int nr = __ldcg(count);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *next_count = 0;
+    if (nr > 0) *rounds += 1;
+  }
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nr;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int u = list[i];
     const long long b0 = (long long)rowptr[u] + u;
     const long long b1 = (long long)rowptr[u + 1] + u + 1;  // deg + 1 bits
     long long bit = b0;
@@ -850,10 +867,7 @@ __global__ void gc_finalize_kernel(const int* __restrict__ rowptr, int n,
       bit = wend;
     }
     color[u] = mex;  // always found: deg neighbours use at most deg colours
-    ++c;
   }
-  c = warp_sum_u64(c);
-  if (lane_id() == 0 && c) atomicAdd(colored, c);
 }
 
 int gc_dev_impl(const int32_t* rowptr, const int32_t* col, int32_t n,
@@ -864,15 +878,17 @@ int gc_dev_impl(const int32_t* rowptr, const int32_t* col, int32_t n,
   if (n < 0 || m < 0) return fail(DP_ERR_INVALID, "bad graph size");
   Workspace* w = workspace(&r);
   if (!w) return r;
+  // used bitmap | wait[n] | two worklists[n] | counts[2] | rounds
   const size_t words = (size_t)((m + n + 31) / 32) + 1;
+  const size_t nn = (size_t)std::max(n, 1);
   if ((r = grow(&w->io[5], &w->io_bytes[5],
-                words * sizeof(unsigned) + (size_t)n * sizeof(int))))
+                words * sizeof(unsigned) + (nn * 3 + 4) * sizeof(int))))
     return r;
   unsigned* used = (unsigned*)w->io[5];
-  int* notmax = (int*)(used + words);
-  DP_CUDA(cudaMemsetAsync(used, 0, words * sizeof(unsigned), s));
-  DP_CUDA(cudaMemsetAsync(notmax, 0, (size_t)n * sizeof(int), s));
-  if (n) DP_CUDA(cudaMemsetAsync(color, 0xff, (size_t)n * sizeof(int), s));
+  int* wait = (int*)(used + words);
+  int* list[2] = {wait + nn, wait + 2 * nn};
+  int* cnt = wait + 3 * nn;  // cnt[0], cnt[1]: worklist lengths
+  int* d_rounds = cnt + 2;
   long long launchers = 0;
   if (c->variant == DP_VARIANT_CDP &&
       (r = count_launchers(w, c, rowptr, n, 0, s, &launchers)))
@@ -882,48 +898,67 @@ int gc_dev_impl(const int32_t* rowptr, const int32_t* col, int32_t n,
   if ((r = begin_run(w, s))) return r;
   RunCounters rc;
   DP_CUDA(cudaEventRecord(w->ev0, s));
-  long long remaining = n;
-  int rounds = 0;
-  const int fin_blocks = std::max(1, std::min(dp::ceil_div(n, 256), 148 * 8));
-  while (remaining > 0) {
-    GcMaxApp a0;
-    a0.rowptr = rowptr;
-    a0.col = col;
-    a0.color = color;
-    a0.notmax = notmax;
-    a0.n = n;
-    a0.pad = 0;
-    if ((r = launch_parent(a0, n, launchers, c, w, s, &rc))) return r;
-    GcGatherApp a1;
-    a1.rowptr = rowptr;
-    a1.col = col;
-    a1.color = color;
-    a1.notmax = notmax;
-    a1.used = used;
-    a1.n = n;
-    a1.pad = 0;
-    if ((r = launch_parent(a1, n, launchers, c, w, s, &rc))) return r;
-    DP_CUDA(cudaMemsetAsync(w->d_scratch + 1, 0, sizeof(unsigned long long),
-                            s));
-    gc_finalize_kernel<<<fin_blocks, 256, 0, s>>>(rowptr, n, color, notmax,
-                                                  used, w->d_scratch + 1);
-    DP_CUDA(cudaGetLastError());
-    rc.kernel_launches += 1;
-    DP_CUDA(cudaMemcpyAsync(w->h_ctr + 1, w->d_scratch + 1,
-                            sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                            s));
-    if ((r = read_state(w, s))) return r;
-    const long long got = (long long)w->h_ctr[1];
-    if (got <= 0) return fail(DP_ERR_ITERATIONS, "colouring made no progress");
-    remaining -= got;
-    ++rounds;
+  DP_CUDA(cudaMemsetAsync(used, 0, words * sizeof(unsigned), s));
+  DP_CUDA(cudaMemsetAsync(wait, 0, nn * sizeof(int), s));
+  DP_CUDA(cudaMemsetAsync(cnt, 0, 3 * sizeof(int), s));
+  if (n) DP_CUDA(cudaMemsetAsync(color, 0xff, (size_t)n * sizeof(int), s));
+  GcCountApp ca;
+  ca.rowptr = rowptr;
+  ca.col = col;
+  ca.wait = wait;
+  ca.n = n;
+  ca.pad = 0;
+  if ((r = launch_parent(ca, n, launchers, c, w, s, &rc))) return r;
+  const int fb = std::max(1, std::min(dp::ceil_div(std::max(n, 1), 256),
+                                      148 * 8));
+  gc_seed_kernel<<<fb, 256, 0, s>>>(wait, n, list[0], cnt);
+  DP_CUDA(cudaGetLastError());
+  rc.kernel_launches += 1;
+  // Rounds are queued in batches without a host round trip each: parents
+  // past the device-side worklist length exit, an empty round is a no-op.
+  // Every vertex is coloured after at most n non-empty rounds.
+  constexpr int kBatch = 8;
+  int cur = 0;
+  for (long long queued = 0;; queued += kBatch) {
+    if (queued > (long long)n + kBatch)
+      return fail(DP_ERR_ITERATIONS, "colouring made no progress");
+    for (int b = 0; b < kBatch; ++b) {
+      GcGatherApp ga;
+      ga.rowptr = rowptr;
+      ga.col = col;
+      ga.ready = list[cur];
+      ga.nready = cnt + cur;
+      ga.color = color;
+      ga.used = used;
+      if ((r = launch_parent(ga, n, launchers, c, w, s, &rc))) return r;
+      gc_mex_kernel<<<fb, 256, 0, s>>>(rowptr, list[cur], cnt + cur,
+                                       cnt + (cur ^ 1), d_rounds, color, used);
+      DP_CUDA(cudaGetLastError());
+      rc.kernel_launches += 1;
+      GcNotifyApp na;
+      na.rowptr = rowptr;
+      na.col = col;
+      na.ready = list[cur];
+      na.nready = cnt + cur;
+      na.wait = wait;
+      na.next = list[cur ^ 1];
+      na.next_count = cnt + (cur ^ 1);
+      if ((r = launch_parent(na, n, launchers, c, w, s, &rc))) return r;
+      cur ^= 1;
+    }
+    int h[3] = {0, 0, 0};
+    DP_CUDA(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, s));
+    if ((r = read_state(w, s))) return r;  // syncs s
+    if (h[cur] == 0) break;  // the next round's worklist is empty: done
   }
   DP_CUDA(cudaEventRecord(w->ev1, s));
   DP_CUDA(cudaEventSynchronize(w->ev1));
   float ms = 0.f;
   DP_CUDA(cudaEventElapsedTime(&ms, w->ev0, w->ev1));
   if ((r = read_state(w, s))) return r;
-  rc.ms_kernel_sum = rc.ms_kernel_max = ms;  // three launches per round
+  int rounds = 0;
+  DP_CUDA(cudaMemcpy(&rounds, d_rounds, sizeof(int), cudaMemcpyDeviceToHost));
+  rc.ms_kernel_sum = rc.ms_kernel_max = ms;
   finish_stats(w, rc, ms, st);
   if (st) st->iterations = rounds;
   return 0;

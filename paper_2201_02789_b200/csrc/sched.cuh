@@ -407,7 +407,8 @@ __global__ void __launch_bounds__(256)
   for (long long c = blockIdx.x; c < nchunks; c += gridDim.x) {
     const long long lu = c * blockDim.x + threadIdx.x;
     Args a{};
-    const int cnt = app.expand((int)(base + lu), lu < nparents, a);
+    const int cnt = app.expand((int)(base + lu),
+                               lu < nparents && base + lu < app.nparents(), a);
     const bool go = cnt > 0 && (k.threshold == 0 || cnt >= k.threshold);
     const int gd = go ? ceil_div(ceil_div(cnt, k.cb), k.cf) : 0;
     const BlockScan s = block_scan(gd > 0, gd, smem);
@@ -450,7 +451,8 @@ __global__ void __launch_bounds__(256)
   for (long long c = blockIdx.x; c < nchunks; c += gridDim.x) {
     const long long lu = c * blockDim.x + threadIdx.x;
     Args a{};
-    const int cnt = app.expand((int)(base + lu), lu < nparents, a);
+    const int cnt = app.expand((int)(base + lu),
+                               lu < nparents && base + lu < app.nparents(), a);
     const bool go = cnt > 0 && (k.threshold == 0 || cnt >= k.threshold);
     serial_arm(app, a, cnt, !go, k.serial_warp != 0, acc);
   }

@@ -1,0 +1,10 @@
+"""One GC run on an RMAT graph under a policy (for ncu)."""
+import json
+import sys
+from pathlib import Path
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2201_02789_b200.bench import BenchConfig, load, run_config  # noqa
+bench, wl = load("gc", sys.argv[1] if len(sys.argv) > 1 else "rmat:20:seed1")
+cfg = BenchConfig(**json.loads(sys.argv[2]))
+rep, _ = run_config(bench, wl, cfg)
+print(rep.ns_device / 1e6, rep.iterations)
