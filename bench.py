@@ -419,11 +419,14 @@ def init_dist(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     launched = world > 1 or ("MASTER_ADDR" in os.environ
                              and "RANK" in os.environ)
-    if launched and not torch.distributed.is_initialized():
-        backend = "nccl" if args.impl == "ours" else "gloo"
-        torch.distributed.init_process_group(backend)
     if torch.cuda.is_available():
         torch.cuda.set_device(local)
+    if launched and not torch.distributed.is_initialized():
+        if args.impl == "ours":  # one process per GPU, bound to LOCAL_RANK
+            torch.distributed.init_process_group(
+                "nccl", device_id=torch.device("cuda", local))
+        else:
+            torch.distributed.init_process_group("gloo")
     return world, rank, local
 
 
