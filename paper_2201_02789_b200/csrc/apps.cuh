@@ -21,7 +21,7 @@
 namespace dp {
 
 #ifndef DP_GRAPH_UNROLL
-#define DP_GRAPH_UNROLL 4
+#define DP_GRAPH_UNROLL 2  // tools/ab.sh: 2 < 4 < 8 (profiles/ab_unroll_r01.txt)
 #endif
 #ifndef DP_MERGE_COUNTS
 #define DP_MERGE_COUNTS 1
