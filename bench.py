@@ -20,8 +20,10 @@ cpu_baseline (the C oracle on the host cores), speed-ups over the naive-CDP
 and aggregation-only (KLAP-style) builds, and the other BASELINE workloads
 (BFS RMAT-22, TC RMAT-22, BT 25k curves) under "workloads".
 
-N > 1: the same SSSP over a cyclic 1D vertex partition (one part per rank,
-per-round NCCL all-to-all of improving remote relaxations; DESIGN.md §8);
+N > 1: the same SSSP over a cyclic 1D vertex partition (one part per rank;
+remote relaxations are atomicMin into the owner's dist through symmetric
+memory, one NCCL max-reduction per round; --exchange a2a uses the NCCL
+all-to-all instead; DESIGN.md §8);
 --workload bfs26 / tc run the other partitioned configs (5 / 4).
 """
 
@@ -455,15 +457,35 @@ def arm_sssp_partitioned(args, world, rank, local):
     g = graphs.rmat_graph(SCALE, SEED)
     w = graphs.edge_weights(g, SEED)
     rp_p, col_p, w_p = pdist.partition_csr(g.rowptr, g.col, world, rank, w)
-    part = pdist.SsspPart(rp_p, col_p, w_p, g.n, world, rank, 0, dev)
-    ops = pdist.DeviceSsspOps(_cfg(BEST["sssp"]))
-    ex = (pdist.CollectiveExchange() if torch.distributed.is_initialized()
-          else pdist.LocalExchange())
+    collective = torch.distributed.is_initialized()
+    exchange = args.exchange
+    part = ex = None
+    if exchange == "peer":
+        # fused exchange: remote relaxations are atomicMin into the owner's
+        # dist through symmetric memory (NVLink peer addresses)
+        try:
+            ex = pdist.PeerCollective() if collective else pdist.PeerLocal()
+            buf = ex.alloc(g.n, world, dev)
+            part = pdist.SsspPeerPart(rp_p, col_p, w_p, g.n, world, rank, 0,
+                                      buf, dev)
+            ex.bind([part])
+            ops = pdist.DeviceSsspPeerOps(_cfg(BEST["sssp"]))
+            run_rounds = pdist.sssp_1d_peer
+        except Exception as e:  # noqa: BLE001 - fall back to the NCCL a2a
+            print(f"[bench] symmetric memory unavailable ({e}); using the "
+                  f"all-to-all exchange", file=sys.stderr)
+            exchange = "a2a"
+    if exchange == "a2a":
+        part = pdist.SsspPart(rp_p, col_p, w_p, g.n, world, rank, 0, dev)
+        ops = pdist.DeviceSsspOps(_cfg(BEST["sssp"]))
+        ex = pdist.CollectiveExchange() if collective else \
+            pdist.LocalExchange()
+        run_rounds = pdist.sssp_1d
     stream_obj = torch.cuda.current_stream()
 
     def step():
         part.reset(0)
-        return pdist.sssp_1d([part], ops, ex)
+        return run_rounds([part], ops, ex)
     with ClockSampler(local) as clk:
         total_ms, outs = timed_steps(step, args.steps, args.warmup,
                                      stream_obj)
@@ -486,7 +508,7 @@ def arm_sssp_partitioned(args, world, rank, local):
         part.col.copy_(hp[1], non_blocking=True)
         part.weight.copy_(hp[2], non_blocking=True)
         part.reset(0)
-        pdist.sssp_1d([part], ops, ex)
+        run_rounds([part], ops, ex)
         out_h.copy_(part.dist, non_blocking=True)
         torch.cuda.synchronize()
         if i:
@@ -510,6 +532,10 @@ def arm_sssp_partitioned(args, world, rank, local):
                    "n": g.n, "m": g.m, "e_reach": e_reach, "rounds": rounds,
                    "policy": BEST["sssp"],
                    "parallelism": f"1d-cyclic-partition x{world}",
+                   "exchange": ("fused: remote atomicMin into the owner's "
+                                "dist via symmetric memory + NCCL max of the "
+                                "round flag" if exchange == "peer" else
+                                "NCCL all-to-all of (v, alt) pairs + apply"),
                    "l2": "inputs exceed L2; no flush"},
         "parity": "bit-exact vs oracle" if np.array_equal(dist_h, want)
         else "MISMATCH",
@@ -773,6 +799,9 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--quick", action="store_true",
                     help="headline only (skip the other workloads)")
+    ap.add_argument("--exchange", choices=("peer", "a2a"), default="peer",
+                    help="N > 1 SSSP: fused peer-memory relaxation (default) "
+                         "or the NCCL all-to-all exchange")
     ap.add_argument("--workload", choices=("sssp", "bfs26", "tc"),
                     default="sssp",
                     help="sssp = headline (BASELINE config 3); bfs26 / tc = "

@@ -311,7 +311,7 @@ struct SsspPartApp {
   static constexpr int kUnroll = DP_SSSP_UNROLL;
   static constexpr bool kBlockMode = false;
   static constexpr bool kPureExpand = true;
-  static constexpr int kMinBlocks = 1;
+  static constexpr int kMinBlocks = DP_SSSP_MINB;
   template <int U, class ArgsOf>
   __device__ __forceinline__ void items(ArgsOf args, const int* e,
                                         const bool* ok, Acc& acc) const {
@@ -331,6 +331,92 @@ struct SsspPartApp {
   __device__ void flush(Acc& acc) const {
     // read before write: after the first success the flag line is only
     // read (shared), not re-written by every succeeding warp
+    if (__any_sync(DP_FULL, acc.changed) && lane_id() == 0 &&
+        __ldcg(changed) == 0)
+      *changed = 1;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// SSSP on one part of the cyclic 1D partition, exchange fused into the
+// relaxation: the parts' dist arrays are mapped into every part's address
+// space (symmetric memory over NVLink / NVSwitch, or plain allocations when
+// all parts share one GPU), and a remote relaxation is an atomicMin straight
+// into the owner's dist — no send buckets, no all-to-all, no apply pass.
+// The per-part best-sent filter still keeps each part from re-sending a value
+// that cannot lower dist[v].  A warp that wrote remotely fences system-wide
+// before it retires, so the round's remote lowerings are visible to every
+// part once the round's flag reduction (the only collective) completes.
+// ---------------------------------------------------------------------------
+struct SsspPeerApp {
+  const int* __restrict__ rowptr;
+  const int* __restrict__ col;
+  const int* __restrict__ weight;
+  int* const* peer_dist;  // [nparts]: every part's dist (local index)
+  int* best;              // dense, global ids: best value sent per vertex
+  int* changed;
+  int n_local;
+  int nparts;
+  int part;
+  int pad;
+
+  struct alignas(16) Args {
+    int start, deg, du, pad;
+  };
+  struct Acc {
+    int changed;
+    int remote;
+  };
+
+  __device__ int nparents() const { return n_local; }
+  __device__ void parent_prologue() const {}
+  __device__ int expand(int lu, bool valid, Args& a) const {
+    if (!valid) return 0;
+    const int du = __ldcg(peer_dist[part] + lu);
+    if (du >= kUnreached) return 0;
+    const int s = __ldg(rowptr + lu);
+    const int d = __ldg(rowptr + lu + 1) - s;
+    a = Args{s, d, du, 0};
+    return d > 0 ? d : 0;
+  }
+  __device__ static int count(const Args& a) { return a.deg; }
+  __device__ void relax(int v, int alt, Acc& acc) const {
+    const int q = v % nparts;
+    int* d = peer_dist[q] + v / nparts;
+    if (q == part) {
+      if (alt < __ldcg(d) && atomicMin(d, alt) > alt) acc.changed = 1;
+    } else if (alt < __ldcg(best + v) && atomicMin(best + v, alt) > alt) {
+      acc.remote = 1;
+      if (atomicMin(d, alt) > alt) acc.changed = 1;
+    }
+  }
+  __device__ void item(const Args& a, int e, Acc& acc) const {
+    relax(ld_stream(col + a.start + e),
+          (int)((unsigned)a.du + (unsigned)ld_stream(weight + a.start + e)),
+          acc);
+  }
+  static constexpr int kUnroll = DP_SSSP_UNROLL;
+  static constexpr bool kBlockMode = false;
+  static constexpr bool kPureExpand = true;
+  static constexpr int kMinBlocks = DP_SSSP_MINB;
+  template <int U, class ArgsOf>
+  __device__ __forceinline__ void items(ArgsOf args, const int* e,
+                                        const bool* ok, Acc& acc) const {
+    int v[U], alt[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int i = ok[j] ? args(j).start + e[j] : 0;
+      v[j] = ok[j] ? ld_stream(col + i) : 0;
+      alt[j] = ok[j] ? (int)((unsigned)args(j).du +
+                             (unsigned)ld_stream(weight + i))
+                     : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j)
+      if (ok[j]) relax(v[j], alt[j], acc);
+  }
+  __device__ void flush(Acc& acc) const {
+    if (__any_sync(DP_FULL, acc.remote)) __threadfence_system();
     if (__any_sync(DP_FULL, acc.changed) && lane_id() == 0 &&
         __ldcg(changed) == 0)
       *changed = 1;

@@ -1595,6 +1595,49 @@ __global__ void sssp_part_apply_kernel(const unsigned long long* __restrict__ re
   if (__any_sync(DP_FULL, c) && lane_id() == 0) *changed = 1;
 }
 
+// One round of the fused-exchange partitioned SSSP (SsspPeerApp).
+int sssp_peer_round_impl(const int32_t* rowptr, const int32_t* col,
+                         const int32_t* weight, int32_t n_local,
+                         int32_t nparts, int32_t part, const dp_config* c,
+                         int32_t* const* peer_dist, int32_t* best,
+                         int32_t* changed, cudaStream_t s, dp_stats* st) {
+  int r;
+  if ((r = validate(c))) return r;
+  if (nparts < 1 || part < 0 || part >= nparts || n_local < 0 || !peer_dist)
+    return fail(DP_ERR_INVALID, "bad partition arguments");
+  Workspace* w = workspace(&r);
+  if (!w) return r;
+  long long launchers = 0;
+  if (c->variant == DP_VARIANT_CDP &&
+      (r = count_launchers(w, c, rowptr, n_local, 0, s, &launchers)))
+    return r;
+  if ((r = ensure_pending_limit(w, c, launch_bound(c, n_local, launchers))))
+    return r;
+  if ((r = begin_run(w, s))) return r;
+  SsspPeerApp a;
+  a.rowptr = rowptr;
+  a.col = col;
+  a.weight = weight;
+  a.peer_dist = (int* const*)peer_dist;
+  a.best = best;
+  a.changed = changed;
+  a.n_local = n_local;
+  a.nparts = nparts;
+  a.part = part;
+  a.pad = 0;
+  RunCounters rc;
+  DP_CUDA(cudaEventRecord(w->ev0, s));
+  if ((r = launch_parent(a, n_local, launchers, c, w, s, &rc))) return r;
+  DP_CUDA(cudaEventRecord(w->ev1, s));
+  if ((r = read_state_fast(w, s))) return r;
+  if ((r = account_step(w, &rc))) return r;
+  float ms = 0.f;
+  DP_CUDA(cudaEventElapsedTime(&ms, w->ev0, w->ev1));
+  finish_stats(w, rc, ms, st);
+  if (st) st->iterations = 1;
+  return 0;
+}
+
 int sssp_part_round_impl(const int32_t* rowptr, const int32_t* col,
                          const int32_t* weight, int32_t n_local,
                          int32_t nparts, int32_t part, const dp_config* c,
@@ -2101,6 +2144,21 @@ int dp_sssp_part_round(const int32_t* d_rowptr_p, const int32_t* d_col_p,
                                nparts, part, cfg, d_dist_p, d_best, d_send_buf,
                                d_send_off, d_send_counts, d_changed,
                                (cudaStream_t)stream, stats);
+  if (stats) stats->ns_host = now_ns() - t0;
+  return r;
+}
+
+int dp_sssp_part_round_peer(const int32_t* d_rowptr_p, const int32_t* d_col_p,
+                            const int32_t* d_weight_p, int32_t n_local,
+                            int32_t nparts, int32_t part,
+                            const dp_config* cfg, int32_t* const* d_peer_dist,
+                            int32_t* d_best, int32_t* d_changed, void* stream,
+                            dp_stats* stats) {
+  clear_stats(stats);
+  const double t0 = now_ns();
+  int r = sssp_peer_round_impl(d_rowptr_p, d_col_p, d_weight_p, n_local,
+                               nparts, part, cfg, d_peer_dist, d_best,
+                               d_changed, (cudaStream_t)stream, stats);
   if (stats) stats->ns_host = now_ns() - t0;
   return r;
 }

@@ -518,3 +518,163 @@ def sssp_1d(parts: list, ops, exchange, max_rounds: int | None = None):
         if not exchange.any_changed(parts):
             return exchange.dist(parts), rnd + 1
     raise RuntimeError("sssp used more rounds than vertices")
+
+
+# ---------------------------------------------------------------------------
+# SSSP over the same partition with the exchange fused into the relaxation
+# (csrc/apps.cuh SsspPeerApp): every part's dist is addressable from every
+# part — torch symmetric memory (peer-mapped over NVLink / NVSwitch) across
+# ranks, plain allocations when all parts share one GPU — so a remote
+# relaxation is an atomicMin into the owner's dist.  A round is one kernel
+# per part plus the max-reduction of the changed flags; no all-to-all.
+# ---------------------------------------------------------------------------
+
+def dist_width(n: int, nparts: int) -> int:
+    """Rows of the largest part (every part's dist is allocated this wide, as
+    symmetric memory requires identical shapes)."""
+    return -(-n // nparts)
+
+
+class SsspPeerPart:
+    """One part's device state for the fused-exchange partitioned SSSP.
+    ``dist`` must be a [dist_width(n, nparts)] int32 tensor the other parts
+    can address (see PeerLocal / PeerCollective)."""
+
+    def __init__(self, rowptr, col, weight, n_global: int, nparts: int,
+                 part: int, src: int, dist, device):
+        import torch
+        self.nparts, self.part, self.n = nparts, part, n_global
+        self.rowptr = torch.as_tensor(rowptr).to(device=device,
+                                                  dtype=torch.int32)
+        self.col = torch.as_tensor(col).to(device=device, dtype=torch.int32)
+        self.weight = torch.as_tensor(weight).to(device=device,
+                                                  dtype=torch.int32)
+        self.n_local = int(self.rowptr.shape[0]) - 1
+        if dist.numel() < self.n_local:
+            raise ValueError("dist buffer narrower than the part")
+        self.dist_full = dist
+        self.dist = dist[:self.n_local]
+        i32 = dict(dtype=torch.int32, device=device)
+        self.best = torch.empty(n_global, **i32)
+        self.changed = torch.zeros(1, **i32)
+        self.peer_ptrs = None  # device int64[nparts], set by the exchange
+        self.stats: list[dict] = []
+        self.reset(src)
+
+    def reset(self, src: int) -> None:
+        self.dist_full.fill_(1 << 30)
+        if src % self.nparts == self.part:
+            self.dist_full[src // self.nparts] = 0
+        self.best.fill_(1 << 30)
+        self.stats = []
+
+
+class DeviceSsspPeerOps:
+    """One fused round of a part on the local GPU through the C-ABI."""
+
+    def __init__(self, cfg, stream=None):
+        from . import _lib
+        self.cfg = cfg
+        self.stream = stream
+        self.lib = _lib.device()
+
+    def round(self, p: SsspPeerPart) -> None:
+        from . import _lib
+        p.changed.zero_()
+        st = _lib.DpStats()
+        _lib.check(self.lib.dp_sssp_part_round_peer(
+            p.rowptr.data_ptr(), p.col.data_ptr(), p.weight.data_ptr(),
+            p.n_local, p.nparts, p.part, ctypes.byref(self.cfg),
+            p.peer_ptrs.data_ptr(), p.best.data_ptr(), p.changed.data_ptr(),
+            self.stream, ctypes.byref(st)))
+        p.stats.append(_lib.stats_dict(st))
+
+
+class PeerLocal:
+    """All parts on one GPU: the pointer table is the parts' own dist
+    buffers (plain device memory)."""
+
+    @staticmethod
+    def alloc(n: int, nparts: int, device):
+        import torch
+        return torch.empty(dist_width(n, nparts), dtype=torch.int32,
+                           device=device)
+
+    def bind(self, parts) -> None:
+        import torch
+        table = torch.tensor([p.dist_full.data_ptr() for p in parts],
+                             dtype=torch.int64, device=parts[0].dist.device)
+        for p in parts:
+            p.peer_ptrs = table
+
+    def any_changed(self, parts) -> bool:
+        return any(int(p.changed.item()) for p in parts)
+
+    def dist(self, parts):
+        import torch
+        n, P = parts[0].n, parts[0].nparts
+        out = torch.empty(n, dtype=torch.int32, device=parts[0].dist.device)
+        for p in parts:
+            out[p.part::P] = p.dist
+        return out
+
+
+class PeerCollective:
+    """One part per rank: dist lives in torch symmetric memory; the
+    rendezvous maps every rank's buffer into every rank (NVLink peer
+    addresses), the changed flags are max-reduced with NCCL."""
+
+    def __init__(self):
+        self.handle = None
+
+    def alloc(self, n: int, nparts: int, device):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+        try:  # older releases need the group enabled explicitly
+            symm_mem.enable_symm_mem_for_group(dist.group.WORLD.group_name)
+        except Exception:  # noqa: BLE001
+            pass
+        t = symm_mem.empty(dist_width(n, nparts), dtype=torch.int32,
+                           device=device)
+        self.handle = symm_mem.rendezvous(t, dist.group.WORLD)
+        return t
+
+    def bind(self, parts) -> None:
+        import torch
+        (p,) = parts
+        p.peer_ptrs = torch.tensor(list(self.handle.buffer_ptrs),
+                                   dtype=torch.int64, device=p.dist.device)
+
+    def any_changed(self, parts) -> bool:
+        import torch.distributed as dist
+        (p,) = parts
+        flag = p.changed.clone()
+        dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+        return bool(int(flag.item()))
+
+    def dist(self, parts):
+        return CollectiveExchange().dist(
+            [_DistView(parts[0])])
+
+
+class _DistView:
+    """Adapter exposing SsspPeerPart's fields to CollectiveExchange.dist."""
+
+    def __init__(self, p):
+        self.nparts, self.n, self.n_local, self.dist = (p.nparts, p.n,
+                                                        p.n_local, p.dist)
+
+
+def sssp_1d_peer(parts: list, ops, exchange, max_rounds: int | None = None):
+    """Bellman-Ford rounds with the fused exchange.  Returns (dist, rounds):
+    the same distances as sssp_1d (Bellman-Ford tolerates the remote
+    lowerings landing while the owner's round runs)."""
+    n = parts[0].n
+    limit = n + 1 if max_rounds is None else max_rounds
+    for rnd in range(limit):
+        for p in parts:
+            ops.round(p)
+        if not exchange.any_changed(parts):
+            return exchange.dist(parts), rnd + 1
+    raise RuntimeError("sssp used more rounds than vertices")

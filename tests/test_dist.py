@@ -252,3 +252,28 @@ def _sssp_collective_job():
 
 def test_sssp_1d_two_ranks_gloo():
     assert _run(2, _sssp_collective_job) == [True, True]
+
+
+def test_peer_part_layout_on_cpu():
+    """Host logic of the fused-exchange SSSP: identical-width dist buffers
+    (symmetric memory), owner rows, source placement, pointer table."""
+    import torch
+    rowptr = np.array([0, 2, 3, 3, 5, 6], np.int32)   # 5 vertices
+    col = np.array([1, 2, 0, 4, 1, 3], np.int32)
+    w = np.ones(6, np.int32)
+    P = 2
+    assert pdist.dist_width(5, P) == 3
+    ex = pdist.PeerLocal()
+    parts = [pdist.SsspPeerPart(*pdist.partition_csr(rowptr, col, P, p, w),
+                                5, P, p, 3, ex.alloc(5, P, "cpu"), "cpu")
+             for p in range(P)]
+    assert [p.n_local for p in parts] == [3, 2]
+    assert parts[1].dist.tolist() == [1 << 30, 0]       # vertex 3 = part 1 [1]
+    assert parts[0].dist.tolist() == [1 << 30] * 3
+    ex.bind(parts)
+    assert parts[0].peer_ptrs.tolist() == [p.dist_full.data_ptr()
+                                           for p in parts]
+    assert ex.dist(parts).tolist() == [1 << 30, 1 << 30, 1 << 30, 0, 1 << 30]
+    with pytest.raises(ValueError):
+        pdist.SsspPeerPart(*pdist.partition_csr(rowptr, col, P, 0, w), 5, P,
+                           0, 0, torch.empty(2, dtype=torch.int32), "cpu")

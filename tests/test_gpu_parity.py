@@ -717,3 +717,32 @@ def test_sssp_host_call_overlaps_copy_in_chunks(spec, monkeypatch):
             np.testing.assert_array_equal(rep.arrays["dist"], want)
         ref = run_reference(bench, wl)
         np.testing.assert_array_equal(ref.arrays["dist"], want)
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 4])
+@pytest.mark.parametrize("policy", [
+    dict(threshold=128, agg="block"),
+    dict(threshold=1024, cfactor=16, agg="multiblock", group_size=1 << 20,
+         parent_block=128, child_block=128, serial="warp"),
+    dict()])
+def test_sssp_fused_peer_exchange_on_device(P, policy):
+    """The fused-exchange partitioned SSSP (remote atomicMin into the
+    owner's dist through the pointer table), P parts on one GPU."""
+    import torch
+    from paper_2201_02789_b200 import dist as pdist
+    g = graphs.rmat_graph(16, 1)
+    w = graphs.edge_weights(g, 1)
+    want, _ = oracle.sssp(g.rowptr, g.col, w, nthreads=0)
+    dev = torch.device("cuda", 0)
+    ex = pdist.PeerLocal()
+    parts = [pdist.SsspPeerPart(*pdist.partition_csr(g.rowptr, g.col, P, p, w),
+                                g.n, P, p, 0, ex.alloc(g.n, P, dev), dev)
+             for p in range(P)]
+    ex.bind(parts)
+    ops = pdist.DeviceSsspPeerOps(BenchConfig(**policy).to_c())
+    d, rounds = pdist.sssp_1d_peer(parts, ops, ex)
+    np.testing.assert_array_equal(d.cpu().numpy(), want)
+    for p in parts:
+        p.reset(0)
+    d2, _ = pdist.sssp_1d_peer(parts, ops, ex)
+    np.testing.assert_array_equal(d2.cpu().numpy(), want)
