@@ -662,16 +662,35 @@ def arm_bfs26(args, world, rank, local):
     dev = torch.device("cuda", torch.cuda.current_device())
     scale = args.scale or 26
     rp, col = pdist.rmat_part_device(scale, SEED, world, rank, dev)
-    part = pdist.BfsPart(rp, col, 1 << scale, world, rank, 0, dev)
+    collective = torch.distributed.is_initialized()
+    exchange = args.exchange
+    part = None
+    if exchange == "peer":
+        # fused exchange: remote discoveries are CAS'd into the owner's dist
+        # through symmetric memory
+        try:
+            ex = pdist.PeerCollective() if collective else pdist.PeerLocal()
+            buf = ex.alloc(1 << scale, world, dev)
+            part = pdist.BfsPart(rp, col, 1 << scale, world, rank, 0, dev,
+                                 dist=buf)
+            ex.bind([part])
+            run_levels = pdist.bfs_1d_peer
+        except Exception as e:  # noqa: BLE001 - fall back to the NCCL a2a
+            print(f"[bench] symmetric memory unavailable ({e}); using the "
+                  f"all-to-all exchange", file=sys.stderr)
+            exchange = "a2a"
+    if exchange == "a2a":
+        part = pdist.BfsPart(rp, col, 1 << scale, world, rank, 0, dev)
+        ex = pdist.CollectiveExchange() if collective else \
+            pdist.LocalExchange()
+        run_levels = pdist.bfs_1d
     del rp, col
-    ex = (pdist.CollectiveExchange() if torch.distributed.is_initialized()
-          else pdist.LocalExchange())
     ops = pdist.DeviceBfsOps(_cfg(BEST["bfs"]))
     stream_obj = torch.cuda.current_stream()
 
     def step():
         part.reset(0)
-        return pdist.bfs_1d([part], ops, ex)
+        return run_levels([part], ops, ex)
     with ClockSampler(local) as clk:
         total_ms, outs = timed_steps(step, args.steps, args.warmup,
                                      stream_obj)
@@ -690,7 +709,12 @@ def arm_bfs26(args, world, rank, local):
             "config": {"workload": f"bfs rmat-{scale} from vertex 0",
                        "levels": levels, "edges_examined": e_t,
                        "policy": BEST["bfs"],
-                       "parallelism": f"1d-cyclic-partition x{world}"},
+                       "parallelism": f"1d-cyclic-partition x{world}",
+                       "exchange": ("fused: remote CAS into the owner's dist "
+                                    "via symmetric memory + NCCL max of the "
+                                    "level flag" if exchange == "peer" else
+                                    "NCCL all-to-all of discovered ids + "
+                                    "apply")},
             "clocks": clk.summary()}
     if scale <= 22:  # the oracle check fits the host quickly
         from oracle import oracle
@@ -800,7 +824,8 @@ def main():
     ap.add_argument("--quick", action="store_true",
                     help="headline only (skip the other workloads)")
     ap.add_argument("--exchange", choices=("peer", "a2a"), default="peer",
-                    help="N > 1 SSSP: fused peer-memory relaxation (default) "
+                    help="partitioned SSSP / BFS-26: fused peer-memory "
+                         "relaxation / discovery (default) "
                          "or the NCCL all-to-all exchange")
     ap.add_argument("--workload", choices=("sssp", "bfs26", "tc"),
                     default="sssp",

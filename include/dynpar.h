@@ -238,6 +238,17 @@ int dp_bfs_part_level(const int32_t* d_rowptr_p, const int32_t* d_col_p,
                       int32_t* d_counts, uint32_t* d_sent, int32_t* d_send_buf,
                       int64_t send_stride, int32_t* d_send_counts,
                       int32_t* d_changed, void* stream, dp_stats* stats);
+/* The same level with the exchange fused into the expansion: d_peer_dist is
+ * a DEVICE array of nparts pointers to every part's dist (symmetric memory
+ * across GPUs, plain pointers when all parts share one GPU; entry `part` ==
+ * d_dist_p); a remote discovery (first per part, d_sent) is a CAS of the
+ * owner's dist from UNREACHED to level + 1.  No buckets, no apply pass. */
+int dp_bfs_part_level_peer(const int32_t* d_rowptr_p, const int32_t* d_col_p,
+                           int32_t n_local, int32_t nparts, int32_t part,
+                           int32_t level, const dp_config* cfg,
+                           int32_t* d_dist_p, int32_t* const* d_peer_dist,
+                           int32_t* d_counts, uint32_t* d_sent,
+                           int32_t* d_changed, void* stream, dp_stats* stats);
 /* discover received global ids at level + 1 (CAS against UNREACHED) */
 int dp_bfs_part_apply(const int32_t* d_recv, int64_t nrecv, int32_t nparts,
                       int32_t level, int32_t* d_dist_p, int32_t* d_changed,

@@ -107,6 +107,8 @@ _SIGNATURES = {
     "dp_bfs_part_level": ([_P, _P, _I32, _I32, _I32, _I32, _CFG, _P, _P,
                            _P, _P, _I64, _P, _P, _P, _ST], ctypes.c_int),
     "dp_bfs_part_apply": ([_P, _I64, _I32, _I32, _P, _P, _P], ctypes.c_int),
+    "dp_bfs_part_level_peer": ([_P, _P, _I32, _I32, _I32, _I32, _CFG, _P, _P,
+                                _P, _P, _P, _P, _ST], ctypes.c_int),
     "dp_sssp_part_round": ([_P, _P, _P, _I32, _I32, _I32, _CFG, _P, _P, _P,
                             _P, _P, _P, _P, _ST], ctypes.c_int),
     "dp_sssp_part_apply": ([_P, _I64, _I32, _P, _P, _P], ctypes.c_int),

@@ -158,6 +158,9 @@ struct BfsPartApp {
   int* send_buf;                   // [nparts][stride]
   int* send_count;                 // [nparts]
   int* changed;
+  // fused exchange (null: buckets): every part's dist, addressable here
+  // (symmetric memory); a remote discovery is a CAS into the owner's dist
+  int* const* peer_dist;
   long long stride;
   int n_local;
   int nparts;
@@ -169,6 +172,7 @@ struct BfsPartApp {
   };
   struct Acc {
     int changed;
+    int remote;
   };
 
   __device__ int nparents() const { return n_local; }
@@ -193,22 +197,30 @@ struct BfsPartApp {
   }
   __device__ void update(int v, int d_or_bits, int lvl, Acc& acc) const {
     atomicAdd(counts + v, 1);
-    const int q = v % nparts;
+    const int q = part_of(v, nparts);
     if (q == part) {
-      const int lv = v / nparts;
+      const int lv = local_of(v, nparts);
       if (d_or_bits == kUnreached &&
           atomicCAS(dist + lv, kUnreached, lvl + 1) == kUnreached)
         acc.changed = 1;
     } else {
       const unsigned bit = 1u << (v & 31);
       if (!((unsigned)d_or_bits & bit) &&
-          !(atomicOr(sent + (v >> 5), bit) & bit))
-        push(q, v);
+          !(atomicOr(sent + (v >> 5), bit) & bit)) {
+        if (peer_dist) {
+          acc.remote = 1;
+          if (atomicCAS(peer_dist[q] + local_of(v, nparts), kUnreached, lvl + 1) ==
+              kUnreached)
+            acc.changed = 1;
+        } else {
+          push(q, v);
+        }
+      }
     }
   }
   // probe: the local dist (L1-cached, see BfsApp) or the sent-bitmap word
   __device__ int probe(int v) const {
-    return v % nparts == part ? __ldca(dist + v / nparts)
+    return part_of(v, nparts) == part ? __ldca(dist + local_of(v, nparts))
                               : (int)__ldcg(sent + (v >> 5));
   }
   __device__ void item(const Args& a, int e, Acc& acc) const {
@@ -233,6 +245,8 @@ struct BfsPartApp {
       if (ok[j]) update(v[j], d[j], args(j).level, acc);
   }
   __device__ void flush(Acc& acc) const {
+    // remote discoveries are visible to every part before this warp retires
+    if (__any_sync(DP_FULL, acc.remote)) __threadfence_system();
     // read before write: after the first success the flag line is only
     // read (shared), not re-written by every succeeding warp
     if (__any_sync(DP_FULL, acc.changed) && lane_id() == 0 &&
@@ -294,9 +308,9 @@ struct SsspPartApp {
         ((unsigned long long)(unsigned)v << 32) | (unsigned)alt;
   }
   __device__ void relax(int v, int alt, Acc& acc) const {
-    const int q = v % nparts;
+    const int q = part_of(v, nparts);
     if (q == part) {
-      const int lv = v / nparts;
+      const int lv = local_of(v, nparts);
       if (alt < __ldca(dist + lv) && atomicMin(dist + lv, alt) > alt)
         acc.changed = 1;
     } else if (alt < __ldca(best + v) && atomicMin(best + v, alt) > alt) {
@@ -381,8 +395,8 @@ struct SsspPeerApp {
   }
   __device__ static int count(const Args& a) { return a.deg; }
   __device__ void relax(int v, int alt, Acc& acc) const {
-    const int q = v % nparts;
-    int* d = peer_dist[q] + v / nparts;
+    const int q = part_of(v, nparts);
+    int* d = peer_dist[q] + local_of(v, nparts);
     if (q == part) {
       if (alt < __ldcg(d) && atomicMin(d, alt) > alt) acc.changed = 1;
     } else if (alt < __ldcg(best + v) && atomicMin(best + v, alt) > alt) {

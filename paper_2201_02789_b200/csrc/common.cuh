@@ -143,6 +143,17 @@ struct DevState {
                    // calls that overlap the H2D copy with the rounds)
 };
 
+// Owner part and local index of vertex v >= 0 under the cyclic partition
+// owner(v) = v % nparts.  Power-of-two part counts (the 1/2/4/8-GPU runs)
+// take a mask and a shift instead of an integer division per edge.
+__device__ __forceinline__ int part_of(int v, int nparts) {
+  return (nparts & (nparts - 1)) == 0 ? v & (nparts - 1) : v % nparts;
+}
+__device__ __forceinline__ int local_of(int v, int nparts) {
+  return (nparts & (nparts - 1)) == 0 ? v >> (__ffs(nparts) - 1)
+                                      : v / nparts;
+}
+
 // Chunks of the edge arrays copied so far (monotone counter written by the
 // copy stream); a parent may read edge slots [0, arrived << shift).
 __device__ __forceinline__ int arrived_chunks(const int* arrived) {

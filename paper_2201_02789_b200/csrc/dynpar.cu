@@ -1527,7 +1527,7 @@ __global__ void bfs_part_apply_kernel(const int* __restrict__ recv,
   int c = 0;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
        i < nrecv; i += (long long)gridDim.x * blockDim.x) {
-    const int lv = __ldg(recv + i) / nparts;
+    const int lv = local_of(__ldg(recv + i), nparts);
     if (__ldcg(dist + lv) == kUnreached &&
         atomicCAS(dist + lv, kUnreached, level + 1) == kUnreached)
       c = 1;
@@ -1540,7 +1540,8 @@ int bfs_part_level_impl(const int32_t* rowptr, const int32_t* col,
                         int32_t level, const dp_config* c, int32_t* dist,
                         int32_t* counts, uint32_t* sent, int32_t* send_buf,
                         int64_t stride, int32_t* send_count, int32_t* changed,
-                        cudaStream_t s, dp_stats* st) {
+                        cudaStream_t s, dp_stats* st,
+                        int32_t* const* peer_dist = nullptr) {
   int r;
   if ((r = validate(c))) return r;
   if (nparts < 1 || part < 0 || part >= nparts || n_local < 0 || level < 0)
@@ -1563,6 +1564,7 @@ int bfs_part_level_impl(const int32_t* rowptr, const int32_t* col,
   a.send_buf = send_buf;
   a.send_count = send_count;
   a.changed = changed;
+  a.peer_dist = (int* const*)peer_dist;
   a.stride = stride;
   a.n_local = n_local;
   a.nparts = nparts;
@@ -1588,7 +1590,7 @@ __global__ void sssp_part_apply_kernel(const unsigned long long* __restrict__ re
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
        i < nrecv; i += (long long)gridDim.x * blockDim.x) {
     const unsigned long long p = __ldg(recv + i);
-    const int lv = (int)(p >> 32) / nparts;
+    const int lv = local_of((int)(p >> 32), nparts);
     const int alt = (int)(unsigned)(p & 0xffffffffull);
     if (alt < __ldcg(dist + lv) && atomicMin(dist + lv, alt) > alt) c = 1;
   }
@@ -2115,6 +2117,24 @@ int dp_bfs_part_level(const int32_t* d_rowptr_p, const int32_t* d_col_p,
                               level, cfg, d_dist_p, d_counts, d_sent,
                               d_send_buf, send_stride, d_send_counts,
                               d_changed, (cudaStream_t)stream, stats);
+  if (stats) stats->ns_host = now_ns() - t0;
+  return r;
+}
+
+int dp_bfs_part_level_peer(const int32_t* d_rowptr_p, const int32_t* d_col_p,
+                           int32_t n_local, int32_t nparts, int32_t part,
+                           int32_t level, const dp_config* cfg,
+                           int32_t* d_dist_p, int32_t* const* d_peer_dist,
+                           int32_t* d_counts, uint32_t* d_sent,
+                           int32_t* d_changed, void* stream,
+                           dp_stats* stats) {
+  clear_stats(stats);
+  if (!d_peer_dist) return fail(DP_ERR_INVALID, "null peer table");
+  const double t0 = now_ns();
+  int r = bfs_part_level_impl(d_rowptr_p, d_col_p, n_local, nparts, part,
+                              level, cfg, d_dist_p, d_counts, d_sent, nullptr,
+                              0, nullptr, d_changed, (cudaStream_t)stream,
+                              stats, d_peer_dist);
   if (stats) stats->ns_host = now_ns() - t0;
   return r;
 }

@@ -196,7 +196,9 @@ class BfsPart:
     """One part's device state (tensors on ``device``)."""
 
     def __init__(self, rowptr, col, n_global: int, nparts: int, part: int,
-                 src: int, device):
+                 src: int, device, dist=None):
+        """``dist``: optional [>= n_local] int32 buffer the other parts can
+        address (the fused exchange, bfs_1d_peer); default a private one."""
         import torch
         self.nparts, self.part, self.n = nparts, part, n_global
         self.rowptr = torch.as_tensor(rowptr).to(device=device,
@@ -204,9 +206,16 @@ class BfsPart:
         self.col = torch.as_tensor(col).to(device=device, dtype=torch.int32)
         self.n_local = int(self.rowptr.shape[0]) - 1
         i32 = dict(dtype=torch.int32, device=device)
-        self.dist = torch.full((self.n_local,), 1 << 30, **i32)
+        if dist is None:
+            dist = torch.empty(self.n_local, **i32)
+        if dist.numel() < self.n_local:
+            raise ValueError("dist buffer narrower than the part")
+        self.dist_full = dist
+        self.dist = dist[:self.n_local]
+        self.dist_full.fill_(1 << 30)
         if src % nparts == part:
             self.dist[src // nparts] = 0
+        self.peer_ptrs = None  # fused exchange: device int64[nparts]
         self.counts = torch.zeros(n_global, **i32)
         self.sent = torch.zeros((n_global + 31) // 32, **i32)
         # a part sends each remote vertex at most once: bucket q never holds
@@ -219,7 +228,7 @@ class BfsPart:
 
     def reset(self, src: int) -> None:
         """Fresh BFS state (keeps the graph and buffers)."""
-        self.dist.fill_(1 << 30)
+        self.dist_full.fill_(1 << 30)
         if src % self.nparts == self.part:
             self.dist[src // self.nparts] = 0
         self.counts.zero_()
@@ -258,6 +267,19 @@ class DeviceBfsOps:
             _lib.check(self.lib.dp_bfs_part_apply(
                 recv.data_ptr(), recv.numel(), p.nparts, level,
                 p.dist.data_ptr(), p.changed.data_ptr(), self.stream))
+
+    def level_peer(self, p: BfsPart, level: int) -> None:
+        """The level with the exchange fused in (remote CAS through
+        p.peer_ptrs, dp_bfs_part_level_peer)."""
+        from . import _lib
+        p.changed.zero_()
+        st = _lib.DpStats()
+        _lib.check(self.lib.dp_bfs_part_level_peer(
+            p.rowptr.data_ptr(), p.col.data_ptr(), p.n_local, p.nparts,
+            p.part, level, ctypes.byref(self.cfg), p.dist.data_ptr(),
+            p.peer_ptrs.data_ptr(), p.counts.data_ptr(), p.sent.data_ptr(),
+            p.changed.data_ptr(), self.stream, ctypes.byref(st)))
+        p.stats.append(_lib.stats_dict(st))
 
 
 class LocalExchange:
@@ -618,6 +640,9 @@ class PeerLocal:
             out[p.part::P] = p.dist
         return out
 
+    def counts(self, parts):
+        return LocalExchange().counts(parts)
+
 
 class PeerCollective:
     """One part per rank: dist lives in torch symmetric memory; the
@@ -657,6 +682,9 @@ class PeerCollective:
         return CollectiveExchange().dist(
             [_DistView(parts[0])])
 
+    def counts(self, parts):
+        return CollectiveExchange().counts(parts)
+
 
 class _DistView:
     """Adapter exposing SsspPeerPart's fields to CollectiveExchange.dist."""
@@ -678,3 +706,18 @@ def sssp_1d_peer(parts: list, ops, exchange, max_rounds: int | None = None):
         if not exchange.any_changed(parts):
             return exchange.dist(parts), rnd + 1
     raise RuntimeError("sssp used more rounds than vertices")
+
+
+def bfs_1d_peer(parts: list, ops, exchange, max_levels: int | None = None):
+    """bfs_1d with the exchange fused into the level kernel: remote
+    discoveries are CAS'd straight into the owner's dist (parts bound to a
+    PeerLocal / PeerCollective pointer table); the only collective per level
+    is the max of the changed flags.  Returns (dist, counts, levels)."""
+    n = parts[0].n
+    limit = n + 1 if max_levels is None else max_levels
+    for level in range(limit):
+        for p in parts:
+            ops.level_peer(p, level)
+        if not exchange.any_changed(parts):
+            return exchange.dist(parts), exchange.counts(parts), level + 1
+    raise RuntimeError("bfs used more levels than vertices")

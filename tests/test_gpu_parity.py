@@ -746,3 +746,29 @@ def test_sssp_fused_peer_exchange_on_device(P, policy):
         p.reset(0)
     d2, _ = pdist.sssp_1d_peer(parts, ops, ex)
     np.testing.assert_array_equal(d2.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("P", [1, 2, 3])
+def test_bfs_fused_peer_exchange_on_device(P):
+    """BFS over the 1D partition with remote discoveries CAS'd straight into
+    the owner's dist (pointer table), P parts on one GPU."""
+    import torch
+    from paper_2201_02789_b200 import dist as pdist
+    g = graphs.rmat_graph(16, 1)
+    want_d, want_c, want_lv = oracle.bfs(g.rowptr, g.col, nthreads=0)
+    dev = torch.device("cuda", 0)
+    ex = pdist.PeerLocal()
+    parts = [pdist.BfsPart(*pdist.rmat_part(16, 1, P, p), g.n, P, p, 0, dev,
+                           dist=ex.alloc(g.n, P, dev)) for p in range(P)]
+    ex.bind(parts)
+    for policy in (dict(threshold=128, agg="block"),
+                   dict(threshold=1024, cfactor=16, agg="multiblock",
+                        group_size=1 << 20, parent_block=256,
+                        child_block=128, serial="warp")):
+        for p in parts:
+            p.reset(0)
+        ops = pdist.DeviceBfsOps(BenchConfig(**policy).to_c())
+        d, c, levels = pdist.bfs_1d_peer(parts, ops, ex)
+        np.testing.assert_array_equal(d.cpu().numpy(), want_d)
+        np.testing.assert_array_equal(c.cpu().numpy(), want_c)
+        assert levels == want_lv
