@@ -270,14 +270,15 @@ int dp_sssp_part_round(const int32_t* d_rowptr_p, const int32_t* d_col_p,
 /* The same round with the exchange fused into the relaxation: d_peer_dist is
  * a DEVICE array of nparts pointers to every part's dist[n_local_q] (peer-
  * mapped symmetric memory across GPUs, or plain pointers when all parts
- * share one GPU); a remote relaxation that lowers d_best[v] is an atomicMin
- * straight into its owner's dist.  No buckets, no apply pass: the caller
+ * share one GPU; entry `part` == d_dist_p); a remote relaxation that lowers
+ * d_best[v] is an atomicMin straight into its owner's dist.  No buckets, no apply pass: the caller
  * only reduces d_changed (max) across parts between rounds. */
 int dp_sssp_part_round_peer(const int32_t* d_rowptr_p, const int32_t* d_col_p,
                             const int32_t* d_weight_p, int32_t n_local,
                             int32_t nparts, int32_t part,
-                            const dp_config* cfg, int32_t* const* d_peer_dist,
-                            int32_t* d_best, int32_t* d_changed, void* stream,
+                            const dp_config* cfg, int32_t* d_dist_p,
+                            int32_t* const* d_peer_dist, int32_t* d_best,
+                            int32_t* d_changed, void* stream,
                             dp_stats* stats);
 /* lower owned dist by received (v << 32 | alt) pairs (atomicMin) */
 int dp_sssp_part_apply(const uint64_t* d_recv, int64_t nrecv, int32_t nparts,

@@ -113,7 +113,7 @@ _SIGNATURES = {
                             _P, _P, _P, _P, _ST], ctypes.c_int),
     "dp_sssp_part_apply": ([_P, _I64, _I32, _P, _P, _P], ctypes.c_int),
     "dp_sssp_part_round_peer": ([_P, _P, _P, _I32, _I32, _I32, _CFG, _P, _P,
-                                 _P, _P, _ST], ctypes.c_int),
+                                 _P, _P, _P, _ST], ctypes.c_int),
     "dp_rmat_part_keys_dev": ([_I32, _I32, _U64, _I32, _I32, _P, _I64,
                                ctypes.POINTER(ctypes.c_int64), _P],
                               ctypes.c_int),

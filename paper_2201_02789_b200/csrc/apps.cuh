@@ -367,6 +367,7 @@ struct SsspPeerApp {
   const int* __restrict__ col;
   const int* __restrict__ weight;
   int* const* peer_dist;  // [nparts]: every part's dist (local index)
+  int* my_dist;           // == peer_dist[part]
   int* best;              // dense, global ids: best value sent per vertex
   int* changed;
   int n_local;
@@ -386,7 +387,7 @@ struct SsspPeerApp {
   __device__ void parent_prologue() const {}
   __device__ int expand(int lu, bool valid, Args& a) const {
     if (!valid) return 0;
-    const int du = __ldcg(peer_dist[part] + lu);
+    const int du = __ldcg(my_dist + lu);
     if (du >= kUnreached) return 0;
     const int s = __ldg(rowptr + lu);
     const int d = __ldg(rowptr + lu + 1) - s;
@@ -394,20 +395,29 @@ struct SsspPeerApp {
     return d > 0 ? d : 0;
   }
   __device__ static int count(const Args& a) { return a.deg; }
-  __device__ void relax(int v, int alt, Acc& acc) const {
+  // probe: the owned dist (L1-cached: values only decrease, a stale copy
+  // costs at most a redundant atomic, see BfsApp::items) or the best-sent
+  // filter of a remote vertex
+  __device__ int probe(int v) const {
+    return part_of(v, nparts) == part ? __ldca(my_dist + local_of(v, nparts))
+                                      : __ldcg(best + v);
+  }
+  __device__ void update(int v, int alt, int d, Acc& acc) const {
+    if (alt >= d) return;
     const int q = part_of(v, nparts);
-    int* d = peer_dist[q] + local_of(v, nparts);
     if (q == part) {
-      if (alt < __ldcg(d) && atomicMin(d, alt) > alt) acc.changed = 1;
-    } else if (alt < __ldcg(best + v) && atomicMin(best + v, alt) > alt) {
+      if (atomicMin(my_dist + local_of(v, nparts), alt) > alt) acc.changed = 1;
+    } else if (atomicMin(best + v, alt) > alt) {
       acc.remote = 1;
-      if (atomicMin(d, alt) > alt) acc.changed = 1;
+      if (atomicMin(peer_dist[q] + local_of(v, nparts), alt) > alt)
+        acc.changed = 1;
     }
   }
   __device__ void item(const Args& a, int e, Acc& acc) const {
-    relax(ld_stream(col + a.start + e),
-          (int)((unsigned)a.du + (unsigned)ld_stream(weight + a.start + e)),
-          acc);
+    const int v = ld_stream(col + a.start + e);
+    update(v,
+           (int)((unsigned)a.du + (unsigned)ld_stream(weight + a.start + e)),
+           probe(v), acc);
   }
   static constexpr int kUnroll = DP_SSSP_UNROLL;
   static constexpr bool kBlockMode = false;
@@ -425,9 +435,12 @@ struct SsspPeerApp {
                              (unsigned)ld_stream(weight + i))
                      : 0;
     }
+    int d[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) d[j] = ok[j] ? probe(v[j]) : 0;
 #pragma unroll
     for (int j = 0; j < U; ++j)
-      if (ok[j]) relax(v[j], alt[j], acc);
+      if (ok[j]) update(v[j], alt[j], d[j], acc);
   }
   __device__ void flush(Acc& acc) const {
     if (__any_sync(DP_FULL, acc.remote)) __threadfence_system();

@@ -1566,6 +1566,8 @@ int bfs_part_level_impl(const int32_t* rowptr, const int32_t* col,
   a.changed = changed;
   a.peer_dist = (int* const*)peer_dist;
   a.stride = stride;
+  if (peer_dist)  // fused exchange: the flag is this level's alone
+    DP_CUDA(cudaMemsetAsync(changed, 0, sizeof(int), s));
   a.n_local = n_local;
   a.nparts = nparts;
   a.part = part;
@@ -1601,11 +1603,13 @@ __global__ void sssp_part_apply_kernel(const unsigned long long* __restrict__ re
 int sssp_peer_round_impl(const int32_t* rowptr, const int32_t* col,
                          const int32_t* weight, int32_t n_local,
                          int32_t nparts, int32_t part, const dp_config* c,
-                         int32_t* const* peer_dist, int32_t* best,
-                         int32_t* changed, cudaStream_t s, dp_stats* st) {
+                         int32_t* dist, int32_t* const* peer_dist,
+                         int32_t* best, int32_t* changed, cudaStream_t s,
+                         dp_stats* st) {
   int r;
   if ((r = validate(c))) return r;
-  if (nparts < 1 || part < 0 || part >= nparts || n_local < 0 || !peer_dist)
+  if (nparts < 1 || part < 0 || part >= nparts || n_local < 0 || !peer_dist ||
+      !dist)
     return fail(DP_ERR_INVALID, "bad partition arguments");
   Workspace* w = workspace(&r);
   if (!w) return r;
@@ -1621,8 +1625,10 @@ int sssp_peer_round_impl(const int32_t* rowptr, const int32_t* col,
   a.col = col;
   a.weight = weight;
   a.peer_dist = (int* const*)peer_dist;
+  a.my_dist = dist;
   a.best = best;
   a.changed = changed;
+  DP_CUDA(cudaMemsetAsync(changed, 0, sizeof(int), s));  // this round's flag
   a.n_local = n_local;
   a.nparts = nparts;
   a.part = part;
@@ -2171,14 +2177,15 @@ int dp_sssp_part_round(const int32_t* d_rowptr_p, const int32_t* d_col_p,
 int dp_sssp_part_round_peer(const int32_t* d_rowptr_p, const int32_t* d_col_p,
                             const int32_t* d_weight_p, int32_t n_local,
                             int32_t nparts, int32_t part,
-                            const dp_config* cfg, int32_t* const* d_peer_dist,
-                            int32_t* d_best, int32_t* d_changed, void* stream,
+                            const dp_config* cfg, int32_t* d_dist_p,
+                            int32_t* const* d_peer_dist, int32_t* d_best,
+                            int32_t* d_changed, void* stream,
                             dp_stats* stats) {
   clear_stats(stats);
   const double t0 = now_ns();
   int r = sssp_peer_round_impl(d_rowptr_p, d_col_p, d_weight_p, n_local,
-                               nparts, part, cfg, d_peer_dist, d_best,
-                               d_changed, (cudaStream_t)stream, stats);
+                               nparts, part, cfg, d_dist_p, d_peer_dist,
+                               d_best, d_changed, (cudaStream_t)stream, stats);
   if (stats) stats->ns_host = now_ns() - t0;
   return r;
 }

@@ -270,9 +270,8 @@ class DeviceBfsOps:
 
     def level_peer(self, p: BfsPart, level: int) -> None:
         """The level with the exchange fused in (remote CAS through
-        p.peer_ptrs, dp_bfs_part_level_peer)."""
+        p.peer_ptrs, dp_bfs_part_level_peer; the call clears the flag)."""
         from . import _lib
-        p.changed.zero_()
         st = _lib.DpStats()
         _lib.check(self.lib.dp_bfs_part_level_peer(
             p.rowptr.data_ptr(), p.col.data_ptr(), p.n_local, p.nparts,
@@ -602,12 +601,12 @@ class DeviceSsspPeerOps:
 
     def round(self, p: SsspPeerPart) -> None:
         from . import _lib
-        p.changed.zero_()
-        st = _lib.DpStats()
+        st = _lib.DpStats()  # the call clears p.changed
         _lib.check(self.lib.dp_sssp_part_round_peer(
             p.rowptr.data_ptr(), p.col.data_ptr(), p.weight.data_ptr(),
             p.n_local, p.nparts, p.part, ctypes.byref(self.cfg),
-            p.peer_ptrs.data_ptr(), p.best.data_ptr(), p.changed.data_ptr(),
+            p.dist.data_ptr(), p.peer_ptrs.data_ptr(), p.best.data_ptr(),
+            p.changed.data_ptr(),
             self.stream, ctypes.byref(st)))
         p.stats.append(_lib.stats_dict(st))
 
@@ -674,9 +673,9 @@ class PeerCollective:
     def any_changed(self, parts) -> bool:
         import torch.distributed as dist
         (p,) = parts
-        flag = p.changed.clone()
-        dist.all_reduce(flag, op=dist.ReduceOp.MAX)
-        return bool(int(flag.item()))
+        # in place: the next round's call clears the flag itself
+        dist.all_reduce(p.changed, op=dist.ReduceOp.MAX)
+        return bool(int(p.changed.item()))
 
     def dist(self, parts):
         return CollectiveExchange().dist(
