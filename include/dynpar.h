@@ -18,6 +18,10 @@
  *   run_config / run_reference for manylaunch          -> dp_manylaunch / _dev
  *     (benchmarks.py:277-332)
  *   (no reference; BASELINE.json configs 2 and 4)      -> dp_tc, dp_bt (+_dev)
+ *   (no reference; paper Table I MSTF / MSTV / SP, and
+ *    the north star's graph colouring)                 -> dp_mst, dp_sp, dp_gc
+ *   (no reference; partitioned BFS / SSSP steps, bucketed
+ *    or with the exchange fused over peer memory)      -> dp_*_part_*
  *   transform(... threshold, cfactor, agg, group_size, agg_threshold)
  *                                 pipeline.py:45-81    -> dp_config (policy knobs)
  *   SimReport counters            sim/report.py:12-28  -> dp_stats
