@@ -318,12 +318,25 @@ def extra_workloads(stream, quick: bool) -> dict:
     e_t = int(counts.astype(np.int64).sum())
     e_reach, alg = graph_traffic("bfs", G, G.dist.cpu().numpy(), 0)
     naive = run_dev("bfs", G, _cfg(dict(parent_block=32)), stream)
+    agg_ms = {a: run_dev("bfs", G, _cfg(dict(agg=a)), stream)["ns_device"]
+              / 1e6 for a in ("warp", "block", "grid")}
     out["bfs_rmat22"] = {"gteps": e_t / ms / 1e6, "ms": ms,
                          "levels": runs[0]["iterations"],
                          "launches": runs[0]["num_launches"],
                          "gbps_alg": alg / (ms * 1e6),
                          "vs_naive_cdp": naive["ns_device"] / 1e6 / ms,
+                         "vs_agg_only": min(agg_ms.values()) / ms,
                          "policy": BEST["bfs"]}
+    if not quick:
+        from oracle import oracle
+        threads = len(os.sched_getaffinity(0))
+        t0 = time.perf_counter()
+        oracle.bfs(G.g.rowptr, G.g.col, nthreads=threads)
+        dt = time.perf_counter() - t0
+        out["bfs_rmat22"]["cpu_baseline"] = {
+            "value": e_t / dt / 1e9, "unit": "GTEPS", "cores": threads,
+            "kind": "port", "seconds": dt,
+            "sample": "full BFS rmat-22 from vertex 0, oracle/oracle.c"}
     del G
     torch.cuda.empty_cache()
     # TC RMAT-22
@@ -346,10 +359,29 @@ def extra_workloads(stream, quick: bool) -> dict:
     ms = statistics.median(r["ns_device"] for r in runs) / 1e6
     from paper_2201_02789_b200.bench.benchmarks import tc_traffic
     alg = tc_traffic(wl.buffers["rowptr"], wl.buffers["col"])
-    out["tc_rmat22"] = {"triangles": int(tri.item()), "ms": ms,
-                        "triangles_per_s": int(tri.item()) / (ms * 1e-3),
+    ntri = int(tri.item())
+    out["tc_rmat22"] = {"triangles": ntri, "ms": ms,
+                        "triangles_per_s": ntri / (ms * 1e-3),
                         "edges_per_s": m / (ms * 1e-3),
                         "gbps_alg": alg / (ms * 1e6), "policy": BEST["tc"]}
+    if not quick:
+        naive_ms = tc_once(_cfg(dict()))["ns_device"] / 1e6
+        agg_ms = {a: tc_once(_cfg(dict(agg=a)))["ns_device"] / 1e6
+                  for a in ("warp", "block", "grid")}
+        from oracle import oracle
+        threads = len(os.sched_getaffinity(0))
+        t0 = time.perf_counter()
+        cpu_tri = oracle.tc(wl.buffers["rowptr"], wl.buffers["col"],
+                            nthreads=threads)
+        dt = time.perf_counter() - t0
+        out["tc_rmat22"].update({
+            "vs_naive_cdp": naive_ms / ms,
+            "vs_agg_only": min(agg_ms.values()) / ms,
+            "parity": "exact vs oracle" if cpu_tri == ntri else "MISMATCH",
+            "cpu_baseline": {"value": cpu_tri / dt, "unit": "triangles/s",
+                             "cores": threads, "kind": "port",
+                             "seconds": dt,
+                             "sample": "full TC rmat-22, oracle/oracle.c"}})
     del rp, col
     # BT 25k curves
     bench, wl = load("bt", "curves:25000:seed1")
@@ -372,8 +404,22 @@ def extra_workloads(stream, quick: bool) -> dict:
         "curves_per_s": 25000 / (ms2 * 1e-3), "ms": ms2,
         "device_launches": reps[-1].num_launches,
         "vs_naive_cdp": naive.ns_device / 1e6 / ms2, "policy": c2}
+    agg_ms = {a: min(run_config(bench, wl, BenchConfig(agg=a))[0].ns_device
+                     for _ in range(3)) / 1e6
+              for a in ("warp", "block", "grid")}
+    out["bt_25k"]["vs_naive_cdp"] = naive.ns_device / 1e6 / ms
+    out["bt_25k"]["vs_agg_only"] = min(agg_ms.values()) / ms
     if quick:
         return out
+    from oracle import oracle
+    t0 = time.perf_counter()
+    for _ in range(10):
+        oracle.bt(wl.buffers["cp"], int(wl.buffers["max_tess"]),
+                  float(wl.buffers["scale"]))
+    dt = (time.perf_counter() - t0) / 10
+    out["bt_25k"]["cpu_baseline"] = {
+        "value": 25000 / dt, "unit": "curves/s", "cores": 1, "kind": "port",
+        "seconds": dt, "sample": "25k curves (fp64 vertices), oracle/oracle.c"}
     from paper_2201_02789_b200.bench import run_reference
     from paper_2201_02789_b200.bench.benchmarks import Workload
 
@@ -386,13 +432,28 @@ def extra_workloads(stream, quick: bool) -> dict:
     ms, rep = med(bench, wl, BEST["mstf"])
     naive_ms, _ = med(bench, wl, dict(), k=1 + 1)
     ref = run_reference(bench, wl)
+    agg_ms = {a: med(bench, wl, dict(agg=a), k=2)[0]
+              for a in ("warp", "block", "grid")}
     m = int(wl.buffers["col"].shape[0])
+    b = wl.buffers
+    t0 = time.perf_counter()
+    cpu = oracle.mst(b["rowptr"], b["col"], b["weight"], b["eid"])
+    dt = time.perf_counter() - t0
     out["mst_rmat22"] = {
         "ms": ms, "edge_slots": m, "edges_per_s": m / (ms * 1e-3),
         "forest_weight": int(rep.arrays["weight"][0]),
         "forest_edges": int(rep.arrays["weight"][1]),
         "rounds": rep.iterations, "vs_naive_cdp": naive_ms / ms,
-        "vs_nocdp": ref.ns_device / 1e6 / ms, "policy": BEST["mstf"]}
+        "vs_agg_only": min(agg_ms.values()) / ms,
+        "vs_nocdp": ref.ns_device / 1e6 / ms, "policy": BEST["mstf"],
+        "parity": ("bit-exact vs oracle"
+                   if np.array_equal(rep.arrays["in_mst"], cpu[0])
+                   and rep.arrays["weight"].tolist() == [cpu[1], cpu[2]]
+                   else "MISMATCH"),
+        "cpu_baseline": {"value": m / dt, "unit": "edge slots/s",
+                         "cores": 1, "kind": "port", "seconds": dt,
+                         "sample": "Kruskal over rmat-22 (symmetrised), "
+                                   "oracle/oracle.c"}}
     del wl
     # SP: 20 synchronous sweeps of random 5-SAT
     bench, wl = load("sp", "ksat5:200000:seed1")
@@ -402,11 +463,22 @@ def extra_workloads(stream, quick: bool) -> dict:
     grid_ms, _ = med(bench, wl, dict(agg="grid"), k=2)
     ref = run_reference(bench, wl)
     ne = int(wl.buffers["lits"].shape[0])
+    t0 = time.perf_counter()
+    cpu = oracle.sp(wl.payload, wl.buffers["eta0"], 20, 0.0)
+    dt = time.perf_counter() - t0
     out["sp_ksat5_200k"] = {
         "ms": ms, "sweeps": rep.iterations, "edges": ne,
         "edge_updates_per_s": ne * rep.iterations / (ms * 1e-3),
         "vs_agg_only_grid": grid_ms / ms,
-        "vs_nocdp": ref.ns_device / 1e6 / ms, "policy": BEST["sp"]}
+        "vs_nocdp": ref.ns_device / 1e6 / ms, "policy": BEST["sp"],
+        "parity": ("within 1e-5 of the oracle"
+                   if np.allclose(rep.arrays["eta"], cpu[0], rtol=1e-5,
+                                  atol=1e-7) else "MISMATCH"),
+        "cpu_baseline": {"value": ne * 20 / dt, "unit": "edge updates/s",
+                         "cores": 1, "kind": "port", "seconds": dt,
+                         "sample": "20 sweeps of ksat5:200000, "
+                                   "oracle/oracle.c (fp64)"},
+        "naive_cdp": "not timed (37 s, 88 M launches; profiles/sp_time_r01)"}
     return out
 
 
