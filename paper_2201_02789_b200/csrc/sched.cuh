@@ -302,7 +302,11 @@ __global__ void __launch_bounds__(256, App::kMinBlocks)
     } else {
       __shared__ int smem[66];
       __shared__ unsigned long long s_old;
-      const BlockScan s = block_scan(gd > 0, gd, smem);
+      // most blocks hold no launching parent once T is in the hundreds:
+      // they skip the scan (one barrier instead of three) and, below, the
+      // record barriers
+      BlockScan s{0, 0, 0, 0};
+      if (__syncthreads_or(gd > 0)) s = block_scan(gd > 0, gd, smem);
       if constexpr (AGG == kAggBlock) {
         if (k.agg_threshold > 0 && s.np < k.agg_threshold) {
           // aggregate.py:376-392: too few participants -> direct launches
@@ -335,21 +339,21 @@ __global__ void __launch_bounds__(256, App::kMinBlocks)
         const int grp = AGG == kAggMulti ? (int)blockIdx.x / k.group : 0;
         const long long sb =
             AGG == kAggMulti ? (long long)grp * k.group * blockDim.x : 0;
-        if (threadIdx.x == 0)
-          s_old = s.np > 0 ? atomicAdd(&t.ctr[grp],
-                                       ((unsigned long long)s.np << 32) +
-                                           (unsigned long long)s.total)
-                           : 0ull;
-        __syncthreads();
-        if (gd > 0) {
-          const unsigned long long old = s_old;
-          const long long row = sb + (long long)(old >> 32) + s.rank;
-          t.args[row] = a;
-          t.scan[row] = (int)(old & 0xffffffffull) + s.excl;
-          __threadfence();  // publish before the done counter (:318-319)
+        if (s.np > 0) {  // block-uniform
+          if (threadIdx.x == 0)
+            s_old = atomicAdd(&t.ctr[grp], ((unsigned long long)s.np << 32) +
+                                               (unsigned long long)s.total);
+          __syncthreads();
+          if (gd > 0) {
+            const unsigned long long old = s_old;
+            const long long row = sb + (long long)(old >> 32) + s.rank;
+            t.args[row] = a;
+            t.scan[row] = (int)(old & 0xffffffffull) + s.excl;
+            __threadfence();  // publish before the done counter (:318-319)
+          }
+          if constexpr (AGG == kAggMulti) __syncthreads();
         }
         if constexpr (AGG == kAggMulti) {
-          __syncthreads();
           if (threadIdx.x == 0) {
             const int nblk = min(k.group, (int)gridDim.x - grp * k.group);
             const int d = atomicAdd(&t.done[grp], 1);
