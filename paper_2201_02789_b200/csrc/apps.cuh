@@ -196,7 +196,14 @@ struct BfsPartApp {
     send_buf[(long long)q * stride + base + __popc(grp & lanemask_lt())] = v;
   }
   __device__ void update(int v, int d_or_bits, int lvl, Acc& acc) const {
+#if DP_MERGE_COUNTS
+    {  // lanes hitting the same vertex merge their increments (BfsApp)
+      const unsigned grp = __match_any_sync(__activemask(), v);
+      if (lane_id() == __ffs(grp) - 1) atomicAdd(counts + v, __popc(grp));
+    }
+#else
     atomicAdd(counts + v, 1);
+#endif
     const int q = part_of(v, nparts);
     if (q == part) {
       const int lv = local_of(v, nparts);
