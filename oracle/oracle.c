@@ -15,7 +15,7 @@
  * reference):
  *   oracle_tc          exact triangle count over a degree-oriented CSR+
  *   oracle_bt          Bezier tessellation, fp64 vertices, fp32 counts
- *   oracle_gc          greedy colouring in Jones-Plassmann priority order
+ *   oracle_gc          greedy colouring in Jones-Plassmann (LLF) priority order
  *   oracle_mst         Kruskal minimum spanning forest in (weight, eid) order
  *   oracle_sp          survey propagation sweeps on a k-SAT factor graph
  *
@@ -195,18 +195,22 @@ int64_t oracle_bt(const float* cp, int32_t ncurves, int32_t max_tess,
 }
 
 /* ---- graph colouring (north-star app; no reference implementation) ------
- * Sequential greedy colouring in decreasing priority key(v) = (hash32(v), v):
- * each vertex takes the smallest colour unused by its already-coloured (=
- * higher-priority) neighbours.  Independent restatement of what the
- * Jones-Plassmann rounds on the device must produce. */
-static uint64_t gc_key(int32_t v) {
+ * Sequential greedy colouring in decreasing priority key(v) =
+ * (floor(log2(deg v + 1)) : 5 bits, high 27 bits of hash32(v), v : 32 bits)
+ * (largest-log-degree-first, hash tie-break): each vertex takes the smallest
+ * colour unused by its already-coloured (= higher-priority) neighbours.
+ * Independent restatement of what the Jones-Plassmann rounds on the device
+ * must produce. */
+static uint64_t gc_key(int32_t v, int32_t deg) {
   uint32_t x = (uint32_t)v * 0x9E3779B1u;
   x ^= x >> 16;
   x *= 0x85EBCA6Bu;
   x ^= x >> 13;
   x *= 0xC2B2AE35u;
   x ^= x >> 16;
-  return ((uint64_t)x << 32) | (uint32_t)v;
+  uint32_t lg = 0;
+  for (uint32_t d = (uint32_t)deg + 1u; d > 1u; d >>= 1) ++lg;
+  return ((uint64_t)lg << 59) | ((uint64_t)(x >> 5) << 32) | (uint32_t)v;
 }
 
 static int gc_cmp_desc(const void* a, const void* b) {
@@ -220,7 +224,7 @@ int32_t oracle_gc(const int32_t* rowptr, const int32_t* col, int32_t n,
   uint64_t* keys = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)(n ? n : 1));
   int32_t maxdeg = 0;
   for (int32_t u = 0; u < n; ++u) {
-    keys[u] = gc_key(u);
+    keys[u] = gc_key(u, rowptr[u + 1] - rowptr[u]);
     color[u] = -1;
     if (rowptr[u + 1] - rowptr[u] > maxdeg) maxdeg = rowptr[u + 1] - rowptr[u];
   }

@@ -818,6 +818,13 @@ int sssp_dev_impl(const int32_t* rowptr, const int32_t* col,
                  st, arr);
 }
 
+__global__ void gc_key_kernel(const int* __restrict__ rowptr, int n,
+                              unsigned long long* key) {
+  for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (long long)gridDim.x * blockDim.x)
+    key[v] = gc_key((int)v, rowptr[v + 1] - rowptr[v]);
+}
+
 // Vertices whose wait count is 0 after the count pass: the first worklist.
 __global__ void gc_seed_kernel(const int* __restrict__ wait, int n, int* list,
                                int* count) {
@@ -878,13 +885,15 @@ int gc_dev_impl(const int32_t* rowptr, const int32_t* col, int32_t n,
   if (n < 0 || m < 0) return fail(DP_ERR_INVALID, "bad graph size");
   Workspace* w = workspace(&r);
   if (!w) return r;
-  // used bitmap | wait[n] | two worklists[n] | counts[2] | rounds
+  // keys[n] | used bitmap | wait[n] | two worklists[n] | counts[2] | rounds
   const size_t words = (size_t)((m + n + 31) / 32) + 1;
   const size_t nn = (size_t)std::max(n, 1);
   if ((r = grow(&w->io[5], &w->io_bytes[5],
-                words * sizeof(unsigned) + (nn * 3 + 4) * sizeof(int))))
+                nn * 8 + words * sizeof(unsigned) +
+                    (nn * 3 + 4) * sizeof(int))))
     return r;
-  unsigned* used = (unsigned*)w->io[5];
+  unsigned long long* keys = (unsigned long long*)w->io[5];
+  unsigned* used = (unsigned*)(keys + nn);
   int* wait = (int*)(used + words);
   int* list[2] = {wait + nn, wait + 2 * nn};
   int* cnt = wait + 3 * nn;  // cnt[0], cnt[1]: worklist lengths
@@ -901,10 +910,16 @@ int gc_dev_impl(const int32_t* rowptr, const int32_t* col, int32_t n,
   DP_CUDA(cudaMemsetAsync(used, 0, words * sizeof(unsigned), s));
   DP_CUDA(cudaMemsetAsync(wait, 0, nn * sizeof(int), s));
   DP_CUDA(cudaMemsetAsync(cnt, 0, 3 * sizeof(int), s));
+  const int kb = std::max(1, std::min(dp::ceil_div(std::max(n, 1), 256),
+                                      148 * 8));
+  gc_key_kernel<<<kb, 256, 0, s>>>(rowptr, n, keys);
+  DP_CUDA(cudaGetLastError());
+  rc.kernel_launches += 1;
   if (n) DP_CUDA(cudaMemsetAsync(color, 0xff, (size_t)n * sizeof(int), s));
   GcCountApp ca;
   ca.rowptr = rowptr;
   ca.col = col;
+  ca.key = keys;
   ca.wait = wait;
   ca.n = n;
   ca.pad = 0;
@@ -926,6 +941,7 @@ int gc_dev_impl(const int32_t* rowptr, const int32_t* col, int32_t n,
       GcGatherApp ga;
       ga.rowptr = rowptr;
       ga.col = col;
+      ga.key = keys;
       ga.ready = list[cur];
       ga.nready = cnt + cur;
       ga.color = color;
@@ -938,6 +954,7 @@ int gc_dev_impl(const int32_t* rowptr, const int32_t* col, int32_t n,
       GcNotifyApp na;
       na.rowptr = rowptr;
       na.col = col;
+      na.key = keys;
       na.ready = list[cur];
       na.nready = cnt + cur;
       na.wait = wait;

@@ -295,14 +295,16 @@ def test_oracle_bt_counts_and_vertices():
 # graph colouring (no reference implementation: brute-force checks here)
 # ---------------------------------------------------------------------------
 
-def _py_gc_key(v):
+def _py_gc_key(v, deg):
+    """largest-log-degree-first, hash tie-break, vertex id last"""
     x = (v * 0x9E3779B1) & 0xFFFFFFFF
     x ^= x >> 16
     x = (x * 0x85EBCA6B) & 0xFFFFFFFF
     x ^= x >> 13
     x = (x * 0xC2B2AE35) & 0xFFFFFFFF
     x ^= x >> 16
-    return (x << 32) | v
+    lg = (deg + 1).bit_length() - 1
+    return (lg << 59) | ((x >> 5) << 32) | v
 
 
 @pytest.mark.parametrize("spec", ["hand", "rmat:9:seed1", "powerlaw:400:seed2",
@@ -314,7 +316,9 @@ def test_oracle_gc_is_priority_greedy_and_proper(spec):
     assert np.all(color[src] != color[g.col])          # proper
     assert color.max() + 1 == k
     want = [-1] * g.n                                   # greedy mirror
-    for u in sorted(range(g.n), key=_py_gc_key, reverse=True):
+    deg = np.diff(g.rowptr).tolist()
+    for u in sorted(range(g.n), key=lambda v: _py_gc_key(v, deg[v]),
+                    reverse=True):
         used = {want[w] for w in g.neighbors(u).tolist() if want[w] >= 0}
         c = 0
         while c in used:
