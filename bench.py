@@ -62,8 +62,10 @@ BEST = {
     # TC over the transposed CSR+ (profiles/tune_tc_rmat22_r01c.txt)
     "tc": dict(threshold=32, cfactor=4, agg="grid", parent_block=128,
                child_block=256, serial="warp"),
-    "bt": dict(threshold=64, cfactor=16, agg="grid", parent_block=256,
-               child_block=32, serial="warp"),
+    # BT 25k is launch-latency-sized: every child launch costs more than the
+    # 2.2 M vertices; T = infinity (children run in the parent warps,
+    # load-balanced) wins (profiles/bt_policies_r01.txt: 46 vs 57-63 us)
+    "bt": dict(threshold=2147483647, parent_block=64, serial="warp"),
     # MSTF (find) row; the verify kernel runs MST_OTHER_POLICY
     "mstf": dict(threshold=1024, cfactor=16, agg="multiblock",
                  group_size=1 << 20, parent_block=256, child_block=128,
