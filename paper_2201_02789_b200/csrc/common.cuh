@@ -141,7 +141,40 @@ struct DevState {
   int skipped[2];  // per round (double-buffered like flag): a parent whose
                    // edges had not arrived yet was deferred (host-buffer
                    // calls that overlap the H2D copy with the rounds)
+  // DP_PROFILE builds: warp-cycles per phase (parent, launch, agg, disagg,
+  // child), the measured counterpart of SimReport.phase_time
+  // (sim/report.py:12-28, folded from per-thread costs at
+  // sim/machine.py:657-666); zero in the default build
+  unsigned long long phase[5];
 };
+
+#ifndef DP_PROFILE
+#define DP_PROFILE 0
+#endif
+enum Phase { kPhParent = 0, kPhLaunch = 1, kPhAgg = 2, kPhDisagg = 3,
+             kPhChild = 4 };
+
+__device__ __forceinline__ long long ph_now() {
+#if DP_PROFILE
+  return clock64();
+#else
+  return 0;
+#endif
+}
+
+// add the time since t0 to a phase, once per (converged part of a) warp
+__device__ __forceinline__ void ph_add(DevState* ds, int ph, long long t0) {
+#if DP_PROFILE
+  const long long d = clock64() - t0;
+  const unsigned am = __activemask();
+  if (lane_id() == __ffs(am) - 1 && d > 0)
+    atomicAdd(&ds->phase[ph], (unsigned long long)d);
+#else
+  (void)ds;
+  (void)ph;
+  (void)t0;
+#endif
+}
 
 // Owner part and local index of vertex v >= 0 under the cyclic partition
 // owner(v) = v % nparts.  Power-of-two part counts (the 1/2/4/8-GPU runs)

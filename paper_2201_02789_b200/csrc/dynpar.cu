@@ -617,6 +617,18 @@ void finish_stats(Workspace* w, const RunCounters& rc, float ms,
   st->launch_lat_ns_mean =
       w->h_ds->lat_cnt ? (double)w->h_ds->lat_sum / (double)w->h_ds->lat_cnt
                        : 0.0;
+  // DP_PROFILE builds: summed warp-cycles per phase -> warp-ns at the SM
+  // clock rate the device reports (zero, and no query, in the default build)
+  bool any = false;
+  for (int i = 0; i < 5; ++i) any |= w->h_ds->phase[i] != 0;
+  if (any) {
+    int dev = 0, khz = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, dev);
+    for (int i = 0; i < 5; ++i)
+      st->ns_phase[i] =
+          khz > 0 ? (double)w->h_ds->phase[i] * 1e6 / (double)khz : 0.0;
+  }
 }
 
 void clear_stats(dp_stats* st) {

@@ -102,10 +102,22 @@ template <class App>
 __global__ void __launch_bounds__(256, App::kMinBlocks) child_kernel(App app, typename App::Args a, int cf,
                                      DevState* ds, unsigned long long ts) {
   note_child_start(ds, ts);
+  const long long t0 = ph_now();
   typename App::Acc acc{};
   run_logical_blocks(app, a, blockIdx.x, cf, acc);
   app.flush(acc);
+  ph_add(ds, kPhChild, t0);
 }
+
+// a device launch, its time added to the launch phase (DP_PROFILE builds)
+// and to `tl`, so the enclosing aggregation phase can leave it out
+#define DP_TIMED_LAUNCH(ds, tl, ...)       \
+  do {                                     \
+    const long long t_ = ph_now();         \
+    __VA_ARGS__;                           \
+    ph_add(ds, kPhLaunch, t_);             \
+    tl += ph_now() - t_;                   \
+  } while (0)
 
 // Largest lo in [0, np) with scan[lo] <= p (scan[0] == 0, strictly
 // increasing).  Whole warp; 32-ary: each round probes 32 evenly spaced rows.
@@ -133,6 +145,7 @@ __global__ void __launch_bounds__(256, App::kMinBlocks) child_agg_kernel(App app
                                  const int* scan, int np, int cf,
                                  DevState* ds, unsigned long long ts) {
   note_child_start(ds, ts);
+  const long long t0 = ph_now();
   __shared__ int s_lo;
   int lo = 0;
   if (threadIdx.x < 32) {
@@ -153,9 +166,12 @@ __global__ void __launch_bounds__(256, App::kMinBlocks) child_agg_kernel(App app
 #pragma unroll
     for (int i = 0; i < (int)(sizeof(a) / 16); ++i) dst[i] = __ldcg(src + i);
   }
+  ph_add(ds, kPhDisagg, t0);
+  const long long t1 = ph_now();
   typename App::Acc acc{};
   run_logical_blocks(app, a, lb, cf, acc);
   app.flush(acc);
+  ph_add(ds, kPhChild, t1);
 }
 
 // ---------------------------------------------------------------------------
@@ -245,6 +261,7 @@ __global__ void __launch_bounds__(256, App::kMinBlocks)
     parent_kernel(App app, Knobs k, AggTables<App> t, DevState* ds,
                   long long base) {
   using Args = typename App::Args;
+  const long long t_parent = ph_now();
   typename App::Acc acc{};
   // wave-local thread index (table rows) and the parent it owns
   const long long lu = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -254,12 +271,17 @@ __global__ void __launch_bounds__(256, App::kMinBlocks)
   // called by every thread (apps may use warp collectives); returns 0 when
   // the thread owns no parent
   const int cnt = app.expand((int)u, u < app.nparents(), a);
+  ph_add(ds, kPhParent, t_parent);
 
   if constexpr (!CDP) {
     // No-CDP variant (e.g. BFS_NOCDP, benchmarks.py:122-141): no launch code
+    const long long t_child = ph_now();
     serial_arm(app, a, cnt, true, k.serial_warp != 0, acc);
     app.flush(acc);
+    ph_add(ds, kPhChild, t_child);
   } else {
+    const long long t_agg = ph_now();
+    long long tl = 0;  // launch time inside the protocol (DP_PROFILE)
     const bool go = cnt > 0 && (k.threshold == 0 || cnt >= k.threshold);
     // physical (coarsened) child grid of this parent thread
     const int gd = go ? ceil_div(ceil_div(cnt, k.cb), k.cf) : 0;
@@ -271,9 +293,10 @@ __global__ void __launch_bounds__(256, App::kMinBlocks)
 
     if constexpr (AGG == kAggNone) {
       if (gd > 0) {
-        child_kernel<App><<<gd, k.cb, 0, cudaStreamFireAndForget>>>(
-            app, a, k.cf, ds, globaltimer_ns());
-        note_launch_error(ds);
+        DP_TIMED_LAUNCH(ds, tl,
+            child_kernel<App><<<gd, k.cb, 0, cudaStreamFireAndForget>>>(
+                app, a, k.cf, ds, globaltimer_ns());
+            note_launch_error(ds));
       }
       count_launches_warp(ds, gd > 0, gd);
     } else if constexpr (AGG == kAggWarp) {
@@ -291,10 +314,12 @@ __global__ void __launch_bounds__(256, App::kMinBlocks)
         }
         __syncwarp();
         if (lane == __ffs(m) - 1) {
-          child_agg_kernel<App><<<total, k.cb, 0, cudaStreamFireAndForget>>>(
-              app, t.args + row0, t.scan + row0, __popc(m), k.cf, ds,
-              globaltimer_ns());
-          note_launch_error(ds);
+          DP_TIMED_LAUNCH(ds, tl,
+              child_agg_kernel<App><<<total, k.cb, 0,
+                                      cudaStreamFireAndForget>>>(
+                  app, t.args + row0, t.scan + row0, __popc(m), k.cf, ds,
+                  globaltimer_ns());
+              note_launch_error(ds));
           atomicAdd(&ds->launches, 1ull);
           atomicAdd(&ds->blocks, (unsigned long long)total);
         }
@@ -311,9 +336,10 @@ __global__ void __launch_bounds__(256, App::kMinBlocks)
         if (k.agg_threshold > 0 && s.np < k.agg_threshold) {
           // aggregate.py:376-392: too few participants -> direct launches
           if (gd > 0) {
-            child_kernel<App><<<gd, k.cb, 0, cudaStreamFireAndForget>>>(
-                app, a, k.cf, ds, globaltimer_ns());
-            note_launch_error(ds);
+            DP_TIMED_LAUNCH(ds, tl,
+                child_kernel<App><<<gd, k.cb, 0, cudaStreamFireAndForget>>>(
+                    app, a, k.cf, ds, globaltimer_ns());
+                note_launch_error(ds));
           }
           count_launches_warp(ds, gd > 0, gd);
         } else if (s.np > 0) {
@@ -325,11 +351,12 @@ __global__ void __launch_bounds__(256, App::kMinBlocks)
           }
           __syncthreads();
           if (threadIdx.x == 0) {
-            child_agg_kernel<App><<<s.total, k.cb, 0,
-                                    cudaStreamFireAndForget>>>(
-                app, t.args + row0, t.scan + row0, s.np, k.cf, ds,
-                globaltimer_ns());
-            note_launch_error(ds);
+            DP_TIMED_LAUNCH(ds, tl,
+                child_agg_kernel<App><<<s.total, k.cb, 0,
+                                        cudaStreamFireAndForget>>>(
+                    app, t.args + row0, t.scan + row0, s.np, k.cf, ds,
+                    globaltimer_ns());
+                note_launch_error(ds));
             atomicAdd(&ds->launches, 1ull);
             atomicAdd(&ds->blocks, (unsigned long long)s.total);
           }
@@ -366,11 +393,12 @@ __global__ void __launch_bounds__(256, App::kMinBlocks)
               const int np = (int)(c >> 32);
               const int total = (int)(c & 0xffffffffull);
               if (np > 0) {
-                child_agg_kernel<App><<<total, k.cb, 0,
-                                        cudaStreamFireAndForget>>>(
-                    app, t.args + sb, t.scan + sb, np, k.cf, ds,
-                    globaltimer_ns());
-                note_launch_error(ds);
+                DP_TIMED_LAUNCH(ds, tl,
+                    child_agg_kernel<App><<<total, k.cb, 0,
+                                            cudaStreamFireAndForget>>>(
+                        app, t.args + sb, t.scan + sb, np, k.cf, ds,
+                        globaltimer_ns());
+                    note_launch_error(ds));
                 atomicAdd(&ds->launches, 1ull);
                 atomicAdd(&ds->blocks, (unsigned long long)total);
               }
@@ -381,8 +409,11 @@ __global__ void __launch_bounds__(256, App::kMinBlocks)
         // and performs the aggregated launch (common.py:144-164)
       }
     }
+    ph_add(ds, kPhAgg, t_agg + tl);  // the protocol minus its launches
+    const long long t_child = ph_now();
     serial_arm(app, a, cnt, !go, k.serial_warp != 0, acc);
     app.flush(acc);
+    ph_add(ds, kPhChild, t_child);
   }
 }
 
