@@ -112,7 +112,7 @@ typedef struct dp_stats {
   uint64_t num_launches;      /* device-side launches with grid, block > 0 */
   uint64_t host_launches;     /* host-side launches with grid, block > 0 */
   uint64_t blocks_scheduled;  /* sum of grid sizes over every launched grid */
-  uint64_t max_pending_depth; /* not observable on hardware: always 0 */
+  uint64_t max_pending_depth; /* deepest device launch queue (issued, not started) */
   uint64_t iterations;        /* host-loop trips (BFS levels / SSSP rounds) */
   uint64_t work_units;        /* child items executed (edges examined, ...) */
   uint64_t bytes_alg;         /* algorithmic HBM bytes (DESIGN.md per app) */

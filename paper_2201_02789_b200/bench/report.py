@@ -5,9 +5,11 @@ Counter semantics follow the simulator (sim/machine.py:165-247, 330-331):
 ``num_launches`` counts device-initiated launches with a non-empty
 configuration, ``host_launches`` host-initiated ones, ``blocks_scheduled`` the
 blocks of every launched grid.  ``makespan`` is the measured device time of
-the run in nanoseconds; ``instructions``, ``max_pending_depth`` and the
-per-phase busy times are not observable on hardware and read 0 (per-phase
-attribution is a profiling build).
+the run in nanoseconds; ``max_pending_depth`` is the deepest device launch
+queue seen (launches issued whose first child block had not started);
+``instructions`` is not observable on hardware and reads 0; the per-phase
+times (``phase_time``, warp-ns) are filled by the ``-DDP_PROFILE=1`` build
+(libdynpar_prof.so) and read 0 in the default build.
 """
 
 from __future__ import annotations

@@ -146,6 +146,11 @@ struct DevState {
   // (sim/report.py:12-28, folded from per-thread costs at
   // sim/machine.py:657-666); zero in the default build
   unsigned long long phase[5];
+  // device launch queue: launches issued whose first child block has not
+  // started yet, and its maximum over the run (SimReport.max_pending_depth,
+  // the pending-queue length at sim/machine.py:237-244)
+  int pending;
+  int max_pending;
 };
 
 #ifndef DP_PROFILE
@@ -207,7 +212,14 @@ __device__ __forceinline__ void note_child_start(DevState* ds,
   if (ts && blockIdx.x == 0 && threadIdx.x == 0) {
     atomicAdd(&ds->lat_sum, globaltimer_ns() - ts);
     atomicAdd(&ds->lat_cnt, 1ull);
+    atomicSub(&ds->pending, 1);
   }
+}
+
+// a device launch is about to be issued (counted before the call, so its
+// child can never leave the queue before it entered)
+__device__ __forceinline__ void note_launch_issue(DevState* ds) {
+  atomicMax(&ds->max_pending, atomicAdd(&ds->pending, 1) + 1);
 }
 
 __device__ __forceinline__ void note_launch_error(DevState* ds) {

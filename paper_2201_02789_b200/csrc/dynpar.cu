@@ -609,7 +609,7 @@ void finish_stats(Workspace* w, const RunCounters& rc, float ms,
   st->num_launches = w->h_ds->launches;
   st->host_launches = rc.host_launches;
   st->blocks_scheduled = w->h_ds->blocks + rc.host_blocks;
-  st->max_pending_depth = 0;
+  st->max_pending_depth = (unsigned long long)std::max(w->h_ds->max_pending, 0);
   st->ns_device = (double)ms * 1e6;
   st->ns_kernel_max = rc.ms_kernel_max * 1e6;
   st->ns_kernel_sum = rc.ms_kernel_sum * 1e6;

@@ -109,10 +109,12 @@ __global__ void __launch_bounds__(256, App::kMinBlocks) child_kernel(App app, ty
   ph_add(ds, kPhChild, t0);
 }
 
-// a device launch, its time added to the launch phase (DP_PROFILE builds)
-// and to `tl`, so the enclosing aggregation phase can leave it out
+// a device launch: queued in the pending count, its time added to the launch
+// phase (DP_PROFILE builds) and to `tl`, so the enclosing aggregation phase
+// can leave it out
 #define DP_TIMED_LAUNCH(ds, tl, ...)       \
   do {                                     \
+    note_launch_issue(ds);                 \
     const long long t_ = ph_now();         \
     __VA_ARGS__;                           \
     ph_add(ds, kPhLaunch, t_);             \
@@ -472,6 +474,7 @@ __global__ void __launch_bounds__(256)
         const int np = (int)(c >> 32);
         const int total = (int)(c & 0xffffffffull);
         if (np > 0) {
+          note_launch_issue(ds);
           child_agg_kernel<App><<<total, k.cb, 0, cudaStreamFireAndForget>>>(
               app, t.args, t.scan, np, k.cf, ds, globaltimer_ns());
           note_launch_error(ds);

@@ -79,3 +79,17 @@ def test_profiled_build_phases(golden):
     for name in ("warp", "multiblock"):
         assert res[name]["phase"]["disagg"] > 0, name
     assert res["naive"]["phase"]["disagg"] == 0
+
+
+def test_max_pending_depth():
+    # SimReport.max_pending_depth (sim/machine.py:237-244): the launch
+    # queue's high-water mark; none without device launches, at most one
+    # per level with a single aggregated launch, bounded by the launches
+    bench, wl = load("bfs", "powerlaw:2000:seed1")
+    rep, _ = run_config(bench, wl, BenchConfig(threshold=1 << 30))
+    assert rep.num_launches == 0 and rep.max_pending_depth == 0
+    rep, _ = run_config(bench, wl, BenchConfig())
+    assert 1 <= rep.max_pending_depth <= rep.num_launches
+    rep, _ = run_config(bench, wl, BenchConfig(agg="multiblock",
+                                               group_size=1 << 20))
+    assert rep.max_pending_depth == 1
