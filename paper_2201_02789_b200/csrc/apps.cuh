@@ -29,6 +29,9 @@ namespace dp {
 #ifndef DP_SSSP_UNROLL
 #define DP_SSSP_UNROLL 2
 #endif
+#ifndef DP_SSSP_CHILD_UNROLL
+#define DP_SSSP_CHILD_UNROLL 1  // hub children: 1 < 2 < 4 < 8
+#endif                          // (profiles/ab_child_unroll_r01.txt)
 #ifndef DP_SSSP_MINB
 #define DP_SSSP_MINB 8  // <= 32 registers: full occupancy for the latency-
 #endif                  // bound relaxations (tools/ab.sh, profiles/)
@@ -536,6 +539,7 @@ struct SsspApp {
       acc.changed = 1;
   }
   static constexpr int kUnroll = DP_SSSP_UNROLL;
+  static constexpr int kChildUnroll = DP_SSSP_CHILD_UNROLL;
   static constexpr bool kBlockMode = false;
   // frontier mode writes last[] in expand: the host never pairs it with the
   // persistent parent (which re-runs expand)

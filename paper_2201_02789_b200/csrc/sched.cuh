@@ -33,6 +33,7 @@
 //     provided.
 // Child launches are CDP2 fire-and-forget launches.
 #pragma once
+#include <type_traits>
 #include "common.cuh"
 
 
@@ -63,14 +64,28 @@ struct AggTables {
 // ---------------------------------------------------------------------------
 
 // Logical blocks [lb*cf, min(lb*cf+cf, ceil(cnt/cb))) of one child grid.
-// Thread t owns item b*cb + t of each logical block b; App::kUnroll logical
-// blocks are processed together so their independent load chains overlap.
+// Thread t owns item b*cb + t of each logical block b; U logical blocks are
+// processed together so their independent load chains overlap.
+#ifndef DP_CHILD_UNROLL
+#define DP_CHILD_UNROLL 0  // items in flight per child thread (0: per app)
+#endif
+// an app's child-side unroll: App::kChildUnroll when it declares one, else
+// the serial arm's App::kUnroll
+template <class App, class = void>
+struct ChildUnroll {
+  static constexpr int value = App::kUnroll;
+};
+template <class App>
+struct ChildUnroll<App, std::void_t<decltype(App::kChildUnroll)>> {
+  static constexpr int value = App::kChildUnroll;
+};
 template <class App>
 __device__ __forceinline__ void run_logical_blocks(const App& app,
                                                    const typename App::Args& a,
                                                    long long lb, int cf,
                                                    typename App::Acc& acc) {
-  constexpr int U = App::kUnroll;
+  constexpr int U =
+      DP_CHILD_UNROLL > 0 ? DP_CHILD_UNROLL : ChildUnroll<App>::value;
   const int cnt = App::count(a);
   const long long cb = blockDim.x;
   const long long gl = ceil_div_ll(cnt, cb);
