@@ -109,6 +109,14 @@ def main():
                                 group_size=gs, parent_block=128,
                                 child_block=cb, serial="warp",
                                 frontier=grid == "frontier"))
+    elif grid == "cf2":
+        # re-tune after the hub children's unroll changed (kChildUnroll)
+        for T, C, cb, pb in itertools.product(
+                (256, 512, 1024, 2048), (4, 8, 16, 32, 64), (64, 128, 256),
+                (128, 256)):
+            configs.append(dict(threshold=T, cfactor=C, agg="multiblock",
+                                group_size=1 << 20, parent_block=pb,
+                                child_block=cb, serial="warp"))
     from paper_2201_02789_b200 import _lib
     for d in configs:
         d = dict(d)
