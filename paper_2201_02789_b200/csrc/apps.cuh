@@ -333,6 +333,7 @@ struct SsspPartApp {
           acc);
   }
   static constexpr int kUnroll = DP_SSSP_UNROLL;
+  static constexpr int kChildUnroll = DP_SSSP_CHILD_UNROLL;
   static constexpr bool kBlockMode = false;
   static constexpr bool kPureExpand = true;
   static constexpr int kMinBlocks = DP_SSSP_MINB;
@@ -430,6 +431,7 @@ struct SsspPeerApp {
            probe(v), acc);
   }
   static constexpr int kUnroll = DP_SSSP_UNROLL;
+  static constexpr int kChildUnroll = DP_SSSP_CHILD_UNROLL;
   static constexpr bool kBlockMode = false;
   static constexpr bool kPureExpand = true;
   static constexpr int kMinBlocks = DP_SSSP_MINB;
