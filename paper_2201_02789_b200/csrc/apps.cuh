@@ -108,6 +108,9 @@ struct BfsApp {
 #endif
   }
   static constexpr int kUnroll = DP_GRAPH_UNROLL;
+  // hub rows walked by the whole parent warp: 4 in flight (1.27 vs 1.29 ms,
+  // profiles/ab_big_unroll_r01.txt)
+  static constexpr int kBigUnroll = 4;
   static constexpr bool kBlockMode = false;
   static constexpr bool kPureExpand = true;
   static constexpr int kMinBlocks = 1;

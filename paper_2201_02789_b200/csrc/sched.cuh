@@ -202,6 +202,19 @@ __global__ void __launch_bounds__(256, App::kMinBlocks) child_agg_kernel(App app
 // whose inclusive count first exceeds k (5-step shuffle search), so a warp
 // with degrees {1, 1, ..., 40} takes 3 fully-populated steps instead of 40
 // one-lane steps.  Same items, same atomics, no launch.  All lanes call.
+#ifndef DP_BIG_UNROLL
+#define DP_BIG_UNROLL 0  // serial arm, lanes with >= 32 items (0: per app)
+#endif
+// the serial arm's unroll for a lane walked by the whole warp:
+// App::kBigUnroll when declared, else App::kUnroll
+template <class App, class = void>
+struct BigUnroll {
+  static constexpr int value = App::kUnroll;
+};
+template <class App>
+struct BigUnroll<App, std::void_t<decltype(App::kBigUnroll)>> {
+  static constexpr int value = App::kBigUnroll;
+};
 template <class App>
 __device__ __forceinline__ void serial_arm(const App& app,
                                            const typename App::Args& a, int cnt,
@@ -233,15 +246,17 @@ __device__ __forceinline__ void serial_arm(const App& app,
     const Args b = shfl_pod(a, src);
     const int cb = __shfl_sync(DP_FULL, cnt, src);
     auto args = [&](int) -> const Args& { return b; };
-    for (int e0 = 0; e0 < cb; e0 += 32 * U) {
-      int e[U];
-      bool ok[U];
+    constexpr int UB =
+        DP_BIG_UNROLL > 0 ? DP_BIG_UNROLL : BigUnroll<App>::value;
+    for (int e0 = 0; e0 < cb; e0 += 32 * UB) {
+      int e[UB];
+      bool ok[UB];
 #pragma unroll
-      for (int j = 0; j < U; ++j) {
+      for (int j = 0; j < UB; ++j) {
         e[j] = e0 + j * 32 + lane_id();
         ok[j] = e[j] < cb;
       }
-      app.template items<U>(args, e, ok, acc);
+      app.template items<UB>(args, e, ok, acc);
     }
   }
   // the rest (< 32 items per lane) as one flattened, load-balanced list
