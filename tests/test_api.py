@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import ctypes
 import re
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -170,3 +171,23 @@ def test_report_text_and_lists():
     text = r.to_text(include_buffers=True)
     assert "buffer dist = 0 1 1073741824" in text
     assert text.splitlines()[0] == "num_launches=0"
+
+
+def test_report_phase_times_and_pending_depth():
+    # dp_stats.ns_phase -> SimReport.phase_time / t_* lines (sim/report.py:
+    # 12-50); max_pending_depth passes through
+    st = {k: 0 for k, _ in _lib.DpStats._fields_}
+    st["ns_phase"] = [10.0, 20.4, 30.0, 40.0, 50.0]
+    st["max_pending_depth"] = 3
+    r = Report.from_stats(st, {"x": np.zeros(1, np.int32)}, {"x": "int"})
+    assert r.phase_time == {"parent": 10, "launch": 20, "agg": 30,
+                            "disagg": 40, "child": 50}
+    assert r.max_pending_depth == 3
+    text = r.to_text()
+    assert "t_launch=20" in text and "max_pending_depth=3" in text
+
+
+def test_profiled_build_target_exists():
+    mk = (Path(__file__).resolve().parents[1] / "paper_2201_02789_b200" /
+          "csrc" / "Makefile").read_text()
+    assert "libdynpar_prof.so" in mk and "-DDP_PROFILE=1" in mk
