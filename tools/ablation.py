@@ -20,10 +20,16 @@ from paper_2201_02789_b200.bench import BenchConfig, load, run_config  # noqa
 AGGS = ("warp", "block", "multiblock", "grid")
 
 
-def variants(best):
-    T, C = best["threshold"], best["cfactor"]
-    base = dict(parent_block=best["parent_block"],
-                child_block=best["child_block"], serial=best["serial"])
+# BT's tuned policy runs every curve in the parent (T = INF, no launches);
+# its ablation uses the config-2 policy's T and C instead
+T_C_OVERRIDE = {"bt": (64, 16)}
+
+
+def variants(best, kind=None):
+    T, C = T_C_OVERRIDE.get(kind, (best["threshold"], best.get("cfactor", 1)))
+    base = dict(parent_block=best.get("parent_block", 32),
+                child_block=best.get("child_block", 32),
+                serial=best.get("serial", "thread"))
     out = {"CDP": [dict(base)], "CDP+T": [dict(base, threshold=T)],
            "CDP+C": [dict(base, cfactor=C)],
            "CDP+T+C": [dict(base, threshold=T, cfactor=C)]}
@@ -50,7 +56,7 @@ def main():
             return statistics.median(run_dev(kind, G, c, stream)["ns_device"]
                                      for _ in range(3)) / 1e6
         row = {"No CDP": t(dict(parent_block=256), _lib.VARIANT_NOCDP)}
-        for name, pols in variants(BEST[kind]).items():
+        for name, pols in variants(BEST[kind], kind).items():
             row[name] = min(t(p) for p in pols)
         table[kind] = row
         del G
@@ -67,7 +73,7 @@ def main():
             return min(run_config(bench, wl, BenchConfig(**pol))[0].ns_device
                        for _ in range(3)) / 1e6
         row = {"No CDP": t({}, nocdp=True)}
-        for name, pols in variants(BEST[kind]).items():
+        for name, pols in variants(BEST[kind], kind).items():
             row[name] = min(t(p) for p in pols)
         table[kind] = row
         print(kind, {k: round(v, 3) for k, v in row.items()}, flush=True)
