@@ -241,9 +241,12 @@ struct BfsPartApp {
     update(v, probe(v), a.level, acc);
   }
   static constexpr int kUnroll = DP_GRAPH_UNROLL;
+  // whole-warp rows: 4 in flight, as BfsApp (BFS-26 P=1: 22.0 vs 22.6 ms)
+  static constexpr int kBigUnroll = 4;
   static constexpr bool kBlockMode = false;
   static constexpr bool kPureExpand = true;
-  static constexpr int kMinBlocks = 1;
+  // <= 48 registers: 5 blocks of 256 per SM (50 registers would fit 4)
+  static constexpr int kMinBlocks = 5;
   template <int U, class ArgsOf>
   __device__ __forceinline__ void items(ArgsOf args, const int* e,
                                         const bool* ok, Acc& acc) const {

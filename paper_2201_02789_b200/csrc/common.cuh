@@ -212,14 +212,19 @@ __device__ __forceinline__ void note_child_start(DevState* ds,
   if (ts && blockIdx.x == 0 && threadIdx.x == 0) {
     atomicAdd(&ds->lat_sum, globaltimer_ns() - ts);
     atomicAdd(&ds->lat_cnt, 1ull);
-    atomicSub(&ds->pending, 1);
+    // the queue length just before this start: its maximum over the starts
+    // is the queue's high-water mark (the first start after the peak sees it)
+    atomicMax(&ds->max_pending, atomicSub(&ds->pending, 1));
   }
 }
 
 // a device launch is about to be issued (counted before the call, so its
-// child can never leave the queue before it entered)
+// child can never leave the queue before it entered); the child's first
+// block takes it out again in note_child_start
+// (a reduction without a return value: no register stays live across the
+// launch for it, which the parent kernels' occupancy depends on)
 __device__ __forceinline__ void note_launch_issue(DevState* ds) {
-  atomicMax(&ds->max_pending, atomicAdd(&ds->pending, 1) + 1);
+  atomicAdd(&ds->pending, 1);
 }
 
 __device__ __forceinline__ void note_launch_error(DevState* ds) {
