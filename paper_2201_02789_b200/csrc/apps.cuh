@@ -29,6 +29,12 @@ namespace dp {
 #ifndef DP_SSSP_UNROLL
 #define DP_SSSP_UNROLL 2
 #endif
+#ifndef DP_SP_RATIO_MINB
+#define DP_SP_RATIO_MINB 1
+#endif
+#ifndef DP_MST_MINB
+#define DP_MST_MINB 5  // <= 48 registers, no spills: MST 4.15 -> 3.98 ms
+#endif
 #ifndef DP_SSSP_CHILD_UNROLL
 #define DP_SSSP_CHILD_UNROLL 1  // hub children: 1 < 2 < 4 < 8
 #endif                          // (profiles/ab_child_unroll_r01.txt)
@@ -1155,7 +1161,7 @@ struct MstFindApp {
   static constexpr int kUnroll = 4;
   static constexpr bool kBlockMode = false;
   static constexpr bool kPureExpand = true;
-  static constexpr int kMinBlocks = 1;
+  static constexpr int kMinBlocks = DP_MST_MINB;
   template <int U, class ArgsOf>
   __device__ __forceinline__ void items(ArgsOf args, const int* e,
                                         const bool* ok, Acc& acc) const {
@@ -1421,7 +1427,7 @@ struct SpRatioApp {
   static constexpr int kUnroll = 1;
   static constexpr bool kBlockMode = false;
   static constexpr bool kPureExpand = true;
-  static constexpr int kMinBlocks = 1;
+  static constexpr int kMinBlocks = DP_SP_RATIO_MINB;
   template <int U, class ArgsOf>
   __device__ __forceinline__ void items(ArgsOf args, const int* e,
                                         const bool* ok, Acc& acc) const {
