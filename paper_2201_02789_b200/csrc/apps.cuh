@@ -29,6 +29,9 @@ namespace dp {
 #ifndef DP_SSSP_UNROLL
 #define DP_SSSP_UNROLL 2
 #endif
+#ifndef DP_BFS_MINB
+#define DP_BFS_MINB 8  // <= 32 registers: 1.26 vs 1.28 ms (ab_bfs_minblocks_r01)
+#endif
 #ifndef DP_SP_RATIO_MINB
 #define DP_SP_RATIO_MINB 1
 #endif
@@ -119,7 +122,7 @@ struct BfsApp {
   static constexpr int kBigUnroll = 4;
   static constexpr bool kBlockMode = false;
   static constexpr bool kPureExpand = true;
-  static constexpr int kMinBlocks = 1;
+  static constexpr int kMinBlocks = DP_BFS_MINB;
   template <int U, class ArgsOf>
   __device__ __forceinline__ void items(ArgsOf args, const int* e,
                                         const bool* ok, Acc& acc) const {
