@@ -29,6 +29,9 @@ namespace dp {
 #ifndef DP_SSSP_UNROLL
 #define DP_SSSP_UNROLL 2
 #endif
+#ifndef DP_BFSPART_MINB
+#define DP_BFSPART_MINB 8  // <= 32 registers: BFS-26 22.0 -> 19.7 ms
+#endif
 #ifndef DP_BFS_MINB
 #define DP_BFS_MINB 8  // <= 32 registers: 1.26 vs 1.28 ms (ab_bfs_minblocks_r01)
 #endif
@@ -254,8 +257,8 @@ struct BfsPartApp {
   static constexpr int kBigUnroll = 4;
   static constexpr bool kBlockMode = false;
   static constexpr bool kPureExpand = true;
-  // <= 48 registers: 5 blocks of 256 per SM (50 registers would fit 4)
-  static constexpr int kMinBlocks = 5;
+  // register cap (8 blocks of 256 per SM at 32 registers; 5 at 48, 4 at 50)
+  static constexpr int kMinBlocks = DP_BFSPART_MINB;
   template <int U, class ArgsOf>
   __device__ __forceinline__ void items(ArgsOf args, const int* e,
                                         const bool* ok, Acc& acc) const {
