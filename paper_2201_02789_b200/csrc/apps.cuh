@@ -29,6 +29,9 @@ namespace dp {
 #ifndef DP_SSSP_UNROLL
 #define DP_SSSP_UNROLL 2
 #endif
+#ifndef DP_TC_MINB
+#define DP_TC_MINB 1  // TC's grid parent is at 31 registers already
+#endif
 #ifndef DP_BFSPART_MINB
 #define DP_BFSPART_MINB 8  // <= 32 registers: BFS-26 22.0 -> 19.7 ms
 #endif
@@ -39,7 +42,7 @@ namespace dp {
 #define DP_SP_RATIO_MINB 1
 #endif
 #ifndef DP_MST_MINB
-#define DP_MST_MINB 5  // <= 48 registers, no spills: MST 4.15 -> 3.98 ms
+#define DP_MST_MINB 8  // <= 32 registers: MST 4.15 (56) -> 3.98 (48) -> 3.70 ms
 #endif
 #ifndef DP_SSSP_CHILD_UNROLL
 #define DP_SSSP_CHILD_UNROLL 1  // hub children: 1 < 2 < 4 < 8
@@ -902,7 +905,7 @@ struct TcApp {
   // merge chains.  Lists longer than kSlots/2 fall back to per-thread merges.
   static constexpr bool kBlockMode = true;
   static constexpr bool kPureExpand = true;
-  static constexpr int kMinBlocks = 1;
+  static constexpr int kMinBlocks = DP_TC_MINB;
   static constexpr int kSlotBits = 12;
   static constexpr int kSlots = 1 << kSlotBits;  // 16 KB of shared memory
 
@@ -1244,7 +1247,7 @@ struct MstVerifyApp {
   static constexpr int kUnroll = 4;
   static constexpr bool kBlockMode = false;
   static constexpr bool kPureExpand = true;
-  static constexpr int kMinBlocks = 1;
+  static constexpr int kMinBlocks = DP_MST_MINB;
   template <int U, class ArgsOf>
   __device__ __forceinline__ void items(ArgsOf args, const int* e,
                                         const bool* ok, Acc& acc) const {
