@@ -38,6 +38,9 @@ namespace dp {
 #ifndef DP_BFS_MINB
 #define DP_BFS_MINB 8  // <= 32 registers: 1.26 vs 1.28 ms (ab_bfs_minblocks_r01)
 #endif
+#ifndef DP_SP_MINB
+#define DP_SP_MINB 1
+#endif
 #ifndef DP_SP_RATIO_MINB
 #define DP_SP_RATIO_MINB 1
 #endif
@@ -1359,7 +1362,7 @@ struct SpVarApp {
   static constexpr int kUnroll = 1;
   static constexpr bool kBlockMode = false;
   static constexpr bool kPureExpand = true;
-  static constexpr int kMinBlocks = 1;
+  static constexpr int kMinBlocks = DP_SP_MINB;
   template <int U, class ArgsOf>
   __device__ __forceinline__ void items(ArgsOf args, const int* e,
                                         const bool* ok, Acc& acc) const {
@@ -1481,7 +1484,7 @@ struct SpClauseApp {
   static constexpr int kUnroll = 1;
   static constexpr bool kBlockMode = false;
   static constexpr bool kPureExpand = true;
-  static constexpr int kMinBlocks = 1;
+  static constexpr int kMinBlocks = DP_SP_MINB;
   template <int U, class ArgsOf>
   __device__ __forceinline__ void items(ArgsOf args, const int* e,
                                         const bool* ok, Acc& acc) const {
