@@ -38,6 +38,9 @@ namespace dp {
 #ifndef DP_BFS_MINB
 #define DP_BFS_MINB 8  // <= 32 registers: 1.26 vs 1.28 ms (ab_bfs_minblocks_r01)
 #endif
+#ifndef DP_BT_MINB
+#define DP_BT_MINB 1
+#endif
 #ifndef DP_SP_MINB
 #define DP_SP_MINB 1
 #endif
@@ -1093,7 +1096,7 @@ struct BtApp {
   static constexpr int kUnroll = 1;
   static constexpr bool kBlockMode = false;
   static constexpr bool kPureExpand = false;  // bump-allocates in expand
-  static constexpr int kMinBlocks = 1;
+  static constexpr int kMinBlocks = DP_BT_MINB;
   template <int U, class ArgsOf>
   __device__ __forceinline__ void items(ArgsOf args, const int* e,
                                         const bool* ok, Acc& acc) const {
