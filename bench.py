@@ -193,6 +193,17 @@ class DeviceGraph:
         self.counts = torch.empty(self.n, dtype=torch.int32, device=dev)
 
 
+def headline_config(n: int, m: int, e_reach: int) -> dict:
+    """The `config` both arms print (identical keys and values, so the
+    driver's same-config check compares like with like); run details such as
+    the policy and round count go under "details"."""
+    return {"workload": f"sssp rmat-{SCALE} from vertex 0",
+            "graph": f"rmat scale {SCALE}, edge factor 16, seed {SEED}",
+            "weights": "U[1,9] (bench/graphs.py:184-187 rule)",
+            "n": n, "m": m, "e_reach": e_reach,
+            "l2": "inputs (col+weight 512 MiB) exceed L2; no flush"}
+
+
 def run_dev(kind: str, G, cfg, stream) -> dict:
     from paper_2201_02789_b200 import _lib
     lib = _lib.device()
@@ -517,6 +528,95 @@ def max_over_ranks(x: float) -> float:
     return float(t.item())
 
 
+def exchange_self_check(kind: str, exchange: str, world: int, rank: int,
+                        dev) -> tuple[bool, str]:
+    """Run the partitioned `kind` ("sssp" | "bfs") on RMAT-16 through
+    `exchange` ("peer" | "a2a") and compare the gathered result with the
+    oracle; the verdict is agreed over ranks (min), so every rank takes the
+    same branch.  Runs before a partitioned timed region: the fused
+    symmetric-memory exchange is used only where it has just proved itself
+    bit-exact on this box."""
+    import torch
+    from paper_2201_02789_b200 import dist as pdist
+    from oracle import oracle
+    collective = torch.distributed.is_initialized()
+    rowptr, col = oracle.rmat(16, SEED)
+    n = rowptr.shape[0] - 1
+    ok, err = False, ""
+    try:
+        if kind == "sssp":
+            w = oracle.edge_weights(n, col.shape[0], SEED)
+            rp_p, col_p, w_p = pdist.partition_csr(rowptr, col, world, rank,
+                                                   w)
+            cfg = _cfg(BEST["sssp"])
+            if exchange == "peer":
+                ex = pdist.PeerCollective() if collective else \
+                    pdist.PeerLocal()
+                buf = ex.alloc(n, world, dev)
+                part = pdist.SsspPeerPart(rp_p, col_p, w_p, n, world, rank, 0,
+                                          buf, dev)
+                ex.bind([part])
+                got, _ = pdist.sssp_1d_peer([part],
+                                            pdist.DeviceSsspPeerOps(cfg), ex)
+            else:
+                part = pdist.SsspPart(rp_p, col_p, w_p, n, world, rank, 0,
+                                      dev)
+                ex = pdist.CollectiveExchange() if collective else \
+                    pdist.LocalExchange()
+                got, _ = pdist.sssp_1d([part], pdist.DeviceSsspOps(cfg), ex)
+            want, _ = oracle.sssp(rowptr, col, w, nthreads=0)
+            ok = bool(np.array_equal(got.cpu().numpy(), want))
+        else:
+            rp_p, col_p = pdist.partition_csr(rowptr, col, world, rank)
+            ops = pdist.DeviceBfsOps(_cfg(BEST["bfs"]))
+            if exchange == "peer":
+                ex = pdist.PeerCollective() if collective else \
+                    pdist.PeerLocal()
+                buf = ex.alloc(n, world, dev)
+                part = pdist.BfsPart(rp_p, col_p, n, world, rank, 0, dev,
+                                     dist=buf, spread=True)
+                ex.bind([part])
+                got_d, got_c, _ = pdist.bfs_1d_peer([part], ops, ex)
+            else:
+                part = pdist.BfsPart(rp_p, col_p, n, world, rank, 0, dev,
+                                     spread=True)
+                ex = pdist.CollectiveExchange() if collective else \
+                    pdist.LocalExchange()
+                got_d, got_c, _ = pdist.bfs_1d([part], ops, ex)
+            wd, wc, _ = oracle.bfs(rowptr, col, nthreads=0)
+            ok = bool(np.array_equal(got_d.cpu().numpy(), wd)
+                      and np.array_equal(got_c.cpu().numpy(), wc))
+        if not ok:
+            err = "result differs from the oracle"
+    except Exception as e:  # noqa: BLE001 - reported, then the fallback
+        err = f"{type(e).__name__}: {e}"
+    if collective:
+        t = torch.tensor([int(ok)], dtype=torch.int32, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MIN)
+        ok = bool(int(t.item()))
+        if not ok and not err:
+            err = "another rank failed"
+    torch.cuda.synchronize()
+    return ok, err
+
+
+def choose_exchange(kind: str, requested: str, world: int, rank: int,
+                    dev) -> tuple[str, str]:
+    """The exchange the timed region will use, after the RMAT-16 self-check
+    (peer falls back to the NCCL all-to-all); returns (exchange, note)."""
+    ok, err = exchange_self_check(kind, requested, world, rank, dev)
+    if ok:
+        return requested, f"{requested}: RMAT-16 self-check bit-exact"
+    note = f"{requested} failed the RMAT-16 self-check ({err})"
+    if requested == "peer":
+        print(f"[bench] {note}; falling back to the all-to-all exchange",
+              file=sys.stderr)
+        ok2, err2 = exchange_self_check(kind, "a2a", world, rank, dev)
+        return "a2a", note + ("; a2a: self-check bit-exact" if ok2 else
+                              f"; a2a ALSO FAILED ({err2})")
+    return requested, note
+
+
 def arm_sssp_partitioned(args, world, rank, local):
     """N > 1: the headline SSSP over a cyclic 1D vertex partition, one part
     per rank, per-round NCCL all-to-all of improving remote relaxations
@@ -532,7 +632,7 @@ def arm_sssp_partitioned(args, world, rank, local):
     w = graphs.edge_weights(g, SEED)
     rp_p, col_p, w_p = pdist.partition_csr(g.rowptr, g.col, world, rank, w)
     collective = torch.distributed.is_initialized()
-    exchange = args.exchange
+    exchange, check = choose_exchange("sssp", args.exchange, world, rank, dev)
     part = ex = None
     if exchange == "peer":
         # fused exchange: remote relaxations are atomicMin into the owner's
@@ -610,6 +710,7 @@ def arm_sssp_partitioned(args, world, rank, local):
                                 "dist via symmetric memory + NCCL max of the "
                                 "round flag" if exchange == "peer" else
                                 "NCCL all-to-all of (v, alt) pairs + apply"),
+                   "exchange_check": check,
                    "l2": "inputs exceed L2; no flush"},
         "parity": "bit-exact vs oracle" if np.array_equal(dist_h, want)
         else "MISMATCH",
@@ -653,12 +754,10 @@ def arm_ours(args, world, rank, local):
             "scaling": "strong", "vs_baseline": None, "dtype": "int32",
             "data": "synthetic RMAT (Graph500 a,b,c=.57,.19,.19, seed 1, "
                     "edge factor 16), weights U[1,9]",
-            "config": {"workload": f"sssp rmat-{SCALE} from vertex 0",
-                       "n": G.n, "m": G.m, "e_reach": e_reach,
-                       "rounds": rounds, "policy": BEST["sssp"],
-                       "parallelism": "single",
-                       "lib_device_ms_per_step": lib_ms,
-                       "l2": "inputs (col+weight 512 MiB) exceed L2; no flush"},
+            "config": headline_config(G.n, G.m, e_reach),
+            "details": {"rounds": rounds, "policy": BEST["sssp"],
+                        "parallelism": "single",
+                        "lib_device_ms_per_step": lib_ms},
             "gpu_launches": int(sum(s["kernel_launches"] + s["num_launches"]
                                     for s in stats))}
     if rank != 0:
@@ -735,9 +834,9 @@ def arm_bfs26(args, world, rank, local):
     _lib.device()
     dev = torch.device("cuda", torch.cuda.current_device())
     scale = args.scale or 26
-    rp, col = pdist.rmat_part_device(scale, SEED, world, rank, dev)
     collective = torch.distributed.is_initialized()
-    exchange = args.exchange
+    exchange, check = choose_exchange("bfs", args.exchange, world, rank, dev)
+    rp, col = pdist.rmat_part_device(scale, SEED, world, rank, dev)
     part = None
     if exchange == "peer":
         # fused exchange: remote discoveries are CAS'd into the owner's dist
@@ -746,7 +845,7 @@ def arm_bfs26(args, world, rank, local):
             ex = pdist.PeerCollective() if collective else pdist.PeerLocal()
             buf = ex.alloc(1 << scale, world, dev)
             part = pdist.BfsPart(rp, col, 1 << scale, world, rank, 0, dev,
-                                 dist=buf)
+                                 dist=buf, spread=True)
             ex.bind([part])
             run_levels = pdist.bfs_1d_peer
         except Exception as e:  # noqa: BLE001 - fall back to the NCCL a2a
@@ -754,7 +853,8 @@ def arm_bfs26(args, world, rank, local):
                   f"all-to-all exchange", file=sys.stderr)
             exchange = "a2a"
     if exchange == "a2a":
-        part = pdist.BfsPart(rp, col, 1 << scale, world, rank, 0, dev)
+        part = pdist.BfsPart(rp, col, 1 << scale, world, rank, 0, dev,
+                             spread=True)
         ex = pdist.CollectiveExchange() if collective else \
             pdist.LocalExchange()
         run_levels = pdist.bfs_1d
@@ -788,17 +888,24 @@ def arm_bfs26(args, world, rank, local):
                                     "via symmetric memory + NCCL max of the "
                                     "level flag" if exchange == "peer" else
                                     "NCCL all-to-all of discovered ids + "
-                                    "apply")},
+                                    "apply"),
+                       "exchange_check": check},
             "clocks": clk.summary()}
-    if scale <= 22:  # the oracle check fits the host quickly
-        from oracle import oracle
-        from paper_2201_02789_b200.bench import graphs
-        g = graphs.rmat_graph(scale, SEED)
-        wd, wc, _ = oracle.bfs(g.rowptr, g.col, nthreads=0)
-        line["parity"] = ("bit-exact vs oracle"
-                          if np.array_equal(dist_t.cpu().numpy(), wd)
-                          and np.array_equal(counts_t.cpu().numpy(), wc)
-                          else "MISMATCH")
+    # parity at every scale (RMAT-26: 1.07 G edges through the OpenMP oracle
+    # on the host; the oracle's own generator, rows unsorted since BFS
+    # outputs do not depend on the row order)
+    from oracle import oracle
+    got_d, got_c = dist_t.cpu().numpy(), counts_t.cpu().numpy()
+    del dist_t, counts_t
+    t0 = time.perf_counter()
+    orp, ocol = oracle.rmat(scale, SEED, sort_rows=False)
+    wd, wc, wl = oracle.bfs(orp, ocol, nthreads=0)
+    del orp, ocol
+    line["parity"] = ("bit-exact vs oracle (dist, counts, levels)"
+                      if np.array_equal(got_d, wd)
+                      and np.array_equal(got_c, wc) and wl == levels
+                      else "MISMATCH")
+    line["parity_check_s"] = time.perf_counter() - t0
     print(json.dumps(line), flush=True)
 
 
@@ -858,20 +965,21 @@ def arm_reference(args, world, rank, local):
     itself is pure Python and cannot travel to the GPU box."""
     if rank != 0:
         return
+    # the input comes from the oracle's own restatement of the generator:
+    # nothing of the product package (nor its library) is loaded in this arm
     from oracle import oracle
-    from paper_2201_02789_b200.bench import graphs
-    from paper_2201_02789_b200.bench.graphs import UNREACHED
-    g = graphs.rmat_graph(SCALE, SEED)
-    w = graphs.edge_weights(g, SEED)
+    rowptr, col = oracle.rmat(SCALE, SEED)
+    n, m = rowptr.shape[0] - 1, col.shape[0]
+    w = oracle.edge_weights(n, m, SEED)
     threads = len(os.sched_getaffinity(0))
     for _ in range(args.warmup):
-        oracle.sssp(g.rowptr, g.col, w, nthreads=threads)
+        oracle.sssp(rowptr, col, w, nthreads=threads)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        dist, rounds = oracle.sssp(g.rowptr, g.col, w, nthreads=threads)
+        dist, rounds = oracle.sssp(rowptr, col, w, nthreads=threads)
     dt = (time.perf_counter() - t0) / args.steps
-    deg = np.diff(g.rowptr.astype(np.int64))
-    e_reach = int(deg[dist < UNREACHED].sum())
+    deg = np.diff(rowptr.astype(np.int64))
+    e_reach = int(deg[dist < (1 << 30)].sum())
     value = e_reach / dt / 1e9
     sample = (f"full SSSP rmat-{SCALE} from vertex 0 ({rounds} rounds) per "
               f"step, oracle/oracle.c OpenMP")
@@ -880,9 +988,13 @@ def arm_reference(args, world, rank, local):
         "value": value, "unit": "GTEPS", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "int32", "data": "synthetic RMAT, weights U[1,9]",
-        "config": {"workload": f"sssp rmat-{SCALE} from vertex 0",
-                   "n": g.n, "m": g.m, "e_reach": e_reach},
+        "dtype": "int32",
+        "data": "synthetic RMAT (Graph500 a,b,c=.57,.19,.19, seed 1, "
+                "edge factor 16), weights U[1,9]",
+        "config": headline_config(n, m, e_reach),
+        "details": {"rounds": rounds, "threads": threads,
+                    "input": "oracle.rmat + oracle.edge_weights "
+                             "(product library not loaded)"},
         "cpu_baseline": {"value": value, "unit": "GTEPS", "cores": threads,
                          "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "GTEPS", "h2d_bytes_per_step": 0,

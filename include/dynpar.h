@@ -104,7 +104,22 @@ typedef struct dp_config {
                             fewer relaxations).  0 = every reached vertex
                             every round, as SSSP_CDP main does
                             (benchmarks.py:207-222) */
-  int32_t reserved[3];
+  int32_t agg_coarsen;   /* 1: the coarsening factor applies to the aggregated
+                            child grid (logical aggregated blocks
+                            [b*C, b*C + C) per physical block, possibly of
+                            several parents): the reference's pass order with
+                            A before C (pipeline.py:60-81).  Requires
+                            agg in {warp, block, multiblock}.  0 = canonical
+                            T -> C -> A (per-parent coarsening) */
+  int32_t counts_spread;  /* partitioned BFS (dp_bfs_part_level*): b > 0 ->
+                            d_counts holds n rounded up to a multiple of 2^b
+                            slots and vertex v counts at slot spread_b(v)
+                            (a bijective hash of v's low b bits that keeps
+                            RMAT hubs out of shared 128 B lines); gather with
+                            dp_unspread_dev.  0 = vertex order.  dp_bfs /
+                            dp_bfs_dev use the spread layout internally and
+                            always return vertex order */
+  int32_t reserved[1];
 } dp_config;
 
 /* SimReport (sim/report.py:12-28) counters, measured on the device */
@@ -253,6 +268,10 @@ int dp_bfs_part_level_peer(const int32_t* d_rowptr_p, const int32_t* d_col_p,
                            int32_t* d_dist_p, int32_t* const* d_peer_dist,
                            int32_t* d_counts, uint32_t* d_sent,
                            int32_t* d_changed, void* stream, dp_stats* stats);
+/* out[v] = work[spread_b(v)] for v < n: counts accumulated with
+ * counts_spread = b back in vertex order */
+int dp_unspread_dev(const int32_t* d_work, int32_t b, int32_t n,
+                    int32_t* d_out, void* stream);
 /* discover received global ids at level + 1 (CAS against UNREACHED) */
 int dp_bfs_part_apply(const int32_t* d_recv, int64_t nrecv, int32_t nparts,
                       int32_t level, int32_t* d_dist_p, int32_t* d_changed,

@@ -423,3 +423,102 @@ int32_t oracle_sp(const int32_t* lits, int32_t k, int32_t nclauses,
   free(nxt);
   return sweeps;
 }
+
+/* ------------------------------------------------------------------------
+ * RMAT generator (builder-defined input of BASELINE configs 3-5; the
+ * reference has none).  Restates the product generator
+ * (paper_2201_02789_b200/csrc/gen.cpp) independently so the reference arm and
+ * the RMAT-26 parity check never load the product library: Graph500
+ * quadrants (.57, .19, .19, .05) drawn bit by bit from the top level down,
+ * each level's draw a 32-bit half of splitmix64(key ^ (16 e + level / 2)),
+ * key = splitmix64(seed ^ "RMAT"); multi-edges and self-loops kept; rows
+ * ascending when sort_rows (the BFS outputs do not depend on the row order,
+ * so the RMAT-26 check may skip the sort).
+ * ------------------------------------------------------------------------ */
+static uint64_t sm64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+static void rmat_pair(uint64_t key, int64_t e, int scale, int32_t* s,
+                      int32_t* d) {
+  /* quadrant thresholds floor(p * 2^32) for the cumulative a, a+b, a+b+c */
+  const uint64_t ta = 2448131358ull, tab = 3264175144ull,
+                 tabc = 4080218931ull;
+  uint32_t src = 0, dst = 0;
+  uint64_t h = 0;
+  for (int l = 0; l < scale; ++l) {
+    if (!(l & 1)) h = sm64(key ^ ((uint64_t)e * 16u + (uint64_t)(l / 2)));
+    const uint64_t r = (l & 1) ? (h >> 32) : (h & 0xffffffffull);
+    /* a: (0,0)  b: (0,1)  c: (1,0)  d: (1,1) */
+    const uint32_t row_bit = r >= tab;
+    const uint32_t col_bit = (r >= ta && r < tab) || r >= tabc;
+    src = src * 2u + row_bit;
+    dst = dst * 2u + col_bit;
+  }
+  *s = (int32_t)src;
+  *d = (int32_t)dst;
+}
+
+static int i32_cmp(const void* a, const void* b) {
+  const int32_t x = *(const int32_t*)a, y = *(const int32_t*)b;
+  return (x > y) - (x < y);
+}
+
+static void sort_row(int32_t* a, int64_t k) {
+  if (k > 24) {
+    qsort(a, (size_t)k, sizeof(int32_t), i32_cmp);
+    return;
+  }
+  for (int64_t i = 1; i < k; ++i) { /* insertion sort for short rows */
+    const int32_t x = a[i];
+    int64_t j = i - 1;
+    while (j >= 0 && a[j] > x) {
+      a[j + 1] = a[j];
+      --j;
+    }
+    a[j + 1] = x;
+  }
+}
+
+/* rowptr int32[2^scale + 1], col int32[edge_factor * 2^scale]; 0 or -1 */
+int oracle_rmat_csr(int32_t scale, int32_t edge_factor, uint64_t seed,
+                    int32_t* rowptr, int32_t* col, int sort_rows,
+                    int nthreads) {
+  if (scale < 1 || scale > 30 || edge_factor < 1) return -1;
+  const int64_t n = (int64_t)1 << scale, m = (int64_t)edge_factor * n;
+  if (m > 0x7fffffffLL) return -1;
+  const uint64_t key = sm64(seed ^ 0x524D4154ull);
+  const int nt = nthr(nthreads);
+  int64_t* fill = (int64_t*)calloc((size_t)n + 1, sizeof(int64_t));
+  if (!fill) return -1;
+#pragma omp parallel for num_threads(nt) schedule(static)
+  for (int64_t e = 0; e < m; ++e) {
+    int32_t s, d;
+    rmat_pair(key, e, scale, &s, &d);
+    __atomic_fetch_add(&fill[s], 1, __ATOMIC_RELAXED);
+  }
+  int64_t run = 0;
+  for (int64_t u = 0; u < n; ++u) { /* exclusive scan -> row starts */
+    rowptr[u] = (int32_t)run;
+    const int64_t c = fill[u];
+    fill[u] = run;
+    run += c;
+  }
+  rowptr[n] = (int32_t)run;
+#pragma omp parallel for num_threads(nt) schedule(static)
+  for (int64_t e = 0; e < m; ++e) {
+    int32_t s, d;
+    rmat_pair(key, e, scale, &s, &d);
+    col[__atomic_fetch_add(&fill[s], 1, __ATOMIC_RELAXED)] = d;
+  }
+  free(fill);
+  if (sort_rows) {
+#pragma omp parallel for num_threads(nt) schedule(dynamic, 4096)
+    for (int64_t u = 0; u < n; ++u)
+      sort_row(col + rowptr[u], (int64_t)rowptr[u + 1] - rowptr[u]);
+  }
+  return 0;
+}

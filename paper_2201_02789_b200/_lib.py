@@ -41,7 +41,9 @@ class DpConfig(ctypes.Structure):
                 ("persistent", ctypes.c_int32),
                 ("device_loop", ctypes.c_int32),
                 ("frontier", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 3)]
+                ("agg_coarsen", ctypes.c_int32),
+                ("counts_spread", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 1)]
 
 
 class DpStats(ctypes.Structure):
@@ -104,6 +106,7 @@ _SIGNATURES = {
               ctypes.c_int),
     "dp_bt_dev": ([_P, _I32, _I32, _F32, _CFG, _P, _P, _P, _I64, _P, _P,
                    _ST], ctypes.c_int),
+    "dp_unspread_dev": ([_P, _I32, _I32, _P, _P], _I32),
     "dp_bfs_part_level": ([_P, _P, _I32, _I32, _I32, _I32, _CFG, _P, _P,
                            _P, _P, _I64, _P, _P, _P, _ST], ctypes.c_int),
     "dp_bfs_part_apply": ([_P, _I64, _I32, _I32, _P, _P, _P], ctypes.c_int),

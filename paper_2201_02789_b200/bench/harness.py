@@ -81,6 +81,10 @@ class BenchConfig:
                     f"{name} must be a multiple of 32 in [32, 256]")
         if not 0 <= self.persistent <= 8:
             raise ValueError("persistent must be in [0, 8] blocks per SM")
+        if self.persistent and self.order_effect(
+                self.threshold, self.cfactor, self.agg)[2]:
+            raise ValueError("a persistent parent cannot coarsen the "
+                             "aggregated grid (order with A before C)")
         if self.serial not in _lib.SERIAL_MODES:
             raise ValueError(f"unknown serial mode {self.serial!r}")
 
@@ -103,11 +107,38 @@ class BenchConfig:
         c.persistent = int(self.persistent)
         c.device_loop = int(bool(self.device_loop))
         c.frontier = int(bool(self.frontier))
-        if "T" not in self.order.upper():
-            c.threshold = 0
-        if "C" not in self.order.upper():
-            c.cfactor = 1
+        c.threshold, c.cfactor, c.agg_coarsen = self.order_effect(
+            c.threshold, c.cfactor, self.agg if agg_on else None)
         return c
+
+    def order_effect(self, threshold: int, cfactor: int,
+                     agg: str | None) -> tuple[int, int, int]:
+        """What the reference's `transform(order=...)` (pipeline.py:45-81)
+        does to the knobs, measured by running it (tests/golden/
+        order_counters.json): a disabled pass (T=0, C<=1, no agg) is a no-op
+        wherever it sits; an absent step never runs; the threshold pass only
+        recognises the original launch, so it is skipped when an active
+        coarsen or aggregate step precedes it; a coarsen step after an active
+        aggregate step rewrites the aggregated clone instead of the child
+        (its logical blocks span parents) -- except at grid granularity,
+        whose clone is host-launched, so nothing is coarsened.
+        Returns (threshold, cfactor, agg_coarsen)."""
+        order = self.order.upper()
+        pos = {s: order.index(s) for s in "TCA" if s in order}
+        t_on = threshold != 0 and "T" in pos
+        c_on = cfactor > 1 and "C" in pos
+        a_on = agg is not None and "A" in pos
+        if t_on and ((c_on and pos["C"] < pos["T"])
+                     or (a_on and pos["A"] < pos["T"])):
+            t_on = False
+        agg_coarsen = 0
+        if c_on and a_on and pos["A"] < pos["C"]:
+            if agg == "grid":
+                c_on = False
+            else:
+                agg_coarsen = 1
+        return (threshold if t_on else 0, cfactor if c_on else 1,
+                agg_coarsen)
 
 
 class EquivalenceError(AssertionError):

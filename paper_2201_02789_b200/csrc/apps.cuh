@@ -53,11 +53,32 @@ namespace dp {
 #ifndef DP_SSSP_CHILD_UNROLL
 #define DP_SSSP_CHILD_UNROLL 1  // hub children: 1 < 2 < 4 < 8
 #endif                          // (profiles/ab_child_unroll_r01.txt)
+// Discovery / relaxation as a fire-and-forget RED.MIN instead of a returning
+// CAS / atomicMin: min(old, new) reaches the same final value, and the round
+// flag is set from the probe (alt < d).  A probe is stale only within the
+// launch that cached it (L1 is invalidated at every kernel launch,
+// B300_MICROARCH.md "Per-launch flush"), so a flagged round is always one in
+// which some vertex really was lowered: the flag, and hence the level /
+// round count, is unchanged.
+#ifndef DP_BFS_RED
+#define DP_BFS_RED 0
+#endif
+#ifndef DP_SSSP_RED
+#define DP_SSSP_RED 0
+#endif
+#ifndef DP_BFS_NO_COUNTS
+#define DP_BFS_NO_COUNTS 0  // ablation only (wrong counts): the cost of counts
+#endif
 #ifndef DP_SSSP_MINB
 #define DP_SSSP_MINB 8  // <= 32 registers: full occupancy for the latency-
 #endif                  // bound relaxations (tools/ab.sh, profiles/)
 
 // items<U> for apps whose item is not latency-chained: plain loop
+__device__ __forceinline__ void red_min(int* p, int v) {
+  asm volatile("red.relaxed.gpu.global.min.s32 [%0], %1;" ::"l"(p), "r"(v)
+               : "memory");
+}
+
 template <int U, class App, class ArgsOf>
 __device__ __forceinline__ void items_loop(const App& app, ArgsOf args,
                                            const int* e, const bool* ok,
@@ -74,11 +95,13 @@ struct BfsApp {
   const int* __restrict__ rowptr;
   const int* __restrict__ col;
   int* dist;
-  int* counts;
+  int* counts;        // counts[spread_slot(v, cmask)] (common.cuh)
   int* changed;       // this level's flag
   int* changed_next;  // next level's flag, cleared here
   int n;
   int level;
+  unsigned cmask;     // spread layout of counts (0: vertex order)
+  unsigned pad_;
 
   struct alignas(16) Args {
     int start, deg, level, pad;
@@ -112,7 +135,7 @@ struct BfsApp {
   // UNREACHED.  The plain pre-check only skips CASes that would fail.
   __device__ void item(const Args& a, int e, Acc& acc) const {
     const int v = __ldg(col + a.start + e);
-    atomicAdd(counts + v, 1);
+    atomicAdd(counts + spread_slot(v, cmask), 1);
     if (__ldcg(dist + v) == kUnreached &&
         atomicCAS(dist + v, kUnreached, a.level + 1) == kUnreached)
       acc.changed = 1;
@@ -123,9 +146,10 @@ struct BfsApp {
 #if DP_MERGE_COUNTS
     const unsigned am = __activemask();
     const unsigned grp = __match_any_sync(am, v);
-    if (lane_id() == __ffs(grp) - 1) atomicAdd(counts + v, __popc(grp));
+    if (lane_id() == __ffs(grp) - 1)
+      atomicAdd(counts + spread_slot(v, cmask), __popc(grp));
 #else
-    atomicAdd(counts + v, 1);
+    atomicAdd(counts + spread_slot(v, cmask), 1);
 #endif
   }
   static constexpr int kUnroll = DP_GRAPH_UNROLL;
@@ -151,10 +175,17 @@ struct BfsApp {
 #pragma unroll
     for (int j = 0; j < U; ++j) {
       if (!ok[j]) continue;
-      count_edge(v[j]);
+      if (!DP_BFS_NO_COUNTS) count_edge(v[j]);
+#if DP_BFS_RED
+      if (d[j] == kUnreached) {
+        red_min(dist + v[j], args(j).level + 1);
+        acc.changed = 1;
+      }
+#else
       if (d[j] == kUnreached &&
           atomicCAS(dist + v[j], kUnreached, args(j).level + 1) == kUnreached)
         acc.changed = 1;
+#endif
     }
   }
   __device__ void flush(Acc& acc) const {
@@ -193,6 +224,8 @@ struct BfsPartApp {
   int nparts;
   int part;
   int level;
+  unsigned cmask;  // counts in the spread layout (common.cuh; 0: vertex order)
+  unsigned pad_;
 
   struct alignas(16) Args {
     int start, deg, level, pad;
@@ -226,10 +259,11 @@ struct BfsPartApp {
 #if DP_MERGE_COUNTS
     {  // lanes hitting the same vertex merge their increments (BfsApp)
       const unsigned grp = __match_any_sync(__activemask(), v);
-      if (lane_id() == __ffs(grp) - 1) atomicAdd(counts + v, __popc(grp));
+      if (lane_id() == __ffs(grp) - 1)
+        atomicAdd(counts + spread_slot(v, cmask), __popc(grp));
     }
 #else
-    atomicAdd(counts + v, 1);
+    atomicAdd(counts + spread_slot(v, cmask), 1);
 #endif
     const int q = part_of(v, nparts);
     if (q == part) {
@@ -590,9 +624,17 @@ struct SsspApp {
 #pragma unroll
     for (int j = 0; j < U; ++j) d[j] = ok[j] ? __ldca(dist + v[j]) : 0;
 #pragma unroll
-    for (int j = 0; j < U; ++j)
+    for (int j = 0; j < U; ++j) {
+#if DP_SSSP_RED
+      if (ok[j] && alt[j] < d[j]) {
+        red_min(dist + v[j], alt[j]);
+        acc.changed = 1;
+      }
+#else
       if (ok[j] && alt[j] < d[j] && atomicMin(dist + v[j], alt[j]) > alt[j])
         acc.changed = 1;
+#endif
+    }
   }
   __device__ void flush(Acc& acc) const {
     // read before write: after the first success the flag line is only

@@ -181,6 +181,25 @@ __device__ __forceinline__ void ph_add(DevState* ds, int ph, long long t0) {
 #endif
 }
 
+// Spread layout of a per-vertex atomic counter (BFS `counts`): within each
+// aligned block of 2^b vertices (mask = 2^b - 1), vertex v's slot is a
+// bijective multiply-xorshift hash of its low b bits; the high bits stay, so
+// the set of blocks touched (the L2 working set) is that of vertex order.
+// mask 0 = vertex order.  RMAT hubs cluster in a few 128 B lines (vertices
+// 0..31 alone take ~1 % of all edges at RMAT-22) and L2 serialises the
+// atomic requests of one line: spreading them over distinct lines took the
+// flat counts pass 0.81 -> 0.46 ms (profiles/ceiling_r02b.txt).  The work
+// array (n rounded up to a whole block) is gathered back into vertex order
+// once per run.
+__host__ __device__ __forceinline__ unsigned spread_slot(unsigned v,
+                                                        unsigned mask) {
+  if (!mask) return v;
+  unsigned x = (v * 0x9E3779B1u) & mask;
+  x ^= x >> 7;
+  x = (x * 0x85EBCA77u) & mask;
+  return (v & ~mask) | x;
+}
+
 // Owner part and local index of vertex v >= 0 under the cyclic partition
 // owner(v) = v % nparts.  Power-of-two part counts (the 1/2/4/8-GPU runs)
 // take a mask and a shift instead of an integer division per edge.

@@ -74,6 +74,9 @@ struct Workspace {
   cudaStream_t copy_stream = nullptr;
   int* d_arrived = nullptr;
   cudaEvent_t chunk_ev[kMaxChunks] = {};
+  // BFS counts in the spread layout (2^k slots)
+  void* cwork = nullptr;
+  size_t cwork_bytes = 0;
 };
 
 Workspace g_ws[64];
@@ -157,6 +160,13 @@ int validate(const dp_config* c) {
   if (c->persistent < 0 || c->persistent > 8)
     return fail(DP_ERR_INVALID, "persistent must be in [0, 8]");
   if (c->threshold < 0) return fail(DP_ERR_INVALID, "threshold must be >= 0");
+  if (c->counts_spread < 0 || c->counts_spread > 30)
+    return fail(DP_ERR_INVALID, "counts_spread must be in [0, 30]");
+  if (c->agg_coarsen &&
+      (c->agg < DP_AGG_WARP || c->agg > DP_AGG_MULTIBLOCK || c->persistent))
+    return fail(DP_ERR_INVALID,
+                "agg_coarsen requires warp, block or multiblock aggregation "
+                "and a non-persistent parent");
   if (c->parent_block < 32 || c->parent_block > 256 ||
       c->parent_block % 32)
     return fail(DP_ERR_INVALID,
@@ -327,6 +337,7 @@ Knobs knobs_of(const dp_config* c) {
   k.group = c->group_size;
   k.agg_threshold = c->agg_threshold;
   k.serial_warp = c->serial_mode == DP_SERIAL_WARP;
+  k.agg_cf = c->agg_coarsen != 0;
   return k;
 }
 
@@ -504,7 +515,7 @@ glue:
     const int total = (int)(cv & 0xffffffffull);
     if (total > 0) {
       child_agg_kernel<App><<<total, c->child_block, 0, s>>>(
-          app, t.args, t.scan, np, c->cfactor, w->ds, 0ull);
+          app, t.args, t.scan, np, c->cfactor, 0, w->ds, 0ull);
       DP_CUDA(cudaGetLastError());
       rc->host_launches += 1;
       rc->host_blocks += total;
@@ -540,6 +551,26 @@ int account_step(Workspace* w, RunCounters* rc) {
   rc->ms_kernel_sum += ms;
   rc->ms_kernel_max = std::max<double>(rc->ms_kernel_max, ms);
   return 0;
+}
+
+#ifndef DP_BFS_SPREAD
+#define DP_BFS_SPREAD 12  // log2 of the spread block (0: vertex order)
+#endif
+
+// spread block of dp_bfs*: DP_BFS_SPREAD, or $DYNPAR_SPREAD_BITS (A/B)
+int spread_bits() {
+  static const int b = [] {
+    const char* e = std::getenv("DYNPAR_SPREAD_BITS");
+    return e ? std::max(0, std::min(30, std::atoi(e))) : DP_BFS_SPREAD;
+  }();
+  return b;
+}
+
+// counts[v] = work[spread_slot(v)] (common.cuh)
+__global__ void unspread_kernel(const int* __restrict__ work, unsigned mask,
+                                int* counts, int n) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v < n) counts[v] = __ldcg(work + spread_slot((unsigned)v, mask));
 }
 
 __global__ void init_dist_kernel(int* dist, int n, int src) {
@@ -701,10 +732,14 @@ struct Arrival {
   int waited = 0;  // chunks the host has already waited for
 };
 
-template <class MakeApp>
+struct NoFinish {
+  void operator()() const {}
+};
+
+template <class MakeApp, class Finish = NoFinish>
 int iterate(Workspace* w, const dp_config* c, long long nparents,
             long long launchers, int max_iter, cudaStream_t s, MakeApp make,
-            dp_stats* st, Arrival* arr = nullptr) {
+            dp_stats* st, Arrival* arr = nullptr, Finish finish = Finish()) {
   RunCounters rc;
   int r;
   if ((r = ensure_pending_limit(w, c, launch_bound(c, nparents, launchers))))
@@ -737,6 +772,7 @@ int iterate(Workspace* w, const dp_config* c, long long nparents,
     if (arr && arr->waited < arr->nchunks && w->h_ds->skipped[it & 1])
       DP_CUDA(cudaEventSynchronize(w->chunk_ev[arr->waited++]));
   }
+  finish();  // run epilogue kernels (inside the timed region)
   DP_CUDA(cudaEventRecord(w->ev1, s));
   DP_CUDA(cudaEventSynchronize(w->ev1));
   float ms = 0.f;
@@ -763,7 +799,21 @@ int bfs_dev_impl(const int32_t* rowptr, const int32_t* col, int32_t n,
   Workspace* w = workspace(&r);
   if (!w) return r;
   init_dist_kernel<<<dp::ceil_div(n, 256), 256, 0, s>>>(dist, n, src);
-  DP_CUDA(cudaMemsetAsync(counts, 0, (size_t)n * sizeof(int), s));
+  // counts accumulate in the spread layout (common.cuh spread_slot) and are
+  // gathered into vertex order after the last level
+  unsigned cmask = 0;
+  int* cw = counts;
+  const int sb = spread_bits();
+  if (sb > 0 && n >= 1024) {
+    const size_t blk = (size_t)1 << sb;
+    const size_t slots = (n + blk - 1) / blk * blk;
+    if ((r = grow(&w->cwork, &w->cwork_bytes, slots * sizeof(int)))) return r;
+    cw = (int*)w->cwork;
+    cmask = (unsigned)(blk - 1);
+    DP_CUDA(cudaMemsetAsync(cw, 0, slots * sizeof(int), s));
+  } else {
+    DP_CUDA(cudaMemsetAsync(counts, 0, (size_t)n * sizeof(int), s));
+  }
   long long launchers = 0;
   if (c->variant == DP_VARIANT_CDP &&
       (r = count_launchers(w, c, rowptr, n, 0, s, &launchers)))
@@ -775,14 +825,20 @@ int bfs_dev_impl(const int32_t* rowptr, const int32_t* col, int32_t n,
                    a.rowptr = rowptr;
                    a.col = col;
                    a.dist = dist;
-                   a.counts = counts;
+                   a.counts = cw;
                    a.changed = &ds->flag[level & 1];
                    a.changed_next = &ds->flag[(level + 1) & 1];
                    a.n = n;
                    a.level = level;
+                   a.cmask = cmask;
+                   a.pad_ = 0;
                    return a;
                  },
-                 st);
+                 st, nullptr, [&] {
+                   if (cmask)
+                     unspread_kernel<<<dp::ceil_div(n, 256), 256, 0, s>>>(
+                         cw, cmask, counts, n);
+                 });
 }
 
 int sssp_dev_impl(const int32_t* rowptr, const int32_t* col,
@@ -1601,6 +1657,9 @@ int bfs_part_level_impl(const int32_t* rowptr, const int32_t* col,
   a.nparts = nparts;
   a.part = part;
   a.level = level;
+  a.cmask = c->counts_spread > 0 ? (unsigned)((1ull << c->counts_spread) - 1)
+                                 : 0u;
+  a.pad_ = 0;
   RunCounters rc;
   DP_CUDA(cudaEventRecord(w->ev0, s));
   if ((r = launch_parent(a, n_local, launchers, c, w, s, &rc))) return r;
@@ -2172,6 +2231,18 @@ int dp_bfs_part_level_peer(const int32_t* d_rowptr_p, const int32_t* d_col_p,
                               stats, d_peer_dist);
   if (stats) stats->ns_host = now_ns() - t0;
   return r;
+}
+
+int dp_unspread_dev(const int32_t* d_work, int32_t b, int32_t n,
+                    int32_t* d_out, void* stream) {
+  if (n < 0 || b < 0 || b > 30 || !d_work || (n > 0 && !d_out))
+    return fail(DP_ERR_INVALID, "bad unspread arguments");
+  if (n == 0) return 0;
+  const unsigned mask = b > 0 ? (unsigned)((1u << b) - 1) : 0u;
+  unspread_kernel<<<dp::ceil_div(n, 256), 256, 0, (cudaStream_t)stream>>>(
+      d_work, mask, d_out, n);
+  DP_CUDA(cudaGetLastError());
+  return 0;
 }
 
 int dp_bfs_part_apply(const int32_t* d_recv, int64_t nrecv, int32_t nparts,

@@ -49,6 +49,9 @@ struct Knobs {
   int group;          // multiblock group size in parent blocks
   int agg_threshold;  // block granularity: direct launches below this
   int serial_warp;    // 1: below-threshold children share the parent warp
+  int agg_cf;         // 1: coarsening applies to the aggregated grid (the
+                      // reference's order "A before C", pipeline.py:60-81:
+                      // logical blocks of the aggregated clone span parents)
 };
 
 template <class App>
@@ -154,41 +157,72 @@ __device__ __forceinline__ int warp_search(const int* __restrict__ scan, int np,
   return lo;
 }
 
-// Aggregated child (`<child>_agg`, aggregate.py:435-495): one physical block
-// = one (parent row, local physical block) pair, found once per block and
-// reused across the coarsening loop.
+// Disaggregation of aggregated block `p`: the row that owns it (warp search,
+// shared with the block) and its Args; returns the block's index within its
+// parent's child grid.  All threads call.
 template <class App>
-__global__ void __launch_bounds__(256, App::kMinBlocks) child_agg_kernel(App app, const typename App::Args* tab,
-                                 const int* scan, int np, int cf,
-                                 DevState* ds, unsigned long long ts) {
-  note_child_start(ds, ts);
-  const long long t0 = ph_now();
+__device__ __forceinline__ long long find_row(const typename App::Args* tab,
+                                              const int* scan, int np, int p,
+                                              typename App::Args& a) {
   __shared__ int s_lo;
   int lo = 0;
   if (threadIdx.x < 32) {
-    lo = warp_search(scan, np, (int)blockIdx.x);
+    lo = warp_search(scan, np, p);
     if (threadIdx.x == 0) s_lo = lo;
   }
   if (blockDim.x > 32) {
     __syncthreads();
     lo = s_lo;
   }
-  const long long lb = (long long)blockIdx.x - __ldcg(scan + lo);
-  typename App::Args a;
-  {
-    // rows are 16-byte multiples: load with 128-bit L2 reads
-    static_assert(sizeof(a) % 16 == 0, "Args rows must be 16-byte multiples");
-    const int4* src = reinterpret_cast<const int4*>(tab + lo);
-    int4* dst = reinterpret_cast<int4*>(&a);
+  // rows are 16-byte multiples: load with 128-bit L2 reads
+  static_assert(sizeof(a) % 16 == 0, "Args rows must be 16-byte multiples");
+  const int4* src = reinterpret_cast<const int4*>(tab + lo);
+  int4* dst = reinterpret_cast<int4*>(&a);
 #pragma unroll
-    for (int i = 0; i < (int)(sizeof(a) / 16); ++i) dst[i] = __ldcg(src + i);
+  for (int i = 0; i < (int)(sizeof(a) / 16); ++i) dst[i] = __ldcg(src + i);
+  return (long long)p - __ldcg(scan + lo);
+}
+
+// Aggregated child (`<child>_agg`, aggregate.py:435-495).
+// agg_total == 0 (canonical order, coarsening before aggregation): one
+// physical block = one (parent row, local physical block) pair, found once
+// per block and reused across that parent's coarsening loop.
+// agg_total > 0 (order "A before C": the coarsening pass rewrote the
+// aggregated clone itself, pipeline.py:60-81): physical block b runs the
+// aggregated logical blocks [b*cf, min(b*cf + cf, agg_total)), each found by
+// its own search, so one physical block may serve several parents.
+template <class App>
+__global__ void __launch_bounds__(256, App::kMinBlocks) child_agg_kernel(App app, const typename App::Args* tab,
+                                 const int* scan, int np, int cf,
+                                 int agg_total, DevState* ds,
+                                 unsigned long long ts) {
+  note_child_start(ds, ts);
+  const long long t0 = ph_now();
+  typename App::Acc acc{};
+  if (agg_total > 0) {
+    const long long l0 = (long long)blockIdx.x * cf;
+    const long long l1 = l0 + cf < agg_total ? l0 + cf : agg_total;
+    for (long long l = l0; l < l1; ++l) {
+      typename App::Args a;
+      const long long lb = find_row<App>(tab, scan, np, (int)l, a);
+      run_logical_blocks(app, a, lb, 1, acc);
+      if (blockDim.x > 32) __syncthreads();  // s_lo is reused
+    }
+    app.flush(acc);
+    return;
   }
+  typename App::Args a;
+  const long long lb = find_row<App>(tab, scan, np, (int)blockIdx.x, a);
   ph_add(ds, kPhDisagg, t0);
   const long long t1 = ph_now();
-  typename App::Acc acc{};
   run_logical_blocks(app, a, lb, cf, acc);
   app.flush(acc);
   ph_add(ds, kPhChild, t1);
+}
+
+// physical blocks of an aggregated launch over `total` aggregated blocks
+__device__ __forceinline__ int agg_grid(const Knobs& k, int total) {
+  return k.agg_cf ? ceil_div(total, k.cf) : total;
 }
 
 // ---------------------------------------------------------------------------
@@ -315,8 +349,11 @@ __global__ void __launch_bounds__(256, App::kMinBlocks)
     const long long t_agg = ph_now();
     long long tl = 0;  // launch time inside the protocol (DP_PROFILE)
     const bool go = cnt > 0 && (k.threshold == 0 || cnt >= k.threshold);
-    // physical (coarsened) child grid of this parent thread
-    const int gd = go ? ceil_div(ceil_div(cnt, k.cb), k.cf) : 0;
+    // physical (coarsened) child grid of this parent thread; under agg_cf
+    // the recorded rows stay uncoarsened and the aggregated grid is
+    // coarsened instead (direct launches are per-parent coarsened always)
+    const int gl = go ? ceil_div(cnt, k.cb) : 0;
+    const int gd = AGG == kAggNone || !k.agg_cf ? ceil_div(gl, k.cf) : gl;
     // The launch / aggregation protocol runs BEFORE the serial arm (the
     // reference places it after the enclosing statement, aggregate.py:
     // 244-249; both orders give the same outputs): children start while the
@@ -346,14 +383,15 @@ __global__ void __launch_bounds__(256, App::kMinBlocks)
         }
         __syncwarp();
         if (lane == __ffs(m) - 1) {
+          const int pg = agg_grid(k, total);
           DP_TIMED_LAUNCH(ds, tl,
-              child_agg_kernel<App><<<total, k.cb, 0,
+              child_agg_kernel<App><<<pg, k.cb, 0,
                                       cudaStreamFireAndForget>>>(
-                  app, t.args + row0, t.scan + row0, __popc(m), k.cf, ds,
-                  globaltimer_ns());
+                  app, t.args + row0, t.scan + row0, __popc(m), k.cf,
+                  k.agg_cf ? total : 0, ds, globaltimer_ns());
               note_launch_error(ds));
           atomicAdd(&ds->launches, 1ull);
-          atomicAdd(&ds->blocks, (unsigned long long)total);
+          atomicAdd(&ds->blocks, (unsigned long long)pg);
         }
       }
     } else {
@@ -367,13 +405,14 @@ __global__ void __launch_bounds__(256, App::kMinBlocks)
       if constexpr (AGG == kAggBlock) {
         if (k.agg_threshold > 0 && s.np < k.agg_threshold) {
           // aggregate.py:376-392: too few participants -> direct launches
-          if (gd > 0) {
+          const int gdd = ceil_div(gl, k.cf);
+          if (gdd > 0) {
             DP_TIMED_LAUNCH(ds, tl,
-                child_kernel<App><<<gd, k.cb, 0, cudaStreamFireAndForget>>>(
+                child_kernel<App><<<gdd, k.cb, 0, cudaStreamFireAndForget>>>(
                     app, a, k.cf, ds, globaltimer_ns());
                 note_launch_error(ds));
           }
-          count_launches_warp(ds, gd > 0, gd);
+          count_launches_warp(ds, gdd > 0, gdd);
         } else if (s.np > 0) {
           const long long row0 = (long long)blockIdx.x * blockDim.x;
           if (gd > 0) {
@@ -383,14 +422,15 @@ __global__ void __launch_bounds__(256, App::kMinBlocks)
           }
           __syncthreads();
           if (threadIdx.x == 0) {
+            const int pg = agg_grid(k, s.total);
             DP_TIMED_LAUNCH(ds, tl,
-                child_agg_kernel<App><<<s.total, k.cb, 0,
+                child_agg_kernel<App><<<pg, k.cb, 0,
                                         cudaStreamFireAndForget>>>(
-                    app, t.args + row0, t.scan + row0, s.np, k.cf, ds,
-                    globaltimer_ns());
+                    app, t.args + row0, t.scan + row0, s.np, k.cf,
+                    k.agg_cf ? s.total : 0, ds, globaltimer_ns());
                 note_launch_error(ds));
             atomicAdd(&ds->launches, 1ull);
-            atomicAdd(&ds->blocks, (unsigned long long)s.total);
+            atomicAdd(&ds->blocks, (unsigned long long)pg);
           }
         }
       } else {
@@ -425,14 +465,15 @@ __global__ void __launch_bounds__(256, App::kMinBlocks)
               const int np = (int)(c >> 32);
               const int total = (int)(c & 0xffffffffull);
               if (np > 0) {
+                const int pg = agg_grid(k, total);
                 DP_TIMED_LAUNCH(ds, tl,
-                    child_agg_kernel<App><<<total, k.cb, 0,
+                    child_agg_kernel<App><<<pg, k.cb, 0,
                                             cudaStreamFireAndForget>>>(
-                        app, t.args + sb, t.scan + sb, np, k.cf, ds,
-                        globaltimer_ns());
+                        app, t.args + sb, t.scan + sb, np, k.cf,
+                        k.agg_cf ? total : 0, ds, globaltimer_ns());
                     note_launch_error(ds));
                 atomicAdd(&ds->launches, 1ull);
-                atomicAdd(&ds->blocks, (unsigned long long)total);
+                atomicAdd(&ds->blocks, (unsigned long long)pg);
               }
             }
           }
@@ -506,7 +547,7 @@ __global__ void __launch_bounds__(256)
         if (np > 0) {
           note_launch_issue(ds);
           child_agg_kernel<App><<<total, k.cb, 0, cudaStreamFireAndForget>>>(
-              app, t.args, t.scan, np, k.cf, ds, globaltimer_ns());
+              app, t.args, t.scan, np, k.cf, 0, ds, globaltimer_ns());
           note_launch_error(ds);
           atomicAdd(&ds->launches, 1ull);
           atomicAdd(&ds->blocks, (unsigned long long)total);

@@ -192,13 +192,23 @@ def bt_device_tessellator(cp_d, max_tess: int, scale: float, cfg,
 # summed at the end.  Levels are synchronous, so dist is bit-identical to the
 # single-GPU run for any P.
 
+def spread_bits() -> int:
+    """log2 of the counts spread block (dp_config.counts_spread): 12 (4096
+    vertices, 16 KiB), or $DYNPAR_SPREAD_BITS for A/B runs."""
+    import os
+    return max(0, min(30, int(os.environ.get("DYNPAR_SPREAD_BITS", "12"))))
+
+
 class BfsPart:
     """One part's device state (tensors on ``device``)."""
 
     def __init__(self, rowptr, col, n_global: int, nparts: int, part: int,
-                 src: int, device, dist=None):
+                 src: int, device, dist=None, spread: bool = False):
         """``dist``: optional [>= n_local] int32 buffer the other parts can
-        address (the fused exchange, bfs_1d_peer); default a private one."""
+        address (the fused exchange, bfs_1d_peer); default a private one.
+        ``spread``: accumulate ``counts`` in the spread layout (2^k slots,
+        dp_config.counts_spread; device ops only), gathered back into vertex
+        order by ``natural_counts``."""
         import torch
         self.nparts, self.part, self.n = nparts, part, n_global
         self.rowptr = torch.as_tensor(rowptr).to(device=device,
@@ -216,7 +226,9 @@ class BfsPart:
         if src % nparts == part:
             self.dist[src // nparts] = 0
         self.peer_ptrs = None  # fused exchange: device int64[nparts]
-        self.counts = torch.zeros(n_global, **i32)
+        self.counts_log2 = spread_bits() if spread else 0
+        blk = 1 << self.counts_log2
+        self.counts = torch.zeros(-(-n_global // blk) * blk, **i32)
         self.sent = torch.zeros((n_global + 31) // 32, **i32)
         # a part sends each remote vertex at most once: bucket q never holds
         # more than the vertices q owns
@@ -238,6 +250,18 @@ class BfsPart:
     def bucket(self, q: int, count: int):
         return self.send_buf[q * self.stride:q * self.stride + count]
 
+    def natural_counts(self, counts):
+        """Summed counts (this part's layout) in vertex order."""
+        if not self.counts_log2:
+            return counts
+        import torch
+        from . import _lib
+        out = torch.empty(self.n, dtype=torch.int32, device=counts.device)
+        _lib.check(_lib.device().dp_unspread_dev(
+            counts.data_ptr(), self.counts_log2, self.n, out.data_ptr(),
+            None))
+        return out
+
 
 class DeviceBfsOps:
     """The per-part steps on the local GPU through the C-ABI."""
@@ -248,6 +272,11 @@ class DeviceBfsOps:
         self.stream = stream
         self.lib = _lib.device()
 
+    def _cfg(self, p: BfsPart):
+        c = type(self.cfg).from_buffer_copy(self.cfg)
+        c.counts_spread = p.counts_log2
+        return c
+
     def level(self, p: BfsPart, level: int) -> None:
         from . import _lib
         p.send_counts.zero_()
@@ -255,7 +284,7 @@ class DeviceBfsOps:
         st = _lib.DpStats()
         _lib.check(self.lib.dp_bfs_part_level(
             p.rowptr.data_ptr(), p.col.data_ptr(), p.n_local, p.nparts,
-            p.part, level, ctypes.byref(self.cfg), p.dist.data_ptr(),
+            p.part, level, ctypes.byref(self._cfg(p)), p.dist.data_ptr(),
             p.counts.data_ptr(), p.sent.data_ptr(), p.send_buf.data_ptr(),
             p.stride, p.send_counts.data_ptr(), p.changed.data_ptr(),
             self.stream, ctypes.byref(st)))
@@ -275,7 +304,7 @@ class DeviceBfsOps:
         st = _lib.DpStats()
         _lib.check(self.lib.dp_bfs_part_level_peer(
             p.rowptr.data_ptr(), p.col.data_ptr(), p.n_local, p.nparts,
-            p.part, level, ctypes.byref(self.cfg), p.dist.data_ptr(),
+            p.part, level, ctypes.byref(self._cfg(p)), p.dist.data_ptr(),
             p.peer_ptrs.data_ptr(), p.counts.data_ptr(), p.sent.data_ptr(),
             p.changed.data_ptr(), self.stream, ctypes.byref(st)))
         p.stats.append(_lib.stats_dict(st))
@@ -379,7 +408,8 @@ def bfs_1d(parts: list, ops, exchange, max_levels: int | None = None):
         for p, r in zip(parts, recv):
             ops.apply(p, r, level)
         if not exchange.any_changed(parts):
-            return exchange.dist(parts), exchange.counts(parts), level + 1
+            return (exchange.dist(parts),
+                    parts[0].natural_counts(exchange.counts(parts)), level + 1)
     raise RuntimeError("bfs used more levels than vertices")
 
 
@@ -718,5 +748,6 @@ def bfs_1d_peer(parts: list, ops, exchange, max_levels: int | None = None):
         for p in parts:
             ops.level_peer(p, level)
         if not exchange.any_changed(parts):
-            return exchange.dist(parts), exchange.counts(parts), level + 1
+            return (exchange.dist(parts),
+                    parts[0].natural_counts(exchange.counts(parts)), level + 1)
     raise RuntimeError("bfs used more levels than vertices")

@@ -39,10 +39,64 @@ def test_library_exports_every_declared_symbol():
     assert lib.dp_abi_version() == 1
 
 
-def test_struct_layouts_match_header():
-    # dp_config: 16 int32; dp_stats: 7 u64 + 4 f64 + 5 f64 + 3 u64
-    assert ctypes.sizeof(_lib.DpConfig) == 64
-    assert ctypes.sizeof(_lib.DpStats) == 7 * 8 + 4 * 8 + 5 * 8 + 3 * 8 + 8
+_C_TYPES = {"int32_t": ctypes.c_int32, "uint32_t": ctypes.c_uint32,
+            "int64_t": ctypes.c_int64, "uint64_t": ctypes.c_uint64,
+            "double": ctypes.c_double, "float": ctypes.c_float}
+
+
+def header_struct(name: str) -> list[tuple[str, object]]:
+    """(field, ctypes type) list of `typedef struct name {...} name;` parsed
+    from include/dynpar.h (comments stripped; arrays as ctypes arrays)."""
+    text = (ROOT / "include" / "dynpar.h").read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    body = re.search(r"typedef struct %s \{(.*?)\} %s;" % (name, name), text,
+                     re.S).group(1)
+    fields = []
+    for decl in body.split(";"):
+        decl = " ".join(decl.split())
+        if not decl:
+            continue
+        m = re.fullmatch(r"(\w+) (\w+)(?:\[(\d+)\])?", decl)
+        assert m, decl
+        t = _C_TYPES[m.group(1)]
+        fields.append((m.group(2), t * int(m.group(3)) if m.group(3) else t))
+    return fields
+
+
+def same_layout(struct, fields) -> bool:
+    got = [(n, t) for n, t in struct._fields_]
+    if [n for n, _ in got] != [n for n, _ in fields]:
+        return False
+    for (_, a), (_, b) in zip(got, fields):
+        if ctypes.sizeof(a) != ctypes.sizeof(b) or \
+                getattr(a, "_type_", a) != getattr(b, "_type_", b):
+            return False
+    return True
+
+
+@pytest.mark.parametrize("name,binding", [("dp_config", "DpConfig"),
+                                          ("dp_stats", "DpStats")])
+def test_struct_layouts_match_header(name, binding):
+    fields = header_struct(name)
+    struct = getattr(_lib, binding)
+    assert same_layout(struct, fields), (name, struct._fields_, fields)
+    # the size the library clears / writes
+    class H(ctypes.Structure):
+        _fields_ = fields
+    assert ctypes.sizeof(struct) == ctypes.sizeof(H)
+
+
+def test_integration_binding_matches_header():
+    """The structs INTEGRATION.md tells a maintainer to paste are the
+    header's (a short dp_stats would let the library write past it)."""
+    doc = (ROOT / "INTEGRATION.md").read_text()
+    blocks = re.findall(r"```python\n(.*?)```", doc, re.S)
+    abi = [b for b in blocks if "class dp_stats" in b]
+    assert len(abi) == 1
+    ns: dict = {}
+    exec(abi[0], ns)  # noqa: S102 - the documented snippet itself
+    for name in ("dp_config", "dp_stats"):
+        assert same_layout(ns[name], header_struct(name)), name
 
 
 def test_no_device_fails_loudly_without_gpu():
@@ -191,3 +245,37 @@ def test_profiled_build_target_exists():
     mk = (Path(__file__).resolve().parents[1] / "paper_2201_02789_b200" /
           "csrc" / "Makefile").read_text()
     assert "libdynpar_prof.so" in mk and "-DDP_PROFILE=1" in mk
+
+
+def _order_rows():
+    import json
+    return json.loads((ROOT / "tests" / "golden" /
+                       "order_counters.json").read_text())
+
+
+def test_order_effect_matches_reference_manifest():
+    """BenchConfig.order reproduces what the reference's transform(order=)
+    did (pipeline.py:45-81), pass by pass, on every golden row: which
+    threshold pass transformed or was skipped, and whether coarsening hit
+    the child, the aggregated clone, or nothing."""
+    rows = _order_rows()
+    assert len(rows) == 320
+    for row in rows:
+        cfg = BenchConfig(order=row["order"], **row["config"])
+        c = cfg.to_c()
+        man = row["manifest"]
+        t_done = any("pass=threshold action=transformed" in e for e in man)
+        coarse = [e.split()[0] for e in man
+                  if "pass=coarsen action=transformed" in e]
+        assert (c.threshold > 0) == t_done, (row["order"], row["config"], man)
+        if not coarse:
+            assert c.cfactor == 1 and c.agg_coarsen == 0, (row, c.cfactor)
+        else:
+            assert c.cfactor == row["config"]["cfactor"]
+            assert bool(c.agg_coarsen) == coarse[0].endswith("_agg"), row
+
+
+def test_order_rejects_unknown_step():
+    # pipeline.py:79 / tests/test_passes.py:672-674
+    with pytest.raises(ValueError, match="unknown pass step"):
+        BenchConfig(threshold=5, order="TXA").to_c()

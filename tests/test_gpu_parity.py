@@ -289,13 +289,14 @@ def test_verify_outputs_detects_corruption():
         verify_outputs(bench, wl, got, ref)
 
 
+@pytest.mark.parametrize("spread", [False, True])
 @pytest.mark.parametrize("P", [1, 2, 4])
 @pytest.mark.parametrize("policy", [
     dict(threshold=128, agg="block"),
     dict(threshold=1024, cfactor=16, agg="multiblock", group_size=1 << 20,
          parent_block=256, child_block=128, serial="warp"),
     dict()])
-def test_bfs_1d_partition_on_device(P, policy):
+def test_bfs_1d_partition_on_device(P, policy, spread):
     """P parts of a cyclic 1D partition run their device steps on one GPU
     (LocalExchange); dist/counts must equal the single-GPU oracle."""
     import torch
@@ -304,7 +305,8 @@ def test_bfs_1d_partition_on_device(P, policy):
     g = graphs.rmat_graph(scale, 1)
     want_d, want_c, want_lv = oracle.bfs(g.rowptr, g.col, nthreads=0)
     parts = [pdist.BfsPart(*pdist.rmat_part(scale, 1, P, p), g.n, P, p, 0,
-                           torch.device("cuda", 0)) for p in range(P)]
+                           torch.device("cuda", 0), spread=spread)
+             for p in range(P)]
     ops = pdist.DeviceBfsOps(BenchConfig(**policy).to_c())
     d, c, levels = pdist.bfs_1d(parts, ops, pdist.LocalExchange())
     np.testing.assert_array_equal(d.cpu().numpy(), want_d)
@@ -748,8 +750,9 @@ def test_sssp_fused_peer_exchange_on_device(P, policy):
     np.testing.assert_array_equal(d2.cpu().numpy(), want)
 
 
+@pytest.mark.parametrize("spread", [False, True])
 @pytest.mark.parametrize("P", [1, 2, 3])
-def test_bfs_fused_peer_exchange_on_device(P):
+def test_bfs_fused_peer_exchange_on_device(P, spread):
     """BFS over the 1D partition with remote discoveries CAS'd straight into
     the owner's dist (pointer table), P parts on one GPU."""
     import torch
@@ -759,7 +762,8 @@ def test_bfs_fused_peer_exchange_on_device(P):
     dev = torch.device("cuda", 0)
     ex = pdist.PeerLocal()
     parts = [pdist.BfsPart(*pdist.rmat_part(16, 1, P, p), g.n, P, p, 0, dev,
-                           dist=ex.alloc(g.n, P, dev)) for p in range(P)]
+                           dist=ex.alloc(g.n, P, dev), spread=spread)
+             for p in range(P)]
     ex.bind(parts)
     for policy in (dict(threshold=128, agg="block"),
                    dict(threshold=1024, cfactor=16, agg="multiblock",
@@ -772,3 +776,58 @@ def test_bfs_fused_peer_exchange_on_device(P):
         np.testing.assert_array_equal(d.cpu().numpy(), want_d)
         np.testing.assert_array_equal(c.cpu().numpy(), want_c)
         assert levels == want_lv
+
+
+# ---------------------------------------------------------------------------
+# pass order (pipeline.py:45-81): every permutation / subset of "TCA" on the
+# golden configurations reproduces the reference's digest and counters,
+# including "A before C" (coarsening of the aggregated grid, logical blocks
+# spanning parents) and a threshold pass skipped after C or A
+# ---------------------------------------------------------------------------
+
+def _order_rows():
+    import json
+    from conftest import GOLDEN
+    return json.loads((GOLDEN / "order_counters.json").read_text())
+
+
+@pytest.mark.parametrize("bench_name,spec", [
+    ("bfs", "powerlaw:2000:seed1"), ("bfs", "road:1000:seed7"),
+    ("manylaunch", "sizes:1024:seed1"), ("sssp", "powerlaw:150:seed3")])
+def test_order_permutations_match_reference(bench_name, spec):
+    rows = [r for r in _order_rows()
+            if r["bench"] == bench_name and r["dataset"] == spec]
+    assert len(rows) == 80
+    bench, wl = load(bench_name, spec)
+    for row in rows:
+        rep, _ = run_config(bench, wl,
+                            BenchConfig(order=row["order"], **row["config"]))
+        key = (row["order"], row["config"])
+        assert rep.memory_digest == row["digest"], key
+        if bench_name == "sssp":
+            continue  # rounds depend on the real schedule
+        assert (rep.num_launches, rep.host_launches, rep.blocks_scheduled) \
+            == (row["num_launches"], row["host_launches"],
+                row["blocks_scheduled"]), key
+
+
+@pytest.mark.parametrize("serial", ["thread", "warp"])
+def test_aggregated_grid_coarsening_rmat(serial):
+    """A-before-C at scale: RMAT-16 BFS / SSSP under block and multiblock
+    aggregation with the aggregated grid coarsened, bit-exact vs oracle."""
+    bfs_b, bfs_wl = _rmat_workload("bfs", 16, 1)
+    sssp_b, sssp_wl = _rmat_workload("sssp", 16, 1)
+    g, w = sssp_wl.payload
+    wd, wc, _ = oracle.bfs(g.rowptr, g.col, nthreads=0)
+    sd, _ = oracle.sssp(g.rowptr, g.col, w, nthreads=0)
+    for agg, gs in (("block", 4), ("multiblock", 4), ("multiblock", 1 << 20),
+                    ("warp", 4)):
+        cfg = BenchConfig(threshold=64, cfactor=4, agg=agg, group_size=gs,
+                          order="TAC", parent_block=128, child_block=128,
+                          serial=serial)
+        assert cfg.to_c().agg_coarsen == 1
+        rep, _ = run_config(bfs_b, bfs_wl, cfg)
+        assert np.array_equal(rep.arrays["dist"], wd), agg
+        assert np.array_equal(rep.arrays["counts"], wc), agg
+        rep, _ = run_config(sssp_b, sssp_wl, cfg)
+        assert np.array_equal(rep.arrays["dist"], sd), agg
