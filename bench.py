@@ -77,6 +77,22 @@ BEST = {
 }
 
 
+def matched_agg_only(pol: dict, time_ms) -> dict:
+    """The aggregation-only (KLAP-style) build like-for-like with a tuned
+    policy: T = 0, C = 1, the policy's own parent / child blocks and serial
+    mode, each granularity including one-group multiblock; time_ms(policy)
+    returns a device time.  {granularity: ms}."""
+    base = {k: pol[k] for k in ("parent_block", "child_block", "serial")
+            if k in pol}
+    out = {}
+    for a in ("warp", "block", "multiblock", "grid"):
+        p = dict(base, agg=a)
+        if a == "multiblock":
+            p["group_size"] = 1 << 20
+        out[a] = time_ms(p)
+    return out
+
+
 # SSSP with the B200 `frontier` knob (profiles/tune_sssp_frontier_r01.txt)
 FRONTIER_POLICY = dict(threshold=1024, cfactor=8, agg="multiblock",
                        group_size=2048, parent_block=128, child_block=128,
@@ -333,7 +349,13 @@ def extra_workloads(stream, quick: bool) -> dict:
     naive = run_dev("bfs", G, _cfg(dict(parent_block=32)), stream)
     agg_ms = {a: run_dev("bfs", G, _cfg(dict(agg=a)), stream)["ns_device"]
               / 1e6 for a in ("warp", "block", "grid")}
+    matched = matched_agg_only(
+        BEST["bfs"], lambda p: statistics.median(
+            run_dev("bfs", G, _cfg(p), stream)["ns_device"]
+            for _ in range(3)) / 1e6)
     out["bfs_rmat22"] = {"gteps": e_t / ms / 1e6, "ms": ms,
+                         "vs_agg_only_matched": min(matched.values()) / ms,
+                         "agg_only_matched_ms": matched,
                          "levels": runs[0]["iterations"],
                          "launches": runs[0]["num_launches"],
                          "gbps_alg": alg / (ms * 1e6),
@@ -387,7 +409,12 @@ def extra_workloads(stream, quick: bool) -> dict:
         cpu_tri = oracle.tc(wl.buffers["rowptr"], wl.buffers["col"],
                             nthreads=threads)
         dt = time.perf_counter() - t0
+        matched = matched_agg_only(
+            BEST["tc"], lambda p: statistics.median(
+                tc_once(_cfg(p))["ns_device"] for _ in range(2)) / 1e6)
         out["tc_rmat22"].update({
+            "vs_agg_only_matched": min(matched.values()) / ms,
+            "agg_only_matched_ms": matched,
             "vs_naive_cdp": naive_ms / ms,
             "vs_agg_only": min(agg_ms.values()) / ms,
             "parity": "exact vs oracle" if cpu_tri == ntri else "MISMATCH",
@@ -420,6 +447,12 @@ def extra_workloads(stream, quick: bool) -> dict:
     agg_ms = {a: min(run_config(bench, wl, BenchConfig(agg=a))[0].ns_device
                      for _ in range(3)) / 1e6
               for a in ("warp", "block", "grid")}
+    matched = matched_agg_only(
+        BEST["bt"], lambda p: statistics.median(
+            run_config(bench, wl, BenchConfig(**p))[0].ns_device
+            for _ in range(5)) / 1e6)
+    out["bt_25k"]["vs_agg_only_matched"] = min(matched.values()) / ms
+    out["bt_25k"]["agg_only_matched_ms"] = matched
     out["bt_25k"]["vs_naive_cdp"] = naive.ns_device / 1e6 / ms
     out["bt_25k"]["vs_agg_only"] = min(agg_ms.values()) / ms
     if quick:
@@ -800,6 +833,12 @@ def arm_ours(args, world, rank, local):
                             "naive_cdp_launches": naive["num_launches"],
                             **{f"agg_only_{a}": r["ns_device"] / 1e6
                                for a, r in aggonly.items()}}
+    matched = matched_agg_only(
+        BEST["sssp"], lambda p: statistics.median(
+            run_dev("sssp", G, _cfg(p), stream)["ns_device"]
+            for _ in range(3)) / 1e6)
+    line["vs_agg_only_matched"] = min(matched.values()) / ms_step
+    line["baselines_ms"]["agg_only_matched"] = matched
     cpu = cpu_baseline_sssp(G, len(os.sched_getaffinity(0)))
     cpu.pop("dist")
     line["cpu_baseline"] = cpu
@@ -821,6 +860,18 @@ def arm_ours(args, world, rank, local):
         del G
         torch.cuda.empty_cache()
         line["workloads"] = extra_workloads(stream, args.quick)
+        wl = line["workloads"]
+        ratios = {"sssp_rmat22": line["vs_agg_only_matched"],
+                  **{k: wl[k]["vs_agg_only_matched"]
+                     for k in ("bfs_rmat22", "tc_rmat22", "bt_25k")
+                     if "vs_agg_only_matched" in wl.get(k, {})}}
+        line["vs_agg_only_matched_geomean"] = {
+            "value": float(np.exp(np.mean(np.log(list(ratios.values()))))),
+            "over": ratios,
+            "definition": "tuned T+C+A device time vs the best aggregation-"
+                          "only build (T=0, C=1) with the same parent/child "
+                          "blocks, over warp / block / one-group multiblock "
+                          "/ grid"}
     print(json.dumps(line), flush=True)
 
 

@@ -77,6 +77,9 @@ extern "C" {
 #define DP_ERR_INVALID (-4)        /* bad knob / argument (ValueError in Python) */
 #define DP_ERR_NO_DEVICE (-5)      /* no CUDA device visible */
 #define DP_ERR_ITERATIONS (-6)     /* "more levels than vertices", benchmarks.py:168 */
+#define DP_ERR_UNPUBLISHED (-7)    /* "unpublished-read" (publication-checker builds
+                                      only: a child read an aggregation-table row
+                                      its writer never published, sim/machine.py:571) */
 
 typedef struct dp_config {
   int32_t threshold;     /* T: child count >= T launches, else serial; 0 = pass off */
@@ -142,6 +145,10 @@ typedef struct dp_stats {
   uint64_t kernel_launches;   /* launches of library kernels issued from the host */
   double launch_lat_ns_mean;  /* device launch -> first child block start
                                  (%globaltimer), mean over device launches */
+  uint64_t unpublished_reads; /* publication-checker builds: child reads of
+                                 aggregation rows never published (0 otherwise) */
+  uint64_t poisoned_reads;    /* publication-checker builds: child reads of rows
+                                 still holding the pre-launch poison bytes */
 } dp_stats;
 
 /* ---- library -------------------------------------------------------------- */

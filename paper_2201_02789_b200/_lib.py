@@ -26,7 +26,7 @@ INF_THRESHOLD = 2147483647  # passes/common.py:10
 # DP_ERR_* -> SimTrap kinds (sim/machine.py:43-50)
 ERROR_KINDS = {-1: "queue-overflow", -2: "launch-config", -3: "cuda-error",
                -4: "invalid-argument", -5: "no-device",
-               -6: "iteration-limit"}
+               -6: "iteration-limit", -7: "unpublished-read"}
 
 
 class DpConfig(ctypes.Structure):
@@ -62,7 +62,9 @@ class DpStats(ctypes.Structure):
                 ("h2d_bytes", ctypes.c_uint64),
                 ("d2h_bytes", ctypes.c_uint64),
                 ("kernel_launches", ctypes.c_uint64),
-                ("launch_lat_ns_mean", ctypes.c_double)]
+                ("launch_lat_ns_mean", ctypes.c_double),
+                ("unpublished_reads", ctypes.c_uint64),
+                ("poisoned_reads", ctypes.c_uint64)]
 
 
 class DeviceTrap(RuntimeError):

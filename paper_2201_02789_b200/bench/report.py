@@ -63,6 +63,8 @@ class Report:
     d2h_bytes: int = 0
     kernel_launches: int = 0
     launch_lat_ns: float = 0.0  # mean device-launch latency (%globaltimer)
+    unpublished_reads: int = 0  # publication-checker builds only
+    poisoned_reads: int = 0     # publication-checker builds only
     extra: dict = field(default_factory=dict)
     _digest: str | None = field(default=None, repr=False)
     _lists: dict | None = field(default=None, repr=False)
@@ -122,4 +124,6 @@ class Report:
                    d2h_bytes=int(st["d2h_bytes"]),
                    kernel_launches=int(st["kernel_launches"]),
                    launch_lat_ns=float(st.get("launch_lat_ns_mean", 0.0)),
+                   unpublished_reads=int(st.get("unpublished_reads", 0)),
+                   poisoned_reads=int(st.get("poisoned_reads", 0)),
                    extra=dict(extra))

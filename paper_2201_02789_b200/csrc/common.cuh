@@ -151,7 +151,38 @@ struct DevState {
   // the pending-queue length at sim/machine.py:237-244)
   int pending;
   int max_pending;
+  // publication checker (DP_CHECK_PUBLISH builds; zero otherwise): child
+  // reads of aggregation-table rows whose writer never published them, the
+  // hardware stand-in for the reference's "unpublished-read" trap
+  // (sim/machine.py:559-574), and reads of rows still holding the poison
+  // pattern written before the parent grid (stale bytes actually observed)
+  unsigned long long unpublished;
+  unsigned long long poisoned;
 };
+
+// ---------------------------------------------------------------------------
+// Publication checker builds (the reference's fence checker, sim/machine.py:
+// 543-649, and its fence-deletion mutation, tests/test_passes.py:541-554).
+//   DP_CHECK_PUBLISH=1  every aggregation-table row carries a stamp that only
+//                       its publication sets: the multiblock protocol's fence
+//                       (aggregate.py:318-319) for cross-block hand-offs, the
+//                       launch itself for warp/block rows, the parent grid's
+//                       end for grid rows (the cases the reference's checker
+//                       publishes on, machine.py:576-598); rows are poisoned
+//                       (0xff bytes) before every parent grid
+//   DP_NO_FENCE=1       deletes the protocol's fences (the mutation); with
+//                       the checker on, the child's reads are then unpublished
+// ---------------------------------------------------------------------------
+#ifndef DP_CHECK_PUBLISH
+#define DP_CHECK_PUBLISH 0
+#endif
+#ifndef DP_NO_FENCE
+#define DP_NO_FENCE 0
+#endif
+#if DP_CHECK_PUBLISH
+__device__ int* g_pub_stamp;      // one stamp per table row
+__device__ const char* g_pub_tab; // base of the Args table
+#endif
 
 #ifndef DP_PROFILE
 #define DP_PROFILE 0

@@ -77,6 +77,9 @@ struct Workspace {
   // BFS counts in the spread layout (2^k slots)
   void* cwork = nullptr;
   size_t cwork_bytes = 0;
+  // publication-checker builds: one stamp per aggregation-table row
+  void* pub = nullptr;
+  size_t pub_bytes = 0;
 };
 
 Workspace g_ws[64];
@@ -371,6 +374,7 @@ void launch_parent_inst(const App& app, int grid, int pb, const Knobs& k,
     prefer_l1(parent_kernel<App, AGG, CDP>);
     prefer_l1(child_kernel<App>);
     prefer_l1(child_agg_kernel<App>);
+    prefer_l1(child_agg_lb_kernel<App>);
     return true;
   }();
   (void)once;
@@ -439,6 +443,34 @@ int prepare_tables(const dp_config* c, int grid, int pb, Workspace* w,
   return 0;
 }
 
+#if DP_CHECK_PUBLISH
+// Checker builds, before every parent grid: stamps cleared, rows poisoned
+// with 0xff bytes, the device-side table base set (common.cuh).
+int arm_checker(Workspace* w, size_t rows, size_t row_bytes, cudaStream_t s) {
+  int r;
+  if ((r = grow(&w->pub, &w->pub_bytes, rows * sizeof(int)))) return r;
+  DP_CUDA(cudaMemsetAsync(w->pub, 0, rows * sizeof(int), s));
+  DP_CUDA(cudaMemsetAsync(w->tab, 0xff, rows * row_bytes, s));
+  const int* stamp = (const int*)w->pub;
+  const char* tab = (const char*)w->tab;
+  DP_CUDA(cudaMemcpyToSymbolAsync(g_pub_stamp, &stamp, sizeof(stamp), 0,
+                                  cudaMemcpyHostToDevice, s));
+  DP_CUDA(cudaMemcpyToSymbolAsync(g_pub_tab, &tab, sizeof(tab), 0,
+                                  cudaMemcpyHostToDevice, s));
+  return 0;
+}
+
+// $DYNPAR_CHECK_TRAP=0: count unpublished reads without trapping (the
+// reference's checked=False run of the mutated program)
+bool checker_traps() {
+  static const bool on = [] {
+    const char* e = std::getenv("DYNPAR_CHECK_TRAP");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+#endif
+
 // One host launch of the parent grid over parents [base, base + nparents)
 // (+ the grid-granularity glue).
 template <class App>
@@ -454,6 +486,13 @@ int launch_wave(const App& app, long long base, long long nparents,
   AggTables<App> t{nullptr, nullptr, nullptr, nullptr};
   const bool cdp = c->variant == DP_VARIANT_CDP;
   if (int r = prepare_tables(c, grid, pb, w, s, &t)) return r;
+#if DP_CHECK_PUBLISH
+  if (t.args) {
+    if (int r = arm_checker(w, (size_t)grid * pb, sizeof(typename App::Args),
+                            s))
+      return r;
+  }
+#endif
   const Knobs k = knobs_of(c);
   const bool single_group =
       c->agg == DP_AGG_GRID ||
@@ -593,6 +632,21 @@ int begin_run(Workspace* w, cudaStream_t s) {
   return 0;
 }
 
+// publication checker: an unpublished read traps like the reference's
+// checked machine (sim/machine.py:559-574); always 0 in default builds
+int check_published(Workspace* w) {
+#if DP_CHECK_PUBLISH
+  if (w->h_ds->unpublished && checker_traps())
+    return fail(DP_ERR_UNPUBLISHED,
+                "unpublished-read: " + std::to_string(w->h_ds->unpublished) +
+                    " aggregated child block(s) read a table row written by "
+                    "another block without an intervening fence");
+#else
+  (void)w;
+#endif
+  return 0;
+}
+
 __global__ void signal_kernel(const DevState* ds, Workspace::Signal* sig,
                               unsigned seq) {
   sig->ds = *ds;
@@ -623,7 +677,7 @@ int read_state_fast(Workspace* w, cudaStream_t s) {
   }
   std::memcpy((void*)w->h_ds, (const void*)&w->h_sig->ds, sizeof(DevState));
   if (w->h_ds->err) return map_device_error(w->h_ds->err);
-  return 0;
+  return check_published(w);
 }
 
 int read_state(Workspace* w, cudaStream_t s) {
@@ -631,7 +685,7 @@ int read_state(Workspace* w, cudaStream_t s) {
                           cudaMemcpyDeviceToHost, s));
   DP_CUDA(cudaStreamSynchronize(s));
   if (w->h_ds->err) return map_device_error(w->h_ds->err);
-  return 0;
+  return check_published(w);
 }
 
 void finish_stats(Workspace* w, const RunCounters& rc, float ms,
@@ -648,6 +702,8 @@ void finish_stats(Workspace* w, const RunCounters& rc, float ms,
   st->launch_lat_ns_mean =
       w->h_ds->lat_cnt ? (double)w->h_ds->lat_sum / (double)w->h_ds->lat_cnt
                        : 0.0;
+  st->unpublished_reads = w->h_ds->unpublished;
+  st->poisoned_reads = w->h_ds->poisoned;
   // DP_PROFILE builds: summed warp-cycles per phase -> warp-ns at the SM
   // clock rate the device reports (zero, and no query, in the default build)
   bool any = false;

@@ -160,10 +160,67 @@ __device__ __forceinline__ int warp_search(const int* __restrict__ scan, int np,
 // Disaggregation of aggregated block `p`: the row that owns it (warp search,
 // shared with the block) and its Args; returns the block's index within its
 // parent's child grid.  All threads call.
+// ---------------------------------------------------------------------------
+// Publication of aggregation-table rows (common.cuh, DP_CHECK_PUBLISH).
+// pub_mark: the row is published by the launch that follows (warp / block
+// rows, the launching thread's barrier) or by the parent grid's end (grid
+// rows, launched by the host glue).  pub_fence: the multiblock protocol's
+// fence (aggregate.py:318-319), which publishes the rows this thread wrote
+// before the group's done counter moves; DP_NO_FENCE deletes it and with it
+// the publication.  Default builds: pub_mark is empty, pub_fence a fence.
+// ---------------------------------------------------------------------------
+template <class Args>
+__device__ __forceinline__ void pub_mark(const Args* row) {
+#if DP_CHECK_PUBLISH
+  g_pub_stamp[((const char*)row - g_pub_tab) / (long long)sizeof(Args)] = 1;
+#else
+  (void)row;
+#endif
+}
+template <class Args>
+__device__ __forceinline__ void pub_fence(const Args* row) {
+#if !DP_NO_FENCE
+  pub_mark(row);  // stamp first: the fence orders it with the row
+  __threadfence();
+#else
+  (void)row;
+#endif
+}
+// acquire side of the hand-off: the group's last block, before it reads the
+// counter and launches (also deleted by the mutation)
+__device__ __forceinline__ void protocol_fence() {
+#if !DP_NO_FENCE
+  __threadfence();
+#endif
+}
+
+// child side: was the row published, and does it still hold the poison?
+template <class Args>
+__device__ __forceinline__ void check_row(const Args* row, const Args& a,
+                                          DevState* ds) {
+#if DP_CHECK_PUBLISH
+  if (threadIdx.x == 0) {
+    const long long i =
+        ((const char*)row - g_pub_tab) / (long long)sizeof(Args);
+    if (__ldcg(g_pub_stamp + i) != 1) atomicAdd(&ds->unpublished, 1ull);
+    const int* w = reinterpret_cast<const int*>(&a);
+    bool poison = true;
+#pragma unroll
+    for (int j = 0; j < (int)(sizeof(Args) / 4); ++j) poison &= w[j] == -1;
+    if (poison) atomicAdd(&ds->poisoned, 1ull);
+  }
+#else
+  (void)row;
+  (void)a;
+  (void)ds;
+#endif
+}
+
 template <class App>
 __device__ __forceinline__ long long find_row(const typename App::Args* tab,
                                               const int* scan, int np, int p,
-                                              typename App::Args& a) {
+                                              typename App::Args& a,
+                                              DevState* ds) {
   __shared__ int s_lo;
   int lo = 0;
   if (threadIdx.x < 32) {
@@ -180,44 +237,68 @@ __device__ __forceinline__ long long find_row(const typename App::Args* tab,
   int4* dst = reinterpret_cast<int4*>(&a);
 #pragma unroll
   for (int i = 0; i < (int)(sizeof(a) / 16); ++i) dst[i] = __ldcg(src + i);
+  check_row(tab + lo, a, ds);
   return (long long)p - __ldcg(scan + lo);
 }
 
-// Aggregated child (`<child>_agg`, aggregate.py:435-495).
-// agg_total == 0 (canonical order, coarsening before aggregation): one
-// physical block = one (parent row, local physical block) pair, found once
-// per block and reused across that parent's coarsening loop.
-// agg_total > 0 (order "A before C": the coarsening pass rewrote the
-// aggregated clone itself, pipeline.py:60-81): physical block b runs the
-// aggregated logical blocks [b*cf, min(b*cf + cf, agg_total)), each found by
-// its own search, so one physical block may serve several parents.
+// Aggregated child (`<child>_agg`, aggregate.py:435-495), canonical order
+// (coarsening before aggregation): one physical block = one (parent row,
+// local physical block) pair, found once per block and reused across that
+// parent's coarsening loop.
 template <class App>
 __global__ void __launch_bounds__(256, App::kMinBlocks) child_agg_kernel(App app, const typename App::Args* tab,
                                  const int* scan, int np, int cf,
                                  int agg_total, DevState* ds,
                                  unsigned long long ts) {
+  (void)agg_total;
   note_child_start(ds, ts);
   const long long t0 = ph_now();
   typename App::Acc acc{};
-  if (agg_total > 0) {
-    const long long l0 = (long long)blockIdx.x * cf;
-    const long long l1 = l0 + cf < agg_total ? l0 + cf : agg_total;
-    for (long long l = l0; l < l1; ++l) {
-      typename App::Args a;
-      const long long lb = find_row<App>(tab, scan, np, (int)l, a);
-      run_logical_blocks(app, a, lb, 1, acc);
-      if (blockDim.x > 32) __syncthreads();  // s_lo is reused
-    }
-    app.flush(acc);
-    return;
-  }
   typename App::Args a;
-  const long long lb = find_row<App>(tab, scan, np, (int)blockIdx.x, a);
+  const long long lb = find_row<App>(tab, scan, np, (int)blockIdx.x, a, ds);
   ph_add(ds, kPhDisagg, t0);
   const long long t1 = ph_now();
   run_logical_blocks(app, a, lb, cf, acc);
   app.flush(acc);
   ph_add(ds, kPhChild, t1);
+}
+
+// Order "A before C" (the coarsening pass rewrote the aggregated clone
+// itself, pipeline.py:60-81): physical block b runs the aggregated logical
+// blocks [b*cf, min(b*cf + cf, agg_total)), each found by its own search, so
+// one physical block may serve several parents.  A kernel of its own: a
+// second inlined copy of the item code in child_agg_kernel cost TcApp's
+// block-mode child 18 registers (32 -> 50) and TC 46 % of its time.
+template <class App>
+__global__ void __launch_bounds__(256, App::kMinBlocks) child_agg_lb_kernel(App app, const typename App::Args* tab,
+                                    const int* scan, int np, int cf,
+                                    int agg_total, DevState* ds,
+                                    unsigned long long ts) {
+  note_child_start(ds, ts);
+  typename App::Acc acc{};
+  const long long l0 = (long long)blockIdx.x * cf;
+  const long long l1 = l0 + cf < agg_total ? l0 + cf : agg_total;
+  for (long long l = l0; l < l1; ++l) {
+    typename App::Args a;
+    const long long lb = find_row<App>(tab, scan, np, (int)l, a, ds);
+    run_logical_blocks(app, a, lb, 1, acc);
+    if (blockDim.x > 32) __syncthreads();  // s_lo is reused
+  }
+  app.flush(acc);
+}
+
+// device launch of an aggregated child grid (fire-and-forget)
+template <class App>
+__device__ __forceinline__ void launch_agg(const App& app, int pg, int cb,
+                                           const typename App::Args* tab,
+                                           const int* scan, int np, int cf,
+                                           int agg_total, DevState* ds) {
+  if (agg_total > 0)
+    child_agg_lb_kernel<App><<<pg, cb, 0, cudaStreamFireAndForget>>>(
+        app, tab, scan, np, cf, agg_total, ds, globaltimer_ns());
+  else
+    child_agg_kernel<App><<<pg, cb, 0, cudaStreamFireAndForget>>>(
+        app, tab, scan, np, cf, 0, ds, globaltimer_ns());
 }
 
 // physical blocks of an aggregated launch over `total` aggregated blocks
@@ -379,16 +460,15 @@ __global__ void __launch_bounds__(256, App::kMinBlocks)
           const int rank = __popc(m & lanemask_lt());
           t.args[row0 + rank] = a;
           t.scan[row0 + rank] = incl - gd;
+          pub_mark(t.args + row0 + rank);
           __threadfence();
         }
         __syncwarp();
         if (lane == __ffs(m) - 1) {
           const int pg = agg_grid(k, total);
           DP_TIMED_LAUNCH(ds, tl,
-              child_agg_kernel<App><<<pg, k.cb, 0,
-                                      cudaStreamFireAndForget>>>(
-                  app, t.args + row0, t.scan + row0, __popc(m), k.cf,
-                  k.agg_cf ? total : 0, ds, globaltimer_ns());
+              launch_agg(app, pg, k.cb, t.args + row0, t.scan + row0,
+                         __popc(m), k.cf, k.agg_cf ? total : 0, ds);
               note_launch_error(ds));
           atomicAdd(&ds->launches, 1ull);
           atomicAdd(&ds->blocks, (unsigned long long)pg);
@@ -418,16 +498,15 @@ __global__ void __launch_bounds__(256, App::kMinBlocks)
           if (gd > 0) {
             t.args[row0 + s.rank] = a;
             t.scan[row0 + s.rank] = s.excl;
+            pub_mark(t.args + row0 + s.rank);
             __threadfence();
           }
           __syncthreads();
           if (threadIdx.x == 0) {
             const int pg = agg_grid(k, s.total);
             DP_TIMED_LAUNCH(ds, tl,
-                child_agg_kernel<App><<<pg, k.cb, 0,
-                                        cudaStreamFireAndForget>>>(
-                    app, t.args + row0, t.scan + row0, s.np, k.cf,
-                    k.agg_cf ? s.total : 0, ds, globaltimer_ns());
+                launch_agg(app, pg, k.cb, t.args + row0, t.scan + row0,
+                           s.np, k.cf, k.agg_cf ? s.total : 0, ds);
                 note_launch_error(ds));
             atomicAdd(&ds->launches, 1ull);
             atomicAdd(&ds->blocks, (unsigned long long)pg);
@@ -448,7 +527,10 @@ __global__ void __launch_bounds__(256, App::kMinBlocks)
             const long long row = sb + (long long)(old >> 32) + s.rank;
             t.args[row] = a;
             t.scan[row] = (int)(old & 0xffffffffull) + s.excl;
-            __threadfence();  // publish before the done counter (:318-319)
+            if constexpr (AGG == kAggMulti)
+              pub_fence(t.args + row);  // publish before the done counter
+            else
+              pub_mark(t.args + row);  // grid: the parent grid's end publishes
           }
           if constexpr (AGG == kAggMulti) __syncthreads();
         }
@@ -457,7 +539,7 @@ __global__ void __launch_bounds__(256, App::kMinBlocks)
             const int nblk = min(k.group, (int)gridDim.x - grp * k.group);
             const int d = atomicAdd(&t.done[grp], 1);
             if (d == nblk - 1) {
-              __threadfence();
+              protocol_fence();
               const unsigned long long c =
                   atomicAdd(&t.ctr[grp], 0ull);  // L2-coherent read
               t.ctr[grp] = 0;                     // re-arm for the next launch
@@ -467,10 +549,8 @@ __global__ void __launch_bounds__(256, App::kMinBlocks)
               if (np > 0) {
                 const int pg = agg_grid(k, total);
                 DP_TIMED_LAUNCH(ds, tl,
-                    child_agg_kernel<App><<<pg, k.cb, 0,
-                                            cudaStreamFireAndForget>>>(
-                        app, t.args + sb, t.scan + sb, np, k.cf,
-                        k.agg_cf ? total : 0, ds, globaltimer_ns());
+                    launch_agg(app, pg, k.cb, t.args + sb, t.scan + sb, np,
+                               k.cf, k.agg_cf ? total : 0, ds);
                     note_launch_error(ds));
                 atomicAdd(&ds->launches, 1ull);
                 atomicAdd(&ds->blocks, (unsigned long long)pg);
@@ -530,7 +610,10 @@ __global__ void __launch_bounds__(256)
       const long long row = (long long)(old >> 32) + s.rank;
       t.args[row] = a;
       t.scan[row] = (int)(old & 0xffffffffull) + s.excl;
-      __threadfence();
+      if constexpr (AGG == kAggMulti)
+        pub_fence(t.args + row);
+      else
+        pub_mark(t.args + row);
     }
     __syncthreads();  // s_old is rewritten by the next chunk
   }
@@ -538,7 +621,7 @@ __global__ void __launch_bounds__(256)
     if (threadIdx.x == 0) {
       const int d = atomicAdd(&t.done[0], 1);
       if (d == (int)gridDim.x - 1) {
-        __threadfence();
+        protocol_fence();
         const unsigned long long c = atomicAdd(&t.ctr[0], 0ull);
         t.ctr[0] = 0;
         t.done[0] = 0;
