@@ -589,8 +589,7 @@ def exchange_self_check(kind: str, exchange: str, world: int, rank: int,
                 part = pdist.SsspPeerPart(rp_p, col_p, w_p, n, world, rank, 0,
                                           buf, dev)
                 ex.bind([part])
-                got, _ = pdist.sssp_1d_peer([part],
-                                            pdist.DeviceSsspPeerOps(cfg), ex)
+                got, _ = pdist.sssp_1d_peer_solve([part], cfg, ex)
             else:
                 part = pdist.SsspPart(rp_p, col_p, w_p, n, world, rank, 0,
                                       dev)
@@ -609,7 +608,8 @@ def exchange_self_check(kind: str, exchange: str, world: int, rank: int,
                 part = pdist.BfsPart(rp_p, col_p, n, world, rank, 0, dev,
                                      dist=buf, spread=True)
                 ex.bind([part])
-                got_d, got_c, _ = pdist.bfs_1d_peer([part], ops, ex)
+                got_d, got_c, _ = pdist.bfs_1d_peer_solve(
+                    [part], _cfg(BEST["bfs"]), ex)
             else:
                 part = pdist.BfsPart(rp_p, col_p, n, world, rank, 0, dev,
                                      spread=True)
@@ -676,8 +676,9 @@ def arm_sssp_partitioned(args, world, rank, local):
             part = pdist.SsspPeerPart(rp_p, col_p, w_p, g.n, world, rank, 0,
                                       buf, dev)
             ex.bind([part])
-            ops = pdist.DeviceSsspPeerOps(_cfg(BEST["sssp"]))
-            run_rounds = pdist.sssp_1d_peer
+            ops = _cfg(BEST["sssp"])
+            # rounds looped in the library, flags OR-ed on the device
+            run_rounds = pdist.sssp_1d_peer_solve
         except Exception as e:  # noqa: BLE001 - fall back to the NCCL a2a
             print(f"[bench] symmetric memory unavailable ({e}); using the "
                   f"all-to-all exchange", file=sys.stderr)
@@ -691,12 +692,27 @@ def arm_sssp_partitioned(args, world, rank, local):
     stream_obj = torch.cuda.current_stream()
 
     def step():
-        part.reset(0)
-        return run_rounds([part], ops, ex)
+        # peer: the solve initialises its own state, and each rank keeps its
+        # owned distances (gathered once after the timed region)
+        if exchange != "peer":
+            part.reset(0)
+            return run_rounds([part], ops, ex)
+        return run_rounds([part], ops, ex, gather=False)
     with ClockSampler(local) as clk:
         total_ms, outs = timed_steps(step, args.steps, args.warmup,
                                      stream_obj)
     dist_t, rounds = outs[-1]
+    if dist_t is None:
+        dist_t = ex.dist([part])
+    # peer: one stats entry per solve (= step); a2a: one per round of the
+    # last step (reset() clears them)
+    launches_timed = int(sum(s["kernel_launches"] + s["num_launches"]
+                             for s in part.stats[-args.steps:])) \
+        if exchange == "peer" else \
+        int(sum(s["kernel_launches"] + s["num_launches"]
+                for s in part.stats)) * args.steps
+    remote_per_round = statistics.mean(
+        s["remote_ops"] / max(s["iterations"], 1) for s in part.stats[-3:])
     t_max = max_over_ranks(total_ms)
     ms_step = t_max / args.steps
     dist_h = dist_t.cpu().numpy()
@@ -714,14 +730,19 @@ def arm_sssp_partitioned(args, world, rank, local):
         part.rowptr.copy_(hp[0], non_blocking=True)
         part.col.copy_(hp[1], non_blocking=True)
         part.weight.copy_(hp[2], non_blocking=True)
-        part.reset(0)
-        run_rounds([part], ops, ex)
+        if exchange != "peer":
+            part.reset(0)
+            run_rounds([part], ops, ex)
+        else:
+            run_rounds([part], ops, ex, gather=False)
         out_h.copy_(part.dist, non_blocking=True)
         torch.cuda.synchronize()
         if i:
             e2e.append(time.perf_counter() - t0)
     e2e_s = max_over_ranks(statistics.median(e2e))
     h2d = sum(x.numel() * 4 for x in hp)
+    subs = None if args.quick else partitioned_workloads(args, world, rank,
+                                                         local)
     if rank != 0:
         return
     from oracle import oracle
@@ -740,10 +761,14 @@ def arm_sssp_partitioned(args, world, rank, local):
                    "policy": BEST["sssp"],
                    "parallelism": f"1d-cyclic-partition x{world}",
                    "exchange": ("fused: remote atomicMin into the owner's "
-                                "dist via symmetric memory + NCCL max of the "
-                                "round flag" if exchange == "peer" else
+                                "dist via symmetric memory; round flags "
+                                "OR-ed on the device through symmetric-memory "
+                                "signal slots, rounds looped in the library "
+                                "(dp_sssp_part_solve_peer)"
+                                if exchange == "peer" else
                                 "NCCL all-to-all of (v, alt) pairs + apply"),
                    "exchange_check": check,
+                   "remote_atomics_per_round_rank0": remote_per_round,
                    "l2": "inputs exceed L2; no flush"},
         "parity": "bit-exact vs oracle" if np.array_equal(dist_h, want)
         else "MISMATCH",
@@ -751,9 +776,9 @@ def arm_sssp_partitioned(args, world, rank, local):
                 "h2d_bytes_per_step": h2d * world,
                 "d2h_bytes_per_step": g.n * 4,
                 "ms_per_step": e2e_s * 1e3},
-        "gpu_launches": int(sum(s["kernel_launches"] + s["num_launches"]
-                                for s in part.stats)) * args.steps,
-        "clocks": clk.summary()}), flush=True)
+        "gpu_launches": launches_timed,
+        "clocks": clk.summary(),
+        "partitioned_workloads": subs}), flush=True)
 
 
 def arm_ours(args, world, rank, local):
@@ -860,6 +885,9 @@ def arm_ours(args, world, rank, local):
         del G
         torch.cuda.empty_cache()
         line["workloads"] = extra_workloads(stream, args.quick)
+        torch.cuda.empty_cache()
+        line["partitioned_workloads"] = partitioned_workloads(args, 1, 0,
+                                                              local)
         wl = line["workloads"]
         ratios = {"sssp_rmat22": line["vs_agg_only_matched"],
                   **{k: wl[k]["vs_agg_only_matched"]
@@ -877,8 +905,19 @@ def arm_ours(args, world, rank, local):
 
 def arm_bfs26(args, world, rank, local):
     """BASELINE config 5: BFS on RMAT-26 over a cyclic 1D vertex partition
-    (one part per rank), per-level all-to-all frontier exchange over NCCL.
-    One step = one full BFS from vertex 0.  GTEPS = examined edges / t."""
+    (one part per rank).  One step = one full BFS from vertex 0.  GTEPS =
+    examined edges / t."""
+    line = measure_bfs26(args, world, rank, local, parity=True)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def measure_bfs26(args, world, rank, local, parity: bool = True,
+                  steps: int = 0):
+    """The config-5 measurement (rank 0 gets the line, others None).
+    parity: check dist / counts / levels against the oracle on the host
+    (RMAT-26: ~25 s of OpenMP); the exchange itself is always verified on
+    RMAT-16 first (choose_exchange)."""
     import torch
     from paper_2201_02789_b200 import _lib
     from paper_2201_02789_b200 import dist as pdist
@@ -898,7 +937,7 @@ def arm_bfs26(args, world, rank, local):
             part = pdist.BfsPart(rp, col, 1 << scale, world, rank, 0, dev,
                                  dist=buf, spread=True)
             ex.bind([part])
-            run_levels = pdist.bfs_1d_peer
+            run_levels = pdist.bfs_1d_peer_solve
         except Exception as e:  # noqa: BLE001 - fall back to the NCCL a2a
             print(f"[bench] symmetric memory unavailable ({e}); using the "
                   f"all-to-all exchange", file=sys.stderr)
@@ -910,24 +949,35 @@ def arm_bfs26(args, world, rank, local):
             pdist.LocalExchange()
         run_levels = pdist.bfs_1d
     del rp, col
-    ops = pdist.DeviceBfsOps(_cfg(BEST["bfs"]))
+    ops = _cfg(BEST["bfs"]) if exchange == "peer" else \
+        pdist.DeviceBfsOps(_cfg(BEST["bfs"]))
     stream_obj = torch.cuda.current_stream()
 
     def step():
-        part.reset(0)
-        return run_levels([part], ops, ex)
+        # peer: the solve initialises its own state, and each rank keeps its
+        # part of dist / counts (combined once after the timed region)
+        if exchange != "peer":
+            part.reset(0)
+            return run_levels([part], ops, ex)
+        return run_levels([part], ops, ex, gather=False)
+    steps = steps or args.steps
     with ClockSampler(local) as clk:
-        total_ms, outs = timed_steps(step, args.steps, args.warmup,
-                                     stream_obj)
+        total_ms, outs = timed_steps(step, steps, args.warmup, stream_obj)
     dist_t, counts_t, levels = outs[-1]
+    if dist_t is None:
+        dist_t = ex.dist([part])
+        counts_t = part.natural_counts(ex.counts([part]))
     e_t = int(counts_t.to(torch.int64).sum().item())
     t_max = max_over_ranks(total_ms)
-    ms_step = t_max / args.steps
+    ms_step = t_max / steps
+    remote = statistics.mean(s["remote_ops"] / max(s["iterations"], 1)
+                             for s in part.stats[-steps:]) \
+        if part.stats and "remote_ops" in part.stats[-1] else 0
     if rank != 0:
-        return
+        return None
     line = {"metric": f"GTEPS (BFS RMAT-{scale}, 1D partition, T+C+A CDP2)",
             "value": e_t / (ms_step * 1e-3) / 1e9, "unit": "GTEPS",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "n_gpus": world, "steps": steps, "warmup": args.warmup,
             "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "int32",
             "data": "synthetic RMAT (Graph500, seed 1, edge factor 16)",
@@ -936,12 +986,19 @@ def arm_bfs26(args, world, rank, local):
                        "policy": BEST["bfs"],
                        "parallelism": f"1d-cyclic-partition x{world}",
                        "exchange": ("fused: remote CAS into the owner's dist "
-                                    "via symmetric memory + NCCL max of the "
-                                    "level flag" if exchange == "peer" else
+                                    "via symmetric memory; level flags OR-ed "
+                                    "on the device through symmetric-memory "
+                                    "signal slots (dp_bfs_part_solve_peer)"
+                                    if exchange == "peer" else
                                     "NCCL all-to-all of discovered ids + "
                                     "apply"),
-                       "exchange_check": check},
+                       "exchange_check": check,
+                       "remote_atomics_per_level_rank0": remote},
             "clocks": clk.summary()}
+    if not parity:
+        line["parity"] = ("not checked at this scale here; the exchange "
+                          "passed the RMAT-16 self-check (" + check + ")")
+        return line
     # parity at every scale (RMAT-26: 1.07 G edges through the OpenMP oracle
     # on the host; the oracle's own generator, rows unsorted since BFS
     # outputs do not depend on the row order)
@@ -957,47 +1014,193 @@ def arm_bfs26(args, world, rank, local):
                       and np.array_equal(got_c, wc) and wl == levels
                       else "MISMATCH")
     line["parity_check_s"] = time.perf_counter() - t0
-    print(json.dumps(line), flush=True)
+    return line
 
 
 def arm_tc(args, world, rank, local):
     """BASELINE config 4: triangle counting on RMAT-22, oriented-edge ranges
     balanced by merge work, one all_reduce(sum).  One step = one count."""
+    line = measure_tc(args, world, rank, local)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def tc_graph(scale: int, world: int, rank: int):
+    """The degree-oriented CSR+ of RMAT-`scale` (host orientation, ~10 s at
+    scale 22): built once by rank 0 and shared through /tmp with the other
+    ranks of this job, instead of every rank re-orienting on the same host
+    cores."""
+    import torch
+    from paper_2201_02789_b200.bench import load
+    if world == 1:
+        _, wl = load("tc", f"rmat:{scale}:seed{SEED}")
+        return wl.buffers["rowptr"], wl.buffers["col"], wl.n
+    tag = os.environ.get("MASTER_PORT", "0")
+    path = Path(f"/tmp/dynpar_tc_{scale}_{SEED}_{tag}_{os.getppid()}.npz")
+    if rank == 0:
+        _, wl = load("tc", f"rmat:{scale}:seed{SEED}")
+        np.savez(path, rowptr=wl.buffers["rowptr"], col=wl.buffers["col"])
+    torch.distributed.barrier()
+    z = np.load(path)
+    rp, col = z["rowptr"], z["col"]
+    torch.distributed.barrier()
+    if rank == 0:
+        path.unlink(missing_ok=True)
+    return rp, col, int(rp.shape[0]) - 1
+
+
+def measure_tc(args, world, rank, local, parity: bool = True,
+               steps: int = 0):
     import torch
     from paper_2201_02789_b200 import _lib
     from paper_2201_02789_b200 import dist as pdist
     from paper_2201_02789_b200.bench import load
     _lib.device()
     dev = torch.device("cuda", torch.cuda.current_device())
-    bench, wl = load("tc", f"rmat:{args.scale or SCALE}:seed{SEED}")
-    rp_h, col_h = wl.buffers["rowptr"], wl.buffers["col"]
+    rp_h, col_h, n = tc_graph(args.scale or SCALE, world, rank)
     rp = torch.from_numpy(rp_h).to(dev)
     col = torch.from_numpy(col_h).to(dev)
-    counter = pdist.tc_device_counter(rp, col, wl.n, int(col_h.shape[0]),
+    counter = pdist.tc_device_counter(rp, col, n, int(col_h.shape[0]),
                                       _cfg(BEST["tc"]))
     stream_obj = torch.cuda.current_stream()
     rng = pdist.tc_shard(rp_h, col_h)  # host-side partitioning, untimed
+    steps = steps or args.steps
     with ClockSampler(local) as clk:
         total_ms, outs = timed_steps(
             lambda: pdist.tc_count_range(rng, counter, dev),
-            args.steps, args.warmup, stream_obj)
+            steps, args.warmup, stream_obj)
     tri = outs[-1]
     t_max = max_over_ranks(total_ms)
-    ms_step = t_max / args.steps
+    ms_step = t_max / steps
     if rank != 0:
-        return
-    print(json.dumps({
-        "metric": "triangles/s (TC RMAT-22, edge-range partition)",
+        return None
+    line = {
+        "metric": f"triangles/s (TC RMAT-{args.scale or SCALE}, edge-range "
+                  f"partition)",
         "value": tri / (ms_step * 1e-3), "unit": "triangles/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "n_gpus": world, "steps": steps, "warmup": args.warmup,
         "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "int32",
         "data": "synthetic RMAT, symmetrised, degree-oriented",
-        "config": {"workload": "tc rmat-22", "triangles": tri,
+        "config": {"workload": f"tc rmat-{args.scale or SCALE}",
+                   "triangles": tri,
                    "oriented_edges": int(col_h.shape[0]),
                    "policy": BEST["tc"],
-                   "parallelism": f"edge-range x{world}"},
-        "clocks": clk.summary()}), flush=True)
+                   "parallelism": f"edge-range x{world}",
+                   "reduce": "one NCCL all_reduce(sum) of the per-rank "
+                             "counts per step (inside the timed region)"},
+        "clocks": clk.summary()}
+    if parity:
+        from oracle import oracle
+        want = oracle.tc(rp_h, col_h, nthreads=len(os.sched_getaffinity(0)))
+        line["parity"] = "exact vs oracle" if want == tri else "MISMATCH"
+    return line
+
+
+def measure_bt(args, world, rank, local, ncurves: int, steps: int = 0):
+    """Bezier tessellation partitioned by curve range (even ranges, one
+    all_reduce(sum) of the vertex counts per step); BT's tuned policy.  The
+    fp64 coordinate checksum and the exact vertex count are compared with
+    the oracle after the timed region."""
+    import torch
+    from paper_2201_02789_b200 import _lib
+    from paper_2201_02789_b200 import dist as pdist
+    from paper_2201_02789_b200.bench.graphs import (BT_CURV_SCALE,
+                                                    BT_MAX_TESS,
+                                                    bezier_curves)
+    lib = _lib.device()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    cp_h = np.ascontiguousarray(bezier_curves(ncurves, 1), dtype=np.float32)
+    lo, hi = pdist.even_ranges(ncurves, world)[rank]
+    k = hi - lo
+    cp = torch.from_numpy(cp_h[lo:hi]).to(dev)
+    cap = k * 128 + (1 << 16)
+    ntess = torch.empty(max(k, 1), dtype=torch.int32, device=dev)
+    offs = torch.empty(max(k, 1), dtype=torch.int64, device=dev)
+    verts = torch.empty((cap, 2), dtype=torch.float32, device=dev)
+    cfg = _cfg(BEST["bt"])
+    stream_obj = torch.cuda.current_stream()
+    used = ctypes.c_int64()
+    nv_t = torch.zeros(1, dtype=torch.int64, device=dev)
+    stats = []
+
+    def step():
+        st = _lib.DpStats()
+        _lib.check(lib.dp_bt_dev(cp.data_ptr(), k, BT_MAX_TESS,
+                                 BT_CURV_SCALE, ctypes.byref(cfg),
+                                 ntess.data_ptr(), offs.data_ptr(),
+                                 verts.data_ptr(), cap, ctypes.byref(used),
+                                 None, ctypes.byref(st)))
+        stats.append(_lib.stats_dict(st))
+        nv_t.fill_(used.value)
+        if torch.distributed.is_initialized():
+            torch.distributed.all_reduce(nv_t)
+        return nv_t
+    steps = steps or args.steps
+    with ClockSampler(local) as clk:
+        total_ms, outs = timed_steps(step, steps, args.warmup, stream_obj)
+    nv = int(outs[-1].item())
+    t_max = max_over_ranks(total_ms)
+    ms_step = t_max / steps
+    cs = float(verts[:used.value].double().sum().item())
+    cs_all = pdist.allreduce_sum_f64([cs], dev)[0] \
+        if torch.distributed.is_initialized() else cs
+    if rank != 0:
+        return None
+    from oracle import oracle
+    want_nt, want_v = oracle.bt(cp_h, BT_MAX_TESS, BT_CURV_SCALE)
+    want_cs = float(np.asarray(want_v, dtype=np.float64).sum())
+    ok = int(want_nt.astype(np.int64).sum()) == nv and \
+        abs(cs_all - want_cs) <= 1e-6 * max(1.0, abs(want_cs))
+    alg = 36 * ncurves + 8 * nv
+    return {
+        "metric": f"curves/s (BT {ncurves} curves, curve-range partition)",
+        "value": ncurves / (ms_step * 1e-3), "unit": "curves/s",
+        "n_gpus": world, "steps": steps, "warmup": args.warmup,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+        "vertices": nv, "gbps_alg": alg / (ms_step * 1e6),
+        "frac_hbm_aggregate": alg / (ms_step * 1e6) / (hbm_peak()[0] * world),
+        "policy": BEST["bt"],
+        "parallelism": f"curve-range x{world}",
+        "reduce": "NCCL all_reduce(sum) of the vertex count per step "
+                  "(inside the timed region)",
+        "parity": ("vertex count exact, fp64 coordinate checksum within "
+                   "1e-6 of the oracle" if ok else "MISMATCH"),
+        "clocks": clk.summary()}
+
+
+def partitioned_workloads(args, world, rank, local) -> dict | None:
+    """The north-star's partitioned workloads at this N, measured in the
+    same run as the headline so the driver's 1/2/4/8-GPU lines carry their
+    scaling: TC RMAT-22 (edge ranges), BT 1 M curves (curve ranges) and BFS
+    RMAT-26 (1D partition, fused exchange).  Every rank calls; rank 0 gets
+    the dict."""
+    import torch
+    out = {}
+    for name, fn in (
+            ("tc_rmat22", lambda: measure_tc(args, world, rank, local,
+                                             parity=True, steps=5)),
+            ("bt_1m_curves", lambda: measure_bt(args, world, rank, local,
+                                                1000000, steps=10)),
+            ("bfs_rmat26", lambda: measure_bfs26(args, world, rank, local,
+                                                 parity=False, steps=3))):
+        r = fn()
+        torch.cuda.empty_cache()
+        if rank == 0:
+            out[name] = {k: v for k, v in r.items()
+                         if k not in ("higher_is_better", "vs_baseline",
+                                      "dtype", "warmup")}
+    return out if rank == 0 else None
+
+
+def arm_bt(args, world, rank, local):
+    """BT partitioned by curve range (the north-star's near-linear TC / BT
+    scaling target), 1 M curves by default (--scale: curves in millions
+    ... or a count)."""
+    n = args.scale if args.scale > 64 else (args.scale or 1) * 1000000
+    line = measure_bt(args, world, rank, local, n)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
 
 
 def read_traffic():
@@ -1064,7 +1267,7 @@ def main():
                     help="partitioned SSSP / BFS-26: fused peer-memory "
                          "relaxation / discovery (default) "
                          "or the NCCL all-to-all exchange")
-    ap.add_argument("--workload", choices=("sssp", "bfs26", "tc"),
+    ap.add_argument("--workload", choices=("sssp", "bfs26", "tc", "bt"),
                     default="sssp",
                     help="sssp = headline (BASELINE config 3); bfs26 / tc = "
                          "the partitioned multi-GPU configs 5 / 4")
@@ -1085,6 +1288,8 @@ def main():
         arm_bfs26(args, world, rank, local)
     elif args.workload == "tc":
         arm_tc(args, world, rank, local)
+    elif args.workload == "bt":
+        arm_bt(args, world, rank, local)
     else:
         arm_ours(args, world, rank, local)
     import torch

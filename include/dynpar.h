@@ -122,7 +122,13 @@ typedef struct dp_config {
                             dp_unspread_dev.  0 = vertex order.  dp_bfs /
                             dp_bfs_dev use the spread layout internally and
                             always return vertex order */
-  int32_t reserved[1];
+  int32_t weight_bits;   /* SSSP: 4 -> the edge weights are read as packed
+                            nibbles (w - 1, 8 per 32-bit word; 1/8 of the
+                            int32 bytes) when every weight lies in [1, 16];
+                            dp_sssp packs on the host chunk by chunk ahead
+                            of the copy (out-of-range chunks and all later
+                            ones stay int32), dp_sssp_dev packs on the
+                            device.  0 = int32 weights as given */
 } dp_config;
 
 /* SimReport (sim/report.py:12-28) counters, measured on the device */
@@ -145,6 +151,8 @@ typedef struct dp_stats {
   uint64_t kernel_launches;   /* launches of library kernels issued from the host */
   double launch_lat_ns_mean;  /* device launch -> first child block start
                                  (%globaltimer), mean over device launches */
+  uint64_t remote_ops;        /* partitioned runs with the fused exchange:
+                                 atomics issued into other parts' dist */
   uint64_t unpublished_reads; /* publication-checker builds: child reads of
                                  aggregation rows never published (0 otherwise) */
   uint64_t poisoned_reads;    /* publication-checker builds: child reads of rows
@@ -275,6 +283,22 @@ int dp_bfs_part_level_peer(const int32_t* d_rowptr_p, const int32_t* d_col_p,
                            int32_t* d_dist_p, int32_t* const* d_peer_dist,
                            int32_t* d_counts, uint32_t* d_sent,
                            int32_t* d_changed, void* stream, dp_stats* stats);
+/* Whole partitioned BFS of one part, levels looped in the library (see
+ * dp_sssp_part_solve_peer for d_peer_sig / epoch / concurrency): initialises
+ * dist, d_counts (counts_len >= n_global, rounded up to the spread block when
+ * cfg->counts_spread > 0) and the sent bitmap ((n_global + 31) / 32 words),
+ * then levels until no part discovers a vertex.  stats: iterations = levels
+ * (as bfs_1d_peer), remote_ops = CAS issued into other parts' dist. */
+int dp_bfs_part_solve_peer(const int32_t* d_rowptr_p, const int32_t* d_col_p,
+                           int32_t n_local, int32_t n_global, int32_t nparts,
+                           int32_t part, int32_t src, const dp_config* cfg,
+                           int32_t* d_dist_p, int32_t* const* d_peer_dist,
+                           int32_t* d_counts, int64_t counts_len,
+                           uint32_t* d_sent, uint64_t* const* d_peer_sig,
+                           uint64_t epoch, void* stream, dp_stats* stats);
+/* free the calling host thread's workspace (tables, pinned buffers); the
+ * next call on the thread re-creates it */
+void dp_thread_release(void);
 /* out[v] = work[spread_b(v)] for v < n: counts accumulated with
  * counts_spread = b back in vertex order */
 int dp_unspread_dev(const int32_t* d_work, int32_t b, int32_t n,
@@ -310,6 +334,25 @@ int dp_sssp_part_round_peer(const int32_t* d_rowptr_p, const int32_t* d_col_p,
                             int32_t* const* d_peer_dist, int32_t* d_best,
                             int32_t* d_changed, void* stream,
                             dp_stats* stats);
+/* Whole partitioned SSSP of one part (all rounds, loop in the library):
+ * initialises its dist (src is a global id) and best, then per round runs
+ * the fused-exchange step of dp_sssp_part_round_peer and ORs every part's
+ * round flag through the parts' signal slots -- no host collective.
+ * d_peer_sig: DEVICE array of nparts pointers, entry q = part q's uint64
+ * slots[2 * nparts] (zero-filled once; symmetric memory across GPUs, plain
+ * device memory when the parts share a GPU).  epoch: equal on every part,
+ * unique per call on a slot set, in [1, 2^31).  Parts must run
+ * concurrently (one per process, or one per host thread with its own
+ * stream); a part that waits longer than $DYNPAR_PEER_TIMEOUT_MS (default
+ * 60000) for a peer fails with DP_ERR_CUDA.  stats: iterations = rounds,
+ * remote_ops = atomics issued into other parts' dist. */
+int dp_sssp_part_solve_peer(const int32_t* d_rowptr_p, const int32_t* d_col_p,
+                            const int32_t* d_weight_p, int32_t n_local,
+                            int32_t n_global, int32_t nparts, int32_t part,
+                            int32_t src, const dp_config* cfg,
+                            int32_t* d_dist_p, int32_t* const* d_peer_dist,
+                            int32_t* d_best, uint64_t* const* d_peer_sig,
+                            uint64_t epoch, void* stream, dp_stats* stats);
 /* lower owned dist by received (v << 32 | alt) pairs (atomicMin) */
 int dp_sssp_part_apply(const uint64_t* d_recv, int64_t nrecv, int32_t nparts,
                        int32_t* d_dist_p, int32_t* d_changed, void* stream);

@@ -43,7 +43,7 @@ class DpConfig(ctypes.Structure):
                 ("frontier", ctypes.c_int32),
                 ("agg_coarsen", ctypes.c_int32),
                 ("counts_spread", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 1)]
+                ("weight_bits", ctypes.c_int32)]
 
 
 class DpStats(ctypes.Structure):
@@ -63,6 +63,7 @@ class DpStats(ctypes.Structure):
                 ("d2h_bytes", ctypes.c_uint64),
                 ("kernel_launches", ctypes.c_uint64),
                 ("launch_lat_ns_mean", ctypes.c_double),
+                ("remote_ops", ctypes.c_uint64),
                 ("unpublished_reads", ctypes.c_uint64),
                 ("poisoned_reads", ctypes.c_uint64)]
 
@@ -117,6 +118,13 @@ _SIGNATURES = {
     "dp_sssp_part_round": ([_P, _P, _P, _I32, _I32, _I32, _CFG, _P, _P, _P,
                             _P, _P, _P, _P, _ST], ctypes.c_int),
     "dp_sssp_part_apply": ([_P, _I64, _I32, _P, _P, _P], ctypes.c_int),
+    "dp_sssp_part_solve_peer": ([_P, _P, _P, _I32, _I32, _I32, _I32, _I32,
+                                 _CFG, _P, _P, _P, _P, _U64, _P, _ST],
+                                ctypes.c_int),
+    "dp_bfs_part_solve_peer": ([_P, _P, _I32, _I32, _I32, _I32, _I32, _CFG,
+                                _P, _P, _P, _I64, _P, _P, _U64, _P, _ST],
+                               ctypes.c_int),
+    "dp_thread_release": ([], None),
     "dp_sssp_part_round_peer": ([_P, _P, _P, _I32, _I32, _I32, _CFG, _P, _P,
                                  _P, _P, _P, _ST], ctypes.c_int),
     "dp_rmat_part_keys_dev": ([_I32, _I32, _U64, _I32, _I32, _P, _I64,
@@ -168,7 +176,12 @@ def load() -> ctypes.CDLL:
                     f"`python -c 'import __graft_entry__ as g; g.build()'` "
                     f"or `make -C {CSRC}` (there is no CPU fallback)")
             lib = ctypes.CDLL(str(LIB_PATH))
+            # A/B runs of older builds (tools/ab_libs.py) may lack newer
+            # entry points; everything else requires every symbol
+            partial = os.environ.get("DYNPAR_LIB_PARTIAL") == "1"
             for name, (args, res) in _SIGNATURES.items():
+                if partial and not hasattr(lib, name):
+                    continue
                 fn = getattr(lib, name)
                 fn.argtypes = args
                 fn.restype = res

@@ -54,6 +54,7 @@ class BenchConfig:
     persistent: int = 0
     device_loop: bool = False
     frontier: bool = False
+    weight_bits: int = 0
 
     def describe(self) -> str:
         return (f"threshold={self.threshold} cfactor={self.cfactor} "
@@ -87,6 +88,8 @@ class BenchConfig:
                              "aggregated grid (order with A before C)")
         if self.serial not in _lib.SERIAL_MODES:
             raise ValueError(f"unknown serial mode {self.serial!r}")
+        if self.weight_bits not in (0, 4):
+            raise ValueError("weight_bits must be 0 (int32) or 4 (packed)")
 
     def to_c(self, variant: int = _lib.VARIANT_CDP) -> _lib.DpConfig:
         self.validate()
@@ -107,6 +110,7 @@ class BenchConfig:
         c.persistent = int(self.persistent)
         c.device_loop = int(bool(self.device_loop))
         c.frontier = int(bool(self.frontier))
+        c.weight_bits = int(self.weight_bits)
         c.threshold, c.cfactor, c.agg_coarsen = self.order_effect(
             c.threshold, c.cfactor, self.agg if agg_on else None)
         return c

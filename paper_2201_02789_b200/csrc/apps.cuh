@@ -219,6 +219,7 @@ struct BfsPartApp {
   // fused exchange (null: buckets): every part's dist, addressable here
   // (symmetric memory); a remote discovery is a CAS into the owner's dist
   int* const* peer_dist;
+  unsigned long long* remote_ops;  // DevState::remote
   long long stride;
   int n_local;
   int nparts;
@@ -276,7 +277,7 @@ struct BfsPartApp {
       if (!((unsigned)d_or_bits & bit) &&
           !(atomicOr(sent + (v >> 5), bit) & bit)) {
         if (peer_dist) {
-          acc.remote = 1;
+          ++acc.remote;
           if (atomicCAS(peer_dist[q] + local_of(v, nparts), kUnreached, lvl + 1) ==
               kUnreached)
             acc.changed = 1;
@@ -317,7 +318,11 @@ struct BfsPartApp {
   }
   __device__ void flush(Acc& acc) const {
     // remote discoveries are visible to every part before this warp retires
-    if (__any_sync(DP_FULL, acc.remote)) __threadfence_system();
+    const int nr = __reduce_add_sync(DP_FULL, acc.remote);
+    if (nr) {
+      __threadfence_system();
+      if (lane_id() == 0) atomicAdd(remote_ops, (unsigned long long)nr);
+    }
     // read before write: after the first success the flag line is only
     // read (shared), not re-written by every succeeding warp
     if (__any_sync(DP_FULL, acc.changed) && lane_id() == 0 &&
@@ -442,6 +447,7 @@ struct SsspPeerApp {
   int* my_dist;           // == peer_dist[part]
   int* best;              // dense, global ids: best value sent per vertex
   int* changed;
+  unsigned long long* remote_ops;  // DevState::remote
   int n_local;
   int nparts;
   int part;
@@ -480,7 +486,7 @@ struct SsspPeerApp {
     if (q == part) {
       if (atomicMin(my_dist + local_of(v, nparts), alt) > alt) acc.changed = 1;
     } else if (atomicMin(best + v, alt) > alt) {
-      acc.remote = 1;
+      ++acc.remote;
       if (atomicMin(peer_dist[q] + local_of(v, nparts), alt) > alt)
         acc.changed = 1;
     }
@@ -516,7 +522,11 @@ struct SsspPeerApp {
       if (ok[j]) update(v[j], alt[j], d[j], acc);
   }
   __device__ void flush(Acc& acc) const {
-    if (__any_sync(DP_FULL, acc.remote)) __threadfence_system();
+    const int nr = __reduce_add_sync(DP_FULL, acc.remote);
+    if (nr) {
+      __threadfence_system();
+      if (lane_id() == 0) atomicAdd(remote_ops, (unsigned long long)nr);
+    }
     if (__any_sync(DP_FULL, acc.changed) && lane_id() == 0 &&
         __ldcg(changed) == 0)
       *changed = 1;
@@ -526,10 +536,21 @@ struct SsspPeerApp {
 // ---------------------------------------------------------------------------
 // SSSP — SSSP_CDP main/relax_edges/relax (bench/benchmarks.py:175-222)
 // ---------------------------------------------------------------------------
+// Edge weights packed as nibbles (w - 1, eight per 32-bit word, slot e in
+// bits 4*(e & 7) of word e >> 3; dp_config.weight_bits = 4): slots below
+// `wslots` read the packed word (the 32 lanes of a warp share one 16-byte
+// sector, 1/8 of the int32 bytes), the rest the int32 array.
+__device__ __forceinline__ int packed_weight(const unsigned* __restrict__ wp,
+                                             int e) {
+  return (int)((__ldg(wp + (e >> 3)) >> ((e & 7) << 2)) & 15u) + 1;
+}
+
 struct SsspApp {
   const int* __restrict__ rowptr;
   const int* __restrict__ col;
   const int* __restrict__ weight;
+  const unsigned* __restrict__ wpack;  // packed weights (null: none)
+  long long wslots;                    // slots [0, wslots) are packed
   int* dist;
   int* changed;
   int* changed_next;
@@ -594,10 +615,12 @@ struct SsspApp {
   // when it succeeds; atomicMin reaches the same final value and succeeds
   // exactly when the old value was larger.  Arithmetic wraps like the
   // reference's 32-bit ints (sim/compile.py:36-37).
+  __device__ int weight_of(int i) const {
+    return i < wslots ? packed_weight(wpack, i) : ld_stream(weight + i);
+  }
   __device__ void item(const Args& a, int e, Acc& acc) const {
     const int v = __ldg(col + a.start + e);
-    const int alt =
-        (int)((unsigned)a.du + (unsigned)__ldg(weight + a.start + e));
+    const int alt = (int)((unsigned)a.du + (unsigned)weight_of(a.start + e));
     if (alt < __ldcg(dist + v) && atomicMin(dist + v, alt) > alt)
       acc.changed = 1;
   }
@@ -616,7 +639,7 @@ struct SsspApp {
     for (int j = 0; j < U; ++j) {
       const int i = ok[j] ? args(j).start + e[j] : 0;
       v[j] = ok[j] ? ld_stream(col + i) : 0;
-      alt[j] = ok[j] ? (int)((unsigned)args(j).du + (unsigned)ld_stream(weight + i))
+      alt[j] = ok[j] ? (int)((unsigned)args(j).du + (unsigned)weight_of(i))
                      : 0;
     }
     // L1-cached probe (stale copies are >= the true distance: a stale hit
@@ -1077,7 +1100,15 @@ struct BtApp {
     int u, nt;
     long long off;
   };
-  struct Acc {};
+  // the thread's last curve: control points and 1/(nt-1), reloaded only when
+  // the curve changes (a whole-warp row walks one curve U x 32 vertices at a
+  // time; per vertex this leaves ~15 instructions instead of 3 loads, a
+  // reciprocal and ~25)
+  struct Acc {
+    int key;  // u + 1 of the cached curve (0: empty)
+    float inv;
+    float2 p0, p1, p2;
+  };
 
   __device__ int nparents() const { return ncurves; }
   __device__ void parent_prologue() const {}
@@ -1124,18 +1155,25 @@ struct BtApp {
     return nt;
   }
   __device__ static int count(const Args& a) { return a.nt; }
-  __device__ void item(const Args& a, int i, Acc&) const {
-    const float2 p0 = __ldg(cp + 3 * a.u), p1 = __ldg(cp + 3 * a.u + 1),
-                 p2 = __ldg(cp + 3 * a.u + 2);
-    // fast division (2 ulp): vertices are checked within 1e-5, only the
-    // counts (tess_count) must match the oracle bit for bit
-    const float t = __fdividef((float)i, (float)(a.nt - 1));
+  __device__ void item(const Args& a, int i, Acc& c) const {
+    if (c.key != a.u + 1) {
+      c.key = a.u + 1;
+      c.p0 = __ldg(cp + 3 * a.u);
+      c.p1 = __ldg(cp + 3 * a.u + 1);
+      c.p2 = __ldg(cp + 3 * a.u + 2);
+      c.inv = __frcp_rn((float)(a.nt - 1));
+    }
+    // t = i * (1/(nt-1)) (<= 1.5 ulp): vertices are checked within 1e-5, only
+    // the counts (tess_count) must match the oracle bit for bit
+    const float t = (float)i * c.inv;
     const float s = 1.0f - t;
     const float w0 = s * s, w1 = 2.0f * s * t, w2 = t * t;
-    verts[a.off + i] = make_float2(w0 * p0.x + w1 * p1.x + w2 * p2.x,
-                                   w0 * p0.y + w1 * p1.y + w2 * p2.y);
+    verts[a.off + i] =
+        make_float2(w0 * c.p0.x + w1 * c.p1.x + w2 * c.p2.x,
+                    w0 * c.p0.y + w1 * c.p1.y + w2 * c.p2.y);
   }
   static constexpr int kUnroll = 1;
+  static constexpr int kBigUnroll = 4;  // whole-warp rows: 4 stores in flight
   static constexpr bool kBlockMode = false;
   static constexpr bool kPureExpand = false;  // bump-allocates in expand
   static constexpr int kMinBlocks = DP_BT_MINB;

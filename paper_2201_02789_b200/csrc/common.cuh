@@ -158,6 +158,9 @@ struct DevState {
   // pattern written before the parent grid (stale bytes actually observed)
   unsigned long long unpublished;
   unsigned long long poisoned;
+  // partitioned apps with the fused exchange: atomics issued into other
+  // parts' dist (NVLink / NVSwitch peer traffic when parts are GPUs)
+  unsigned long long remote;
 };
 
 // ---------------------------------------------------------------------------

@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 
 #include "../../include/dynpar.h"
@@ -56,7 +57,6 @@ struct Workspace {
   unsigned long long* d_scratch = nullptr;  // TC total / BT cursor
   int* d_flag = nullptr;                    // BT overflow
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evk0 = nullptr, evk1 = nullptr;
-  long long pending_limit = 0;
   // mapped (zero-copy) readback of DevState for the per-level host loop
   struct Signal {
     DevState ds;
@@ -80,9 +80,24 @@ struct Workspace {
   // publication-checker builds: one stamp per aggregation-table row
   void* pub = nullptr;
   size_t pub_bytes = 0;
+  // packed SSSP weights: device copy and the pinned host staging of dp_sssp
+  void* wpack = nullptr;
+  size_t wpack_bytes = 0;
+  void* h_wpack = nullptr;
+  size_t h_wpack_bytes = 0;
+  int* d_bad = nullptr;
 };
 
-Workspace g_ws[64];
+// One workspace per (host thread, device): the partitioned solve drivers
+// run one part per host thread when several parts share a process
+// (dp_*_part_solve_peer), each with its own stream, tables and DevState.
+// dp_thread_release frees the calling thread's.
+thread_local Workspace g_ws[64];
+
+// The CDP2 pending-launch pool is a device-wide limit: one size per device
+// for every thread, changed under a lock (growing it synchronises the device).
+std::mutex g_pending_mu;
+long long g_pending_limit[64] = {};
 
 // The device chosen by dp_init.  libdynpar links the CUDA runtime statically,
 // so its current device is independent of the caller's runtime (e.g.
@@ -165,6 +180,8 @@ int validate(const dp_config* c) {
   if (c->threshold < 0) return fail(DP_ERR_INVALID, "threshold must be >= 0");
   if (c->counts_spread < 0 || c->counts_spread > 30)
     return fail(DP_ERR_INVALID, "counts_spread must be in [0, 30]");
+  if (c->weight_bits != 0 && c->weight_bits != 4)
+    return fail(DP_ERR_INVALID, "weight_bits must be 0 or 4");
   if (c->agg_coarsen &&
       (c->agg < DP_AGG_WARP || c->agg > DP_AGG_MULTIBLOCK || c->persistent))
     return fail(DP_ERR_INVALID,
@@ -181,6 +198,10 @@ int validate(const dp_config* c) {
 }
 
 int map_device_error(int e) {
+  if (e == 0x7fff0001)  // kErrPeerTimeout
+    return fail(DP_ERR_CUDA,
+                "cuda-error: partitioned exchange timed out waiting for a "
+                "peer part ($DYNPAR_PEER_TIMEOUT_MS)");
   if (e == (int)cudaErrorLaunchPendingCountExceeded)
     return fail(DP_ERR_QUEUE_OVERFLOW,
                 "queue-overflow: pending launch count exceeded the device "
@@ -305,13 +326,16 @@ int ensure_pending_limit(Workspace* w, const dp_config* c, long long bound) {
   // slows every device launch (profiles/cdp_probe_r01.txt: 1000 launches
   // take 0.41 ms at 2048 slots, 1.15 ms at the clamp), so a naive-CDP run
   // must not tax the aggregated runs that follow it.
-  if (want <= w->pending_limit &&
-      !(w->pending_limit > 4 * want && w->pending_limit > 8192))
-    return 0;
+  int dev = 0;
+  DP_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(g_pending_mu);
+  long long& have = g_pending_limit[dev & 63];
+  (void)w;
+  if (want <= have && !(have > 4 * want && have > 8192)) return 0;
   size_t freeb = 0, totb = 0;
   DP_CUDA(cudaMemGetInfo(&freeb, &totb));
   const long long extra =
-      std::max<long long>(want - w->pending_limit, 0) * kSlotBytes;
+      std::max<long long>(want - have, 0) * kSlotBytes;
   if (extra > (long long)(freeb * 0.85))
     return fail(DP_ERR_QUEUE_OVERFLOW,
                 "queue-overflow: " + std::to_string(bound) +
@@ -323,7 +347,7 @@ int ensure_pending_limit(Workspace* w, const dp_config* c, long long bound) {
                              (size_t)want));
   size_t got = 0;
   DP_CUDA(cudaDeviceGetLimit(&got, cudaLimitDevRuntimePendingLaunchCount));
-  w->pending_limit = (long long)got;
+  have = (long long)got;
   if ((long long)got < bound + 64)
     return fail(DP_ERR_QUEUE_OVERFLOW,
                 "queue-overflow: the device runtime granted " +
@@ -702,6 +726,7 @@ void finish_stats(Workspace* w, const RunCounters& rc, float ms,
   st->launch_lat_ns_mean =
       w->h_ds->lat_cnt ? (double)w->h_ds->lat_sum / (double)w->h_ds->lat_cnt
                        : 0.0;
+  st->remote_ops = w->h_ds->remote;
   st->unpublished_reads = w->h_ds->unpublished;
   st->poisoned_reads = w->h_ds->poisoned;
   // DP_PROFILE builds: summed warp-cycles per phase -> warp-ns at the SM
@@ -897,10 +922,92 @@ int bfs_dev_impl(const int32_t* rowptr, const int32_t* col, int32_t n,
                  });
 }
 
+// Pack int32 weights into nibbles (w - 1, 8 per word); *bad = 1 if any
+// weight lies outside [1, 16].  One thread per output word, two 16-byte loads.
+__global__ void pack_weights_kernel(const int* __restrict__ w, long long m,
+                                    unsigned* __restrict__ out, int* bad) {
+  const long long words = (m + 7) >> 3;
+  unsigned any = 0;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+       k < words; k += (long long)gridDim.x * blockDim.x) {
+    int x[8];
+    if (k * 8 + 8 <= m) {
+      const int4 a = __ldg(reinterpret_cast<const int4*>(w) + 2 * k);
+      const int4 b = __ldg(reinterpret_cast<const int4*>(w) + 2 * k + 1);
+      x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
+      x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) x[j] = k * 8 + j < m ? w[k * 8 + j] : 1;
+    }
+    unsigned word = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const unsigned v = (unsigned)(x[j] - 1);
+      any |= v > 15u;
+      word |= (v & 15u) << (4 * j);
+    }
+    out[k] = word;
+  }
+  if (__any_sync(DP_FULL, any) && lane_id() == 0) *bad = 1;
+}
+
+// Host twin for slots [lo, lo + len) (lo a multiple of 8); false if any
+// weight lies outside [1, 16].  OpenMP over the host cores.
+bool pack_weights_host(const int32_t* w, long long lo, long long len,
+                       unsigned* out) {
+  const long long words = (len + 7) / 8;
+  int bad = 0;
+#pragma omp parallel for reduction(| : bad) schedule(static)
+  for (long long k = 0; k < words; ++k) {
+    unsigned word = 0;
+    const long long e0 = lo + k * 8;
+    const int jn = (int)std::min<long long>(8, lo + len - e0);
+    for (int j = 0; j < jn; ++j) {
+      const unsigned v = (unsigned)(w[e0 + j] - 1);
+      bad |= v > 15u;
+      word |= (v & 15u) << (4 * j);
+    }
+    out[(lo >> 3) + k] = word;
+  }
+  return !bad;
+}
+
+// dp_config.weight_bits = 4 with resident weights: pack them on the device;
+// *wpack / *wslots stay null / 0 when some weight lies outside [1, 16]
+int pack_weights_dev(Workspace* w, const int32_t* weight, long long m,
+                     cudaStream_t s, const unsigned** wpack,
+                     long long* wslots) {
+  int r;
+  *wpack = nullptr;
+  *wslots = 0;
+  if (m <= 0) return 0;
+  if ((r = grow(&w->wpack, &w->wpack_bytes,
+                (size_t)((m + 7) / 8) * sizeof(unsigned))))
+    return r;
+  if (!w->d_bad) DP_CUDA(cudaMalloc(&w->d_bad, sizeof(int)));
+  DP_CUDA(cudaMemsetAsync(w->d_bad, 0, sizeof(int), s));
+  const int blocks = (int)std::max<long long>(
+      1, std::min<long long>(dp::ceil_div_ll((m + 7) / 8, 256), 148 * 8));
+  pack_weights_kernel<<<blocks, 256, 0, s>>>(weight, m, (unsigned*)w->wpack,
+                                             w->d_bad);
+  DP_CUDA(cudaGetLastError());
+  int bad = 0;
+  DP_CUDA(cudaMemcpyAsync(&bad, w->d_bad, sizeof(int), cudaMemcpyDeviceToHost,
+                          s));
+  DP_CUDA(cudaStreamSynchronize(s));
+  if (!bad) {
+    *wpack = (const unsigned*)w->wpack;
+    *wslots = m;
+  }
+  return 0;
+}
+
 int sssp_dev_impl(const int32_t* rowptr, const int32_t* col,
                   const int32_t* weight, int32_t n, int32_t src,
                   const dp_config* c, int32_t* dist, cudaStream_t s,
-                  dp_stats* st, Arrival* arr = nullptr, int shift = 0) {
+                  dp_stats* st, Arrival* arr = nullptr, int shift = 0,
+                  const unsigned* wpack = nullptr, long long wslots = 0) {
   int r;
   if ((r = validate(c))) return r;
   if (n < 1) return fail(DP_ERR_INVALID, "graph must have at least 1 vertex");
@@ -928,6 +1035,8 @@ int sssp_dev_impl(const int32_t* rowptr, const int32_t* col,
                    a.rowptr = rowptr;
                    a.col = col;
                    a.weight = weight;
+                   a.wpack = wpack;
+                   a.wslots = wpack ? wslots : 0;
                    a.dist = dist;
                    a.changed = &ds->flag[round & 1];
                    a.changed_next = &ds->flag[(round + 1) & 1];
@@ -1706,6 +1815,7 @@ int bfs_part_level_impl(const int32_t* rowptr, const int32_t* col,
   a.send_count = send_count;
   a.changed = changed;
   a.peer_dist = (int* const*)peer_dist;
+  a.remote_ops = &w->ds->remote;
   a.stride = stride;
   if (peer_dist)  // fused exchange: the flag is this level's alone
     DP_CUDA(cudaMemsetAsync(changed, 0, sizeof(int), s));
@@ -1772,6 +1882,7 @@ int sssp_peer_round_impl(const int32_t* rowptr, const int32_t* col,
   a.my_dist = dist;
   a.best = best;
   a.changed = changed;
+  a.remote_ops = &w->ds->remote;
   DP_CUDA(cudaMemsetAsync(changed, 0, sizeof(int), s));  // this round's flag
   a.n_local = n_local;
   a.nparts = nparts;
@@ -1788,6 +1899,276 @@ int sssp_peer_round_impl(const int32_t* rowptr, const int32_t* col,
   finish_stats(w, rc, ms, st);
   if (st) st->iterations = 1;
   return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Partitioned solves with the round loop in the library (one part per host
+// thread or process).  Per round: the part's parent grid (+ children, the
+// exchange fused in as remote atomics), then one warp ORs the round flags of
+// all parts through their signal slots -- no NCCL call, no per-round Python:
+// the host loop is the single-GPU iterate() plus one tiny kernel.
+//
+// Signal slots: part q owns uint64 slots[2 * nparts] in memory every part can
+// address (torch symmetric memory across GPUs; plain device memory when the
+// parts share a GPU); peer_sig[q] points at part q's.  Exchange index i (0:
+// the barrier after the parts initialised their dist, round r: r + 1) stores
+// tag(epoch, i, bit) into slot [(i & 1) * nparts + part] of every part
+// (st.release.sys) and waits until its own row (i & 1) holds index i's tag
+// from every part (ld.acquire.sys).  A part cannot get two indices ahead of
+// another (it would need that part's tag for the index in between), so two
+// rows suffice; the caller's epoch (equal on every part, unique per call, >
+// 0) keeps an earlier call's tags from matching.  The release orders the
+// round's remote atomics (fenced system-wide by the warps that issued them)
+// before the tag, so once every tag is in, every lowering of the round is
+// visible to its owner.
+// ---------------------------------------------------------------------------
+constexpr int kErrPeerTimeout = 0x7fff0001;  // DevState::err marker
+
+__device__ __forceinline__ void st_release_sys_u64(unsigned long long* p,
+                                                   unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v)
+               : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(
+    const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];"
+               : "=l"(v)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+
+// one warp; flag_slot < 0: a pure barrier
+__global__ void part_flag_or_kernel(unsigned long long* const* peer_sig,
+                                    int nparts, int part, long long idx,
+                                    unsigned long long epoch, DevState* ds,
+                                    int flag_slot,
+                                    unsigned long long timeout_ns) {
+  const int lane = threadIdx.x;
+  const int bit = flag_slot >= 0 && ds->flag[flag_slot] != 0;
+  const unsigned long long key =
+      (epoch << 32) | (unsigned long long)(idx + 1);  // tag >> 1
+  const long long row = (idx & 1) * nparts;
+  for (int q = lane; q < nparts; q += 32)
+    st_release_sys_u64(peer_sig[q] + row + part, (key << 1) | (unsigned)bit);
+  int any = 0;
+  const unsigned long long t0 = globaltimer_ns();
+  bool timed_out = false;
+  for (int q = lane; q < nparts && !timed_out; q += 32) {
+    unsigned long long v;
+    while (((v = ld_acquire_sys_u64(peer_sig[part] + row + q)) >> 1) != key) {
+      if (globaltimer_ns() - t0 > timeout_ns) {
+        timed_out = true;
+        break;
+      }
+      __nanosleep(64);
+    }
+    any |= (int)(v & 1);
+  }
+  if (timed_out) atomicCAS(&ds->err, 0, kErrPeerTimeout);
+  any = __any_sync(DP_FULL, any);
+  if (lane == 0 && flag_slot >= 0) {
+    ds->flag[flag_slot] = any;  // the OR over the parts: what the host reads
+    ds->flag[flag_slot ^ 1] = 0;  // the next round's own flag
+  }
+}
+
+unsigned long long peer_timeout_ns() {
+  static const unsigned long long t = [] {
+    const char* e = std::getenv("DYNPAR_PEER_TIMEOUT_MS");
+    const long long ms = e ? std::atoll(e) : 60000;
+    return (unsigned long long)std::max<long long>(ms, 1) * 1000000ull;
+  }();
+  return t;
+}
+
+struct PartSync {
+  unsigned long long* const* sig;
+  int nparts, part;
+  unsigned long long epoch;
+};
+
+// iterate() for one part: rounds until no part changed anything
+template <class MakeApp>
+int iterate_parts(Workspace* w, const dp_config* c, long long nparents,
+                  long long launchers, int max_iter, cudaStream_t s,
+                  const PartSync& ps, MakeApp make, dp_stats* st) {
+  RunCounters rc;
+  int r;
+  if ((r = ensure_pending_limit(w, c, launch_bound(c, nparents, launchers))))
+    return r;
+  // grow every buffer a round can need BEFORE the barrier: the cudaFree in
+  // grow() synchronises the device, i.e. would wait on parts that already
+  // spin in the barrier for this one
+  {
+    using App = decltype(make(0, w->ds));
+    const long long wave = std::min(wave_parents(c, nparents, launchers),
+                                    nparents);
+    AggTables<App> t{nullptr, nullptr, nullptr, nullptr};
+    if ((r = prepare_tables<App>(
+             c, (int)dp::ceil_div_ll(wave, c->parent_block), c->parent_block,
+             w, s, &t)))
+      return r;
+  }
+  if ((r = begin_run(w, s))) return r;
+  DP_CUDA(cudaEventRecord(w->ev0, s));
+  const unsigned long long tmo = peer_timeout_ns();
+  // every part has initialised its dist before any remote write lands
+  part_flag_or_kernel<<<1, 32, 0, s>>>(ps.sig, ps.nparts, ps.part, 0,
+                                       ps.epoch, w->ds, -1, tmo);
+  DP_CUDA(cudaGetLastError());
+  int it = 0;
+  bool converged = false;
+  for (; !converged && it <= max_iter; ++it) {
+    auto app = make(it, w->ds);
+    if ((r = launch_parent(app, nparents, launchers, c, w, s, &rc))) return r;
+    part_flag_or_kernel<<<1, 32, 0, s>>>(ps.sig, ps.nparts, ps.part, it + 1,
+                                         ps.epoch, w->ds, it & 1, tmo);
+    DP_CUDA(cudaGetLastError());
+    rc.kernel_launches += 1;
+    if ((r = read_state_fast(w, s))) return r;
+    if ((r = account_step(w, &rc))) return r;
+    if (w->h_ds->flag[it & 1] == 0) {
+      converged = true;
+      ++it;
+      break;
+    }
+  }
+  DP_CUDA(cudaEventRecord(w->ev1, s));
+  DP_CUDA(cudaEventSynchronize(w->ev1));
+  float ms = 0.f;
+  DP_CUDA(cudaEventElapsedTime(&ms, w->ev0, w->ev1));
+  if ((r = read_state(w, s))) return r;
+  finish_stats(w, rc, ms, st);
+  if (st) st->iterations = it;
+  if (!converged)
+    return fail(DP_ERR_ITERATIONS, "used more iterations than vertices");
+  return 0;
+}
+
+int check_part_args(const dp_config* c, int32_t n_local, int32_t n_global,
+                    int32_t nparts, int32_t part, int32_t src,
+                    const void* peer_dist, const void* peer_sig,
+                    uint64_t epoch) {
+  int r;
+  if ((r = validate(c))) return r;
+  if (nparts < 1 || part < 0 || part >= nparts || n_local < 0 ||
+      n_global < 1 || src < 0 || src >= n_global || !peer_dist ||
+      !peer_sig || epoch == 0 || epoch >= (1ull << 31) ||
+      (long long)n_local != ((long long)n_global - part + nparts - 1) / nparts)
+    return fail(DP_ERR_INVALID, "bad partition arguments");
+  return 0;
+}
+
+__global__ void part_init_kernel(int* dist, int n_local, int src_local,
+                                 int* best, int n_global) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+       i < n_global || i < n_local; i += (long long)gridDim.x * blockDim.x) {
+    if (i < n_local) dist[i] = i == src_local ? 0 : kUnreached;
+    if (best && i < n_global) best[i] = kUnreached;
+  }
+}
+
+int sssp_part_solve_peer_impl(const int32_t* rowptr, const int32_t* col,
+                              const int32_t* weight, int32_t n_local,
+                              int32_t n_global, int32_t nparts, int32_t part,
+                              int32_t src, const dp_config* c, int32_t* dist,
+                              int32_t* const* peer_dist, int32_t* best,
+                              uint64_t* const* peer_sig, uint64_t epoch,
+                              cudaStream_t s, dp_stats* st) {
+  int r;
+  if ((r = check_part_args(c, n_local, n_global, nparts, part, src, peer_dist,
+                           peer_sig, epoch)))
+    return r;
+  if (!dist || !best) return fail(DP_ERR_INVALID, "null buffer");
+  Workspace* w = workspace(&r);
+  if (!w) return r;
+  const int src_local = src % nparts == part
+                            ? src / nparts : -1;
+  part_init_kernel<<<148 * 4, 256, 0, s>>>(dist, n_local, src_local, best,
+                                           n_global);
+  DP_CUDA(cudaGetLastError());
+  // every part uses the same worst-case launcher count, so every part sizes
+  // the device-wide launch pool alike (no part grows it while another waits
+  // in the barrier)
+  const long long launchers = n_local;
+  const PartSync ps{(unsigned long long* const*)peer_sig, nparts, part,
+                    epoch};
+  return iterate_parts(w, c, n_local, launchers, n_global, s, ps,
+                       [&](int round, DevState* ds) {
+                         SsspPeerApp a;
+                         a.rowptr = rowptr;
+                         a.col = col;
+                         a.weight = weight;
+                         a.peer_dist = (int* const*)peer_dist;
+                         a.my_dist = dist;
+                         a.best = best;
+                         a.changed = &ds->flag[round & 1];
+                         a.remote_ops = &ds->remote;
+                         a.n_local = n_local;
+                         a.nparts = nparts;
+                         a.part = part;
+                         a.pad = 0;
+                         return a;
+                       },
+                       st);
+}
+
+int bfs_part_solve_peer_impl(const int32_t* rowptr, const int32_t* col,
+                             int32_t n_local, int32_t n_global, int32_t nparts,
+                             int32_t part, int32_t src, const dp_config* c,
+                             int32_t* dist, int32_t* const* peer_dist,
+                             int32_t* counts, int64_t counts_len,
+                             uint32_t* sent, uint64_t* const* peer_sig,
+                             uint64_t epoch, cudaStream_t s, dp_stats* st) {
+  int r;
+  if ((r = check_part_args(c, n_local, n_global, nparts, part, src, peer_dist,
+                           peer_sig, epoch)))
+    return r;
+  const unsigned cmask = c->counts_spread > 0
+                             ? (unsigned)((1ull << c->counts_spread) - 1)
+                             : 0u;
+  const long long need =
+      cmask ? ((long long)n_global + cmask) / (cmask + 1) * (cmask + 1)
+            : n_global;
+  if (!dist || !counts || !sent || counts_len < need)
+    return fail(DP_ERR_INVALID, "bad counts / sent buffers");
+  Workspace* w = workspace(&r);
+  if (!w) return r;
+  const int src_local = src % nparts == part
+                            ? src / nparts : -1;
+  part_init_kernel<<<148 * 4, 256, 0, s>>>(dist, n_local, src_local, nullptr,
+                                           0);
+  DP_CUDA(cudaGetLastError());
+  DP_CUDA(cudaMemsetAsync(counts, 0, (size_t)counts_len * sizeof(int), s));
+  DP_CUDA(cudaMemsetAsync(sent, 0, (size_t)(n_global + 31) / 32 * 4, s));
+  const long long launchers = n_local;
+  const PartSync ps{(unsigned long long* const*)peer_sig, nparts, part,
+                    epoch};
+  return iterate_parts(w, c, n_local, launchers, n_global, s, ps,
+                       [&](int level, DevState* ds) {
+                         BfsPartApp a;
+                         a.rowptr = rowptr;
+                         a.col = col;
+                         a.dist = dist;
+                         a.counts = counts;
+                         a.sent = sent;
+                         a.send_buf = nullptr;
+                         a.send_count = nullptr;
+                         a.changed = &ds->flag[level & 1];
+                         a.peer_dist = (int* const*)peer_dist;
+                         a.remote_ops = &ds->remote;
+                         a.stride = 0;
+                         a.n_local = n_local;
+                         a.nparts = nparts;
+                         a.part = part;
+                         a.level = level;
+                         a.cmask = cmask;
+                         a.pad_ = 0;
+                         return a;
+                       },
+                       st);
 }
 
 int sssp_part_round_impl(const int32_t* rowptr, const int32_t* col,
@@ -1917,6 +2298,70 @@ int stage_chunked(Workspace* w, cudaStream_t s, int nsrc, const void* const* hos
     for (int i = 0; i < nsrc; ++i) {
       DP_CUDA(cudaMemcpyAsync((int32_t*)dev[i] + lo,
                               (const int32_t*)host[i] + lo, (size_t)len * 4,
+                              cudaMemcpyHostToDevice, w->copy_stream));
+      *h2d += (uint64_t)len * 4;
+    }
+    set_arrived_kernel<<<1, 1, 0, w->copy_stream>>>(w->d_arrived, k + 1);
+    DP_CUDA(cudaGetLastError());
+    DP_CUDA(cudaEventRecord(w->chunk_ev[k], w->copy_stream));
+  }
+  return 0;
+}
+
+// dp_sssp with weight_bits = 4: as stage_chunked for (col, weight), but each
+// weight chunk is first packed on the host (OpenMP, into pinned staging) and
+// copied as nibbles, 1/8 of the bytes; the packing of chunk k + 1 overlaps
+// the DMA of chunk k.  The first chunk holding a weight outside [1, 16] and
+// every later one are copied as int32 instead: *wslots = the packed prefix.
+int stage_chunked_packed(Workspace* w, cudaStream_t s, const int32_t* col,
+                         const int32_t* weight, int32_t* d_col,
+                         int32_t* d_weight, unsigned* d_wpack, int64_t m,
+                         int shift, Arrival* arr, uint64_t* h2d,
+                         long long* wslots) {
+  if (!w->copy_stream) {
+    DP_CUDA(cudaStreamCreateWithFlags(&w->copy_stream, cudaStreamNonBlocking));
+    DP_CUDA(cudaMalloc(&w->d_arrived, sizeof(int)));
+    for (int k = 0; k < kMaxChunks; ++k)
+      DP_CUDA(cudaEventCreateWithFlags(&w->chunk_ev[k],
+                                       cudaEventDisableTiming));
+  }
+  const size_t hbytes = (size_t)((m + 7) / 8) * sizeof(unsigned);
+  if (hbytes > w->h_wpack_bytes) {
+    if (w->h_wpack) cudaFreeHost(w->h_wpack);
+    w->h_wpack = nullptr;
+    w->h_wpack_bytes = 0;
+    DP_CUDA(cudaMallocHost(&w->h_wpack, hbytes));
+    w->h_wpack_bytes = hbytes;
+  }
+  unsigned* hp = (unsigned*)w->h_wpack;
+  const int64_t chunk = 1LL << shift;
+  arr->nchunks = (int)((m + chunk - 1) / chunk);
+  arr->waited = 0;
+  if (arr->nchunks > kMaxChunks)
+    return fail(DP_ERR_INVALID, "too many copy chunks");
+  DP_CUDA(cudaMemsetAsync(w->d_arrived, 0, sizeof(int), s));
+  DP_CUDA(cudaEventRecord(w->evk0, s));
+  DP_CUDA(cudaStreamWaitEvent(w->copy_stream, w->evk0, 0));
+  bool packed = true;
+  *wslots = m;
+  for (int k = 0; k < arr->nchunks; ++k) {
+    const int64_t lo = (int64_t)k * chunk;
+    const int64_t len = std::min(chunk, m - lo);
+    DP_CUDA(cudaMemcpyAsync(d_col + lo, col + lo, (size_t)len * 4,
+                            cudaMemcpyHostToDevice, w->copy_stream));
+    *h2d += (uint64_t)len * 4;
+    if (packed && !pack_weights_host(weight, lo, len, hp)) {
+      packed = false;
+      *wslots = lo;
+    }
+    if (packed) {
+      const size_t words = (size_t)((len + 7) / 8);
+      DP_CUDA(cudaMemcpyAsync(d_wpack + (lo >> 3), hp + (lo >> 3),
+                              words * sizeof(unsigned),
+                              cudaMemcpyHostToDevice, w->copy_stream));
+      *h2d += words * sizeof(unsigned);
+    } else {
+      DP_CUDA(cudaMemcpyAsync(d_weight + lo, weight + lo, (size_t)len * 4,
                               cudaMemcpyHostToDevice, w->copy_stream));
       *h2d += (uint64_t)len * 4;
     }
@@ -2071,14 +2516,25 @@ int dp_sssp(const int32_t* rowptr, const int32_t* col, const int32_t* weight,
     // compute)
     DP_TRY(stage(w_, 1, nullptr, (size_t)m * 4, s_, &h2d_));
     DP_TRY(stage(w_, 4, nullptr, (size_t)m * 4, s_, &h2d_));
-    const void* hsrc[2] = {col, weight};
-    void* ddst[2] = {w_->io[1], w_->io[4]};
     Arrival arr;
     const int shift = chunk_shift(m);
-    DP_TRY(stage_chunked(w_, s_, 2, hsrc, ddst, m, shift, &arr, &h2d_));
+    const unsigned* wpack = nullptr;
+    long long wslots = 0;
+    if (cfg && cfg->weight_bits == 4) {
+      DP_TRY(stage(w_, 3, nullptr, (size_t)((m + 7) / 8 + 1) * 4, s_, &h2d_));
+      wpack = (const unsigned*)w_->io[3];
+      DP_TRY(stage_chunked_packed(w_, s_, col, weight, (int32_t*)w_->io[1],
+                                  (int32_t*)w_->io[4], (unsigned*)w_->io[3],
+                                  m, shift, &arr, &h2d_, &wslots));
+    } else {
+      const void* hsrc[2] = {col, weight};
+      void* ddst[2] = {w_->io[1], w_->io[4]};
+      DP_TRY(stage_chunked(w_, s_, 2, hsrc, ddst, m, shift, &arr, &h2d_));
+    }
     const int rs = sssp_dev_impl((int*)w_->io[0], (int*)w_->io[1],
                                  (int*)w_->io[4], n, src, cfg,
-                                 (int*)w_->io[2], s_, stats, &arr, shift);
+                                 (int*)w_->io[2], s_, stats, &arr, shift,
+                                 wpack, wslots);
     DP_TRY(join_chunked(w_, s_, arr));
     if (rs) {
       cudaStreamSynchronize(s_);
@@ -2094,10 +2550,19 @@ int dp_sssp_dev(const int32_t* d_rowptr, const int32_t* d_col,
                 const dp_config* cfg, int32_t* d_dist, void* stream,
                 dp_stats* stats) {
   clear_stats(stats);
-  (void)m;
   const double t0 = now_ns();
-  int r = sssp_dev_impl(d_rowptr, d_col, d_weight, n, src, cfg, d_dist,
-                        (cudaStream_t)stream, stats);
+  const unsigned* wpack = nullptr;
+  long long wslots = 0;
+  int r = 0;
+  if (cfg && cfg->weight_bits == 4) {
+    Workspace* w = workspace(&r);
+    if (!w) return r;
+    if ((r = pack_weights_dev(w, d_weight, m, (cudaStream_t)stream, &wpack,
+                              &wslots)))
+      return r;
+  }
+  r = sssp_dev_impl(d_rowptr, d_col, d_weight, n, src, cfg, d_dist,
+                    (cudaStream_t)stream, stats, nullptr, 0, wpack, wslots);
   if (stats) stats->ns_host = now_ns() - t0;
   return r;
 }
@@ -2344,6 +2809,71 @@ int dp_sssp_part_round_peer(const int32_t* d_rowptr_p, const int32_t* d_col_p,
                                d_best, d_changed, (cudaStream_t)stream, stats);
   if (stats) stats->ns_host = now_ns() - t0;
   return r;
+}
+
+int dp_sssp_part_solve_peer(const int32_t* d_rowptr_p, const int32_t* d_col_p,
+                            const int32_t* d_weight_p, int32_t n_local,
+                            int32_t n_global, int32_t nparts, int32_t part,
+                            int32_t src, const dp_config* cfg,
+                            int32_t* d_dist_p, int32_t* const* d_peer_dist,
+                            int32_t* d_best, uint64_t* const* d_peer_sig,
+                            uint64_t epoch, void* stream, dp_stats* stats) {
+  clear_stats(stats);
+  const double t0 = now_ns();
+  int r = sssp_part_solve_peer_impl(
+      d_rowptr_p, d_col_p, d_weight_p, n_local, n_global, nparts, part, src,
+      cfg, d_dist_p, d_peer_dist, d_best, d_peer_sig, epoch,
+      (cudaStream_t)stream, stats);
+  if (stats) stats->ns_host = now_ns() - t0;
+  return r;
+}
+
+int dp_bfs_part_solve_peer(const int32_t* d_rowptr_p, const int32_t* d_col_p,
+                           int32_t n_local, int32_t n_global, int32_t nparts,
+                           int32_t part, int32_t src, const dp_config* cfg,
+                           int32_t* d_dist_p, int32_t* const* d_peer_dist,
+                           int32_t* d_counts, int64_t counts_len,
+                           uint32_t* d_sent, uint64_t* const* d_peer_sig,
+                           uint64_t epoch, void* stream, dp_stats* stats) {
+  clear_stats(stats);
+  const double t0 = now_ns();
+  int r = bfs_part_solve_peer_impl(
+      d_rowptr_p, d_col_p, n_local, n_global, nparts, part, src, cfg,
+      d_dist_p, d_peer_dist, d_counts, counts_len, d_sent, d_peer_sig, epoch,
+      (cudaStream_t)stream, stats);
+  if (stats) stats->ns_host = now_ns() - t0;
+  return r;
+}
+
+void dp_thread_release(void) {
+  for (Workspace& w : g_ws) {
+    if (!w.ready) continue;
+    cudaFree(w.tab);
+    cudaFree(w.scan);
+    cudaFree(w.ctr);
+    cudaFree(w.done);
+    cudaFree(w.ds);
+    cudaFreeHost(w.h_ds);
+    cudaFreeHost(w.h_ctr);
+    cudaFree(w.d_scratch);
+    cudaFree(w.d_flag);
+    cudaEventDestroy(w.ev0);
+    cudaEventDestroy(w.ev1);
+    cudaEventDestroy(w.evk0);
+    cudaEventDestroy(w.evk1);
+    cudaFreeHost(w.h_sig);
+    for (void* p : w.io) cudaFree(p);
+    if (w.copy_stream) cudaStreamDestroy(w.copy_stream);
+    cudaFree(w.d_arrived);
+    for (cudaEvent_t e : w.chunk_ev)
+      if (e) cudaEventDestroy(e);
+    cudaFree(w.cwork);
+    cudaFree(w.pub);
+    cudaFree(w.wpack);
+    cudaFreeHost(w.h_wpack);
+    cudaFree(w.d_bad);
+    w = Workspace();
+  }
 }
 
 int dp_sssp_part_apply(const uint64_t* d_recv, int64_t nrecv, int32_t nparts,

@@ -657,6 +657,17 @@ class PeerLocal:
                              dtype=torch.int64, device=parts[0].dist.device)
         for p in parts:
             p.peer_ptrs = table
+        # the parts' round-flag signal slots (dp_*_part_solve_peer)
+        dev = parts[0].dist.device
+        self.sig = [torch.zeros(2 * len(parts), dtype=torch.int64, device=dev)
+                    for _ in parts]
+        self.sig_table = torch.tensor([t.data_ptr() for t in self.sig],
+                                      dtype=torch.int64, device=dev)
+        self.epoch = 0
+
+    def next_epoch(self) -> int:
+        self.epoch += 1
+        return self.epoch
 
     def any_changed(self, parts) -> bool:
         return any(int(p.changed.item()) for p in parts)
@@ -696,9 +707,25 @@ class PeerCollective:
 
     def bind(self, parts) -> None:
         import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
         (p,) = parts
         p.peer_ptrs = torch.tensor(list(self.handle.buffer_ptrs),
                                    dtype=torch.int64, device=p.dist.device)
+        # round-flag signal slots (dp_*_part_solve_peer), mapped like dist
+        self.sig = symm_mem.empty(2 * p.nparts, dtype=torch.int64,
+                                  device=p.dist.device)
+        self.sig.zero_()
+        self.sig_handle = symm_mem.rendezvous(self.sig, dist.group.WORLD)
+        self.sig_table = torch.tensor(list(self.sig_handle.buffer_ptrs),
+                                      dtype=torch.int64, device=p.dist.device)
+        self.epoch = 0
+        torch.cuda.synchronize()
+        dist.barrier()  # every rank's slots are zero before any tag lands
+
+    def next_epoch(self) -> int:
+        self.epoch += 1  # the same sequence of calls on every rank
+        return self.epoch
 
     def any_changed(self, parts) -> bool:
         import torch.distributed as dist
@@ -751,3 +778,97 @@ def bfs_1d_peer(parts: list, ops, exchange, max_levels: int | None = None):
             return (exchange.dist(parts),
                     parts[0].natural_counts(exchange.counts(parts)), level + 1)
     raise RuntimeError("bfs used more levels than vertices")
+
+
+def run_parts(parts, fn, streams=None) -> None:
+    """fn(part, stream) for every part: directly for one part, else one host
+    thread per part, each on its own CUDA stream (the solve drivers block in
+    their round loop until every part has finished the round, so parts that
+    share a process must run concurrently).  Re-raises the first failure."""
+    import threading
+    import torch
+    from . import _lib
+    if len(parts) == 1:
+        fn(parts[0], streams[0] if streams else None)
+        return
+    if streams is None:
+        streams = [torch.cuda.Stream() for _ in parts]
+    errs = [None] * len(parts)
+    lib = _lib.device()
+    torch.cuda.synchronize()  # part state written on the default stream
+
+    def body(i):
+        try:
+            fn(parts[i], ctypes.c_void_p(streams[i].cuda_stream))
+        except BaseException as e:  # noqa: BLE001 - re-raised below
+            errs[i] = e
+        finally:
+            lib.dp_thread_release()
+    threads = [threading.Thread(target=body, args=(i,))
+               for i in range(len(parts))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    torch.cuda.synchronize()
+    for e in errs:
+        if e is not None:
+            raise e
+
+
+def sssp_1d_peer_solve(parts: list, cfg, exchange, src: int = 0,
+                       stream=None, gather: bool = True):
+    """sssp_1d_peer with the round loop in the library
+    (dp_sssp_part_solve_peer): per round one parent grid + one warp that ORs
+    the parts' flags through the signal slots -- no host collective per
+    round.  Returns (dist, rounds); dist is None when gather=False (each
+    part keeps its owned distances in p.dist)."""
+    from . import _lib
+    lib = _lib.device()
+    epoch = exchange.next_epoch()
+
+    def one(p, s):
+        st = _lib.DpStats()
+        _lib.check(lib.dp_sssp_part_solve_peer(
+            p.rowptr.data_ptr(), p.col.data_ptr(), p.weight.data_ptr(),
+            p.n_local, p.n, p.nparts, p.part, src, ctypes.byref(cfg),
+            p.dist.data_ptr(), p.peer_ptrs.data_ptr(), p.best.data_ptr(),
+            exchange.sig_table.data_ptr(), epoch, s, ctypes.byref(st)))
+        p.stats.append(_lib.stats_dict(st))
+    run_parts(parts, one, [stream] if stream is not None and
+              len(parts) == 1 else None)
+    rounds = {int(p.stats[-1]["iterations"]) for p in parts}
+    if len(rounds) != 1:
+        raise RuntimeError(f"parts disagree on the round count: {rounds}")
+    return (exchange.dist(parts) if gather else None), rounds.pop()
+
+
+def bfs_1d_peer_solve(parts: list, cfg, exchange, src: int = 0,
+                      stream=None, gather: bool = True):
+    """bfs_1d_peer with the level loop in the library
+    (dp_bfs_part_solve_peer).  Returns (dist, counts, levels); dist and
+    counts are None when gather=False (p.dist, p.counts hold the parts')."""
+    from . import _lib
+    lib = _lib.device()
+    epoch = exchange.next_epoch()
+
+    def one(p, s):
+        c = type(cfg).from_buffer_copy(cfg)
+        c.counts_spread = p.counts_log2
+        st = _lib.DpStats()
+        _lib.check(lib.dp_bfs_part_solve_peer(
+            p.rowptr.data_ptr(), p.col.data_ptr(), p.n_local, p.n, p.nparts,
+            p.part, src, ctypes.byref(c), p.dist.data_ptr(),
+            p.peer_ptrs.data_ptr(), p.counts.data_ptr(), p.counts.numel(),
+            p.sent.data_ptr(), exchange.sig_table.data_ptr(), epoch, s,
+            ctypes.byref(st)))
+        p.stats.append(_lib.stats_dict(st))
+    run_parts(parts, one, [stream] if stream is not None and
+              len(parts) == 1 else None)
+    levels = {int(p.stats[-1]["iterations"]) for p in parts}
+    if len(levels) != 1:
+        raise RuntimeError(f"parts disagree on the level count: {levels}")
+    if not gather:
+        return None, None, levels.pop()
+    return (exchange.dist(parts),
+            parts[0].natural_counts(exchange.counts(parts)), levels.pop())

@@ -23,8 +23,10 @@ torch.cuda.set_device(0)
 s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 G = DeviceGraph(scale, 1, weights=True)
 out = {}
+import os
+extra = json.loads(os.environ.get("AB_POLICY", "{}"))
 for kind in kinds:
-    cfg = _cfg(BEST[kind])
+    cfg = _cfg(dict(BEST[kind], **extra))
     ts = []
     for _ in range(8):
         st = run_dev(kind, G, cfg, s)
@@ -63,7 +65,8 @@ def main():
     res = {lib: [] for lib in libs}
     for _ in range(2):
         for lib in libs:
-            env = dict(os.environ, DYNPAR_LIB=str(Path(lib).resolve()))
+            env = dict(os.environ, DYNPAR_LIB=str(Path(lib).resolve()),
+                       DYNPAR_LIB_PARTIAL="1")
             p = subprocess.run([sys.executable, "-c", CHILD, str(ROOT), kinds,
                                 scale], env=env, capture_output=True, text=True,
                                timeout=600)

@@ -22,6 +22,18 @@ from paper_2201_02789_b200.bench.graphs import (BT_CURV_SCALE,  # noqa: E402
                                                 BT_MAX_TESS, bezier_curves)
 
 POLICIES = [
+    dict(threshold=INF_THRESHOLD, serial="warp", parent_block=32),
+    dict(threshold=INF_THRESHOLD, serial="warp", parent_block=128),
+    dict(threshold=256, cfactor=1, agg="multiblock", group_size=1 << 20,
+         parent_block=64, child_block=256, serial="warp"),
+    dict(threshold=512, cfactor=1, agg="multiblock", group_size=1 << 20,
+         parent_block=64, child_block=256, serial="warp"),
+    dict(threshold=512, cfactor=2, agg="multiblock", group_size=1 << 20,
+         parent_block=64, child_block=128, serial="warp"),
+    dict(threshold=1024, cfactor=1, agg="multiblock", group_size=1 << 20,
+         parent_block=64, child_block=256, serial="warp"),
+    dict(threshold=512, cfactor=1, agg="multiblock", group_size=64,
+         parent_block=64, child_block=256, serial="warp"),
     dict(threshold=INF_THRESHOLD, serial="warp", parent_block=64),
     dict(threshold=INF_THRESHOLD, serial="warp", parent_block=256),
     dict(threshold=INF_THRESHOLD, serial="thread", parent_block=64),
@@ -108,6 +120,8 @@ def main():
                               "gbps_alg": round(alg / (t * 1e3), 1),
                               "frac_hbm": round(alg / (t * 1e3) / hbm, 3),
                               "launches": st["num_launches"],
+                              "launch_lat_us": round(
+                                  st["launch_lat_ns_mean"] / 1e3, 2),
                               "policy": pol}), flush=True)
         best = min(res, key=lambda r: r[0])
         bt.run(best[1])
