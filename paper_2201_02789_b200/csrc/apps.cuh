@@ -545,12 +545,15 @@ __device__ __forceinline__ int packed_weight(const unsigned* __restrict__ wp,
   return (int)((__ldg(wp + (e >> 3)) >> ((e & 7) << 2)) & 15u) + 1;
 }
 
-struct SsspApp {
+// kPacked: the weights are read from `wpack` only (a separate
+// instantiation: a per-edge choice between the two arrays cost the headline
+// kernel its register budget, 1.66 -> 3.1 ms)
+template <bool kPacked>
+struct SsspAppT {
   const int* __restrict__ rowptr;
   const int* __restrict__ col;
   const int* __restrict__ weight;
-  const unsigned* __restrict__ wpack;  // packed weights (null: none)
-  long long wslots;                    // slots [0, wslots) are packed
+  const unsigned* __restrict__ wpack;  // kPacked: nibble-packed weights
   int* dist;
   int* changed;
   int* changed_next;
@@ -578,8 +581,8 @@ struct SsspApp {
       if (arrived) *skipped_next = 0;
     }
   }
-  __device__ SsspApp for_round(int r, int* flags) const {
-    SsspApp a = *this;
+  __device__ SsspAppT for_round(int r, int* flags) const {
+    SsspAppT a = *this;
     a.changed = flags + (r & 1);
     a.changed_next = flags + ((r + 1) & 1);
     return a;
@@ -616,7 +619,10 @@ struct SsspApp {
   // exactly when the old value was larger.  Arithmetic wraps like the
   // reference's 32-bit ints (sim/compile.py:36-37).
   __device__ int weight_of(int i) const {
-    return i < wslots ? packed_weight(wpack, i) : ld_stream(weight + i);
+    if constexpr (kPacked)
+      return packed_weight(wpack, i);
+    else
+      return ld_stream(weight + i);
   }
   __device__ void item(const Args& a, int e, Acc& acc) const {
     const int v = __ldg(col + a.start + e);
@@ -667,6 +673,9 @@ struct SsspApp {
       *changed = 1;
   }
 };
+
+using SsspApp = SsspAppT<false>;
+using SsspPackedApp = SsspAppT<true>;
 
 // ---------------------------------------------------------------------------
 // manylaunch — MANYLAUNCH_CDP main/spawn (bench/benchmarks.py:283-300)

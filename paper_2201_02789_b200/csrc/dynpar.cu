@@ -956,31 +956,39 @@ __global__ void pack_weights_kernel(const int* __restrict__ w, long long m,
 // weight lies outside [1, 16].  OpenMP over the host cores.
 bool pack_weights_host(const int32_t* w, long long lo, long long len,
                        unsigned* out) {
-  const long long words = (len + 7) / 8;
-  int bad = 0;
+  const long long full = len / 8;  // whole words: fixed trip count (SIMD)
+  unsigned bad = 0;
 #pragma omp parallel for reduction(| : bad) schedule(static)
-  for (long long k = 0; k < words; ++k) {
-    unsigned word = 0;
-    const long long e0 = lo + k * 8;
-    const int jn = (int)std::min<long long>(8, lo + len - e0);
-    for (int j = 0; j < jn; ++j) {
-      const unsigned v = (unsigned)(w[e0 + j] - 1);
-      bad |= v > 15u;
+  for (long long k = 0; k < full; ++k) {
+    const int32_t* x = w + lo + k * 8;
+    unsigned word = 0, b = 0;
+#pragma GCC unroll 8
+    for (int j = 0; j < 8; ++j) {
+      const unsigned v = (unsigned)(x[j] - 1);
+      b |= v;
       word |= (v & 15u) << (4 * j);
     }
+    bad |= b;
     out[(lo >> 3) + k] = word;
   }
-  return !bad;
+  if (full * 8 < len) {  // tail word
+    unsigned word = 0;
+    for (long long e = lo + full * 8; e < lo + len; ++e) {
+      const unsigned v = (unsigned)(w[e] - 1);
+      bad |= v;
+      word |= (v & 15u) << (4 * (e & 7));
+    }
+    out[(lo >> 3) + full] = word;
+  }
+  return bad <= 15u;  // the OR of every (w - 1) fits 4 bits
 }
 
 // dp_config.weight_bits = 4 with resident weights: pack them on the device;
-// *wpack / *wslots stay null / 0 when some weight lies outside [1, 16]
+// *wpack stays null when some weight lies outside [1, 16]
 int pack_weights_dev(Workspace* w, const int32_t* weight, long long m,
-                     cudaStream_t s, const unsigned** wpack,
-                     long long* wslots) {
+                     cudaStream_t s, const unsigned** wpack) {
   int r;
   *wpack = nullptr;
-  *wslots = 0;
   if (m <= 0) return 0;
   if ((r = grow(&w->wpack, &w->wpack_bytes,
                 (size_t)((m + 7) / 8) * sizeof(unsigned))))
@@ -996,10 +1004,7 @@ int pack_weights_dev(Workspace* w, const int32_t* weight, long long m,
   DP_CUDA(cudaMemcpyAsync(&bad, w->d_bad, sizeof(int), cudaMemcpyDeviceToHost,
                           s));
   DP_CUDA(cudaStreamSynchronize(s));
-  if (!bad) {
-    *wpack = (const unsigned*)w->wpack;
-    *wslots = m;
-  }
+  if (!bad) *wpack = (const unsigned*)w->wpack;
   return 0;
 }
 
@@ -1007,7 +1012,7 @@ int sssp_dev_impl(const int32_t* rowptr, const int32_t* col,
                   const int32_t* weight, int32_t n, int32_t src,
                   const dp_config* c, int32_t* dist, cudaStream_t s,
                   dp_stats* st, Arrival* arr = nullptr, int shift = 0,
-                  const unsigned* wpack = nullptr, long long wslots = 0) {
+                  const unsigned* wpack = nullptr) {
   int r;
   if ((r = validate(c))) return r;
   if (n < 1) return fail(DP_ERR_INVALID, "graph must have at least 1 vertex");
@@ -1029,26 +1034,29 @@ int sssp_dev_impl(const int32_t* rowptr, const int32_t* col,
   // bench/benchmarks.py:259-270: rounds until a full round changes nothing
   // (and, while edges are still landing, no parent was deferred)
   const int max_iter = n + (arr ? arr->nchunks + 1 : 0);
-  return iterate(w, c, n, launchers, max_iter, s,
-                 [&](int round, DevState* ds) {
-                   SsspApp a;
-                   a.rowptr = rowptr;
-                   a.col = col;
-                   a.weight = weight;
-                   a.wpack = wpack;
-                   a.wslots = wpack ? wslots : 0;
-                   a.dist = dist;
-                   a.changed = &ds->flag[round & 1];
-                   a.changed_next = &ds->flag[(round + 1) & 1];
-                   a.last = last;
-                   a.arrived = arr ? w->d_arrived : nullptr;
-                   a.skipped = &ds->skipped[round & 1];
-                   a.skipped_next = &ds->skipped[(round + 1) & 1];
-                   a.n = n;
-                   a.shift = shift;
-                   return a;
-                 },
-                 st, arr);
+  auto run = [&](auto tag) {
+    using App = decltype(tag);
+    return iterate(w, c, n, launchers, max_iter, s,
+                   [&](int round, DevState* ds) {
+                     App a;
+                     a.rowptr = rowptr;
+                     a.col = col;
+                     a.weight = weight;
+                     a.wpack = wpack;
+                     a.dist = dist;
+                     a.changed = &ds->flag[round & 1];
+                     a.changed_next = &ds->flag[(round + 1) & 1];
+                     a.last = last;
+                     a.arrived = arr ? w->d_arrived : nullptr;
+                     a.skipped = &ds->skipped[round & 1];
+                     a.skipped_next = &ds->skipped[(round + 1) & 1];
+                     a.n = n;
+                     a.shift = shift;
+                     return a;
+                   },
+                   st, arr);
+  };
+  return wpack ? run(SsspPackedApp{}) : run(SsspApp{});
 }
 
 __global__ void gc_key_kernel(const int* __restrict__ rowptr, int n,
@@ -2311,13 +2319,15 @@ int stage_chunked(Workspace* w, cudaStream_t s, int nsrc, const void* const* hos
 // dp_sssp with weight_bits = 4: as stage_chunked for (col, weight), but each
 // weight chunk is first packed on the host (OpenMP, into pinned staging) and
 // copied as nibbles, 1/8 of the bytes; the packing of chunk k + 1 overlaps
-// the DMA of chunk k.  The first chunk holding a weight outside [1, 16] and
-// every later one are copied as int32 instead: *wslots = the packed prefix.
+// the DMA of chunk k.  At the first chunk holding a weight outside [1, 16]
+// the call reverts to int32 weights: the earlier chunks' int32 weights are
+// copied and awaited (before any round can read them), the rest stream as
+// int32.  *packed: every chunk went packed.
 int stage_chunked_packed(Workspace* w, cudaStream_t s, const int32_t* col,
                          const int32_t* weight, int32_t* d_col,
                          int32_t* d_weight, unsigned* d_wpack, int64_t m,
                          int shift, Arrival* arr, uint64_t* h2d,
-                         long long* wslots) {
+                         bool* packed_all) {
   if (!w->copy_stream) {
     DP_CUDA(cudaStreamCreateWithFlags(&w->copy_stream, cudaStreamNonBlocking));
     DP_CUDA(cudaMalloc(&w->d_arrived, sizeof(int)));
@@ -2343,7 +2353,6 @@ int stage_chunked_packed(Workspace* w, cudaStream_t s, const int32_t* col,
   DP_CUDA(cudaEventRecord(w->evk0, s));
   DP_CUDA(cudaStreamWaitEvent(w->copy_stream, w->evk0, 0));
   bool packed = true;
-  *wslots = m;
   for (int k = 0; k < arr->nchunks; ++k) {
     const int64_t lo = (int64_t)k * chunk;
     const int64_t len = std::min(chunk, m - lo);
@@ -2352,7 +2361,12 @@ int stage_chunked_packed(Workspace* w, cudaStream_t s, const int32_t* col,
     *h2d += (uint64_t)len * 4;
     if (packed && !pack_weights_host(weight, lo, len, hp)) {
       packed = false;
-      *wslots = lo;
+      if (lo > 0) {  // chunks [0, k) arrived packed only: add their int32
+        DP_CUDA(cudaMemcpyAsync(d_weight, weight, (size_t)lo * 4,
+                                cudaMemcpyHostToDevice, w->copy_stream));
+        *h2d += (uint64_t)lo * 4;
+        DP_CUDA(cudaStreamSynchronize(w->copy_stream));
+      }
     }
     if (packed) {
       const size_t words = (size_t)((len + 7) / 8);
@@ -2369,6 +2383,7 @@ int stage_chunked_packed(Workspace* w, cudaStream_t s, const int32_t* col,
     DP_CUDA(cudaGetLastError());
     DP_CUDA(cudaEventRecord(w->chunk_ev[k], w->copy_stream));
   }
+  *packed_all = packed;
   return 0;
 }
 
@@ -2519,13 +2534,13 @@ int dp_sssp(const int32_t* rowptr, const int32_t* col, const int32_t* weight,
     Arrival arr;
     const int shift = chunk_shift(m);
     const unsigned* wpack = nullptr;
-    long long wslots = 0;
     if (cfg && cfg->weight_bits == 4) {
       DP_TRY(stage(w_, 3, nullptr, (size_t)((m + 7) / 8 + 1) * 4, s_, &h2d_));
-      wpack = (const unsigned*)w_->io[3];
+      bool all = false;
       DP_TRY(stage_chunked_packed(w_, s_, col, weight, (int32_t*)w_->io[1],
                                   (int32_t*)w_->io[4], (unsigned*)w_->io[3],
-                                  m, shift, &arr, &h2d_, &wslots));
+                                  m, shift, &arr, &h2d_, &all));
+      if (all) wpack = (const unsigned*)w_->io[3];
     } else {
       const void* hsrc[2] = {col, weight};
       void* ddst[2] = {w_->io[1], w_->io[4]};
@@ -2534,7 +2549,7 @@ int dp_sssp(const int32_t* rowptr, const int32_t* col, const int32_t* weight,
     const int rs = sssp_dev_impl((int*)w_->io[0], (int*)w_->io[1],
                                  (int*)w_->io[4], n, src, cfg,
                                  (int*)w_->io[2], s_, stats, &arr, shift,
-                                 wpack, wslots);
+                                 wpack);
     DP_TRY(join_chunked(w_, s_, arr));
     if (rs) {
       cudaStreamSynchronize(s_);
@@ -2552,17 +2567,15 @@ int dp_sssp_dev(const int32_t* d_rowptr, const int32_t* d_col,
   clear_stats(stats);
   const double t0 = now_ns();
   const unsigned* wpack = nullptr;
-  long long wslots = 0;
   int r = 0;
   if (cfg && cfg->weight_bits == 4) {
     Workspace* w = workspace(&r);
     if (!w) return r;
-    if ((r = pack_weights_dev(w, d_weight, m, (cudaStream_t)stream, &wpack,
-                              &wslots)))
+    if ((r = pack_weights_dev(w, d_weight, m, (cudaStream_t)stream, &wpack)))
       return r;
   }
   r = sssp_dev_impl(d_rowptr, d_col, d_weight, n, src, cfg, d_dist,
-                    (cudaStream_t)stream, stats, nullptr, 0, wpack, wslots);
+                    (cudaStream_t)stream, stats, nullptr, 0, wpack);
   if (stats) stats->ns_host = now_ns() - t0;
   return r;
 }

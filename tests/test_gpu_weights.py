@@ -1,0 +1,91 @@
+"""Packed SSSP weights (dp_config.weight_bits = 4): weights in [1, 16] are
+read as nibbles; outside that range the device path falls back to int32 and
+the host-buffer path keeps int32 for the first chunk holding such a weight
+and every later one.  Distances must equal the oracle's bit for bit in all
+cases, and the host path must copy fewer bytes when it packs."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import oracle
+from paper_2201_02789_b200.bench import BenchConfig, load, run_config
+from paper_2201_02789_b200.bench.benchmarks import Workload
+
+pytestmark = pytest.mark.gpu
+
+POLICIES = [
+    dict(weight_bits=4),
+    dict(threshold=64, cfactor=4, agg="multiblock", group_size=1 << 20,
+         serial="warp", weight_bits=4),
+    dict(threshold=1024, cfactor=16, agg="multiblock", group_size=1 << 20,
+         parent_block=128, child_block=128, serial="warp", weight_bits=4),
+    dict(threshold=32, agg="grid", frontier=True, weight_bits=4),
+]
+
+
+def _with_weights(wl, weight):
+    return Workload(wl.spec, dict(wl.buffers, weight=weight), wl.n,
+                    wl.payload)
+
+
+def _device_dist(wl, policy):
+    import ctypes
+    import torch
+    from paper_2201_02789_b200 import _lib
+    b = wl.buffers
+    dev = torch.device("cuda", 0)
+    t = {k: torch.from_numpy(np.ascontiguousarray(b[k], np.int32)).to(dev)
+         for k in ("rowptr", "col", "weight")}
+    dist = torch.empty(wl.n, dtype=torch.int32, device=dev)
+    st = _lib.DpStats()
+    _lib.check(_lib.device().dp_sssp_dev(
+        t["rowptr"].data_ptr(), t["col"].data_ptr(), t["weight"].data_ptr(),
+        wl.n, int(b["col"].shape[0]), 0,
+        ctypes.byref(BenchConfig(**policy).to_c()), dist.data_ptr(), None,
+        ctypes.byref(st)))
+    return dist.cpu().numpy()
+
+
+@pytest.mark.parametrize("spec", ["powerlaw:2000:seed1", "road:1000:seed7",
+                                  "rmat:16:seed1"])
+@pytest.mark.parametrize("pi", range(len(POLICIES)))
+def test_packed_weights_exact(spec, pi):
+    bench, wl = load("sssp", spec)
+    b = wl.buffers
+    want, _ = oracle.sssp(b["rowptr"], b["col"], b["weight"], nthreads=0)
+    np.testing.assert_array_equal(_device_dist(wl, POLICIES[pi]), want)
+    rep, _ = run_config(bench, wl, BenchConfig(**POLICIES[pi]))  # dp_sssp
+    np.testing.assert_array_equal(rep.arrays["dist"], want)
+
+
+@pytest.mark.parametrize("where", ["first", "middle", "last", "none"])
+def test_out_of_range_weights_fall_back(where, monkeypatch):
+    """Weights > 16 (or < 1) in some chunk: that chunk and the later ones
+    travel as int32, the earlier ones packed; the device path drops packing
+    altogether."""
+    monkeypatch.setenv("DP_COPY_CHUNK_SHIFT", "12")  # many small chunks
+    bench, wl = load("sssp", "rmat:14:seed1")
+    w = np.array(wl.buffers["weight"], dtype=np.int32)
+    m = w.shape[0]
+    if where != "none":
+        at = {"first": 5, "middle": m // 2, "last": m - 1}[where]
+        w[at] = 40
+        w[(at * 7) % m] = 17
+    wl2 = _with_weights(wl, w)
+    want, _ = oracle.sssp(wl.buffers["rowptr"], wl.buffers["col"], w,
+                          nthreads=0)
+    for pol in POLICIES[:3]:
+        np.testing.assert_array_equal(_device_dist(wl2, pol), want)
+        rep, _ = run_config(bench, wl2, BenchConfig(**pol))
+        np.testing.assert_array_equal(rep.arrays["dist"], want)
+
+
+def test_host_packing_copies_fewer_bytes():
+    bench, wl = load("sssp", "rmat:16:seed1")
+    m = wl.buffers["col"].shape[0]
+    r0, _ = run_config(bench, wl, BenchConfig())
+    r4, _ = run_config(bench, wl, BenchConfig(weight_bits=4))
+    np.testing.assert_array_equal(r0.arrays["dist"], r4.arrays["dist"])
+    # int32 weights: 4 B per slot; packed: 0.5 B per slot
+    assert r0.h2d_bytes - r4.h2d_bytes >= int(m * 3.4)
