@@ -357,7 +357,24 @@ def extra_workloads(stream, quick: bool) -> dict:
         BEST["bfs"], lambda p: statistics.median(
             run_dev("bfs", G, _cfg(p), stream)["ns_device"]
             for _ in range(3)) / 1e6)
+    ceil = read_ceilings()
+    vs = ceil.get("visit_spread")
+    l2c = None
+    if vs and ceil.get("m"):
+        # the same per-edge visit as a flat, perfectly balanced kernel over
+        # all m edges (L2-atomic / probe bound): time for e_t edges
+        flat_ms = vs["ms"] * e_t / ceil["m"]
+        l2c = {"ceiling": "flat visit of every edge, spread counts + merged "
+                          "RED + probe + CAS (tools/ceiling.cu visit_spread)",
+               "ceiling_g_edges_per_s": ceil["m"] / vs["ms"] / 1e6,
+               "frac": flat_ms / ms,
+               "red_hashed_g_ops_per_s":
+                   ceil.get("red_hashed", {}).get("g_ops_per_s"),
+               "probe_g_ops_per_s":
+                   ceil.get("probe_targets", {}).get("g_ops_per_s"),
+               "source": "profiles/ceilings.json"}
     out["bfs_rmat22"] = {"gteps": e_t / ms / 1e6, "ms": ms,
+                         "l2_ceiling": l2c,
                          "vs_agg_only_matched": min(matched.values()) / ms,
                          "agg_only_matched_ms": matched,
                          "levels": runs[0]["iterations"],
@@ -841,6 +858,10 @@ def arm_ours(args, world, rank, local):
                                   "(+CDP2 children)",
                         "alg_bytes_per_launch": alg_round,
                         "ms_per_launch": per_round / 1e6,
+                        # the same round against its measured DRAM bytes
+                        # (ncu, profiles/traffic.json): dist probes hit L1/L2
+                        "achieved_dram": (read_traffic() or 0) / per_round,
+                        "frac_dram": (read_traffic() or 0) / per_round / peak,
                         "share_of_step": sum(s["ns_kernel_sum"] for s in stats)
                         / (total_ms * 1e6)}
     line["clocks"] = clk.summary()
@@ -1210,6 +1231,16 @@ def arm_bt(args, world, rank, local):
     line = measure_bt(args, world, rank, local, n)
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def read_ceilings() -> dict:
+    """Flat-kernel ceilings of the BFS / SSSP edge work measured on the same
+    RMAT-22 target stream (tools/ceiling.py --write -> profiles/
+    ceilings.json), or {}."""
+    try:
+        return json.loads((ROOT / "profiles" / "ceilings.json").read_text())
+    except Exception:  # noqa: BLE001
+        return {}
 
 
 def read_traffic():

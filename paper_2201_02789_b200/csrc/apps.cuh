@@ -69,6 +69,9 @@ namespace dp {
 #ifndef DP_BFS_NO_COUNTS
 #define DP_BFS_NO_COUNTS 0  // ablation only (wrong counts): the cost of counts
 #endif
+#ifndef DP_SSSPPEER_MINB
+#define DP_SSSPPEER_MINB DP_SSSP_MINB  // fused-exchange SSSP (A/B knob)
+#endif
 #ifndef DP_SSSP_MINB
 #define DP_SSSP_MINB 8  // <= 32 registers: full occupancy for the latency-
 #endif                  // bound relaxations (tools/ab.sh, profiles/)
@@ -501,7 +504,7 @@ struct SsspPeerApp {
   static constexpr int kChildUnroll = DP_SSSP_CHILD_UNROLL;
   static constexpr bool kBlockMode = false;
   static constexpr bool kPureExpand = true;
-  static constexpr int kMinBlocks = DP_SSSP_MINB;
+  static constexpr int kMinBlocks = DP_SSSPPEER_MINB;
   template <int U, class ArgsOf>
   __device__ __forceinline__ void items(ArgsOf args, const int* e,
                                         const bool* ok, Acc& acc) const {

@@ -244,6 +244,47 @@ __global__ void red_one_line(const int* __restrict__ col, long long m,
 
 extern "C" {
 
+// the BFS visit exactly as BfsApp does it since round 2: counts in the
+// spread layout (common.cuh spread_slot, 4096-vertex blocks), lanes hitting
+// the same vertex merged, L1 probe, CAS on discovery -- flat and perfectly
+// balanced: the ceiling of the nested BFS's per-edge work
+__device__ __forceinline__ uint32_t spread_slot(uint32_t v, uint32_t mask) {
+  uint32_t x = (v * 0x9E3779B1u) & mask;
+  x ^= x >> 7;
+  x = (x * 0x85EBCA77u) & mask;
+  return (v & ~mask) | x;
+}
+
+__global__ void visit_spread(const int* __restrict__ col, long long m,
+                             int* dist, int* counts, int level, int* changed) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long nit = (m + stride * 2 - 1) / (stride * 2);
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  int ch = 0;
+  for (long long it = 0; it < nit; ++it) {
+    int v[2], d[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const long long e = t + (it * 2 + j) * stride;
+      v[j] = e < m ? ld_stream(col + e) : -1;
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) d[j] = v[j] >= 0 ? __ldca(dist + v[j]) : 0;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const unsigned g = __match_any_sync(FULL, v[j]);
+      if (v[j] < 0) continue;
+      if ((threadIdx.x & 31) == __ffs(g) - 1)
+        atomicAdd(counts + spread_slot((uint32_t)v[j], 4095u), __popc(g));
+      if (d[j] == kUnreached &&
+          atomicCAS(dist + v[j], kUnreached, level + 1) == kUnreached)
+        ch = 1;
+    }
+  }
+  if (__any_sync(FULL, ch) && (threadIdx.x & 31) == 0 && __ldcg(changed) == 0)
+    *changed = 1;
+}
+
 int ceil_run(int which, const int* col, const int* w, long long m, int* dist,
              int* counts, uint32_t nmask, int grid, int block, int* scratch,
              cudaStream_t s) {
@@ -264,6 +305,9 @@ int ceil_run(int which, const int* col, const int* w, long long m, int* dist,
     case 9: red_hashed<<<grid, block, 0, s>>>(col, m, counts, nmask); break;
     case 10: red_single<<<grid, block, 0, s>>>(col, m, counts); break;
     case 11: red_one_line<<<grid, block, 0, s>>>(col, m, counts); break;
+    case 12: visit_spread<<<grid, block, 0, s>>>(col, m, dist, counts, 0,
+                                                 scratch);
+             break;
     default: return -1;
   }
   return (int)cudaGetLastError();

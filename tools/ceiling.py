@@ -18,7 +18,8 @@ SO = ROOT / "tools" / "libceiling.so"
 
 
 def build():
-    if not SO.exists():
+    if not SO.exists() or SO.stat().st_mtime < (
+            ROOT / "tools" / "ceiling.cu").stat().st_mtime:
         subprocess.run(["nvcc", "-O3", "-lineinfo", "-gencode",
                         "arch=compute_100a,code=sm_100a", "-Xcompiler", "-fPIC",
                         "-shared", "-o", str(SO),
@@ -33,12 +34,13 @@ def build():
 NAMES = {0: "stream_col", 1: "stream_col_int4", 2: "red_uniform",
          3: "red_targets", 4: "red_merged", 5: "probe_targets",
          6: "visit_flat", 7: "relax_flat", 8: "cas_uniform", 9: "red_hashed",
-         10: "red_single_address", 11: "red_one_line"}
+         10: "red_single_address", 11: "red_one_line", 12: "visit_spread"}
 
 
 def main():
-    scale = int(sys.argv[1]) if len(sys.argv) > 1 else 22
-    only = [int(x) for x in sys.argv[2].split(",")] if len(sys.argv) > 2 \
+    argv = [a for a in sys.argv[1:] if a != "--write"]
+    scale = int(argv[0]) if argv else 22
+    only = [int(x) for x in argv[1].split(",")] if len(argv) > 1 \
         else list(NAMES)
     L = build()
     from bench import BEST, DeviceGraph, _cfg, run_dev
@@ -61,7 +63,7 @@ def main():
             ts = []
             for it in range(6):
                 G.counts.zero_()
-                if which == 6:
+                if which in (6, 12):
                     G.dist.fill_(1 << 30)
                     G.dist[0] = 0
                 elif which == 7:
@@ -108,11 +110,18 @@ def main():
             r["g_edges_per_s"] = e_t / r["ms"] / 1e6
             r["frac_of_visit_flat"] = (
                 out["visit_flat"]["ms"] * e_t / m) / r["ms"]
+            if "visit_spread" in out:
+                r["frac_of_visit_spread"] = (
+                    out["visit_spread"]["ms"] * e_t / m) / r["ms"]
         else:
             r["ms_per_round"] = st["ns_kernel_sum"] / 1e6 / st["iterations"]
             r["frac_of_relax_flat_per_round"] = (
                 out["relax_flat"]["ms"] / r["ms_per_round"])
+        out[r["kernel"]] = r
         print(json.dumps(r), flush=True)
+    if "--write" in sys.argv:  # the summary bench.py reports against
+        (ROOT / "profiles" / "ceilings.json").write_text(
+            json.dumps(out, indent=1) + "\n")
 
 
 if __name__ == "__main__":
