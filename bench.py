@@ -77,6 +77,90 @@ BEST = {
 }
 
 
+def bt_stream_row(ncurves: int, quick: bool) -> dict:
+    """BT at a streaming size on one GPU (the 25k config is
+    launch-sized): device time of the tessellation (CUDA events inside
+    libdynpar), algorithmic bytes 36 B/curve + 8 B/vertex against HBM."""
+    import torch
+    from paper_2201_02789_b200 import _lib
+    from paper_2201_02789_b200.bench.graphs import (BT_CURV_SCALE,
+                                                    BT_MAX_TESS,
+                                                    bezier_curves)
+    lib = _lib.device()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    cp_h = np.ascontiguousarray(bezier_curves(ncurves, 1), dtype=np.float32)
+    cp = torch.from_numpy(cp_h).to(dev)
+    cap = ncurves * 128 + (1 << 16)
+    ntess = torch.empty(ncurves, dtype=torch.int32, device=dev)
+    offs = torch.empty(ncurves, dtype=torch.int64, device=dev)
+    verts = torch.empty((cap, 2), dtype=torch.float32, device=dev)
+    used = ctypes.c_int64()
+    cfg = _cfg(BEST["bt"])
+    ts = []
+    for _ in range(7):
+        st = _lib.DpStats()
+        _lib.check(lib.dp_bt_dev(cp.data_ptr(), ncurves, BT_MAX_TESS,
+                                 BT_CURV_SCALE, ctypes.byref(cfg),
+                                 ntess.data_ptr(), offs.data_ptr(),
+                                 verts.data_ptr(), cap, ctypes.byref(used),
+                                 None, ctypes.byref(st)))
+        ts.append(st.ns_device / 1e6)
+    ms = statistics.median(ts[2:])
+    nv = int(used.value)
+    alg = 36 * ncurves + 8 * nv
+    peak, src = hbm_peak()
+    row = {"curves": ncurves, "ms": ms, "curves_per_s": ncurves / ms * 1e3,
+           "vertices": nv, "gbps_alg": alg / (ms * 1e6),
+           "frac_hbm": alg / (ms * 1e6) / peak, "peak_source": src,
+           "policy": BEST["bt"]}
+    if not quick:
+        from oracle import oracle
+        want_nt, want_v = oracle.bt(cp_h, BT_MAX_TESS, BT_CURV_SCALE)
+        cs = float(verts[:nv].double().sum().item())
+        want_cs = float(np.asarray(want_v, dtype=np.float64).sum())
+        ok = (np.array_equal(ntess.cpu().numpy(), want_nt)
+              and abs(cs - want_cs) <= 1e-6 * max(1.0, abs(want_cs)))
+        row["parity"] = ("vertex counts exact, fp64 checksum within 1e-6 of "
+                         "the oracle" if ok else "MISMATCH")
+    del verts
+    torch.cuda.empty_cache()
+    return row
+
+
+def reference_cpu_bfs(rowptr, col) -> dict | None:
+    """BASELINE.md §3 `cpu_ref_s`: the reference's own CPU path,
+    `dynoptc.bench.run_reference` (BFS_NOCDP on its pure-Python simulator,
+    one core), on our RMAT CSR injected through its Workload
+    (tests/golden/make_golden.py does the same).  Runs the unmodified
+    reference installed in baseline/_ref (pip --target, git-ignored, shipped
+    to the box); None when it is not installed."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "dynoptc").is_dir():
+        return None
+    sys.path.insert(0, str(ref))
+    try:
+        from dynoptc.bench import get_benchmark, run_reference
+        from dynoptc.bench.benchmarks import Workload
+        from dynoptc.bench.graphs import UNREACHED, DatasetSpec, Graph
+        rp = [int(x) for x in rowptr]
+        cl = [int(x) for x in col]
+        g = Graph(tuple(rp), tuple(cl))
+        dist = [UNREACHED] * g.n
+        dist[0] = 0
+        bufs = {"rowptr": rp, "col": cl, "dist": dist, "counts": [0] * g.n,
+                "changed": [0]}
+        wl = Workload(DatasetSpec("rmat", 16, SEED, f"rmat:16:seed{SEED}"),
+                      bufs, g.n, g)
+        t0 = time.perf_counter()
+        rep = run_reference(get_benchmark("bfs"), wl)
+        dt = time.perf_counter() - t0
+        return {"seconds": dt, "cores": 1, "kind": "reference",
+                "dist": np.asarray(rep.buffers["dist"], dtype=np.int64),
+                "counts": np.asarray(rep.buffers["counts"], dtype=np.int64)}
+    finally:
+        sys.path.remove(str(ref))
+
+
 def matched_agg_only(pol: dict, time_ms) -> dict:
     """The aggregation-only (KLAP-style) build like-for-like with a tuned
     policy: T = 0, C = 1, the policy's own parent / child blocks and serial
@@ -339,8 +423,25 @@ def extra_workloads(stream, quick: bool) -> dict:
         "launch_lat_us": runs[0]["launch_lat_ns_mean"] / 1e3,
         "vs_naive_cdp": naive16["ns_device"] / 1e6 / ms,
         "naive_cdp_launches": naive16["num_launches"],
-        "reference_python_cpu_s": 3.08,  # BASELINE.md §2 (own RMAT, 1 core)
         "policy": c1}
+    ref = None if quick else reference_cpu_bfs(G16.g.rowptr, G16.g.col)
+    row = out["config1_bfs_rmat16_t128_block"]
+    if ref is None:
+        row["cpu_baseline"] = {
+            "value": None, "note": "reference not installed in baseline/_ref;"
+            " BASELINE.md §2 measured 3.08 s (1 core) in the build container"}
+    else:
+        ok = (np.array_equal(ref["dist"], G16.dist.cpu().numpy())
+              and np.array_equal(ref["counts"], G16.counts.cpu().numpy()))
+        row["cpu_baseline"] = {
+            "value": e16 / ref["seconds"] / 1e9, "unit": "GTEPS",
+            "seconds": ref["seconds"], "cores": 1, "kind": "reference",
+            "sample": "dynoptc.bench.run_reference (BFS_NOCDP on the "
+                      "reference's simulator) on the same RMAT-16 CSR, "
+                      "unmodified reference from baseline/_ref"}
+        row["parity"] = ("dist and counts equal the reference's own run"
+                         if ok else "MISMATCH vs the reference")
+        row["vs_reference_cpu"] = ref["seconds"] * 1e3 / ms
     del G16
     # BFS RMAT-22
     G = DeviceGraph(SCALE, SEED, weights=False)
@@ -476,17 +577,21 @@ def extra_workloads(stream, quick: bool) -> dict:
     out["bt_25k"]["agg_only_matched_ms"] = matched
     out["bt_25k"]["vs_naive_cdp"] = naive.ns_device / 1e6 / ms
     out["bt_25k"]["vs_agg_only"] = min(agg_ms.values()) / ms
+    out["bt_1m_streaming"] = bt_stream_row(1000000, quick)
     if quick:
         return out
     from oracle import oracle
+    threads = len(os.sched_getaffinity(0))
     t0 = time.perf_counter()
     for _ in range(10):
         oracle.bt(wl.buffers["cp"], int(wl.buffers["max_tess"]),
-                  float(wl.buffers["scale"]))
+                  float(wl.buffers["scale"]), nthreads=threads)
     dt = (time.perf_counter() - t0) / 10
     out["bt_25k"]["cpu_baseline"] = {
-        "value": 25000 / dt, "unit": "curves/s", "cores": 1, "kind": "port",
-        "seconds": dt, "sample": "25k curves (fp64 vertices), oracle/oracle.c"}
+        "value": 25000 / dt, "unit": "curves/s", "cores": threads,
+        "kind": "port", "seconds": dt,
+        "sample": "25k curves (fp64 vertices), oracle/oracle.c OpenMP over "
+                  "curves"}
     from paper_2201_02789_b200.bench import run_reference
     from paper_2201_02789_b200.bench.benchmarks import Workload
 
@@ -520,7 +625,10 @@ def extra_workloads(stream, quick: bool) -> dict:
         "cpu_baseline": {"value": m / dt, "unit": "edge slots/s",
                          "cores": 1, "kind": "port", "seconds": dt,
                          "sample": "Kruskal over rmat-22 (symmetrised), "
-                                   "oracle/oracle.c"}}
+                                   "oracle/oracle.c; one core: Kruskal's "
+                                   "sorted union-find sweep is sequential "
+                                   "(it is the checker's unique-forest "
+                                   "definition, not a parallel MST)"}}
     del wl
     # SP: 20 synchronous sweeps of random 5-SAT
     bench, wl = load("sp", "ksat5:200000:seed1")
@@ -531,7 +639,8 @@ def extra_workloads(stream, quick: bool) -> dict:
     ref = run_reference(bench, wl)
     ne = int(wl.buffers["lits"].shape[0])
     t0 = time.perf_counter()
-    cpu = oracle.sp(wl.payload, wl.buffers["eta0"], 20, 0.0)
+    cpu = oracle.sp(wl.payload, wl.buffers["eta0"], 20, 0.0,
+                    nthreads=threads)
     dt = time.perf_counter() - t0
     out["sp_ksat5_200k"] = {
         "ms": ms, "sweeps": rep.iterations, "edges": ne,
@@ -542,9 +651,10 @@ def extra_workloads(stream, quick: bool) -> dict:
                    if np.allclose(rep.arrays["eta"], cpu[0], rtol=1e-5,
                                   atol=1e-7) else "MISMATCH"),
         "cpu_baseline": {"value": ne * 20 / dt, "unit": "edge updates/s",
-                         "cores": 1, "kind": "port", "seconds": dt,
+                         "cores": threads, "kind": "port", "seconds": dt,
                          "sample": "20 sweeps of ksat5:200000, "
-                                   "oracle/oracle.c (fp64)"},
+                                   "oracle/oracle.c (fp64, OpenMP over "
+                                   "variables and clauses)"},
         "naive_cdp": "not timed (37 s, 88 M launches; profiles/sp_time_r01)"}
     return out
 

@@ -172,7 +172,9 @@ static int32_t tess_count(const float* p, float scale, int32_t max_tess) {
 /* ntess[c]; canonical offsets[c] = exclusive prefix; verts[2*V] in fp64.
  * Returns total vertex count (call with verts == NULL to size). */
 int64_t oracle_bt(const float* cp, int32_t ncurves, int32_t max_tess,
-                  float scale, int32_t* ntess, int64_t* offsets, double* verts) {
+                  float scale, int32_t* ntess, int64_t* offsets, double* verts,
+                  int nthreads) {
+  const int nt_ = nthr(nthreads);
   int64_t acc = 0;
   for (int32_t c = 0; c < ncurves; ++c) {
     ntess[c] = tess_count(cp + 6 * (int64_t)c, scale, max_tess);
@@ -180,6 +182,7 @@ int64_t oracle_bt(const float* cp, int32_t ncurves, int32_t max_tess,
     acc += ntess[c];
   }
   if (!verts) return acc;
+#pragma omp parallel for num_threads(nt_) schedule(dynamic, 64)
   for (int32_t c = 0; c < ncurves; ++c) {
     const float* p = cp + 6 * (int64_t)c;
     const int32_t nt = ntess[c];
@@ -335,7 +338,10 @@ typedef struct {
 
 static void sp_var_pass(int32_t nvars, const int32_t* occ_row,
                         const int32_t* occ, const int32_t* lits,
-                        const double* eta, sp_prod* prod) {
+                        const double* eta, sp_prod* prod, int nt) {
+  /* one thread per variable, its occurrences in CSR order: the same
+   * products whatever the thread count */
+#pragma omp parallel for num_threads(nt) schedule(static, 1024)
   for (int32_t i = 0; i < nvars; ++i) {
     sp_prod q = {{1.0, 1.0}, {0, 0}};
     for (int32_t t = occ_row[i]; t < occ_row[i + 1]; ++t) {
@@ -376,7 +382,9 @@ static float sp_f32_up(double x) {
 int32_t oracle_sp(const int32_t* lits, int32_t k, int32_t nclauses,
                   const int32_t* occ_row, const int32_t* occ, int32_t nvars,
                   const double* eta0, int32_t max_sweeps, float eps,
-                  double* eta, float* wpos, float* wneg, float* last_delta) {
+                  double* eta, float* wpos, float* wneg, float* last_delta,
+                  int nthreads) {
+  const int nt = nthr(nthreads);
   const int64_t ne = (int64_t)nclauses * k;
   sp_prod* prod = (sp_prod*)malloc(sizeof(sp_prod) * (size_t)(nvars ? nvars : 1));
   double* nxt = (double*)malloc(sizeof(double) * (size_t)(ne ? ne : 1));
@@ -389,8 +397,10 @@ int32_t oracle_sp(const int32_t* lits, int32_t k, int32_t nclauses,
   int32_t sweeps = 0;
   float delta = 0.f;
   while (sweeps < max_sweeps) {
-    sp_var_pass(nvars, occ_row, occ, lits, eta, prod);
+    sp_var_pass(nvars, occ_row, occ, lits, eta, prod, nt);
     delta = 0.f;
+    /* one thread per clause (synchronous sweep: reads eta, writes nxt) */
+#pragma omp parallel for num_threads(nt) schedule(static, 1024) reduction(max : delta)
     for (int32_t a = 0; a < nclauses; ++a) {
       const int64_t base = (int64_t)a * k;
       for (int32_t t = 0; t < k; ++t) {
@@ -409,7 +419,7 @@ int32_t oracle_sp(const int32_t* lits, int32_t k, int32_t nclauses,
     ++sweeps;
     if (delta <= eps) break;
   }
-  sp_var_pass(nvars, occ_row, occ, lits, eta, prod);
+  sp_var_pass(nvars, occ_row, occ, lits, eta, prod, nt);
   for (int32_t i = 0; i < nvars; ++i) {
     const double pp = prod[i].z[0] == 0 ? prod[i].p[0] : 0.0;
     const double pn = prod[i].z[1] == 0 ? prod[i].p[1] : 0.0;
