@@ -129,6 +129,11 @@ typedef struct dp_config {
                             of the copy (out-of-range chunks and all later
                             ones stay int32), dp_sssp_dev packs on the
                             device.  0 = int32 weights as given */
+  int32_t donate;        /* serial_mode warp, apps that support it (BT): a
+                            below-threshold row of >= donate items is
+                            published as chunks that any parent warp out of
+                            work may claim (work donation inside the parent
+                            grid, no launch).  0 = off */
 } dp_config;
 
 /* SimReport (sim/report.py:12-28) counters, measured on the device */
@@ -195,7 +200,8 @@ int dp_manylaunch_dev(const int32_t* d_sizes, int32_t n, const dp_config* cfg,
                       dp_stats* stats);
 
 /* ---- triangle counting (no reference) -------------- */
-/* oriented CSR+ (u->v iff (deg u, u) < (deg v, v)), rows sorted ascending.
+/* rank-ordered CSR+ (dp_tc_orient: every edge u -> v has u < v, rows sorted
+ * ascending; the kernels probe only the part of N+(u) above v).
  * [edge_lo, edge_hi) restricts the count to a range of oriented edges
  * (the multi-GPU shard); pass 0, m for the whole graph. */
 int dp_tc(const int32_t* rowptr, const int32_t* col, int32_t n, int64_t m,
@@ -299,6 +305,11 @@ int dp_bfs_part_solve_peer(const int32_t* d_rowptr_p, const int32_t* d_col_p,
 /* free the calling host thread's workspace (tables, pinned buffers); the
  * next call on the thread re-creates it */
 void dp_thread_release(void);
+/* diagnostics: device time (ms, CUDA events) of every host-launched step
+ * (parent grid + its children [+ grid glue]) of the calling thread's last
+ * run, in order -- one per BFS level / SSSP round; copies min(count, cap)
+ * into ms and returns the count */
+int64_t dp_step_times(double* ms, int64_t cap);
 /* out[v] = work[spread_b(v)] for v < n: counts accumulated with
  * counts_spread = b back in vertex order */
 int dp_unspread_dev(const int32_t* d_work, int32_t b, int32_t n,
@@ -393,7 +404,10 @@ int dp_rmat_csr_part(int32_t scale, int32_t edge_factor, uint64_t seed,
 int dp_rmat_part_keys_dev(int32_t scale, int32_t edge_factor, uint64_t seed,
                           int32_t nparts, int32_t part, uint64_t* d_keys,
                           int64_t capacity, int64_t* count, void* stream);
-/* symmetrise, drop self-loops and duplicates, orient by (degree, id).
+/* symmetrise, drop self-loops and duplicates, relabel the vertices by
+ * ascending (degree, id) rank and keep u -> v iff rank u < rank v: the
+ * rank-ordered CSR+ dp_tc expects (rows ascending, every edge u -> v has
+ * u < v; same triangle count as the input).
  * Allocates *rowptr_plus (n+1) and *col_plus (*m_plus); free with dp_free. */
 int dp_tc_orient(const int32_t* rowptr, const int32_t* col, int32_t n,
                  int32_t** rowptr_plus, int32_t** col_plus, int64_t* m_plus,

@@ -43,7 +43,8 @@ class DpConfig(ctypes.Structure):
                 ("frontier", ctypes.c_int32),
                 ("agg_coarsen", ctypes.c_int32),
                 ("counts_spread", ctypes.c_int32),
-                ("weight_bits", ctypes.c_int32)]
+                ("weight_bits", ctypes.c_int32),
+                ("donate", ctypes.c_int32)]
 
 
 class DpStats(ctypes.Structure):
@@ -125,6 +126,7 @@ _SIGNATURES = {
                                 _P, _P, _P, _I64, _P, _P, _U64, _P, _ST],
                                ctypes.c_int),
     "dp_thread_release": ([], None),
+    "dp_step_times": ([_P, _I64], _I64),
     "dp_sssp_part_round_peer": ([_P, _P, _P, _I32, _I32, _I32, _CFG, _P, _P,
                                  _P, _P, _P, _ST], ctypes.c_int),
     "dp_rmat_part_keys_dev": ([_I32, _I32, _U64, _I32, _I32, _P, _I64,
@@ -225,6 +227,13 @@ def ptr(a) -> int | None:
             raise ValueError("arrays passed to libdynpar must be contiguous")
         return a.ctypes.data
     return a.data_ptr()
+
+
+def step_times() -> list[float]:
+    """Per-step device ms of this thread's last run (dp_step_times)."""
+    buf = (ctypes.c_double * 4096)()
+    k = load().dp_step_times(buf, 4096)
+    return [buf[i] for i in range(min(k, 4096))]
 
 
 def stats_dict(st: DpStats) -> dict:

@@ -916,19 +916,22 @@ struct GcNotifyApp {
 
 // ---------------------------------------------------------------------------
 // Triangle counting (no reference implementation)
-//   Input: the degree-oriented CSR+ (out-lists N+, ascending).  The call
-//   builds its transpose on the device (in-lists N-, restricted to the
-//   oriented-edge range [edge_lo, edge_hi) of a shard).
-//   parent = vertex v, child item = in-edge (u, v), work = |N+(u) ∩ N+(v)|.
-//   Probing N+(u) into a set of N+(v) (built once per child block) costs
-//   sum_u d+(u)^2 probes; the forward form, N+(v) into a set of N+(u), costs
-//   sum_v d-(v) d+(v): 14.5 G vs 28.9 G on RMAT-22.
+//   Input: the rank-ordered CSR+ (dp_tc_orient: vertices relabelled by
+//   (degree, id) rank, u -> v iff u < v, out-lists N+ ascending).  The call
+//   builds its transpose on the device (in-edges, restricted to the
+//   oriented-edge range [edge_lo, edge_hi) of a shard), each in-edge (u, v)
+//   stored as the slot range of N+(u) above v.
+//   parent = vertex v, child item = in-edge (u, v), work = |N+(u)>v ∩ N+(v)|.
+//   A triangle u < v < w is found once, at v, from u's list past v: probing
+//   that suffix into a set of N+(v) (built once per child block) costs
+//   sum_u d+(u)(d+(u)-1)/2 probes -- half of probing all of N+(u), 14.5 G on
+//   RMAT-22; the forward form, N+(v) into a set of N+(u), costs 28.9 G.
 // ---------------------------------------------------------------------------
 struct TcApp {
   const int* __restrict__ rowptr;     // CSR+ (out)
   const int* __restrict__ col;
   const int* __restrict__ in_rowptr;  // transpose (in), shard edges only
-  const int* __restrict__ in_src;
+  const int2* __restrict__ in_rng;    // per in-edge (u, v): N+(u) slots > v
   unsigned long long* total;
   int n;
   int pad;
@@ -973,11 +976,10 @@ struct TcApp {
   }
 
   __device__ void item(const Args& a, int e, Acc& acc) const {
-    const int u = __ldg(in_src + a.first + e);
-    const int ub = __ldg(rowptr + u), ue = __ldg(rowptr + u + 1);
+    const int2 ur = __ldg(in_rng + a.first + e);
     const int vb = __ldg(rowptr + a.v), ve = __ldg(rowptr + a.v + 1);
-    acc.tri += (unsigned long long)intersect(col + ub, ue - ub, col + vb,
-                                             ve - vb);
+    acc.tri += (unsigned long long)intersect(col + ur.x, ur.y - ur.x,
+                                             col + vb, ve - vb);
   }
   static constexpr int kUnroll = 1;
 
@@ -1034,9 +1036,9 @@ struct TcApp {
       const long long e = base + lane;
       int ub = 0, du = 0;
       if (e < e1) {
-        const int u = __ldg(in_src + a.first + e);
-        ub = __ldg(rowptr + u);
-        du = __ldg(rowptr + u + 1) - ub;
+        const int2 ur = __ldg(in_rng + a.first + e);
+        ub = ur.x;
+        du = ur.y - ur.x;
       }
       // long lists: the whole warp walks one list at a time, four
       // coalesced loads in flight per lane
@@ -1186,6 +1188,10 @@ struct BtApp {
   }
   static constexpr int kUnroll = 1;
   static constexpr int kBigUnroll = 4;  // whole-warp rows: 4 stores in flight
+  // long curves (up to 2048 vertices) are donated to idle parent warps
+  // (dp_config.donate): at 25k curves the warp holding the longest curves
+  // otherwise sets the kernel's length (ncu: SMs active 52 % of it)
+  static constexpr bool kDonate = true;
   static constexpr bool kBlockMode = false;
   static constexpr bool kPureExpand = false;  // bump-allocates in expand
   static constexpr int kMinBlocks = DP_BT_MINB;

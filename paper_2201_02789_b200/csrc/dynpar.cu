@@ -14,6 +14,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/dynpar.h"
 #include "apps.cuh"
@@ -80,6 +81,10 @@ struct Workspace {
   // publication-checker builds: one stamp per aggregation-table row
   void* pub = nullptr;
   size_t pub_bytes = 0;
+  // work donation queue (header + entries) and the launch epoch
+  void* dq = nullptr;
+  size_t dq_bytes = 0;
+  unsigned dq_epoch = 0;
   // packed SSSP weights: device copy and the pinned host staging of dp_sssp
   void* wpack = nullptr;
   size_t wpack_bytes = 0;
@@ -182,6 +187,7 @@ int validate(const dp_config* c) {
     return fail(DP_ERR_INVALID, "counts_spread must be in [0, 30]");
   if (c->weight_bits != 0 && c->weight_bits != 4)
     return fail(DP_ERR_INVALID, "weight_bits must be 0 or 4");
+  if (c->donate < 0) return fail(DP_ERR_INVALID, "donate must be >= 0");
   if (c->agg_coarsen &&
       (c->agg < DP_AGG_WARP || c->agg > DP_AGG_MULTIBLOCK || c->persistent))
     return fail(DP_ERR_INVALID,
@@ -365,6 +371,11 @@ Knobs knobs_of(const dp_config* c) {
   k.agg_threshold = c->agg_threshold;
   k.serial_warp = c->serial_mode == DP_SERIAL_WARP;
   k.agg_cf = c->agg_coarsen != 0;
+  k.donate = 0;  // set per launch by arm_donation
+  k.dq_cap = 0;
+  k.epoch = 0;
+  k.dq = nullptr;
+  k.dq_entries = nullptr;
   return k;
 }
 
@@ -467,6 +478,35 @@ int prepare_tables(const dp_config* c, int grid, int pb, Workspace* w,
   return 0;
 }
 
+// Work donation (dp_config.donate, apps with App::kDonate): a queue of up to
+// one entry per parent thread of the launch, its header cleared and a fresh
+// epoch per launch (entries of earlier launches never match it).
+template <class App>
+int arm_donation(const dp_config* c, long long parents, Workspace* w,
+                 cudaStream_t s, Knobs* k) {
+  if constexpr (Donates<App>::value) {
+    if (c->donate <= 0 || c->serial_mode != DP_SERIAL_WARP ||
+        c->variant != DP_VARIANT_CDP)
+      return 0;
+    const long long cap = std::min<long long>(std::max(parents, 1LL), 1 << 22);
+    const size_t need =
+        64 + (size_t)cap * sizeof(DonateEntry<typename App::Args>);
+    const size_t had = w->dq_bytes;
+    int r;
+    if ((r = grow(&w->dq, &w->dq_bytes, need))) return r;
+    if (w->dq_bytes != had)  // fresh memory: no stale tag can match
+      DP_CUDA(cudaMemsetAsync(w->dq, 0, w->dq_bytes, s));
+    else
+      DP_CUDA(cudaMemsetAsync(w->dq, 0, sizeof(DonateHdr), s));
+    k->donate = c->donate;
+    k->dq_cap = (int)cap;
+    k->epoch = ++w->dq_epoch ? w->dq_epoch : ++w->dq_epoch;
+    k->dq = (DonateHdr*)w->dq;
+    k->dq_entries = (char*)w->dq + 64;
+  }
+  return 0;
+}
+
 #if DP_CHECK_PUBLISH
 // Checker builds, before every parent grid: stamps cleared, rows poisoned
 // with 0xff bytes, the device-side table base set (common.cuh).
@@ -517,7 +557,8 @@ int launch_wave(const App& app, long long base, long long nparents,
       return r;
   }
 #endif
-  const Knobs k = knobs_of(c);
+  Knobs k = knobs_of(c);
+  if (int r = arm_donation<App>(c, grid_ll * pb, w, s, &k)) return r;
   const bool single_group =
       c->agg == DP_AGG_GRID ||
       (c->agg == DP_AGG_MULTIBLOCK && (long long)c->group_size >= grid);
@@ -608,9 +649,14 @@ int launch_parent(const App& app, long long nparents, long long launchers,
 }
 
 // after the stream has been synchronised
+// per-step device times of the calling thread's last run (dp_step_times)
+thread_local std::vector<double> g_step_ms;
+
 int account_step(Workspace* w, RunCounters* rc) {
   float ms = 0.f;
   DP_CUDA(cudaEventElapsedTime(&ms, w->evk0, w->evk1));
+  if (rc->ms_kernel_sum == 0.0 && rc->ms_kernel_max == 0.0) g_step_ms.clear();
+  g_step_ms.push_back(ms);
   rc->ms_kernel_sum += ms;
   rc->ms_kernel_max = std::max<double>(rc->ms_kernel_max, ms);
   return 0;
@@ -1658,20 +1704,25 @@ __global__ void scan_add_kernel(int* y, int* y2, long long n,
   }
 }
 
-// warp per source vertex: its out-edges in [lo, hi) land in the in-lists
+// warp per source vertex: its out-edges in [lo, hi) land in the in-lists.
+// In-edge (u -> v) at slot i records the slots of N+(u) above v, [i + 1,
+// rowptr[u + 1]) (the rank-ordered CSR+ keeps rows ascending, so these are
+// exactly the w > v that can close a triangle at v)
 __global__ void tc_scatter_in_kernel(const int* __restrict__ rowptr,
                                      const int* __restrict__ col, int n,
                                      long long lo, long long hi, int* cursor,
-                                     int* in_src) {
+                                     int2* in_rng) {
   const int lane = lane_id();
   const long long warps = ((long long)gridDim.x * blockDim.x) >> 5;
   for (long long u = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
        u < n; u += warps) {
-    long long b = __ldg(rowptr + u), e = __ldg(rowptr + u + 1);
+    const int end = __ldg(rowptr + u + 1);
+    long long b = __ldg(rowptr + u), e = end;
     if (b < lo) b = lo;
     if (e > hi) e = hi;
     for (long long i = b + lane; i < e; i += 32)
-      in_src[atomicAdd(cursor + __ldg(col + i), 1)] = (int)u;
+      in_rng[atomicAdd(cursor + __ldg(col + i), 1)] =
+          make_int2((int)i + 1, end);
   }
 }
 
@@ -1686,15 +1737,16 @@ int tc_dev_impl(const int32_t* rowptr, const int32_t* col, int32_t n,
   if (hi < lo) hi = lo;
   Workspace* w = workspace(&r);
   if (!w) return r;
-  // in_rowptr[n+1] | cursor[n+1] | in_src[hi-lo] | tile sums
+  // tile sums | in_rng[hi-lo] | in_rowptr[n+1] | cursor[n+1]
   const long long ntiles = std::max(1LL, dp::ceil_div_ll(n, kScanTile));
-  const size_t need = (size_t)(n + 1) * 8 + (size_t)std::max<long long>(hi - lo, 1) * 4 +
+  const size_t need = (size_t)(n + 1) * 8 +
+                      (size_t)std::max<long long>(hi - lo, 1) * 8 +
                       (size_t)ntiles * 8 + 16;
   if ((r = grow(&w->io[5], &w->io_bytes[5], need))) return r;
   long long* tile_sum = (long long*)w->io[5];
-  int* in_rowptr = (int*)(tile_sum + ntiles);
+  int2* in_rng = (int2*)(tile_sum + ntiles);  // 8-byte aligned
+  int* in_rowptr = (int*)(in_rng + std::max<long long>(hi - lo, 1));
   int* cursor = in_rowptr + (n + 1);
-  int* in_src = cursor + (n + 1);
   RunCounters rc;
   DP_CUDA(cudaMemsetAsync(tri, 0, sizeof(uint64_t), s));
   DP_CUDA(cudaEventRecord(w->ev0, s));
@@ -1708,14 +1760,14 @@ int tc_dev_impl(const int32_t* rowptr, const int32_t* col, int32_t n,
   scan_add_kernel<<<gb, 256, 0, s>>>(in_rowptr, cursor, n, tile_sum);
   if (hi > lo)
     tc_scatter_in_kernel<<<gb, 256, 0, s>>>(rowptr, col, n, lo, hi, cursor,
-                                            in_src);
+                                            in_rng);
   DP_CUDA(cudaGetLastError());
   rc.kernel_launches += 5;
   TcApp a;
   a.rowptr = rowptr;
   a.col = col;
   a.in_rowptr = in_rowptr;
-  a.in_src = in_src;
+  a.in_rng = in_rng;
   a.total = (unsigned long long*)tri;
   a.n = n;
   a.pad = 0;
@@ -2858,6 +2910,12 @@ int dp_bfs_part_solve_peer(const int32_t* d_rowptr_p, const int32_t* d_col_p,
   return r;
 }
 
+int64_t dp_step_times(double* ms, int64_t cap) {
+  const int64_t k = (int64_t)g_step_ms.size();
+  for (int64_t i = 0; i < std::min(k, cap); ++i) ms[i] = g_step_ms[i];
+  return k;
+}
+
 void dp_thread_release(void) {
   for (Workspace& w : g_ws) {
     if (!w.ready) continue;
@@ -2885,6 +2943,7 @@ void dp_thread_release(void) {
     cudaFree(w.wpack);
     cudaFreeHost(w.h_wpack);
     cudaFree(w.d_bad);
+    cudaFree(w.dq);
     w = Workspace();
   }
 }

@@ -173,16 +173,26 @@ int dp_tc_orient(const int32_t* rowptr, const int32_t* col, int32_t n,
     std::sort(b, e);
     deg[u] = (int32_t)(std::unique(b, e) - b);
   }
-  // 3) orient u -> v iff (deg u, u) < (deg v, v); rows stay sorted
-  auto keep = [&](int64_t u, int32_t v) {
-    return deg[u] < deg[v] || (deg[u] == deg[v] && u < v);
-  };
+  // 3) relabel by degree rank: rank(u) = position of u in ascending
+  //    (deg u, u) order; the output vertex r = rank(u) keeps the edges to
+  //    the higher-ranked neighbours, u -> v iff (deg u, u) < (deg v, v), now
+  //    simply r(u) < r(v).  Rows ascending in the new ids, so the out-list
+  //    of u past v's slot is exactly {w in N+(u) : w > v}, the only part
+  //    that can close a triangle (u, v, w) at v -- TcApp probes that suffix.
+  //    The triangle count is that of the input graph.
+  std::vector<int32_t> order(n), rank(n);
+  for (int64_t u = 0; u < n; ++u) order[u] = (int32_t)u;
+  std::sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
+    return deg[a] < deg[b] || (deg[a] == deg[b] && a < b);
+  });
+#pragma omp parallel for num_threads(nt) schedule(static)
+  for (int64_t i = 0; i < n; ++i) rank[order[i]] = (int32_t)i;
   std::vector<int64_t> op(n + 1, 0);
 #pragma omp parallel for num_threads(nt) schedule(dynamic, 4096)
   for (int64_t u = 0; u < n; ++u) {
     int64_t c = 0;
-    for (int64_t i = sp[u]; i < sp[u] + deg[u]; ++i) c += keep(u, sym[i]);
-    op[u + 1] = c;
+    for (int64_t i = sp[u]; i < sp[u] + deg[u]; ++i) c += rank[sym[i]] > rank[u];
+    op[rank[u] + 1] = c;
   }
   for (int64_t i = 0; i < n; ++i) op[i + 1] += op[i];
   if (op[n] > 0x7fffffffLL) return DP_ERR_INVALID;
@@ -196,9 +206,11 @@ int dp_tc_orient(const int32_t* rowptr, const int32_t* col, int32_t n,
   for (int64_t i = 0; i <= n; ++i) rp[i] = (int32_t)op[i];
 #pragma omp parallel for num_threads(nt) schedule(dynamic, 4096)
   for (int64_t u = 0; u < n; ++u) {
-    int64_t o = op[u];
+    const int32_t ru = rank[u];
+    int64_t o = op[ru];
     for (int64_t i = sp[u]; i < sp[u] + deg[u]; ++i)
-      if (keep(u, sym[i])) cp[o++] = sym[i];
+      if (rank[sym[i]] > ru) cp[o++] = rank[sym[i]];
+    std::sort(cp + op[ru], cp + o);
   }
   *rowptr_plus = rp;
   *col_plus = cp;

@@ -29,12 +29,14 @@ import numpy as np
 # ---------------------------------------------------------------------------
 
 def tc_edge_cost(rowptr: np.ndarray, col: np.ndarray) -> np.ndarray:
-    """Work of each oriented edge (u, v) in the transposed counter
-    (csrc/apps.cuh TcApp): the d+(u) elements of N+(u) probed into v's set,
-    plus one unit for the edge itself (set setup is amortised per block)."""
-    deg = np.diff(rowptr.astype(np.int64))
-    src = np.repeat(np.arange(deg.shape[0]), deg)
-    return deg[src] + 1
+    """Work of each oriented edge (u, v) at slot e in the transposed counter
+    (csrc/apps.cuh TcApp): the elements of N+(u) above v, slots (e,
+    rowptr[u+1]), probed into v's set, plus one unit for the edge itself
+    (set setup is amortised per block)."""
+    rp = rowptr.astype(np.int64)
+    deg = np.diff(rp)
+    end = np.repeat(rp[1:], deg)
+    return end - np.arange(end.shape[0], dtype=np.int64)
 
 
 def balanced_ranges(cost: np.ndarray, parts: int) -> list[tuple[int, int]]:

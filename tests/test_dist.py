@@ -99,8 +99,9 @@ def test_balanced_ranges_cover_and_balance(parts):
 def test_tc_edge_cost():
     rowptr = np.array([0, 2, 3, 3], np.int32)
     col = np.array([1, 2, 2], np.int32)
+    # slots of N+(u) above v, plus one: 0->1 probes {2}, 0->2 and 1->2 none
     np.testing.assert_array_equal(pdist.tc_edge_cost(rowptr, col),
-                                  [2 + 1, 2 + 1, 1 + 1])
+                                  [1 + 1, 0 + 1, 0 + 1])
 
 
 # ---------------------------------------------------------------------------

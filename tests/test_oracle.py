@@ -238,17 +238,24 @@ def brute_triangles(g) -> int:
 
 
 def test_tc_orient_matches_numpy_restatement():
+    """Rank-ordered CSR+: vertices relabelled by ascending (degree, id),
+    u -> v iff rank u < rank v, rows ascending in the new ids."""
     g = graphs.rmat_graph(10, 2)
     gp = graphs.tc_orient(g)
     a, b = _simple_undirected(g)
     deg = np.bincount(a, minlength=g.n)
-    keep = (deg[a] < deg[b]) | ((deg[a] == deg[b]) & (a < b))
-    a, b = a[keep], b[keep]
-    order = np.lexsort((b, a))
-    rowptr = np.concatenate(([0], np.cumsum(np.bincount(a, minlength=g.n))))
+    rank = np.empty(g.n, np.int64)
+    rank[np.lexsort((np.arange(g.n), deg))] = np.arange(g.n)
+    ra, rb = rank[a], rank[b]
+    keep = ra < rb
+    ra, rb = ra[keep], rb[keep]
+    order = np.lexsort((rb, ra))
+    rowptr = np.concatenate(([0], np.cumsum(np.bincount(ra, minlength=g.n))))
     np.testing.assert_array_equal(gp.rowptr, rowptr)
-    np.testing.assert_array_equal(gp.col, b[order])
+    np.testing.assert_array_equal(gp.col, rb[order])
     assert gp.m * 2 == len(_simple_undirected(g)[0])
+    src = np.repeat(np.arange(g.n), np.diff(gp.rowptr))
+    assert (src < gp.col).all()
 
 
 @pytest.mark.parametrize("spec", ["rmat:8:seed1", "rmat:9:seed4",
