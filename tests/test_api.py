@@ -31,7 +31,8 @@ from conftest import ROOT
 def test_library_exports_every_declared_symbol():
     header = (ROOT / "include" / "dynpar.h").read_text()
     declared = set(re.findall(
-        r"^(?:int|void|const char\*)\s+(dp_[a-z0-9_]+)\(", header, re.M))
+        r"^(?:int|int64_t|void|const char\*)\s+(dp_[a-z0-9_]+)\(", header,
+        re.M))
     lib = _lib.load()
     for name in declared:
         assert hasattr(lib, name), name
