@@ -129,11 +129,6 @@ typedef struct dp_config {
                             of the copy (out-of-range chunks and all later
                             ones stay int32), dp_sssp_dev packs on the
                             device.  0 = int32 weights as given */
-  int32_t donate;        /* serial_mode warp, apps that support it (BT): a
-                            below-threshold row of >= donate items is
-                            published as chunks that any parent warp out of
-                            work may claim (work donation inside the parent
-                            grid, no launch).  0 = off */
 } dp_config;
 
 /* SimReport (sim/report.py:12-28) counters, measured on the device */

@@ -55,7 +55,6 @@ class BenchConfig:
     device_loop: bool = False
     frontier: bool = False
     weight_bits: int = 0
-    donate: int = 0
 
     def describe(self) -> str:
         return (f"threshold={self.threshold} cfactor={self.cfactor} "
@@ -91,8 +90,6 @@ class BenchConfig:
             raise ValueError(f"unknown serial mode {self.serial!r}")
         if self.weight_bits not in (0, 4):
             raise ValueError("weight_bits must be 0 (int32) or 4 (packed)")
-        if self.donate < 0:
-            raise ValueError("donate must be >= 0")
 
     def to_c(self, variant: int = _lib.VARIANT_CDP) -> _lib.DpConfig:
         self.validate()
@@ -114,7 +111,6 @@ class BenchConfig:
         c.device_loop = int(bool(self.device_loop))
         c.frontier = int(bool(self.frontier))
         c.weight_bits = int(self.weight_bits)
-        c.donate = int(self.donate)
         c.threshold, c.cfactor, c.agg_coarsen = self.order_effect(
             c.threshold, c.cfactor, self.agg if agg_on else None)
         return c

@@ -1188,10 +1188,6 @@ struct BtApp {
   }
   static constexpr int kUnroll = 1;
   static constexpr int kBigUnroll = 4;  // whole-warp rows: 4 stores in flight
-  // long curves (up to 2048 vertices) are donated to idle parent warps
-  // (dp_config.donate): at 25k curves the warp holding the longest curves
-  // otherwise sets the kernel's length (ncu: SMs active 52 % of it)
-  static constexpr bool kDonate = true;
   static constexpr bool kBlockMode = false;
   static constexpr bool kPureExpand = false;  // bump-allocates in expand
   static constexpr int kMinBlocks = DP_BT_MINB;

@@ -81,10 +81,6 @@ struct Workspace {
   // publication-checker builds: one stamp per aggregation-table row
   void* pub = nullptr;
   size_t pub_bytes = 0;
-  // work donation queue (header + entries) and the launch epoch
-  void* dq = nullptr;
-  size_t dq_bytes = 0;
-  unsigned dq_epoch = 0;
   // packed SSSP weights: device copy and the pinned host staging of dp_sssp
   void* wpack = nullptr;
   size_t wpack_bytes = 0;
@@ -187,7 +183,6 @@ int validate(const dp_config* c) {
     return fail(DP_ERR_INVALID, "counts_spread must be in [0, 30]");
   if (c->weight_bits != 0 && c->weight_bits != 4)
     return fail(DP_ERR_INVALID, "weight_bits must be 0 or 4");
-  if (c->donate < 0) return fail(DP_ERR_INVALID, "donate must be >= 0");
   if (c->agg_coarsen &&
       (c->agg < DP_AGG_WARP || c->agg > DP_AGG_MULTIBLOCK || c->persistent))
     return fail(DP_ERR_INVALID,
@@ -371,11 +366,6 @@ Knobs knobs_of(const dp_config* c) {
   k.agg_threshold = c->agg_threshold;
   k.serial_warp = c->serial_mode == DP_SERIAL_WARP;
   k.agg_cf = c->agg_coarsen != 0;
-  k.donate = 0;  // set per launch by arm_donation
-  k.dq_cap = 0;
-  k.epoch = 0;
-  k.dq = nullptr;
-  k.dq_entries = nullptr;
   return k;
 }
 
@@ -478,35 +468,6 @@ int prepare_tables(const dp_config* c, int grid, int pb, Workspace* w,
   return 0;
 }
 
-// Work donation (dp_config.donate, apps with App::kDonate): a queue of up to
-// one entry per parent thread of the launch, its header cleared and a fresh
-// epoch per launch (entries of earlier launches never match it).
-template <class App>
-int arm_donation(const dp_config* c, long long parents, Workspace* w,
-                 cudaStream_t s, Knobs* k) {
-  if constexpr (Donates<App>::value) {
-    if (c->donate <= 0 || c->serial_mode != DP_SERIAL_WARP ||
-        c->variant != DP_VARIANT_CDP)
-      return 0;
-    const long long cap = std::min<long long>(std::max(parents, 1LL), 1 << 22);
-    const size_t need =
-        64 + (size_t)cap * sizeof(DonateEntry<typename App::Args>);
-    const size_t had = w->dq_bytes;
-    int r;
-    if ((r = grow(&w->dq, &w->dq_bytes, need))) return r;
-    if (w->dq_bytes != had)  // fresh memory: no stale tag can match
-      DP_CUDA(cudaMemsetAsync(w->dq, 0, w->dq_bytes, s));
-    else
-      DP_CUDA(cudaMemsetAsync(w->dq, 0, sizeof(DonateHdr), s));
-    k->donate = c->donate;
-    k->dq_cap = (int)cap;
-    k->epoch = ++w->dq_epoch ? w->dq_epoch : ++w->dq_epoch;
-    k->dq = (DonateHdr*)w->dq;
-    k->dq_entries = (char*)w->dq + 64;
-  }
-  return 0;
-}
-
 #if DP_CHECK_PUBLISH
 // Checker builds, before every parent grid: stamps cleared, rows poisoned
 // with 0xff bytes, the device-side table base set (common.cuh).
@@ -557,8 +518,7 @@ int launch_wave(const App& app, long long base, long long nparents,
       return r;
   }
 #endif
-  Knobs k = knobs_of(c);
-  if (int r = arm_donation<App>(c, grid_ll * pb, w, s, &k)) return r;
+  const Knobs k = knobs_of(c);
   const bool single_group =
       c->agg == DP_AGG_GRID ||
       (c->agg == DP_AGG_MULTIBLOCK && (long long)c->group_size >= grid);
@@ -2943,7 +2903,6 @@ void dp_thread_release(void) {
     cudaFree(w.wpack);
     cudaFreeHost(w.h_wpack);
     cudaFree(w.d_bad);
-    cudaFree(w.dq);
     w = Workspace();
   }
 }

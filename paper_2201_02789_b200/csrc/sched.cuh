@@ -42,23 +42,6 @@ namespace dp {
 enum AggKind { kAggNone = 0, kAggWarp = 1, kAggBlock = 2, kAggMulti = 3,
                kAggGrid = 4 };
 
-// Work donation of the warp-mode serial arm (B200, dp_config.donate = D):
-// a below-threshold row of >= D items is published as chunks that any parent
-// warp which ran out of work may claim, so one warp holding a long row no
-// longer sets the parent grid's length.
-struct DonateHdr {
-  int tail;    // entries published
-  int cursor;  // entries below are exhausted (thieves start here)
-};
-template <class Args>
-struct alignas(16) DonateEntry {
-  Args a;
-  int cnt;       // items of the row
-  int nchunk;    // chunks of kDonateChunk items
-  int next;      // next chunk to claim (atomic)
-  unsigned ready;  // == the launch's epoch once published
-};
-
 struct Knobs {
   int threshold;      // 0: pass off (every non-empty child launches)
   int cf;             // coarsening factor >= 1
@@ -69,11 +52,6 @@ struct Knobs {
   int agg_cf;         // 1: coarsening applies to the aggregated grid (the
                       // reference's order "A before C", pipeline.py:60-81:
                       // logical blocks of the aggregated clone span parents)
-  int donate;         // work donation: rows of >= donate items (0: off)
-  int dq_cap;         // donation entries available
-  unsigned epoch;     // this parent launch's tag of published entries
-  DonateHdr* dq;      // donation queue header (null: off)
-  void* dq_entries;   // DonateEntry<App::Args>[dq_cap]
 };
 
 template <class App>
@@ -352,81 +330,11 @@ template <class App>
 struct BigUnroll<App, std::void_t<decltype(App::kBigUnroll)>> {
   static constexpr int value = App::kBigUnroll;
 };
-// Work donation is compiled only into apps that declare App::kDonate = true
-// (the extra code would cost the register-capped BFS / SSSP parents)
-template <class App, class = void>
-struct Donates {
-  static constexpr bool value = false;
-};
-template <class App>
-struct Donates<App, std::void_t<decltype(App::kDonate)>> {
-  static constexpr bool value = App::kDonate;
-};
-
-// Work donation: the whole warp drains donated entry `idx`, claiming one
-// chunk at a time (an atomic per chunk keeps every chunk processed once).
-template <class App>
-__device__ __forceinline__ void drain_donated(const App& app, const Knobs& k,
-                                              int idx,
-                                              typename App::Acc& acc) {
-  using Args = typename App::Args;
-  constexpr int UB = DP_BIG_UNROLL > 0 ? DP_BIG_UNROLL : BigUnroll<App>::value;
-  constexpr int CH = 64 * UB;  // items per chunk: two warp steps
-  DonateEntry<Args>* E = (DonateEntry<Args>*)k.dq_entries + idx;
-  Args b;
-  {  // rows are 16-byte multiples (find_row): 128-bit L2 reads
-    const int4* src = reinterpret_cast<const int4*>(&E->a);
-    int4* dst = reinterpret_cast<int4*>(&b);
-#pragma unroll
-    for (int i = 0; i < (int)(sizeof(b) / 16); ++i) dst[i] = __ldcg(src + i);
-  }
-  const int cnt = __ldcg(&E->cnt), nch = __ldcg(&E->nchunk);
-  auto args = [&](int) -> const Args& { return b; };
-  for (;;) {
-    int c = 0;
-    if (lane_id() == 0) c = atomicAdd(&E->next, 1);
-    c = __shfl_sync(DP_FULL, c, 0);
-    if (c >= nch) break;
-    const int c1 = min((c + 1) * CH, cnt);
-    for (int e0 = c * CH; e0 < c1; e0 += 32 * UB) {
-      int e[UB];
-      bool ok[UB];
-#pragma unroll
-      for (int j = 0; j < UB; ++j) {
-        e[j] = e0 + j * 32 + lane_id();
-        ok[j] = e[j] < c1;
-      }
-      app.template items<UB>(args, e, ok, acc);
-    }
-  }
-}
-
-// a warp out of work helps with every published entry not yet exhausted
-template <class App>
-__device__ __forceinline__ void steal_donated(const App& app, const Knobs& k,
-                                              typename App::Acc& acc) {
-  using Args = typename App::Args;
-  DonateEntry<Args>* ent = (DonateEntry<Args>*)k.dq_entries;
-  const int tail = min(__ldcg(&k.dq->tail), k.dq_cap);
-  for (int j = __ldcg(&k.dq->cursor); j < tail; ++j) {
-    unsigned ready;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];"
-                 : "=r"(ready)
-                 : "l"(&ent[j].ready));
-    if (ready != k.epoch) continue;  // still being published: its owner
-                                     // drains it
-    if (__ldcg(&ent[j].next) < __ldcg(&ent[j].nchunk))
-      drain_donated(app, k, j, acc);
-    if (lane_id() == 0) atomicMax(&k.dq->cursor, j + 1);
-  }
-}
-
 template <class App>
 __device__ __forceinline__ void serial_arm(const App& app,
                                            const typename App::Args& a, int cnt,
                                            bool mine, bool warp_mode,
-                                           typename App::Acc& acc,
-                                           const Knobs& k) {
+                                           typename App::Acc& acc) {
   constexpr int U = App::kUnroll;
   using Args = typename App::Args;
   if (!warp_mode) {
@@ -447,38 +355,6 @@ __device__ __forceinline__ void serial_arm(const App& app,
   // lanes with >= 32 items: the whole warp walks that lane's items, U x 32
   // at a time (no owner search)
   unsigned big = __ballot_sync(DP_FULL, mine && cnt >= 32);
-  // work donation: rows of >= k.donate items are published for any warp to
-  // share (the queue full: the owner walks them as big rows)
-  int my_entry = -1;
-  unsigned don = 0;
-  if constexpr (Donates<App>::value) if (k.dq) {
-    using E = DonateEntry<Args>;
-    constexpr int UB = DP_BIG_UNROLL > 0 ? DP_BIG_UNROLL
-                                         : BigUnroll<App>::value;
-    const bool want = mine && cnt >= k.donate;
-    const unsigned wm = __ballot_sync(DP_FULL, want);
-    if (wm) {
-      const int leader = __ffs(wm) - 1;
-      int base = 0;
-      if (lane_id() == leader) base = atomicAdd(&k.dq->tail, __popc(wm));
-      base = __shfl_sync(DP_FULL, base, leader);
-      const int idx = base + __popc(wm & lanemask_lt());
-      if (want && idx < k.dq_cap) {
-        E* e = (E*)k.dq_entries + idx;
-        e->a = a;
-        e->cnt = cnt;
-        e->nchunk = ceil_div(cnt, 64 * UB);
-        e->next = 0;
-        __threadfence();
-        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&e->ready),
-                     "r"(k.epoch)
-                     : "memory");
-        my_entry = idx;
-      }
-      don = __ballot_sync(DP_FULL, my_entry >= 0);
-      big &= ~don;
-    }
-  }
   while (big) {
     const int src = __ffs(big) - 1;
     big &= big - 1;
@@ -525,14 +401,6 @@ __device__ __forceinline__ void serial_arm(const App& app,
     app.template items<U>([&](int j) -> const Args& { return b[j]; }, e, ok,
                           acc);
   }
-  if constexpr (Donates<App>::value) if (k.dq) {
-    while (don) {  // own donated rows first, then any other warp's
-      const int src = __ffs(don) - 1;
-      don &= don - 1;
-      drain_donated(app, k, __shfl_sync(DP_FULL, my_entry, src), acc);
-    }
-    steal_donated(app, k, acc);
-  }
 }
 
 template <class App, int AGG, bool CDP>
@@ -555,7 +423,7 @@ __global__ void __launch_bounds__(256, App::kMinBlocks)
   if constexpr (!CDP) {
     // No-CDP variant (e.g. BFS_NOCDP, benchmarks.py:122-141): no launch code
     const long long t_child = ph_now();
-    serial_arm(app, a, cnt, true, k.serial_warp != 0, acc, k);
+    serial_arm(app, a, cnt, true, k.serial_warp != 0, acc);
     app.flush(acc);
     ph_add(ds, kPhChild, t_child);
   } else {
@@ -696,7 +564,7 @@ __global__ void __launch_bounds__(256, App::kMinBlocks)
     }
     ph_add(ds, kPhAgg, t_agg + tl);  // the protocol minus its launches
     const long long t_child = ph_now();
-    serial_arm(app, a, cnt, !go, k.serial_warp != 0, acc, k);
+    serial_arm(app, a, cnt, !go, k.serial_warp != 0, acc);
     app.flush(acc);
     ph_add(ds, kPhChild, t_child);
   }
@@ -778,7 +646,7 @@ __global__ void __launch_bounds__(256)
     const int cnt = app.expand((int)(base + lu),
                                lu < nparents && base + lu < app.nparents(), a);
     const bool go = cnt > 0 && (k.threshold == 0 || cnt >= k.threshold);
-    serial_arm(app, a, cnt, !go, k.serial_warp != 0, acc, k);
+    serial_arm(app, a, cnt, !go, k.serial_warp != 0, acc);
   }
   app.flush(acc);
 }

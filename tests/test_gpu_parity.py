@@ -247,15 +247,7 @@ def test_tc_vs_oracle(spec):
     BenchConfig(), BenchConfig(threshold=4096),
     BenchConfig(cfactor=4, agg="multiblock", group_size=4),
     BenchConfig(threshold=64, cfactor=2, agg="block", parent_block=128),
-    BenchConfig(agg="grid", child_block=64),
-    # work donation of the long curves among the parent warps
-    BenchConfig(threshold=2147483647, serial="warp", parent_block=64,
-                donate=64),
-    BenchConfig(threshold=2147483647, serial="warp", parent_block=32,
-                donate=32),
-    BenchConfig(threshold=512, cfactor=2, agg="multiblock",
-                group_size=1 << 20, serial="warp", child_block=128,
-                donate=128)])
+    BenchConfig(agg="grid", child_block=64)])
 def test_bt_vs_oracle(cfg):
     bench, wl = load("bt", "curves:25000:seed1")
     ntess, verts = oracle.bt(wl.buffers["cp"], graphs.BT_MAX_TESS,

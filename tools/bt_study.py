@@ -22,12 +22,6 @@ from paper_2201_02789_b200.bench.graphs import (BT_CURV_SCALE,  # noqa: E402
                                                 BT_MAX_TESS, bezier_curves)
 
 POLICIES = [
-    dict(threshold=INF_THRESHOLD, serial="warp", parent_block=64, donate=64),
-    dict(threshold=INF_THRESHOLD, serial="warp", parent_block=64, donate=128),
-    dict(threshold=INF_THRESHOLD, serial="warp", parent_block=64, donate=256),
-    dict(threshold=INF_THRESHOLD, serial="warp", parent_block=32, donate=128),
-    dict(threshold=INF_THRESHOLD, serial="warp", parent_block=128,
-         donate=128),
     dict(threshold=INF_THRESHOLD, serial="warp", parent_block=32),
     dict(threshold=INF_THRESHOLD, serial="warp", parent_block=128),
     dict(threshold=256, cfactor=1, agg="multiblock", group_size=1 << 20,
