@@ -53,12 +53,15 @@ SEED = 1
 BEST = {
     # one aggregation group spanning the parent grid: the last parent block
     # issues ONE CDP2 launch per round (tools/tune.py, profiles/tune_*)
+    # cf_wave: the source hub's child (160k edges at RMAT-22, 1,247 logical
+    # blocks) runs uncoarsened: BFS level 0 80 -> 58 us, SSSP round 0
+    # 72 -> 57 us (profiles/r02/ab_cfwave_r02.txt)
     "sssp": dict(threshold=1024, cfactor=16, agg="multiblock",
                  group_size=1 << 20, parent_block=128, child_block=128,
-                 serial="warp"),
+                 serial="warp", cf_wave=592),
     "bfs": dict(threshold=1024, cfactor=16, agg="multiblock",
                 group_size=1 << 20, parent_block=256, child_block=128,
-                serial="warp"),
+                serial="warp", cf_wave=592),
     # TC over the transposed CSR+ (profiles/tune_tc_rmat22_r01c.txt)
     "tc": dict(threshold=32, cfactor=4, agg="grid", parent_block=128,
                child_block=256, serial="warp"),

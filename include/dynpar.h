@@ -129,6 +129,11 @@ typedef struct dp_config {
                             of the copy (out-of-range chunks and all later
                             ones stay int32), dp_sssp_dev packs on the
                             device.  0 = int32 weights as given */
+  int32_t cf_wave;       /* B200: a row whose logical child grid has >=
+                            cf_wave blocks runs uncoarsened (coarsening
+                            amortises setup over many small children; one
+                            huge child would only be serialised).  0 = every
+                            row coarsened by cfactor (the reference) */
 } dp_config;
 
 /* SimReport (sim/report.py:12-28) counters, measured on the device */

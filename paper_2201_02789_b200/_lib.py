@@ -43,7 +43,8 @@ class DpConfig(ctypes.Structure):
                 ("frontier", ctypes.c_int32),
                 ("agg_coarsen", ctypes.c_int32),
                 ("counts_spread", ctypes.c_int32),
-                ("weight_bits", ctypes.c_int32)]
+                ("weight_bits", ctypes.c_int32),
+                ("cf_wave", ctypes.c_int32)]
 
 
 class DpStats(ctypes.Structure):

@@ -55,6 +55,7 @@ class BenchConfig:
     device_loop: bool = False
     frontier: bool = False
     weight_bits: int = 0
+    cf_wave: int = 0
 
     def describe(self) -> str:
         return (f"threshold={self.threshold} cfactor={self.cfactor} "
@@ -90,6 +91,8 @@ class BenchConfig:
             raise ValueError(f"unknown serial mode {self.serial!r}")
         if self.weight_bits not in (0, 4):
             raise ValueError("weight_bits must be 0 (int32) or 4 (packed)")
+        if self.cf_wave < 0:
+            raise ValueError("cf_wave must be >= 0")
 
     def to_c(self, variant: int = _lib.VARIANT_CDP) -> _lib.DpConfig:
         self.validate()
@@ -111,6 +114,7 @@ class BenchConfig:
         c.device_loop = int(bool(self.device_loop))
         c.frontier = int(bool(self.frontier))
         c.weight_bits = int(self.weight_bits)
+        c.cf_wave = int(self.cf_wave)
         c.threshold, c.cfactor, c.agg_coarsen = self.order_effect(
             c.threshold, c.cfactor, self.agg if agg_on else None)
         return c

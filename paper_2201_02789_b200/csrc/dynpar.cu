@@ -183,6 +183,10 @@ int validate(const dp_config* c) {
     return fail(DP_ERR_INVALID, "counts_spread must be in [0, 30]");
   if (c->weight_bits != 0 && c->weight_bits != 4)
     return fail(DP_ERR_INVALID, "weight_bits must be 0 or 4");
+  if (c->cf_wave < 0) return fail(DP_ERR_INVALID, "cf_wave must be >= 0");
+  if (c->cf_wave > 0 && c->agg_coarsen)
+    return fail(DP_ERR_INVALID,
+                "cf_wave applies to per-row coarsening (canonical order)");
   if (c->agg_coarsen &&
       (c->agg < DP_AGG_WARP || c->agg > DP_AGG_MULTIBLOCK || c->persistent))
     return fail(DP_ERR_INVALID,
@@ -366,6 +370,7 @@ Knobs knobs_of(const dp_config* c) {
   k.agg_threshold = c->agg_threshold;
   k.serial_warp = c->serial_mode == DP_SERIAL_WARP;
   k.agg_cf = c->agg_coarsen != 0;
+  k.cf_wave = c->cf_wave;
   return k;
 }
 
@@ -579,7 +584,7 @@ glue:
     const int total = (int)(cv & 0xffffffffull);
     if (total > 0) {
       child_agg_kernel<App><<<total, c->child_block, 0, s>>>(
-          app, t.args, t.scan, np, c->cfactor, 0, w->ds, 0ull);
+          app, t.args, t.scan, np, c->cfactor, c->cf_wave, w->ds, 0ull);
       DP_CUDA(cudaGetLastError());
       rc->host_launches += 1;
       rc->host_blocks += total;

@@ -39,7 +39,10 @@ B200_VARIANTS = [dict(), dict(parent_block=256), dict(child_block=128),
                  dict(serial="warp"), dict(parent_block=128, serial="warp",
                                            child_block=64),
                  dict(persistent=2, parent_block=128, serial="warp"),
-                 dict(device_loop=True, parent_block=64)]
+                 dict(device_loop=True, parent_block=64),
+                 # rows of >= cf_wave logical blocks run uncoarsened
+                 dict(cf_wave=2), dict(cf_wave=1, child_block=64),
+                 dict(weight_bits=4, serial="warp")]
 
 
 def _cfg(d):
