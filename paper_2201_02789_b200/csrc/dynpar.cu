@@ -255,6 +255,8 @@ int effective_threshold(const dp_config* c) {
 
 long long launch_bound(const dp_config* c, long long parents,
                        long long launchers);
+long long launch_bound_agg(const dp_config* c, long long launchers,
+                           long long warps, long long blocks);
 
 // kind 0: CSR rowptr degrees, 1: per-parent values.  Skipped (returns the
 // parent count) when the policy's structural bound -- warps, blocks or
@@ -293,6 +295,14 @@ long long launch_bound(const dp_config* c, long long parents,
   if (c->variant != DP_VARIANT_CDP) return 0;
   const long long warps = dp::ceil_div_ll(parents, 32);
   const long long blocks = dp::ceil_div_ll(parents, c->parent_block);
+  // cf_wave: every launching row may be big enough for a launch of its own
+  const long long solo =
+      c->cf_wave > 0 && c->agg != DP_AGG_NONE ? launchers : 0;
+  return solo + launch_bound_agg(c, launchers, warps, blocks);
+}
+
+long long launch_bound_agg(const dp_config* c, long long launchers,
+                           long long warps, long long blocks) {
   switch (c->agg) {
     case DP_AGG_NONE: return launchers;
     case DP_AGG_WARP: return std::min(launchers, warps);
@@ -418,7 +428,7 @@ long long wave_parents(const dp_config* c, long long nparents,
   if (c->variant != DP_VARIANT_CDP) return nparents;
   if (launch_bound(c, nparents, launchers) <= kMaxPending) return nparents;
   long long per_launch = 1;  // parents that share one potential launch
-  switch (c->agg) {
+  if (c->cf_wave <= 0) switch (c->agg) {
     case DP_AGG_WARP: per_launch = 32; break;
     case DP_AGG_BLOCK:
       per_launch = c->agg_threshold > 0 ? 1 : c->parent_block;
@@ -584,7 +594,7 @@ glue:
     const int total = (int)(cv & 0xffffffffull);
     if (total > 0) {
       child_agg_kernel<App><<<total, c->child_block, 0, s>>>(
-          app, t.args, t.scan, np, c->cfactor, c->cf_wave, w->ds, 0ull);
+          app, t.args, t.scan, np, c->cfactor, 0, w->ds, 0ull);
       DP_CUDA(cudaGetLastError());
       rc->host_launches += 1;
       rc->host_blocks += total;

@@ -56,16 +56,7 @@ struct Knobs {
                       // not coarsened (0: every row uses cf), see row_cf
 };
 
-// Coarsening factor of one row (B200, dp_config.cf_wave): a row whose
-// logical child grid alone reaches cf_wave blocks (about one wave of the
-// GPU) runs uncoarsened -- coarsening exists to amortise per-block setup
-// over many small children, and would only serialise one huge child (the
-// RMAT-22 source's 160k edges: 1,247 logical blocks folded onto 78 physical
-// ones made BFS level 0 / SSSP round 0 take ~75 us).
-__host__ __device__ __forceinline__ int row_cf(int cf, int cf_wave,
-                                               long long gl) {
-  return cf_wave > 0 && gl >= cf_wave ? 1 : cf;
-}
+
 
 template <class App>
 struct AggTables {
@@ -78,6 +69,19 @@ struct AggTables {
 // ---------------------------------------------------------------------------
 // children
 // ---------------------------------------------------------------------------
+
+// Coarsening factor of one row (B200, dp_config.cf_wave): a row whose
+// logical child grid alone reaches cf_wave blocks (about one wave of the
+// GPU) runs uncoarsened -- coarsening exists to amortise per-block setup
+// over many small children, and would only serialise one huge child (the
+// RMAT-22 source's 160k edges: 1,247 logical blocks folded onto 78 physical
+// ones made BFS level 0 / SSSP round 0 take ~75 us).  Under aggregation such
+// a row gets a launch of its own (parent_kernel): computing a per-row factor
+// inside the aggregated child cost the SSSP child 76 bytes of spills.
+__host__ __device__ __forceinline__ int row_cf(int cf, int cf_wave,
+                                               long long gl) {
+  return cf_wave > 0 && gl >= cf_wave ? 1 : cf;
+}
 
 // Logical blocks [lb*cf, min(lb*cf+cf, ceil(cnt/cb))) of one child grid.
 // Thread t owns item b*cb + t of each logical block b; U logical blocks are
@@ -261,8 +265,9 @@ __device__ __forceinline__ long long find_row(const typename App::Args* tab,
 template <class App>
 __global__ void __launch_bounds__(256, App::kMinBlocks) child_agg_kernel(App app, const typename App::Args* tab,
                                  const int* scan, int np, int cf,
-                                 int cf_wave, DevState* ds,
+                                 int agg_total, DevState* ds,
                                  unsigned long long ts) {
+  (void)agg_total;
   note_child_start(ds, ts);
   const long long t0 = ph_now();
   typename App::Acc acc{};
@@ -270,9 +275,7 @@ __global__ void __launch_bounds__(256, App::kMinBlocks) child_agg_kernel(App app
   const long long lb = find_row<App>(tab, scan, np, (int)blockIdx.x, a, ds);
   ph_add(ds, kPhDisagg, t0);
   const long long t1 = ph_now();
-  const int cfr =
-      row_cf(cf, cf_wave, ceil_div_ll(App::count(a), (long long)blockDim.x));
-  run_logical_blocks(app, a, lb, cfr, acc);
+  run_logical_blocks(app, a, lb, cf, acc);
   app.flush(acc);
   ph_add(ds, kPhChild, t1);
 }
@@ -306,14 +309,13 @@ template <class App>
 __device__ __forceinline__ void launch_agg(const App& app, int pg, int cb,
                                            const typename App::Args* tab,
                                            const int* scan, int np, int cf,
-                                           int agg_total, int cf_wave,
-                                           DevState* ds) {
+                                           int agg_total, DevState* ds) {
   if (agg_total > 0)
     child_agg_lb_kernel<App><<<pg, cb, 0, cudaStreamFireAndForget>>>(
         app, tab, scan, np, cf, agg_total, ds, globaltimer_ns());
   else
     child_agg_kernel<App><<<pg, cb, 0, cudaStreamFireAndForget>>>(
-        app, tab, scan, np, cf, cf_wave, ds, globaltimer_ns());
+        app, tab, scan, np, cf, 0, ds, globaltimer_ns());
 }
 
 // physical blocks of an aggregated launch over `total` aggregated blocks
@@ -448,8 +450,22 @@ __global__ void __launch_bounds__(256, App::kMinBlocks)
     // physical (coarsened) child grid of this parent thread; under agg_cf
     // the recorded rows stay uncoarsened and the aggregated grid is
     // coarsened instead (direct launches are per-parent coarsened always)
-    const int gl = go ? ceil_div(cnt, k.cb) : 0;
+    int gl = go ? ceil_div(cnt, k.cb) : 0;
     const int cfr = row_cf(k.cf, k.cf_wave, gl);
+    if constexpr (AGG != kAggNone) {
+      // cf_wave: a row whose child fills a GPU wave is launched on its own,
+      // uncoarsened, and stays out of the aggregated grid (whose per-row
+      // coarsening stays uniform)
+      if (cfr != k.cf) {
+        DP_TIMED_LAUNCH(ds, tl,
+            child_kernel<App><<<gl, k.cb, 0, cudaStreamFireAndForget>>>(
+                app, a, 1, ds, globaltimer_ns());
+            note_launch_error(ds));
+        atomicAdd(&ds->launches, 1ull);
+        atomicAdd(&ds->blocks, (unsigned long long)gl);
+        gl = 0;
+      }
+    }
     const int gd = AGG == kAggNone || !k.agg_cf ? ceil_div(gl, cfr) : gl;
     // The launch / aggregation protocol runs BEFORE the serial arm (the
     // reference places it after the enclosing statement, aggregate.py:
@@ -484,8 +500,7 @@ __global__ void __launch_bounds__(256, App::kMinBlocks)
           const int pg = agg_grid(k, total);
           DP_TIMED_LAUNCH(ds, tl,
               launch_agg(app, pg, k.cb, t.args + row0, t.scan + row0,
-                         __popc(m), k.cf, k.agg_cf ? total : 0, k.cf_wave,
-                         ds);
+                         __popc(m), k.cf, k.agg_cf ? total : 0, ds);
               note_launch_error(ds));
           atomicAdd(&ds->launches, 1ull);
           atomicAdd(&ds->blocks, (unsigned long long)pg);
@@ -502,11 +517,11 @@ __global__ void __launch_bounds__(256, App::kMinBlocks)
       if constexpr (AGG == kAggBlock) {
         if (k.agg_threshold > 0 && s.np < k.agg_threshold) {
           // aggregate.py:376-392: too few participants -> direct launches
-          const int gdd = ceil_div(gl, cfr);
+          const int gdd = ceil_div(gl, k.cf);
           if (gdd > 0) {
             DP_TIMED_LAUNCH(ds, tl,
                 child_kernel<App><<<gdd, k.cb, 0, cudaStreamFireAndForget>>>(
-                    app, a, cfr, ds, globaltimer_ns());
+                    app, a, k.cf, ds, globaltimer_ns());
                 note_launch_error(ds));
           }
           count_launches_warp(ds, gdd > 0, gdd);
@@ -523,8 +538,7 @@ __global__ void __launch_bounds__(256, App::kMinBlocks)
             const int pg = agg_grid(k, s.total);
             DP_TIMED_LAUNCH(ds, tl,
                 launch_agg(app, pg, k.cb, t.args + row0, t.scan + row0,
-                           s.np, k.cf, k.agg_cf ? s.total : 0, k.cf_wave,
-                           ds);
+                           s.np, k.cf, k.agg_cf ? s.total : 0, ds);
                 note_launch_error(ds));
             atomicAdd(&ds->launches, 1ull);
             atomicAdd(&ds->blocks, (unsigned long long)pg);
@@ -568,7 +582,7 @@ __global__ void __launch_bounds__(256, App::kMinBlocks)
                 const int pg = agg_grid(k, total);
                 DP_TIMED_LAUNCH(ds, tl,
                     launch_agg(app, pg, k.cb, t.args + sb, t.scan + sb, np,
-                               k.cf, k.agg_cf ? total : 0, k.cf_wave, ds);
+                               k.cf, k.agg_cf ? total : 0, ds);
                     note_launch_error(ds));
                 atomicAdd(&ds->launches, 1ull);
                 atomicAdd(&ds->blocks, (unsigned long long)pg);
@@ -617,7 +631,7 @@ __global__ void __launch_bounds__(256)
                                lu < nparents && base + lu < app.nparents(), a);
     const bool go = cnt > 0 && (k.threshold == 0 || cnt >= k.threshold);
     const int gl = go ? ceil_div(cnt, k.cb) : 0;
-    const int gd = ceil_div(gl, row_cf(k.cf, k.cf_wave, gl));
+    const int gd = ceil_div(gl, k.cf);
     const BlockScan s = block_scan(gd > 0, gd, smem);
     if (threadIdx.x == 0)
       s_old = s.np > 0 ? atomicAdd(&t.ctr[0], ((unsigned long long)s.np << 32) +
@@ -649,7 +663,7 @@ __global__ void __launch_bounds__(256)
         if (np > 0) {
           note_launch_issue(ds);
           child_agg_kernel<App><<<total, k.cb, 0, cudaStreamFireAndForget>>>(
-              app, t.args, t.scan, np, k.cf, k.cf_wave, ds, globaltimer_ns());
+              app, t.args, t.scan, np, k.cf, 0, ds, globaltimer_ns());
           note_launch_error(ds);
           atomicAdd(&ds->launches, 1ull);
           atomicAdd(&ds->blocks, (unsigned long long)total);

@@ -23,16 +23,20 @@ def main():
     torch.cuda.set_device(0)
     G = bench.DeviceGraph(scale, 1, weights=True)
     s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    nocdp = extra.pop("nocdp", False)
     for kind in ("bfs", "sssp"):
         pol = dict(bench.BEST[kind], **extra)
+        from paper_2201_02789_b200.bench import BenchConfig
+        cfg = (BenchConfig(**pol).to_c(_lib.VARIANT_NOCDP) if nocdp
+               else bench._cfg(pol))
         runs = []
         for _ in range(6):
-            st = bench.run_dev(kind, G, bench._cfg(pol), s)
+            st = bench.run_dev(kind, G, cfg, s)
             runs.append((st["ns_device"] / 1e6, _lib.step_times()))
         runs = runs[1:]
         steps = [statistics.median(r[1][i] for r in runs)
                  for i in range(len(runs[0][1]))]
-        print(json.dumps({"kind": kind, "policy": pol,
+        print(json.dumps({"kind": kind, "policy": pol, "nocdp": nocdp,
                           "ms": statistics.median(r[0] for r in runs),
                           "step_ms": [round(x, 4) for x in steps],
                           "sum_steps": round(sum(steps), 4)}), flush=True)
