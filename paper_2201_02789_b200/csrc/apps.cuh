@@ -101,6 +101,12 @@ struct BfsApp {
   int* counts;        // counts[spread_slot(v, cmask)] (common.cuh)
   int* changed;       // this level's flag
   int* changed_next;  // next level's flag, cleared here
+  // launch bits (bit v: v's row would launch under the policy's threshold)
+  // and the flag "the next level holds such a vertex" (DevState::big); null
+  // when the host does not pick the parent variant per level
+  const unsigned* __restrict__ lbits;
+  int* big_next;
+  int* big_after;  // the level after next's flag, cleared here
   int n;
   int level;
   unsigned cmask;     // spread layout of counts (0: vertex order)
@@ -111,11 +117,15 @@ struct BfsApp {
   };
   struct Acc {
     int changed;
+    int big;
   };
 
   __device__ int nparents() const { return n; }
   __device__ void parent_prologue() const {
-    if (blockIdx.x == 0 && threadIdx.x == 0) *changed_next = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      *changed_next = 0;
+      if (lbits) *big_after = 0;
+    }
   }
   // the app of level r (device-side level loop)
   __device__ BfsApp for_round(int r, int* flags) const {
@@ -123,7 +133,12 @@ struct BfsApp {
     a.level = r;
     a.changed = flags + (r & 1);
     a.changed_next = flags + ((r + 1) & 1);
+    a.lbits = nullptr;  // the device loop keeps the launching variant
     return a;
+  }
+  // a discovered vertex whose row would launch next level
+  __device__ __forceinline__ void note_big(int v, Acc& acc) const {
+    if (lbits && (__ldg(lbits + (v >> 5)) >> (v & 31) & 1u)) acc.big = 1;
   }
   // main (:105-119): u with dist[u] == level owns deg = rowptr[u+1]-rowptr[u]
   __device__ int expand(int u, bool valid, Args& a) const {
@@ -140,8 +155,10 @@ struct BfsApp {
     const int v = __ldg(col + a.start + e);
     atomicAdd(counts + spread_slot(v, cmask), 1);
     if (__ldcg(dist + v) == kUnreached &&
-        atomicCAS(dist + v, kUnreached, a.level + 1) == kUnreached)
+        atomicCAS(dist + v, kUnreached, a.level + 1) == kUnreached) {
       acc.changed = 1;
+      note_big(v, acc);
+    }
   }
   // counts[v] += 1 with lanes that hit the same v merged into one atomic:
   // RMAT hub destinations otherwise serialise at one L2 slice
@@ -186,8 +203,11 @@ struct BfsApp {
       }
 #else
       if (d[j] == kUnreached &&
-          atomicCAS(dist + v[j], kUnreached, args(j).level + 1) == kUnreached)
+          atomicCAS(dist + v[j], kUnreached, args(j).level + 1) ==
+              kUnreached) {
         acc.changed = 1;
+        note_big(v[j], acc);
+      }
 #endif
     }
   }
@@ -197,6 +217,9 @@ struct BfsApp {
     if (__any_sync(DP_FULL, acc.changed) && lane_id() == 0 &&
         __ldcg(changed) == 0)
       *changed = 1;
+    if (lbits && __any_sync(DP_FULL, acc.big) && lane_id() == 0 &&
+        __ldcg(big_next) == 0)
+      *big_next = 1;
   }
 };
 

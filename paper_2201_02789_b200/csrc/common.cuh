@@ -161,6 +161,10 @@ struct DevState {
   // partitioned apps with the fused exchange: atomics issued into other
   // parts' dist (NVLink / NVSwitch peer traffic when parts are GPUs)
   unsigned long long remote;
+  // BFS: a vertex discovered for the next level would launch (degree >= T):
+  // double-buffered like flag; 0 lets the host run that level's parent grid
+  // as the launch-free variant
+  int big[2];
 };
 
 // ---------------------------------------------------------------------------

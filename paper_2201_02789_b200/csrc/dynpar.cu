@@ -81,6 +81,9 @@ struct Workspace {
   // publication-checker builds: one stamp per aggregation-table row
   void* pub = nullptr;
   size_t pub_bytes = 0;
+  // BFS launch bits (bit v: v's row reaches the threshold)
+  void* lbits = nullptr;
+  size_t lbits_bytes = 0;
   // packed SSSP weights: device copy and the pinned host staging of dp_sssp
   void* wpack = nullptr;
   size_t wpack_bytes = 0;
@@ -837,11 +840,22 @@ struct Arrival {
 struct NoFinish {
   void operator()() const {}
 };
+// which levels need the launching parent variant (default: all of them)
+struct AlwaysCdp {
+  bool operator()(int, const DevState*) const { return true; }
+};
 
-template <class MakeApp, class Finish = NoFinish>
+template <class MakeApp, class Finish = NoFinish, class Pick = AlwaysCdp>
 int iterate(Workspace* w, const dp_config* c, long long nparents,
             long long launchers, int max_iter, cudaStream_t s, MakeApp make,
-            dp_stats* st, Arrival* arr = nullptr, Finish finish = Finish()) {
+            dp_stats* st, Arrival* arr = nullptr, Finish finish = Finish(),
+            Pick pick = Pick()) {
+  // a level in which no parent can reach the threshold runs the launch-free
+  // parent variant: same serial arm, same outputs and counters, but without
+  // the ~11 us a CDP-capable parent grid costs even when it launches nothing
+  // (profiles/r02/floor_probe_r02.txt)
+  dp_config c_flat = *c;
+  c_flat.variant = DP_VARIANT_NOCDP;
   RunCounters rc;
   int r;
   if ((r = ensure_pending_limit(w, c, launch_bound(c, nparents, launchers))))
@@ -859,7 +873,9 @@ int iterate(Workspace* w, const dp_config* c, long long nparents,
   }
   for (; !converged && it <= max_iter; ++it) {
     auto app = make(it, w->ds);
-    if ((r = launch_parent(app, nparents, launchers, c, w, s, &rc))) return r;
+    const dp_config* cl =
+        c->variant == DP_VARIANT_CDP && !pick(it, w->h_ds) ? &c_flat : c;
+    if ((r = launch_parent(app, nparents, launchers, cl, w, s, &rc))) return r;
     if ((r = read_state_fast(w, s))) return r;
     if ((r = account_step(w, &rc))) return r;
     if (w->h_ds->flag[it & 1] == 0 &&
@@ -891,6 +907,25 @@ int iterate(Workspace* w, const dp_config* c, long long nparents,
   return 0;
 }
 
+// bit v = 1 iff row v would launch under threshold t (cnt > 0 and (t == 0
+// or cnt >= t), sched.cuh parent_kernel); one warp per 32 words
+__global__ void launch_bits_kernel(const int* __restrict__ rowptr, int n,
+                                   int t, unsigned* bits) {
+  const long long words = (n + 31) / 32;
+  for (long long wd = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+       wd * 32 < (long long)n + 0 && wd < words;
+       wd += ((long long)gridDim.x * blockDim.x) >> 5) {
+    const long long v = wd * 32 + lane_id();
+    bool go = false;
+    if (v < n) {
+      const int d = __ldg(rowptr + v + 1) - __ldg(rowptr + v);
+      go = d > 0 && (t == 0 || d >= t);
+    }
+    const unsigned m = __ballot_sync(DP_FULL, go);
+    if (lane_id() == 0) bits[wd] = m;
+  }
+}
+
 int bfs_dev_impl(const int32_t* rowptr, const int32_t* col, int32_t n,
                  int32_t src, const dp_config* c, int32_t* dist,
                  int32_t* counts, cudaStream_t s, dp_stats* st) {
@@ -920,6 +955,20 @@ int bfs_dev_impl(const int32_t* rowptr, const int32_t* col, int32_t n,
   if (c->variant == DP_VARIANT_CDP &&
       (r = count_launchers(w, c, rowptr, n, 0, s, &launchers)))
     return r;
+  // launch bits: the host picks each level's parent variant from whether the
+  // previous level discovered any vertex whose row would launch
+  const unsigned* lbits = nullptr;
+  const bool per_level = c->variant == DP_VARIANT_CDP && !c->device_loop;
+  if (per_level) {
+    if ((r = grow(&w->lbits, &w->lbits_bytes,
+                  (size_t)(n + 31) / 32 * sizeof(unsigned))))
+      return r;
+    lbits = (const unsigned*)w->lbits;
+    launch_bits_kernel<<<std::min(dp::ceil_div(dp::ceil_div(n, 32), 8), 148 * 8),
+                         256, 0, s>>>(rowptr, n, effective_threshold(c),
+                                      (unsigned*)w->lbits);
+    DP_CUDA(cudaGetLastError());
+  }
   // bench/benchmarks.py:157-168: one launch per level until nothing changes
   return iterate(w, c, n, launchers, n, s,
                  [&](int level, DevState* ds) {
@@ -930,6 +979,9 @@ int bfs_dev_impl(const int32_t* rowptr, const int32_t* col, int32_t n,
                    a.counts = cw;
                    a.changed = &ds->flag[level & 1];
                    a.changed_next = &ds->flag[(level + 1) & 1];
+                   a.lbits = lbits;
+                   a.big_next = &ds->big[(level + 1) & 1];
+                   a.big_after = &ds->big[level & 1];
                    a.n = n;
                    a.level = level;
                    a.cmask = cmask;
@@ -940,6 +992,10 @@ int bfs_dev_impl(const int32_t* rowptr, const int32_t* col, int32_t n,
                    if (cmask)
                      unspread_kernel<<<dp::ceil_div(n, 256), 256, 0, s>>>(
                          cw, cmask, counts, n);
+                 },
+                 [&](int level, const DevState* h) {
+                   // level 0 (the source alone) keeps the launching variant
+                   return !per_level || level == 0 || h->big[level & 1] != 0;
                  });
 }
 
@@ -2918,6 +2974,7 @@ void dp_thread_release(void) {
     cudaFree(w.wpack);
     cudaFreeHost(w.h_wpack);
     cudaFree(w.d_bad);
+    cudaFree(w.lbits);
     w = Workspace();
   }
 }
