@@ -15,7 +15,10 @@ METRICS = [
     "sm__throughput.avg.pct_of_peak_sustained_elapsed",
     "sm__warps_active.avg.pct_of_peak_sustained_active",
     "launch__registers_per_thread", "lts__t_sector_hit_rate.pct",
-    "l1tex__t_sector_hit_rate.pct"]
+    "l1tex__t_sector_hit_rate.pct",
+    # register spills actually executed (local-memory traffic)
+    "l1tex__t_requests_pipe_lsu_mem_local_op_ld.sum",
+    "l1tex__t_requests_pipe_lsu_mem_local_op_st.sum"]
 STALL = "smsp__average_warps_issue_stalled_"
 
 raw = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv"],
