@@ -165,6 +165,9 @@ struct DevState {
   // double-buffered like flag; 0 lets the host run that level's parent grid
   // as the launch-free variant
   int big[2];
+  // partitioned BFS: this part's next frontier holds a launching row (set
+  // by part_big_kernel, OR-ed over the parts into big[] by the flag OR)
+  int big_local;
 };
 
 // ---------------------------------------------------------------------------

@@ -2030,39 +2030,64 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys_u64(
   return v;
 }
 
-// one warp; flag_slot < 0: a pure barrier
+// one warp; flag_slot < 0: a pure barrier.  Each tag carries two bits: the
+// round's `changed` flag and (partitioned BFS) whether the part's next
+// frontier holds a launching row; both are OR-ed over the parts.
 __global__ void part_flag_or_kernel(unsigned long long* const* peer_sig,
                                     int nparts, int part, long long idx,
                                     unsigned long long epoch, DevState* ds,
                                     int flag_slot,
                                     unsigned long long timeout_ns) {
   const int lane = threadIdx.x;
-  const int bit = flag_slot >= 0 && ds->flag[flag_slot] != 0;
+  const unsigned bits =
+      flag_slot >= 0
+          ? (ds->flag[flag_slot] != 0 ? 1u : 0u) | (ds->big_local ? 2u : 0u)
+          : 0u;
   const unsigned long long key =
-      (epoch << 32) | (unsigned long long)(idx + 1);  // tag >> 1
+      (epoch << 32) | (unsigned long long)(idx + 1);  // tag >> 2
   const long long row = (idx & 1) * nparts;
   for (int q = lane; q < nparts; q += 32)
-    st_release_sys_u64(peer_sig[q] + row + part, (key << 1) | (unsigned)bit);
-  int any = 0;
+    st_release_sys_u64(peer_sig[q] + row + part, (key << 2) | bits);
+  unsigned any = 0;
   const unsigned long long t0 = globaltimer_ns();
   bool timed_out = false;
   for (int q = lane; q < nparts && !timed_out; q += 32) {
     unsigned long long v;
-    while (((v = ld_acquire_sys_u64(peer_sig[part] + row + q)) >> 1) != key) {
+    while (((v = ld_acquire_sys_u64(peer_sig[part] + row + q)) >> 2) != key) {
       if (globaltimer_ns() - t0 > timeout_ns) {
         timed_out = true;
         break;
       }
       __nanosleep(64);
     }
-    any |= (int)(v & 1);
+    any |= (unsigned)(v & 3);
   }
   if (timed_out) atomicCAS(&ds->err, 0, kErrPeerTimeout);
-  any = __any_sync(DP_FULL, any);
+  any = __reduce_or_sync(DP_FULL, any);
   if (lane == 0 && flag_slot >= 0) {
-    ds->flag[flag_slot] = any;  // the OR over the parts: what the host reads
-    ds->flag[flag_slot ^ 1] = 0;  // the next round's own flag
+    ds->flag[flag_slot] = any & 1;  // the OR over the parts: what the host reads
+    ds->flag[flag_slot ^ 1] = 0;    // the next round's own flag
+    ds->big[flag_slot ^ 1] = (any >> 1) & 1;  // the next level's variant
+    ds->big_local = 0;
   }
+}
+
+// partitioned BFS: does this part's next frontier (owned u with dist[u] ==
+// level) hold a row that would launch (degree >= t)?  -> DevState::big_local
+__global__ void part_big_kernel(const int* __restrict__ rowptr,
+                                const int* __restrict__ dist, int n_local,
+                                int level, int t, DevState* ds) {
+  int found = 0;
+  for (long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+       u < n_local; u += (long long)gridDim.x * blockDim.x) {
+    if (__ldcg(dist + u) == level) {
+      const int d = __ldg(rowptr + u + 1) - __ldg(rowptr + u);
+      found |= d > 0 && d >= t;
+    }
+  }
+  if (__any_sync(DP_FULL, found) && lane_id() == 0 &&
+      __ldcg(&ds->big_local) == 0)
+    ds->big_local = 1;
 }
 
 unsigned long long peer_timeout_ns() {
@@ -2084,7 +2109,15 @@ struct PartSync {
 template <class MakeApp>
 int iterate_parts(Workspace* w, const dp_config* c, long long nparents,
                   long long launchers, int max_iter, cudaStream_t s,
-                  const PartSync& ps, MakeApp make, dp_stats* st) {
+                  const PartSync& ps, MakeApp make, dp_stats* st,
+                  const int* big_rowptr = nullptr,
+                  const int* big_dist = nullptr) {
+  // big_rowptr / big_dist (partitioned BFS): after each level the part scans
+  // its next frontier for a launching row; when no part has one, the next
+  // level runs the launch-free parent variant (as iterate() does for BFS)
+  const bool per_level = big_rowptr && c->variant == DP_VARIANT_CDP;
+  dp_config c_flat = *c;
+  c_flat.variant = DP_VARIANT_NOCDP;
   RunCounters rc;
   int r;
   if ((r = ensure_pending_limit(w, c, launch_bound(c, nparents, launchers))))
@@ -2113,7 +2146,15 @@ int iterate_parts(Workspace* w, const dp_config* c, long long nparents,
   bool converged = false;
   for (; !converged && it <= max_iter; ++it) {
     auto app = make(it, w->ds);
-    if ((r = launch_parent(app, nparents, launchers, c, w, s, &rc))) return r;
+    const dp_config* cl =
+        per_level && it > 0 && w->h_ds->big[it & 1] == 0 ? &c_flat : c;
+    if ((r = launch_parent(app, nparents, launchers, cl, w, s, &rc))) return r;
+    if (per_level) {
+      part_big_kernel<<<148 * 4, 256, 0, s>>>(
+          big_rowptr, big_dist, (int)nparents, it + 1, effective_threshold(c),
+          w->ds);
+      rc.kernel_launches += 1;
+    }
     part_flag_or_kernel<<<1, 32, 0, s>>>(ps.sig, ps.nparts, ps.part, it + 1,
                                          ps.epoch, w->ds, it & 1, tmo);
     DP_CUDA(cudaGetLastError());
@@ -2259,7 +2300,7 @@ int bfs_part_solve_peer_impl(const int32_t* rowptr, const int32_t* col,
                          a.pad_ = 0;
                          return a;
                        },
-                       st);
+                       st, rowptr, dist);
 }
 
 int sssp_part_round_impl(const int32_t* rowptr, const int32_t* col,
