@@ -233,7 +233,11 @@ struct BfsApp {
 // ids with the same CAS (dp_bfs_part_apply).  dist stays a level labelling,
 // bit-identical to the single-part run.
 // ---------------------------------------------------------------------------
-struct BfsPartApp {
+// kPeer: the fused exchange (remote CAS through peer_dist) compiled alone;
+// the bucketed exchange (send_buf) otherwise -- one runtime branch per edge
+// between them had cost the register-capped kernels 28-36 B of spills
+template <bool kPeer>
+struct BfsPartAppT {
   const int* __restrict__ rowptr;  // local CSR over owned vertices
   const int* __restrict__ col;     // global target ids
   int* dist;                       // owned vertices (local index)
@@ -302,7 +306,7 @@ struct BfsPartApp {
       const unsigned bit = 1u << (v & 31);
       if (!((unsigned)d_or_bits & bit) &&
           !(atomicOr(sent + (v >> 5), bit) & bit)) {
-        if (peer_dist) {
+        if constexpr (kPeer) {
           ++acc.remote;
           if (atomicCAS(peer_dist[q] + local_of(v, nparts), kUnreached, lvl + 1) ==
               kUnreached)
@@ -356,6 +360,8 @@ struct BfsPartApp {
       *changed = 1;
   }
 };
+using BfsPartApp = BfsPartAppT<false>;
+using BfsPeerApp = BfsPartAppT<true>;
 
 // ---------------------------------------------------------------------------
 // SSSP on one part of the cyclic 1D partition.  Local relaxations lower the

@@ -1896,30 +1896,39 @@ int bfs_part_level_impl(const int32_t* rowptr, const int32_t* col,
   if ((r = ensure_pending_limit(w, c, launch_bound(c, n_local, launchers))))
     return r;
   if ((r = begin_run(w, s))) return r;
-  BfsPartApp a;
-  a.rowptr = rowptr;
-  a.col = col;
-  a.dist = dist;
-  a.counts = counts;
-  a.sent = sent;
-  a.send_buf = send_buf;
-  a.send_count = send_count;
-  a.changed = changed;
-  a.peer_dist = (int* const*)peer_dist;
-  a.remote_ops = &w->ds->remote;
-  a.stride = stride;
   if (peer_dist)  // fused exchange: the flag is this level's alone
     DP_CUDA(cudaMemsetAsync(changed, 0, sizeof(int), s));
-  a.n_local = n_local;
-  a.nparts = nparts;
-  a.part = part;
-  a.level = level;
-  a.cmask = c->counts_spread > 0 ? (unsigned)((1ull << c->counts_spread) - 1)
-                                 : 0u;
-  a.pad_ = 0;
+  auto fill = [&](auto& a) {
+    a.rowptr = rowptr;
+    a.col = col;
+    a.dist = dist;
+    a.counts = counts;
+    a.sent = sent;
+    a.send_buf = send_buf;
+    a.send_count = send_count;
+    a.changed = changed;
+    a.peer_dist = (int* const*)peer_dist;
+    a.remote_ops = &w->ds->remote;
+    a.stride = stride;
+    a.n_local = n_local;
+    a.nparts = nparts;
+    a.part = part;
+    a.level = level;
+    a.cmask = c->counts_spread > 0 ? (unsigned)((1ull << c->counts_spread) - 1)
+                                   : 0u;
+    a.pad_ = 0;
+  };
   RunCounters rc;
   DP_CUDA(cudaEventRecord(w->ev0, s));
-  if ((r = launch_parent(a, n_local, launchers, c, w, s, &rc))) return r;
+  if (peer_dist) {
+    BfsPeerApp a;
+    fill(a);
+    if ((r = launch_parent(a, n_local, launchers, c, w, s, &rc))) return r;
+  } else {
+    BfsPartApp a;
+    fill(a);
+    if ((r = launch_parent(a, n_local, launchers, c, w, s, &rc))) return r;
+  }
   DP_CUDA(cudaEventRecord(w->ev1, s));
   if ((r = read_state_fast(w, s))) return r;
   if ((r = account_step(w, &rc))) return r;
@@ -2077,17 +2086,24 @@ __global__ void part_flag_or_kernel(unsigned long long* const* peer_sig,
 __global__ void part_big_kernel(const int* __restrict__ rowptr,
                                 const int* __restrict__ dist, int n_local,
                                 int level, int t, DevState* ds) {
-  int found = 0;
-  for (long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-       u < n_local; u += (long long)gridDim.x * blockDim.x) {
-    if (__ldcg(dist + u) == level) {
+  // warp-uniform trip count; stops as soon as any warp has found one (the
+  // levels that need the launching variant end the scan early)
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long u0 = (long long)blockIdx.x * blockDim.x + threadIdx.x -
+                       lane_id();
+  for (long long b = u0, i = 0; b < n_local; b += stride, ++i) {
+    if ((i & 7) == 0 && __ldcg(&ds->big_local)) return;
+    const long long u = b + lane_id();
+    bool found = false;
+    if (u < n_local && __ldcg(dist + u) == level) {
       const int d = __ldg(rowptr + u + 1) - __ldg(rowptr + u);
-      found |= d > 0 && d >= t;
+      found = d > 0 && d >= t;
+    }
+    if (__any_sync(DP_FULL, found)) {
+      if (lane_id() == 0) ds->big_local = 1;
+      return;
     }
   }
-  if (__any_sync(DP_FULL, found) && lane_id() == 0 &&
-      __ldcg(&ds->big_local) == 0)
-    ds->big_local = 1;
 }
 
 unsigned long long peer_timeout_ns() {
@@ -2223,8 +2239,12 @@ int sssp_part_solve_peer_impl(const int32_t* rowptr, const int32_t* col,
   DP_CUDA(cudaGetLastError());
   // every part uses the same worst-case launcher count, so every part sizes
   // the device-wide launch pool alike (no part grows it while another waits
-  // in the barrier)
+  // in the barrier); cf_wave's solo launches are off here: with that bound
+  // they would split every round into waves
   const long long launchers = n_local;
+  dp_config cs = *c;
+  cs.cf_wave = 0;
+  c = &cs;
   const PartSync ps{(unsigned long long* const*)peer_sig, nparts, part,
                     epoch};
   return iterate_parts(w, c, n_local, launchers, n_global, s, ps,
@@ -2276,11 +2296,14 @@ int bfs_part_solve_peer_impl(const int32_t* rowptr, const int32_t* col,
   DP_CUDA(cudaMemsetAsync(counts, 0, (size_t)counts_len * sizeof(int), s));
   DP_CUDA(cudaMemsetAsync(sent, 0, (size_t)(n_global + 31) / 32 * 4, s));
   const long long launchers = n_local;
+  dp_config cs = *c;  // as sssp_part_solve_peer_impl
+  cs.cf_wave = 0;
+  c = &cs;
   const PartSync ps{(unsigned long long* const*)peer_sig, nparts, part,
                     epoch};
   return iterate_parts(w, c, n_local, launchers, n_global, s, ps,
                        [&](int level, DevState* ds) {
-                         BfsPartApp a;
+                         BfsPeerApp a;
                          a.rowptr = rowptr;
                          a.col = col;
                          a.dist = dist;
