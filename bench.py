@@ -1315,7 +1315,7 @@ def measure_bt(args, world, rank, local, ncurves: int, steps: int = 0):
 def partitioned_workloads(args, world, rank, local) -> dict | None:
     """The north-star's partitioned workloads at this N, measured in the
     same run as the headline so the driver's 1/2/4/8-GPU lines carry their
-    scaling: TC RMAT-22 (edge ranges), BT 1 M curves (curve ranges) and BFS
+    scaling: TC RMAT-22 (edge ranges), BT 4 M curves (curve ranges) and BFS
     RMAT-26 (1D partition, fused exchange).  Every rank calls; rank 0 gets
     the dict."""
     import torch
@@ -1323,8 +1323,10 @@ def partitioned_workloads(args, world, rank, local) -> dict | None:
     for name, fn in (
             ("tc_rmat22", lambda: measure_tc(args, world, rank, local,
                                              parity=True, steps=5)),
-            ("bt_1m_curves", lambda: measure_bt(args, world, rank, local,
-                                                1000000, steps=10)),
+            # 4 M curves (350 M vertices, 0.7 ms on one B200): large enough
+            # that the per-step all_reduce does not hide the 8-GPU scaling
+            ("bt_4m_curves", lambda: measure_bt(args, world, rank, local,
+                                                4000000, steps=10)),
             ("bfs_rmat26", lambda: measure_bfs26(args, world, rank, local,
                                                  parity=False, steps=3))):
         r = fn()
