@@ -14,7 +14,12 @@ POLICIES = [dict(), dict(agg="warp"), dict(threshold=4, agg="block"),
             dict(threshold=2, agg="grid", serial="warp", parent_block=64),
             dict(agg="block", agg_threshold=3, child_block=64),
             dict(threshold=8, cfactor=4, agg="multiblock", group_size=1 << 20,
-                 serial="warp", parent_block=128)]
+                 serial="warp", parent_block=128),
+            # round 2: solo launches of big rows, packed weights (SSSP host
+            # path), order "A before C"
+            dict(threshold=4, cfactor=4, agg="multiblock", group_size=1 << 20,
+                 serial="warp", cf_wave=1, weight_bits=4),
+            dict(threshold=2, cfactor=3, agg="block", order="ACT")]
 fails = 0
 for app, spec in (("bfs", "powerlaw:300:seed2"), ("sssp", "powerlaw:300:seed3"),
                   ("manylaunch", "sizes:200:seed1"), ("tc", "rmat:8:seed1"),
@@ -52,5 +57,36 @@ for app, spec in (("bfs", "powerlaw:300:seed2"), ("sssp", "powerlaw:300:seed3"),
                 fails += 1
                 print("MISMATCH", app, k, pol, flush=True)
     print("ok", app, flush=True)
+# round 2: the partitioned solve drivers, P = 2 parts as host threads
+import torch  # noqa: E402
+from paper_2201_02789_b200 import dist as pdist  # noqa: E402
+g = graphs.rmat_graph(10, 1)
+w = graphs.edge_weights(g, 1)
+dev = torch.device("cuda", 0)
+ex = pdist.PeerLocal()
+parts = [pdist.SsspPeerPart(*pdist.partition_csr(g.rowptr, g.col, 2, p, w),
+                            g.n, 2, p, 0, ex.alloc(g.n, 2, dev), dev)
+         for p in range(2)]
+ex.bind(parts)
+d, _ = pdist.sssp_1d_peer_solve(
+    parts, BenchConfig(threshold=8, agg="multiblock", group_size=1 << 20,
+                       serial="warp").to_c(), ex)
+if not np.array_equal(d.cpu().numpy(), oracle.sssp(g.rowptr, g.col, w)[0]):
+    fails += 1
+    print("MISMATCH sssp solve P=2", flush=True)
+ex = pdist.PeerLocal()
+bparts = [pdist.BfsPart(*pdist.rmat_part(10, 1, 2, p), g.n, 2, p, 0, dev,
+                        dist=ex.alloc(g.n, 2, dev), spread=True)
+          for p in range(2)]
+ex.bind(bparts)
+d, c, _ = pdist.bfs_1d_peer_solve(
+    bparts, BenchConfig(threshold=8, agg="multiblock", group_size=1 << 20,
+                        serial="warp").to_c(), ex)
+wd, wc, _ = oracle.bfs(g.rowptr, g.col)
+if not (np.array_equal(d.cpu().numpy(), wd)
+        and np.array_equal(c.cpu().numpy(), wc)):
+    fails += 1
+    print("MISMATCH bfs solve P=2", flush=True)
+print("ok solve", flush=True)
 print("FAILS", fails)
 sys.exit(1 if fails else 0)
