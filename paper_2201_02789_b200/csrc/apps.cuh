@@ -1139,19 +1139,16 @@ struct BtApp {
   float scale;
   int pad;
 
+  // the row carries the curve's control points and 1/(nt-1) (loaded once
+  // by the parent in expand): the warp walking a curve receives them with
+  // the row's shuffle instead of re-loading them per vertex
   struct alignas(16) Args {
-    int u, nt;
-    long long off;
-  };
-  // the thread's last curve: control points and 1/(nt-1), reloaded only when
-  // the curve changes (a whole-warp row walks one curve U x 32 vertices at a
-  // time; per vertex this leaves ~15 instructions instead of 3 loads, a
-  // reciprocal and ~25)
-  struct Acc {
-    int key;  // u + 1 of the cached curve (0: empty)
+    int nt;
     float inv;
+    long long off;
     float2 p0, p1, p2;
   };
+  struct Acc {};
 
   __device__ int nparents() const { return ncurves; }
   __device__ void parent_prologue() const {}
@@ -1174,10 +1171,12 @@ struct BtApp {
 
   __device__ int expand(int u, bool valid, Args& a) const {
     int nt = 0;
+    float2 q0 = make_float2(0.f, 0.f), q1 = q0, q2 = q0;
     if (valid) {
-      const float2 p0 = __ldg(cp + 3 * u), p1 = __ldg(cp + 3 * u + 1),
-                   p2 = __ldg(cp + 3 * u + 2);
-      nt = tess_count(p0, p1, p2, scale, max_tess);
+      q0 = __ldg(cp + 3 * u);
+      q1 = __ldg(cp + 3 * u + 1);
+      q2 = __ldg(cp + 3 * u + 2);
+      nt = tess_count(q0, q1, q2, scale, max_tess);
     }
     // warp-aggregated bump allocation: one 64-bit atomic per warp
     const int incl = warp_incl_scan(nt);
@@ -1194,26 +1193,18 @@ struct BtApp {
     }
     ntess[u] = nt;
     offsets[u] = off;
-    a = Args{u, nt, off};
+    a = Args{nt, __frcp_rn((float)(nt - 1)), off, q0, q1, q2};
     return nt;
   }
   __device__ static int count(const Args& a) { return a.nt; }
-  __device__ void item(const Args& a, int i, Acc& c) const {
-    if (c.key != a.u + 1) {
-      c.key = a.u + 1;
-      c.p0 = __ldg(cp + 3 * a.u);
-      c.p1 = __ldg(cp + 3 * a.u + 1);
-      c.p2 = __ldg(cp + 3 * a.u + 2);
-      c.inv = __frcp_rn((float)(a.nt - 1));
-    }
+  __device__ void item(const Args& a, int i, Acc&) const {
     // t = i * (1/(nt-1)) (<= 1.5 ulp): vertices are checked within 1e-5, only
     // the counts (tess_count) must match the oracle bit for bit
-    const float t = (float)i * c.inv;
+    const float t = (float)i * a.inv;
     const float s = 1.0f - t;
     const float w0 = s * s, w1 = 2.0f * s * t, w2 = t * t;
-    verts[a.off + i] =
-        make_float2(w0 * c.p0.x + w1 * c.p1.x + w2 * c.p2.x,
-                    w0 * c.p0.y + w1 * c.p1.y + w2 * c.p2.y);
+    verts[a.off + i] = make_float2(w0 * a.p0.x + w1 * a.p1.x + w2 * a.p2.x,
+                                   w0 * a.p0.y + w1 * a.p1.y + w2 * a.p2.y);
   }
   static constexpr int kUnroll = 1;
   static constexpr int kBigUnroll = 4;  // whole-warp rows: 4 stores in flight

@@ -57,27 +57,31 @@ for app, spec in (("bfs", "powerlaw:300:seed2"), ("sssp", "powerlaw:300:seed3"),
                 fails += 1
                 print("MISMATCH", app, k, pol, flush=True)
     print("ok", app, flush=True)
-# round 2: the partitioned solve drivers, P = 2 parts as host threads
+# round 2: the partitioned solve drivers at P = 1 (P >= 2 parts run as
+# concurrent host threads whose barrier kernels wait on each other, and
+# memcheck serialises kernel execution, so they would only time out here;
+# tests/test_gpu_solve.py runs P = 2..4 without the tool)
 import torch  # noqa: E402
 from paper_2201_02789_b200 import dist as pdist  # noqa: E402
 g = graphs.rmat_graph(10, 1)
 w = graphs.edge_weights(g, 1)
 dev = torch.device("cuda", 0)
 ex = pdist.PeerLocal()
-parts = [pdist.SsspPeerPart(*pdist.partition_csr(g.rowptr, g.col, 2, p, w),
-                            g.n, 2, p, 0, ex.alloc(g.n, 2, dev), dev)
-         for p in range(2)]
+P = 1
+parts = [pdist.SsspPeerPart(*pdist.partition_csr(g.rowptr, g.col, P, p, w),
+                            g.n, P, p, 0, ex.alloc(g.n, P, dev), dev)
+         for p in range(P)]
 ex.bind(parts)
 d, _ = pdist.sssp_1d_peer_solve(
     parts, BenchConfig(threshold=8, agg="multiblock", group_size=1 << 20,
                        serial="warp").to_c(), ex)
 if not np.array_equal(d.cpu().numpy(), oracle.sssp(g.rowptr, g.col, w)[0]):
     fails += 1
-    print("MISMATCH sssp solve P=2", flush=True)
+    print("MISMATCH sssp solve", flush=True)
 ex = pdist.PeerLocal()
-bparts = [pdist.BfsPart(*pdist.rmat_part(10, 1, 2, p), g.n, 2, p, 0, dev,
-                        dist=ex.alloc(g.n, 2, dev), spread=True)
-          for p in range(2)]
+bparts = [pdist.BfsPart(*pdist.rmat_part(10, 1, P, p), g.n, P, p, 0, dev,
+                        dist=ex.alloc(g.n, P, dev), spread=True)
+          for p in range(P)]
 ex.bind(bparts)
 d, c, _ = pdist.bfs_1d_peer_solve(
     bparts, BenchConfig(threshold=8, agg="multiblock", group_size=1 << 20,
@@ -86,7 +90,7 @@ wd, wc, _ = oracle.bfs(g.rowptr, g.col)
 if not (np.array_equal(d.cpu().numpy(), wd)
         and np.array_equal(c.cpu().numpy(), wc)):
     fails += 1
-    print("MISMATCH bfs solve P=2", flush=True)
+    print("MISMATCH bfs solve", flush=True)
 print("ok solve", flush=True)
 print("FAILS", fails)
 sys.exit(1 if fails else 0)
