@@ -873,8 +873,12 @@ int iterate(Workspace* w, const dp_config* c, long long nparents,
   }
   for (; !converged && it <= max_iter; ++it) {
     auto app = make(it, w->ds);
-    const dp_config* cl =
-        c->variant == DP_VARIANT_CDP && !pick(it, w->h_ds) ? &c_flat : c;
+    // no parent can ever reach the threshold (an exact launcher count of 0,
+    // e.g. road graphs below T): every level runs launch-free
+    const dp_config* cl = c->variant == DP_VARIANT_CDP &&
+                                  (launchers == 0 || !pick(it, w->h_ds))
+                              ? &c_flat
+                              : c;
     if ((r = launch_parent(app, nparents, launchers, cl, w, s, &rc))) return r;
     if ((r = read_state_fast(w, s))) return r;
     if ((r = account_step(w, &rc))) return r;
