@@ -9,20 +9,22 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2201_02789_b200.bench import (BenchConfig, INF_THRESHOLD, load,
                                          run_config, run_reference)
 
-spec = sys.argv[1] if len(sys.argv) > 1 else "road:200000:seed1"
+args = [a for a in sys.argv[1:] if a != "--fast"]
+spec = args[0] if args else "road:200000:seed1"
+fast = "--fast" in sys.argv  # skip naive CDP and block aggregation (minutes)
 for app in ("bfs", "sssp"):
     bench, wl = load(app, spec)
     ref = [run_reference(bench, wl) for _ in range(3)]
     print(f"{app} {spec} no-cdp: {statistics.median(r.ns_device for r in ref)/1e6:.3f} ms"
           f" iterations={ref[0].iterations}", flush=True)
-    for d in (dict(), dict(agg="block"), dict(agg="grid"),
+    for d in (([] if fast else [dict(), dict(agg="block")]) + [dict(agg="grid"),
               dict(threshold=INF_THRESHOLD),
               dict(threshold=INF_THRESHOLD, parent_block=256, serial="warp"),
               dict(threshold=8, agg="grid", parent_block=256, serial="warp"),
               dict(threshold=INF_THRESHOLD, parent_block=256, serial="warp",
                    device_loop=True),
               dict(threshold=8, agg="block", parent_block=256, serial="warp",
-                   device_loop=True)):
+                   device_loop=True)]):
         reps = [run_config(bench, wl, BenchConfig(**d))[0] for _ in range(3)]
         assert reps[0].memory_digest == ref[0].memory_digest
         print(f"  {statistics.median(r.ns_device for r in reps)/1e6:9.3f} ms"
