@@ -520,9 +520,21 @@ def extra_workloads(stream, quick: bool) -> dict:
     from paper_2201_02789_b200.bench.benchmarks import tc_traffic
     alg = tc_traffic(wl.buffers["rowptr"], wl.buffers["col"])
     ntri = int(tri.item())
+    # TC is bound by hash probes (instruction issue), not by HBM: the
+    # probes of the rank-ordered CSR+ (the part of N+(u) above v for every
+    # edge u -> v) per second, next to the SM throughput ncu measured
+    deg = np.diff(wl.buffers["rowptr"].astype(np.int64))
+    probes = int((deg * (deg - 1) // 2).sum())
     out["tc_rmat22"] = {"triangles": ntri, "ms": ms,
                         "triangles_per_s": ntri / (ms * 1e-3),
                         "edges_per_s": m / (ms * 1e-3),
+                        "probes": probes,
+                        "probes_per_s": probes / (ms * 1e-3),
+                        "bound": "hash probes (SM issue; ncu child SM "
+                                 "throughput 78 %, profiles/r02/"
+                                 "ncu_full_tc_r02.json); gbps_alg is the "
+                                 "§8(d) model, which counts L2-resident list "
+                                 "reads as HBM bytes",
                         "gbps_alg": alg / (ms * 1e6), "policy": BEST["tc"]}
     if not quick:
         naive_ms = tc_once(_cfg(dict()))["ns_device"] / 1e6
