@@ -561,16 +561,7 @@ int launch_wave(const App& app, long long base, long long nparents,
     }
   }
   if (!cdp) {
-    // launch-free: kFlatPpt parents per thread, a quarter of the waves (the
-    // host-side counters keep the logical one-thread-per-parent grid)
-    static bool once = [] {
-      prefer_l1(parent_flat_kernel<App>);
-      return true;
-    }();
-    (void)once;
-    parent_flat_kernel<App>
-        <<<(int)dp::ceil_div_ll(grid, kFlatPpt), pb, 0, s>>>(app, k, w->ds,
-                                                              base, nparents);
+    launch_parent_inst<App, kAggNone, false>(app, grid, pb, k, t, w->ds, base, s);
   } else {
     switch (c->agg) {
       case DP_AGG_NONE:

@@ -603,49 +603,6 @@ __global__ void __launch_bounds__(256, App::kMinBlocks)
 }
 
 // ---------------------------------------------------------------------------
-// Launch-free parent with kFlatPpt parents per thread (B200): the No-CDP
-// variant and the launch-free levels of a CDP run.  Without launches or an
-// aggregation protocol nothing ties a parent to a thread, so each thread
-// expands kFlatPpt parents (their loads in flight together) and a 4 M-parent
-// level runs in a quarter of the block waves -- the floor of a level with a
-// tiny frontier is those waves.  Parent p of the wave is thread
-// (p / (kFlatPpt * bd)) * bd + p % bd of iteration (p / bd) % kFlatPpt, so a
-// warp's lanes still hold consecutive parents (coalesced expand loads).
-// ---------------------------------------------------------------------------
-#ifndef DP_FLAT_PPT
-#define DP_FLAT_PPT 4
-#endif
-constexpr int kFlatPpt = DP_FLAT_PPT;
-
-template <class App>
-__global__ void __launch_bounds__(256, App::kMinBlocks)
-    parent_flat_kernel(App app, Knobs k, DevState* ds, long long base,
-                       long long nparents) {
-  using Args = typename App::Args;
-  const long long t_parent = ph_now();
-  typename App::Acc acc{};
-  app.parent_prologue();
-  Args a[kFlatPpt];
-  int cnt[kFlatPpt];
-#pragma unroll
-  for (int i = 0; i < kFlatPpt; ++i) {
-    const long long lu =
-        ((long long)blockIdx.x * kFlatPpt + i) * blockDim.x + threadIdx.x;
-    a[i] = Args{};
-    cnt[i] = app.expand((int)(base + lu),
-                        lu < nparents && base + lu < app.nparents(), a[i]);
-  }
-  ph_add(ds, kPhParent, t_parent);
-  const long long t_child = ph_now();
-#pragma unroll 1
-  for (int i = 0; i < kFlatPpt; ++i)
-    if (__any_sync(DP_FULL, cnt[i] > 0))
-      serial_arm(app, a[i], cnt[i], true, k.serial_warp != 0, acc);
-  app.flush(acc);
-  ph_add(ds, kPhChild, t_child);
-}
-
-// ---------------------------------------------------------------------------
 // Persistent parent (B200): a grid of a few blocks per SM walks the parents in
 // chunks of blockDim.x twice.  Pass 1 only expands and records the launches
 // (one fused atomic per chunk into the single group); the last block to
