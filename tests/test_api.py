@@ -143,6 +143,10 @@ def test_parse_spec_rejects(bad, needle):
     (BenchConfig(parent_block=48), "parent_block"),
     (BenchConfig(child_block=16), "child_block"),
     (BenchConfig(serial="lane"), "serial mode"),
+    # round-2 B200 knobs
+    (BenchConfig(weight_bits=3), "weight_bits"),
+    (BenchConfig(cf_wave=-1), "cf_wave"),
+    (BenchConfig(persistent=9), "persistent"),
 ])
 def test_knob_validation_matches_reference_errors(cfg, needle):
     with pytest.raises(ValueError, match=needle):
