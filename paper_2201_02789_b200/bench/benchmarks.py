@@ -463,6 +463,30 @@ BENCHMARKS: dict[str, Benchmark] = {
 }
 
 
+def register_benchmark(bench: Benchmark, replace: bool = False) -> Benchmark:
+    """The plug-in point, mirroring the reference's ``Benchmark(name,
+    cdp_source, nocdp_source, outputs, prepare, drive)`` registration
+    (bench/benchmarks.py:56-68): ``prepare`` turns a dataset spec into a
+    Workload, ``run(workload, dp_config)`` drives the device (the CDP or
+    No-CDP variant is in ``dp_config.variant``; the reference's two sources
+    are one App functor in csrc/apps.cuh here) and returns
+    (outputs, stats).  After registration every harness entry point --
+    ``load``, ``run_config``, ``run_reference``, ``run_benchmark``,
+    ``sweep`` and the CLI -- serves the benchmark by name."""
+    if not bench.name or not isinstance(bench.name, str):
+        raise ValueError("benchmark name must be a non-empty string")
+    if bench.name in BENCHMARKS and not replace:
+        raise ValueError(f"benchmark {bench.name!r} is already registered")
+    missing = [o for o in bench.outputs if o not in bench.kinds]
+    if missing:
+        raise ValueError(f"outputs without an element kind: {missing}")
+    for fn in ("prepare", "run", "traffic"):
+        if not callable(getattr(bench, fn)):
+            raise ValueError(f"benchmark {fn} must be callable")
+    BENCHMARKS[bench.name] = bench
+    return bench
+
+
 def get_benchmark(name: str) -> Benchmark:
     try:
         return BENCHMARKS[name]

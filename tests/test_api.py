@@ -284,3 +284,25 @@ def test_order_rejects_unknown_step():
     # pipeline.py:79 / tests/test_passes.py:672-674
     with pytest.raises(ValueError, match="unknown pass step"):
         BenchConfig(threshold=5, order="TXA").to_c()
+
+
+def test_register_benchmark_plugin_contract():
+    """register_benchmark (the reference's Benchmark registration,
+    bench/benchmarks.py:56-68): validation, then every harness entry point
+    serves the new name."""
+    from paper_2201_02789_b200.bench import (BENCHMARKS, Benchmark,
+                                             register_benchmark)
+    base = BENCHMARKS["bfs"]
+    with pytest.raises(ValueError, match="already registered"):
+        register_benchmark(base)
+    with pytest.raises(ValueError, match="element kind"):
+        register_benchmark(Benchmark("bfs_x", ("dist", "zz"), {"dist": "int"},
+                                     base.prepare, base.run, base.traffic))
+    b = Benchmark("bfs_copy", base.outputs, base.kinds, base.prepare,
+                  base.run, base.traffic, "plug-in test")
+    try:
+        register_benchmark(b)
+        bench, wl = load("bfs_copy", "hand")
+        assert bench is b and wl.n > 0
+    finally:
+        BENCHMARKS.pop("bfs_copy", None)

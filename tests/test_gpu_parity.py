@@ -834,3 +834,50 @@ def test_aggregated_grid_coarsening_rmat(serial):
         assert np.array_equal(rep.arrays["counts"], wc), agg
         rep, _ = run_config(sssp_b, sssp_wl, cfg)
         assert np.array_equal(rep.arrays["dist"], sd), agg
+
+
+def test_registered_benchmark_runs_everywhere():
+    """A benchmark registered from Python (register_benchmark, the
+    reference's plug-in point) -- here BFS from source 7 with its own
+    prepare / drive over the existing device App -- runs through
+    run_config, run_reference, verify_outputs and sweep, bit-exact vs the
+    oracle."""
+    import ctypes
+    from paper_2201_02789_b200 import _lib
+    from paper_2201_02789_b200.bench import (Benchmark, register_benchmark,
+                                             sweep, verify_outputs)
+    base = BENCHMARKS["bfs"]
+
+    def prepare(spec):
+        wl = base.prepare(spec)
+        wl.buffers["dist"][:] = UNREACHED
+        wl.buffers["dist"][7] = 0
+        return wl
+
+    def run(wl, cfg):
+        b = wl.buffers
+        dist = np.empty(wl.n, np.int32)
+        counts = np.empty(wl.n, np.int32)
+        st = _lib.DpStats()
+        _lib.check(_lib.device().dp_bfs(
+            _lib.ptr(b["rowptr"]), _lib.ptr(b["col"]), wl.n,
+            b["col"].shape[0], 7, ctypes.byref(cfg), _lib.ptr(dist),
+            _lib.ptr(counts), ctypes.byref(st)))
+        return {"dist": dist, "counts": counts}, _lib.stats_dict(st)
+
+    register_benchmark(Benchmark("bfs_src7", base.outputs, base.kinds,
+                                 prepare, run, base.traffic, "BFS from 7"))
+    try:
+        bench, wl = load("bfs_src7", "powerlaw:2000:seed1")
+        b = wl.buffers
+        want_d, want_c, _ = oracle.bfs(b["rowptr"], b["col"], src=7)
+        for pol in (dict(), dict(threshold=8, cfactor=2, agg="multiblock",
+                                 group_size=3)):
+            rep, _ = run_config(bench, wl, BenchConfig(**pol))
+            np.testing.assert_array_equal(rep.arrays["dist"], want_d)
+            np.testing.assert_array_equal(rep.arrays["counts"], want_c)
+            verify_outputs(bench, wl, rep, run_reference(bench, wl))
+        rows = sweep("bfs_src7", "powerlaw:2000:seed1")
+        assert rows and all(r["error"] == "" for r in rows)
+    finally:
+        BENCHMARKS.pop("bfs_src7", None)
