@@ -69,9 +69,6 @@ namespace dp {
 #ifndef DP_BFS_NO_COUNTS
 #define DP_BFS_NO_COUNTS 0  // ablation only (wrong counts): the cost of counts
 #endif
-#ifndef DP_SSSP_REFRESH
-#define DP_SSSP_REFRESH 0
-#endif
 #ifndef DP_SSSPPEER_MINB
 #define DP_SSSPPEER_MINB DP_SSSP_MINB  // fused-exchange SSSP (A/B knob)
 #endif
@@ -645,7 +642,7 @@ struct SsspAppT {
       if (__ldcg(last + u) == du) return 0;
       last[u] = du;
     }
-    a = Args{s, d, du, u};  // pad: the parent (Refresh)
+    a = Args{s, d, du, 0};
     return d;
   }
   __device__ static int count(const Args& a) { return a.deg; }
@@ -666,15 +663,6 @@ struct SsspAppT {
       acc.changed = 1;
   }
   static constexpr int kUnroll = DP_SSSP_UNROLL;
-  // DP_SSSP_REFRESH (A/B): a child block re-reads its parent's distance
-  // once (the parent may have been lowered since it expanded): any lowering
-  // is a real path length, so outputs are unchanged and a round propagates
-  // further
-  static constexpr bool kRefresh = DP_SSSP_REFRESH;
-  __device__ void refresh(Args& a) const {
-    const int cur = __ldcg(dist + a.pad);
-    if (cur < a.du) a.du = cur;
-  }
   static constexpr int kChildUnroll = DP_SSSP_CHILD_UNROLL;
   static constexpr bool kBlockMode = false;
   // frontier mode writes last[] in expand: the host never pairs it with the

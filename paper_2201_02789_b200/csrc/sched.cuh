@@ -132,16 +132,6 @@ __device__ __forceinline__ void run_logical_blocks(const App& app,
   }
 }
 
-// App::kRefresh: a child refreshes its row's arguments once (App::refresh)
-template <class App, class = void>
-struct Refresh {
-  static constexpr bool value = false;
-};
-template <class App>
-struct Refresh<App, std::void_t<decltype(App::kRefresh)>> {
-  static constexpr bool value = App::kRefresh;
-};
-
 // Plain child: BFS `visit` etc. (benchmarks.py:92-103), coarsened.
 template <class App>
 __global__ void __launch_bounds__(256, App::kMinBlocks) child_kernel(App app, typename App::Args a, int cf,
@@ -149,7 +139,6 @@ __global__ void __launch_bounds__(256, App::kMinBlocks) child_kernel(App app, ty
   note_child_start(ds, ts);
   const long long t0 = ph_now();
   typename App::Acc acc{};
-  if constexpr (Refresh<App>::value) app.refresh(a);
   run_logical_blocks(app, a, blockIdx.x, cf, acc);  // cf: the row's (row_cf)
   app.flush(acc);
   ph_add(ds, kPhChild, t0);
@@ -284,7 +273,6 @@ __global__ void __launch_bounds__(256, App::kMinBlocks) child_agg_kernel(App app
   typename App::Acc acc{};
   typename App::Args a;
   const long long lb = find_row<App>(tab, scan, np, (int)blockIdx.x, a, ds);
-  if constexpr (Refresh<App>::value) app.refresh(a);
   ph_add(ds, kPhDisagg, t0);
   const long long t1 = ph_now();
   run_logical_blocks(app, a, lb, cf, acc);
