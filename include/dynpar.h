@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define DP_ABI_VERSION 1
+#define DP_ABI_VERSION 2
 
 /* aggregation granularity (passes/aggregate.py:84 GRANULARITIES, + warp) */
 #define DP_AGG_NONE 0
@@ -134,6 +134,13 @@ typedef struct dp_config {
                             amortises setup over many small children; one
                             huge child would only be serialised).  0 = every
                             row coarsened by cfactor (the reference) */
+  int32_t col_bits;      /* dp_sssp (host buffers): 24 -> each chunk of col
+                            crosses PCIe as 3-byte values (3/4 of the int32
+                            bytes), packed on the host ahead of the copy and
+                            expanded into the int32 col on the device before
+                            the chunk is published; a chunk holding a value
+                            outside [0, 2^24) travels as int32.  The rounds
+                            read int32 col either way.  0 = int32 */
 } dp_config;
 
 /* SimReport (sim/report.py:12-28) counters, measured on the device */

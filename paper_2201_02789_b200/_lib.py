@@ -44,7 +44,8 @@ class DpConfig(ctypes.Structure):
                 ("agg_coarsen", ctypes.c_int32),
                 ("counts_spread", ctypes.c_int32),
                 ("weight_bits", ctypes.c_int32),
-                ("cf_wave", ctypes.c_int32)]
+                ("cf_wave", ctypes.c_int32),
+                ("col_bits", ctypes.c_int32)]
 
 
 class DpStats(ctypes.Structure):
@@ -162,6 +163,10 @@ _SIGNATURES = {
 
 EXPORTED = tuple(_SIGNATURES)
 
+# include/dynpar.h DP_ABI_VERSION: bumped whenever a struct or signature
+# changes (2: dp_config.col_bits)
+ABI_VERSION = 2
+
 _lock = threading.Lock()
 _lib = None
 _device_ready = False
@@ -187,6 +192,11 @@ def load() -> ctypes.CDLL:
                 fn = getattr(lib, name)
                 fn.argtypes = args
                 fn.restype = res
+            if not partial and lib.dp_abi_version() != ABI_VERSION:
+                raise ImportError(
+                    f"{LIB_PATH} has ABI {lib.dp_abi_version()}, this binding "
+                    f"expects {ABI_VERSION} (include/dynpar.h DP_ABI_VERSION): "
+                    f"rebuild it")
             _lib = lib
         return _lib
 

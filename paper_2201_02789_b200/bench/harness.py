@@ -56,6 +56,7 @@ class BenchConfig:
     frontier: bool = False
     weight_bits: int = 0
     cf_wave: int = 0
+    col_bits: int = 0
 
     def describe(self) -> str:
         return (f"threshold={self.threshold} cfactor={self.cfactor} "
@@ -93,6 +94,9 @@ class BenchConfig:
             raise ValueError("weight_bits must be 0 (int32) or 4 (packed)")
         if self.cf_wave < 0:
             raise ValueError("cf_wave must be >= 0")
+        if self.col_bits not in (0, 24):
+            raise ValueError("col_bits must be 0 (int32) or 24 (3-byte "
+                             "transfer)")
 
     def to_c(self, variant: int = _lib.VARIANT_CDP) -> _lib.DpConfig:
         self.validate()
@@ -115,6 +119,7 @@ class BenchConfig:
         c.frontier = int(bool(self.frontier))
         c.weight_bits = int(self.weight_bits)
         c.cf_wave = int(self.cf_wave)
+        c.col_bits = int(self.col_bits)
         c.threshold, c.cfactor, c.agg_coarsen = self.order_effect(
             c.threshold, c.cfactor, self.agg if agg_on else None)
         return c

@@ -90,6 +90,12 @@ struct Workspace {
   void* h_wpack = nullptr;
   size_t h_wpack_bytes = 0;
   int* d_bad = nullptr;
+  // dp_config.col_bits = 24: 3-byte col values in flight (pinned host
+  // staging, device landing buffer unpacked into the int32 col)
+  void* cpack = nullptr;
+  size_t cpack_bytes = 0;
+  void* h_cpack = nullptr;
+  size_t h_cpack_bytes = 0;
 };
 
 // One workspace per (host thread, device): the partitioned solve drivers
@@ -187,6 +193,8 @@ int validate(const dp_config* c) {
   if (c->weight_bits != 0 && c->weight_bits != 4)
     return fail(DP_ERR_INVALID, "weight_bits must be 0 or 4");
   if (c->cf_wave < 0) return fail(DP_ERR_INVALID, "cf_wave must be >= 0");
+  if (c->col_bits != 0 && c->col_bits != 24)
+    return fail(DP_ERR_INVALID, "col_bits must be 0 or 24");
   if (c->cf_wave > 0 && c->agg_coarsen)
     return fail(DP_ERR_INVALID,
                 "cf_wave applies to per-row coarsening (canonical order)");
@@ -2467,18 +2475,75 @@ int stage_chunked(Workspace* w, cudaStream_t s, int nsrc, const void* const* hos
   return 0;
 }
 
-// dp_sssp with weight_bits = 4: as stage_chunked for (col, weight), but each
-// weight chunk is first packed on the host (OpenMP, into pinned staging) and
-// copied as nibbles, 1/8 of the bytes; the packing of chunk k + 1 overlaps
-// the DMA of chunk k.  At the first chunk holding a weight outside [1, 16]
-// the call reverts to int32 weights: the earlier chunks' int32 weights are
-// copied and awaited (before any round can read them), the rest stream as
-// int32.  *packed: every chunk went packed.
-int stage_chunked_packed(Workspace* w, cudaStream_t s, const int32_t* col,
-                         const int32_t* weight, int32_t* d_col,
-                         int32_t* d_weight, unsigned* d_wpack, int64_t m,
-                         int shift, Arrival* arr, uint64_t* h2d,
-                         bool* packed_all) {
+// col_bits = 24: four col values travel as three 32-bit words (v0 | v1 << 24,
+// v1 >> 8 | v2 << 16, v2 >> 16 | v3 << 8).  Host packer for slots [lo, lo +
+// len) (lo a multiple of 4) into out + 3 * lo / 4; false if a value lies
+// outside [0, 2^24) (the chunk then travels as int32).  OpenMP.
+bool pack_col24_host(const int32_t* c, long long lo, long long len,
+                     unsigned* out) {
+  const long long groups = (len + 3) / 4;
+  unsigned bad = 0;
+#pragma omp parallel for reduction(| : bad) schedule(static)
+  for (long long g = 0; g < groups; ++g) {
+    const long long e = lo + g * 4;
+    unsigned v[4];
+    if (e + 4 <= lo + len) {
+#pragma GCC unroll 4
+      for (int j = 0; j < 4; ++j) v[j] = (unsigned)c[e + j];
+    } else {
+      for (int j = 0; j < 4; ++j) v[j] = e + j < lo + len ? (unsigned)c[e + j] : 0u;
+    }
+    bad |= v[0] | v[1] | v[2] | v[3];
+    unsigned* o = out + (lo >> 2) * 3 + g * 3;
+    o[0] = v[0] | v[1] << 24;
+    o[1] = v[1] >> 8 | v[2] << 16;
+    o[2] = v[2] >> 16 | v[3] << 8;
+  }
+  return (bad >> 24) == 0;
+}
+
+// Device twin: expand groups [g0, g0 + groups) of 3 words into 4 int32 slots
+// (the last group may be partial: slots < m only).
+__global__ void unpack_col24_kernel(const unsigned* __restrict__ in,
+                                    long long g0, long long groups,
+                                    long long m, int* __restrict__ col) {
+  for (long long g = g0 + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+       g < g0 + groups; g += (long long)gridDim.x * blockDim.x) {
+    const unsigned a = __ldg(in + g * 3), b = __ldg(in + g * 3 + 1),
+                   c = __ldg(in + g * 3 + 2);
+    const int4 v = make_int4((int)(a & 0xffffffu),
+                             (int)((a >> 24) | ((b & 0xffffu) << 8)),
+                             (int)((b >> 16) | ((c & 0xffu) << 16)),
+                             (int)(c >> 8));
+    if (g * 4 + 4 <= m) {
+      reinterpret_cast<int4*>(col)[g] = v;
+    } else {
+      const int x[4] = {v.x, v.y, v.z, v.w};
+      for (int j = 0; j < 4 && g * 4 + j < m; ++j) col[g * 4 + j] = x[j];
+    }
+  }
+}
+
+// dp_sssp's host-buffer staging with transfer codecs: as stage_chunked for
+// (col, weight), and
+//   pack_w (weight_bits = 4): each weight chunk is packed on the host
+//     (OpenMP, into pinned staging) and copied as nibbles, 1/8 of the bytes.
+//     At the first chunk holding a weight outside [1, 16] the call reverts to
+//     int32 weights: the earlier chunks' int32 weights are copied and awaited
+//     (before any round can read them), the rest stream as int32.
+//     *packed_all: every weight chunk went packed (the rounds read nibbles)
+//   pack_c (col_bits = 24): each col chunk is packed to 3-byte values on the
+//     host, copied (3/4 of the bytes) and expanded into the int32 col on the
+//     copy stream before the chunk is published; a chunk holding a value
+//     outside [0, 2^24) travels as int32 (per chunk: the device col is int32
+//     either way)
+// The packing of chunk k + 1 overlaps the DMA of chunk k.
+int stage_chunked_codec(Workspace* w, cudaStream_t s, const int32_t* col,
+                        const int32_t* weight, int32_t* d_col,
+                        int32_t* d_weight, unsigned* d_wpack, int64_t m,
+                        int shift, bool pack_w, bool pack_c, Arrival* arr,
+                        uint64_t* h2d, bool* packed_all) {
+  int r;
   if (!w->copy_stream) {
     DP_CUDA(cudaStreamCreateWithFlags(&w->copy_stream, cudaStreamNonBlocking));
     DP_CUDA(cudaMalloc(&w->d_arrived, sizeof(int)));
@@ -2486,15 +2551,25 @@ int stage_chunked_packed(Workspace* w, cudaStream_t s, const int32_t* col,
       DP_CUDA(cudaEventCreateWithFlags(&w->chunk_ev[k],
                                        cudaEventDisableTiming));
   }
-  const size_t hbytes = (size_t)((m + 7) / 8) * sizeof(unsigned);
-  if (hbytes > w->h_wpack_bytes) {
-    if (w->h_wpack) cudaFreeHost(w->h_wpack);
-    w->h_wpack = nullptr;
-    w->h_wpack_bytes = 0;
-    DP_CUDA(cudaMallocHost(&w->h_wpack, hbytes));
-    w->h_wpack_bytes = hbytes;
-  }
+  auto pinned = [](void** p, size_t* have, size_t need) -> int {
+    if (need <= *have) return 0;
+    if (*p) cudaFreeHost(*p);
+    *p = nullptr;
+    *have = 0;
+    DP_CUDA(cudaMallocHost(p, need));
+    *have = need;
+    return 0;
+  };
+  if (pack_w &&
+      (r = pinned(&w->h_wpack, &w->h_wpack_bytes,
+                  (size_t)((m + 7) / 8) * sizeof(unsigned))))
+    return r;
+  const size_t cbytes = (size_t)((m + 3) / 4) * 3 * sizeof(unsigned);
+  if (pack_c && ((r = pinned(&w->h_cpack, &w->h_cpack_bytes, cbytes)) ||
+                 (r = grow(&w->cpack, &w->cpack_bytes, cbytes))))
+    return r;
   unsigned* hp = (unsigned*)w->h_wpack;
+  unsigned* hc = (unsigned*)w->h_cpack;
   const int64_t chunk = 1LL << shift;
   arr->nchunks = (int)((m + chunk - 1) / chunk);
   arr->waited = 0;
@@ -2503,13 +2578,26 @@ int stage_chunked_packed(Workspace* w, cudaStream_t s, const int32_t* col,
   DP_CUDA(cudaMemsetAsync(w->d_arrived, 0, sizeof(int), s));
   DP_CUDA(cudaEventRecord(w->evk0, s));
   DP_CUDA(cudaStreamWaitEvent(w->copy_stream, w->evk0, 0));
-  bool packed = true;
+  bool packed = pack_w;
   for (int k = 0; k < arr->nchunks; ++k) {
     const int64_t lo = (int64_t)k * chunk;
     const int64_t len = std::min(chunk, m - lo);
-    DP_CUDA(cudaMemcpyAsync(d_col + lo, col + lo, (size_t)len * 4,
-                            cudaMemcpyHostToDevice, w->copy_stream));
-    *h2d += (uint64_t)len * 4;
+    if (pack_c && pack_col24_host(col, lo, len, hc)) {
+      const int64_t g0 = lo >> 2, groups = (len + 3) / 4;
+      DP_CUDA(cudaMemcpyAsync((unsigned*)w->cpack + g0 * 3, hc + g0 * 3,
+                              (size_t)groups * 3 * sizeof(unsigned),
+                              cudaMemcpyHostToDevice, w->copy_stream));
+      *h2d += (uint64_t)groups * 3 * sizeof(unsigned);
+      const int blocks = (int)std::max<int64_t>(
+          1, std::min<int64_t>(dp::ceil_div_ll(groups, 256), 148 * 8));
+      unpack_col24_kernel<<<blocks, 256, 0, w->copy_stream>>>(
+          (const unsigned*)w->cpack, g0, groups, m, d_col);
+      DP_CUDA(cudaGetLastError());
+    } else {
+      DP_CUDA(cudaMemcpyAsync(d_col + lo, col + lo, (size_t)len * 4,
+                              cudaMemcpyHostToDevice, w->copy_stream));
+      *h2d += (uint64_t)len * 4;
+    }
     if (packed && !pack_weights_host(weight, lo, len, hp)) {
       packed = false;
       if (lo > 0) {  // chunks [0, k) arrived packed only: add their int32
@@ -2685,12 +2773,15 @@ int dp_sssp(const int32_t* rowptr, const int32_t* col, const int32_t* weight,
     Arrival arr;
     const int shift = chunk_shift(m);
     const unsigned* wpack = nullptr;
-    if (cfg && cfg->weight_bits == 4) {
-      DP_TRY(stage(w_, 3, nullptr, (size_t)((m + 7) / 8 + 1) * 4, s_, &h2d_));
+    const bool pack_w = cfg && cfg->weight_bits == 4;
+    const bool pack_c = cfg && cfg->col_bits == 24;
+    if (pack_w || pack_c) {
+      if (pack_w)
+        DP_TRY(stage(w_, 3, nullptr, (size_t)((m + 7) / 8 + 1) * 4, s_, &h2d_));
       bool all = false;
-      DP_TRY(stage_chunked_packed(w_, s_, col, weight, (int32_t*)w_->io[1],
-                                  (int32_t*)w_->io[4], (unsigned*)w_->io[3],
-                                  m, shift, &arr, &h2d_, &all));
+      DP_TRY(stage_chunked_codec(w_, s_, col, weight, (int32_t*)w_->io[1],
+                                 (int32_t*)w_->io[4], (unsigned*)w_->io[3], m,
+                                 shift, pack_w, pack_c, &arr, &h2d_, &all));
       if (all) wpack = (const unsigned*)w_->io[3];
     } else {
       const void* hsrc[2] = {col, weight};
@@ -3042,6 +3133,8 @@ void dp_thread_release(void) {
     cudaFree(w.wpack);
     cudaFreeHost(w.h_wpack);
     cudaFree(w.d_bad);
+    cudaFree(w.cpack);
+    cudaFreeHost(w.h_cpack);
     cudaFree(w.lbits);
     w = Workspace();
   }

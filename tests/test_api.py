@@ -37,7 +37,8 @@ def test_library_exports_every_declared_symbol():
     for name in declared:
         assert hasattr(lib, name), name
     assert declared == set(_lib.EXPORTED)
-    assert lib.dp_abi_version() == 1
+    assert lib.dp_abi_version() == _lib.ABI_VERSION == 2
+    assert f"#define DP_ABI_VERSION {_lib.ABI_VERSION}" in header
 
 
 _C_TYPES = {"int32_t": ctypes.c_int32, "uint32_t": ctypes.c_uint32,
@@ -146,6 +147,7 @@ def test_parse_spec_rejects(bad, needle):
     # round-2 B200 knobs
     (BenchConfig(weight_bits=3), "weight_bits"),
     (BenchConfig(cf_wave=-1), "cf_wave"),
+    (BenchConfig(col_bits=16), "col_bits"),
     (BenchConfig(persistent=9), "persistent"),
 ])
 def test_knob_validation_matches_reference_errors(cfg, needle):

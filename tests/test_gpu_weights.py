@@ -1,8 +1,11 @@
 """Packed SSSP weights (dp_config.weight_bits = 4): weights in [1, 16] are
 read as nibbles; outside that range the device path falls back to int32 and
 the host-buffer path keeps int32 for the first chunk holding such a weight
-and every later one.  Distances must equal the oracle's bit for bit in all
-cases, and the host path must copy fewer bytes when it packs."""
+and every later one.  The 3-byte col transfer (dp_config.col_bits = 24):
+chunks of col cross PCIe packed and are expanded on the device; a chunk with
+a value outside [0, 2^24) travels as int32.  Distances must equal the
+oracle's bit for bit in all cases, and the host path must copy fewer bytes
+when it packs."""
 from __future__ import annotations
 
 import numpy as np
@@ -89,3 +92,65 @@ def test_host_packing_copies_fewer_bytes():
     np.testing.assert_array_equal(r0.arrays["dist"], r4.arrays["dist"])
     # int32 weights: 4 B per slot; packed: 0.5 B per slot
     assert r0.h2d_bytes - r4.h2d_bytes >= int(m * 3.4)
+
+
+@pytest.mark.parametrize("spec", ["rmat:16:seed1", "road:1000:seed7",
+                                  "powerlaw:2000:seed1"])
+@pytest.mark.parametrize("shift", ["", "2", "5", "12"])
+def test_col24_transfer_exact(spec, shift, monkeypatch):
+    """Chunk sizes 4, 32, 4096 slots and the default, with and without the
+    packed weights: ragged last chunks and partial 4-slot groups."""
+    if shift:
+        monkeypatch.setenv("DP_COPY_CHUNK_SHIFT", shift)
+    bench, wl = load("sssp", spec)
+    b = wl.buffers
+    want, _ = oracle.sssp(b["rowptr"], b["col"], b["weight"], nthreads=0)
+    m = b["col"].shape[0]
+    r0, _ = run_config(bench, wl, BenchConfig())
+    for extra in (dict(col_bits=24), dict(col_bits=24, weight_bits=4)):
+        rep, _ = run_config(bench, wl, BenchConfig(**extra))
+        np.testing.assert_array_equal(rep.arrays["dist"], want)
+        # 4 B per col slot -> 3 B (whole 4-slot groups per chunk)
+        saved = r0.h2d_bytes - rep.h2d_bytes
+        if "weight_bits" in extra:
+            saved -= int(m * 3.4)
+        assert saved >= int(m * 0.9), (extra, saved, m)
+
+
+def test_col24_out_of_range_chunk_travels_int32(monkeypatch):
+    """n > 2^24: the chunks naming a vertex >= 2^24 go as int32, the others
+    packed; distances still exact."""
+    monkeypatch.setenv("DP_COPY_CHUNK_SHIFT", "6")
+    rng = np.random.default_rng(3)
+    n = (1 << 24) + 64
+    hubs = np.array([0, 1, 2, 3, n - 1, n - 2, (1 << 24) + 5, 12345],
+                    np.int64)
+    src_of = np.repeat(np.arange(hubs.size), 96)
+    dst = rng.choice(hubs, size=src_of.size)
+    dst[::7] = rng.integers(0, n, size=dst[::7].size)
+    rows = hubs[src_of]
+    order = np.lexsort((dst, rows))
+    rows, dst = rows[order], dst[order]
+    rowptr = np.zeros(n + 1, np.int64)
+    np.add.at(rowptr, rows + 1, 1)
+    rowptr = np.cumsum(rowptr).astype(np.int32)
+    col = dst.astype(np.int32)
+    w = rng.integers(1, 17, size=col.size).astype(np.int32)
+    want, _ = oracle.sssp(rowptr, col, w, nthreads=0)
+    d0, h0 = _host_sssp(rowptr, col, w, n, BenchConfig())
+    d24, h24 = _host_sssp(rowptr, col, w, n, BenchConfig(col_bits=24))
+    np.testing.assert_array_equal(d0, want)
+    np.testing.assert_array_equal(d24, want)
+    assert (col >= (1 << 24)).any()
+    assert 0 < h0 - h24 < col.size
+
+
+def _host_sssp(rowptr, col, w, n, cfg):
+    import ctypes
+    from paper_2201_02789_b200 import _lib
+    dist = np.empty(n, dtype=np.int32)
+    st = _lib.DpStats()
+    _lib.check(_lib.device().dp_sssp(
+        _lib.ptr(rowptr), _lib.ptr(col), _lib.ptr(w), n, col.shape[0], 0,
+        ctypes.byref(cfg.to_c()), _lib.ptr(dist), ctypes.byref(st)))
+    return dist, int(st.h2d_bytes)
