@@ -887,6 +887,17 @@ int iterate(Workspace* w, const dp_config* c, long long nparents,
                                   (launchers == 0 || !pick(it, w->h_ds))
                               ? &c_flat
                               : c;
+    // chunks known to have landed before this round starts (it sees them)
+    while (arr && arr->waited < arr->nchunks) {
+      const cudaError_t q = cudaEventQuery(w->chunk_ev[arr->waited]);
+      if (q == cudaSuccess) {
+        ++arr->waited;
+        continue;
+      }
+      if (q != cudaErrorNotReady) DP_CUDA(q);
+      if (cudaPeekAtLastError() == cudaErrorNotReady) (void)cudaGetLastError();
+      break;
+    }
     if ((r = launch_parent(app, nparents, launchers, cl, w, s, &rc))) return r;
     if ((r = read_state_fast(w, s))) return r;
     if ((r = account_step(w, &rc))) return r;
@@ -899,6 +910,8 @@ int iterate(Workspace* w, const dp_config* c, long long nparents,
     // edges still landing: the next round starts when the next chunk has
     // (rounds re-scanning unchanged data would only compete with the DMA
     // for L2: measured 13.2 vs 12.1 ms with back-to-back rounds)
+    // (waiting only after a round that lowered nothing measured no better:
+    // 7.95-8.03 vs 7.89-7.91 ms, profiles/r02/e2e_eager_r02.txt)
     if (arr && arr->waited < arr->nchunks && w->h_ds->skipped[it & 1])
       DP_CUDA(cudaEventSynchronize(w->chunk_ev[arr->waited++]));
   }
