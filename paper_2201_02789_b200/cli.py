@@ -1,9 +1,14 @@
-"""``sweep`` command line, compatible with ``dynoptc sweep``
-(pkg/src/dynoptc/cli.py:139-165, 345-367): same flags, same CSV (the
-reference's 18 columns first, measured B200 columns after), exit code 1 when
-any row failed.  B200 knobs: --parent-block, --child-block, --serial.
+"""Command line: ``python -m paper_2201_02789_b200 sweep ...``.
 
-    python -m paper_2201_02789_b200.cli sweep --bench bfs \\
+Flag-compatible with the ``sweep`` subcommand of ``dynoptc``
+(pkg/src/dynoptc/cli.py:139-165 flags, 345-367 behaviour): the same list
+flags and spellings (``inf`` thresholds, ``none`` granularity), the same CSV
+(reference columns first, measured B200 columns after), the CSV on stdout or
+in ``--report``, one line per failed row on stderr and exit status 1 when any
+row failed.  The compiler subcommands (``emit`` / ``run``) are out of scope
+(DESIGN.md §1): the kernels here are written, not emitted.
+
+    python -m paper_2201_02789_b200 sweep --bench bfs \\
         --dataset rmat:16:seed1 --thresholds 0,128,inf --aggs none,block
 """
 
@@ -11,123 +16,145 @@ from __future__ import annotations
 
 import argparse
 import sys
+from typing import Callable
 
-from .bench import (BenchConfig, INF_THRESHOLD, render_csv, write_csv)
-from .bench import sweep as bench_sweep
+from .bench import BenchConfig, INF_THRESHOLD, render_csv, sweep, write_csv
 from .bench.harness import GRANULARITIES
+
+PROG = "paper_2201_02789_b200"
 
 
 class CliError(Exception):
-    pass
+    """A usage problem reported as ``PROG: error: ...`` with status 1."""
 
 
-def _threshold_value(text: str) -> int:
-    t = text.strip().lower()
-    if t in ("inf", "infinity"):
+def _threshold(token: str) -> int:
+    word = token.strip().lower()
+    if word in ("inf", "infinity"):
         return INF_THRESHOLD
-    try:
-        v = int(t)
-    except ValueError:
+    if not word.lstrip("-").isdigit():
         raise argparse.ArgumentTypeError(
-            f"threshold must be an integer or 'inf', got {text!r}") from None
-    if v < 0:
+            f"threshold must be an integer or 'inf', got {token!r}")
+    if int(word) < 0:
         raise argparse.ArgumentTypeError("threshold must be >= 0")
-    return v
+    return int(word)
 
 
-def _int_list(text: str) -> list[int]:
-    return [_threshold_value(t) for t in text.split(",") if t.strip()]
-
-
-def _agg_value(text: str):
-    t = text.strip().lower()
-    if t in ("", "none"):
+def _granularity(token: str):
+    word = token.strip().lower()
+    if word in ("", "none"):
         return None
-    if t not in GRANULARITIES:
-        raise argparse.ArgumentTypeError(
-            f"aggregation granularity must be one of "
-            f"{', '.join(GRANULARITIES)} or 'none', got {text!r}")
-    return t
+    if word in GRANULARITIES:
+        return word
+    raise argparse.ArgumentTypeError(
+        f"aggregation granularity must be one of {', '.join(GRANULARITIES)} "
+        f"or 'none', got {token!r}")
 
 
-def _agg_list(text: str) -> list:
-    return [_agg_value(t) for t in text.split(",") if t.strip()]
+def _listed(item: Callable) -> Callable[[str], list]:
+    """Comma-separated list of ``item`` values (empty entries skipped)."""
+    return lambda text: [item(t) for t in text.split(",") if t.strip()]
+
+
+# grid axes (one BenchConfig per combination) and per-sweep knobs:
+# (flag, type, default, metavar, help)
+_AXES = (
+    ("--thresholds", _listed(_threshold), [0, 32, INF_THRESHOLD], "N,...",
+     "thresholds T (integers or inf)"),
+    ("--cfactors", _listed(_threshold), [1], "F,...", "coarsening factors C"),
+    ("--aggs", _listed(_granularity), [None, "block", "multiblock", "grid"],
+     "G,...", "aggregation granularities A (or none)"),
+)
+_KNOBS = (
+    ("--group-size", int, 4, "G", "multiblock group size"),
+    ("--agg-threshold", int, 0, "N", "aggregation threshold (block only)"),
+)
+_B200_KNOBS = (
+    ("--parent-block", int, 32, "B", "parent grid block size"),
+    ("--child-block", int, 32, "B", "child grid block size"),
+)
 
 
 def build_parser() -> argparse.ArgumentParser:
-    parser = argparse.ArgumentParser(
-        prog="paper_2201_02789_b200",
-        description="Sweep the nested-parallel (CDP2 + T/C/A) kernels on a "
-                    "B200.")
-    sub = parser.add_subparsers(dest="command", required=True)
-    p = sub.add_parser("sweep",
-                       help="run a benchmark across a configuration grid")
+    top = argparse.ArgumentParser(
+        prog=PROG, description="Sweep the nested-parallel (CDP2 + T/C/A) "
+                               "kernels on a B200.")
+    cmds = top.add_subparsers(dest="command", required=True)
+    p = cmds.add_parser("sweep", help="run a benchmark across a grid of "
+                                      "configurations")
     p.add_argument("--bench", required=True,
-                   help="benchmark name (bfs, sssp, manylaunch, tc, bt)")
+                   help="benchmark name (bfs, sssp, manylaunch, tc, bt, ...)")
     p.add_argument("--dataset", required=True, metavar="SPEC",
                    help="dataset spec, e.g. rmat:16:seed1")
     p.add_argument("--report", metavar="CSV", default=None,
                    help="write the CSV here instead of stdout")
-    p.add_argument("--thresholds", type=_int_list,
-                   default=[0, 32, INF_THRESHOLD], metavar="N,...")
-    p.add_argument("--cfactors", type=_int_list, default=[1],
-                   metavar="F,...")
-    p.add_argument("--aggs", type=_agg_list,
-                   default=[None, "block", "multiblock", "grid"],
-                   metavar="G,...")
-    p.add_argument("--group-size", type=int, default=4, metavar="G")
-    p.add_argument("--agg-threshold", type=int, default=0, metavar="N")
+    for flag, typ, default, metavar, help_ in _AXES + _KNOBS:
+        p.add_argument(flag, type=typ, default=default, metavar=metavar,
+                       help=help_)
     p.add_argument("--cost", metavar="K=V,...", default="",
-                   help="accepted for compatibility; hardware has no cost "
-                        "model")
+                   help="accepted for compatibility (hardware has no cost "
+                        "model)")
     p.add_argument("--no-verify", action="store_true",
-                   help="skip checking outputs against the serial variant")
-    g = p.add_argument_group("B200 knobs")
-    g.add_argument("--parent-block", type=int, default=32)
-    g.add_argument("--child-block", type=int, default=32)
-    g.add_argument("--serial", choices=("thread", "warp"), default="thread")
-    return parser
+                   help="do not check outputs against the serial variant")
+    b200 = p.add_argument_group("B200 knobs")
+    for flag, typ, default, metavar, help_ in _B200_KNOBS:
+        b200.add_argument(flag, type=typ, default=default, metavar=metavar,
+                          help=help_)
+    b200.add_argument("--serial", choices=("thread", "warp"),
+                      default="thread", help="serial arm mode")
+    return top
 
 
-def _cmd_sweep(args) -> int:
-    configs = [BenchConfig(threshold=t, cfactor=c, agg=a,
-                           group_size=args.group_size,
-                           agg_threshold=args.agg_threshold,
-                           parent_block=args.parent_block,
-                           child_block=args.child_block, serial=args.serial)
-               for t in args.thresholds for c in args.cfactors
-               for a in args.aggs]
-    try:
-        rows = bench_sweep(args.bench, args.dataset, configs=configs,
-                           verify=not args.no_verify)
-    except ValueError as e:
-        raise CliError(str(e)) from None
-    if args.report is not None:
-        try:
-            write_csv(args.report, rows)
-        except OSError as e:
-            raise CliError(f"cannot write '{args.report}': "
-                           f"{e.strerror or e}") from None
-        print(f"wrote {args.report} ({len(rows)} rows)", file=sys.stderr)
-    else:
+def _grid(args) -> list[BenchConfig]:
+    shared = dict(group_size=args.group_size,
+                  agg_threshold=args.agg_threshold,
+                  parent_block=args.parent_block,
+                  child_block=args.child_block, serial=args.serial)
+    return [BenchConfig(threshold=t, cfactor=c, agg=a, **shared)
+            for t in args.thresholds for c in args.cfactors
+            for a in args.aggs]
+
+
+def _emit(args, rows: list[dict]) -> None:
+    if args.report is None:
         sys.stdout.write(render_csv(rows))
-    failed = [r for r in rows if r["error"]]
-    for r in failed:
-        print(f"row {r['threshold']}/{r['cfactor']}/{r['agg']}: "
-              f"{r['error']}", file=sys.stderr)
-    return 1 if failed else 0
+        return
+    try:
+        write_csv(args.report, rows)
+    except OSError as e:
+        raise CliError(f"cannot write '{args.report}': {e.strerror or e}") \
+            from None
+    print(f"wrote {args.report} ({len(rows)} rows)", file=sys.stderr)
+
+
+def run_sweep(args) -> int:
+    try:
+        rows = sweep(args.bench, args.dataset, configs=_grid(args),
+                     verify=not args.no_verify)
+    except ValueError as e:  # unknown benchmark / bad dataset spec
+        raise CliError(str(e)) from None
+    _emit(args, rows)
+    status = 0
+    for row in rows:
+        if row["error"]:
+            status = 1
+            print(f"row {row['threshold']}/{row['cfactor']}/{row['agg']}: "
+                  f"{row['error']}", file=sys.stderr)
+    return status
+
+
+COMMANDS = {"sweep": run_sweep}
 
 
 def main(argv=None) -> int:
-    parser = build_parser()
     try:
-        args = parser.parse_args(argv)
-    except SystemExit as e:
+        args = build_parser().parse_args(argv)
+    except SystemExit as e:  # argparse already printed the usage error
         return int(e.code or 0)
     try:
-        return {"sweep": _cmd_sweep}[args.command](args)
+        return COMMANDS[args.command](args)
     except (CliError, ValueError) as e:
-        print(f"paper_2201_02789_b200: error: {e}", file=sys.stderr)
+        print(f"{PROG}: error: {e}", file=sys.stderr)
         return 1
 
 
