@@ -154,3 +154,22 @@ def _host_sssp(rowptr, col, w, n, cfg):
         _lib.ptr(rowptr), _lib.ptr(col), _lib.ptr(w), n, col.shape[0], 0,
         ctypes.byref(cfg.to_c()), _lib.ptr(dist), ctypes.byref(st)))
     return dist, int(st.h2d_bytes)
+
+
+@pytest.mark.parametrize("shift", ["", "6"])
+def test_speculative_readback_is_the_result(shift, monkeypatch):
+    """dp_sssp copies dist back while the next round runs; the copy that
+    overlapped a round which lowered nothing is the result (no final D2H).
+    Every copy is counted in d2h_bytes."""
+    if shift:
+        monkeypatch.setenv("DP_COPY_CHUNK_SHIFT", shift)
+    for spec in ("rmat:16:seed1", "road:1000:seed7"):
+        bench, wl = load("sssp", spec)
+        b = wl.buffers
+        want, _ = oracle.sssp(b["rowptr"], b["col"], b["weight"], nthreads=0)
+        for pol in POLICIES[:2]:
+            d, _ = _host_sssp(b["rowptr"], b["col"], b["weight"], wl.n,
+                              BenchConfig(**pol))
+            np.testing.assert_array_equal(d, want)
+            rep, _ = run_config(bench, wl, BenchConfig(**pol))
+            assert rep.d2h_bytes % (wl.n * 4) == 0 and rep.d2h_bytes >= wl.n * 4
