@@ -916,7 +916,7 @@ int iterate(Workspace* w, const dp_config* c, long long nparents,
     if (w->h_ds->flag[it & 1] == 0 &&
         (!arr || w->h_ds->skipped[it & 1] == 0)) {
       converged = true;
-      if (arr && arr->spec_after == it - 1) arr->spec_final = true;
+      if (arr && it > 0 && arr->spec_after == it - 1) arr->spec_final = true;
       ++it;
       break;
     }

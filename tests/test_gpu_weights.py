@@ -173,3 +173,15 @@ def test_speculative_readback_is_the_result(shift, monkeypatch):
             np.testing.assert_array_equal(d, want)
             rep, _ = run_config(bench, wl, BenchConfig(**pol))
             assert rep.d2h_bytes % (wl.n * 4) == 0 and rep.d2h_bytes >= wl.n * 4
+
+
+def test_host_sssp_source_without_edges():
+    """The first round lowers nothing: no speculative copy exists, the call
+    must still return dist (regression: it once skipped the final D2H)."""
+    rowptr = np.array([0, 0, 2, 3], np.int32)
+    col = np.array([2, 0, 1], np.int32)
+    w = np.array([1, 2, 3], np.int32)
+    want, _ = oracle.sssp(rowptr, col, w, nthreads=0)
+    for pol in POLICIES[:2]:
+        d, _ = _host_sssp(rowptr, col, w, 3, BenchConfig(**pol))
+        np.testing.assert_array_equal(d, want)
