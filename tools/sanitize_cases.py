@@ -19,7 +19,11 @@ POLICIES = [dict(), dict(agg="warp"), dict(threshold=4, agg="block"),
             # path), order "A before C"
             dict(threshold=4, cfactor=4, agg="multiblock", group_size=1 << 20,
                  serial="warp", cf_wave=1, weight_bits=4),
-            dict(threshold=2, cfactor=3, agg="block", order="ACT")]
+            dict(threshold=2, cfactor=3, agg="block", order="ACT"),
+            # 3-byte col transfer + speculative readback over many chunks
+            dict(threshold=4, agg="block", col_bits=24, weight_bits=4)]
+import os
+os.environ.setdefault("DP_COPY_CHUNK_SHIFT", "6")  # host-path SSSP: chunks
 fails = 0
 for app, spec in (("bfs", "powerlaw:300:seed2"), ("sssp", "powerlaw:300:seed3"),
                   ("manylaunch", "sizes:200:seed1"), ("tc", "rmat:8:seed1"),
