@@ -191,6 +191,12 @@ int dp_bfs_dev(const int32_t* d_rowptr, const int32_t* d_col, int32_t n,
                int32_t* d_counts, void* stream, dp_stats* stats);
 
 /* ---- SSSP (benchmarks.py:175-270) ---------------------------------------- */
+/* host buffers: rowptr[n+1], col[m], weight[m]; out dist[n].  col / weight
+ * stream in behind the rounds (chunked copy; weight_bits / col_bits pick the
+ * transfer codecs).  Once every chunk has landed the call copies dist back
+ * while the next round runs and returns as soon as a round lowers nothing:
+ * `dist` may be written more than once during the call (its final contents
+ * are the result) and stats->d2h_bytes counts every copy. */
 int dp_sssp(const int32_t* rowptr, const int32_t* col, const int32_t* weight,
             int32_t n, int64_t m, int32_t src, const dp_config* cfg,
             int32_t* dist, dp_stats* stats);

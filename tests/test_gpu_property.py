@@ -136,9 +136,11 @@ def _graph_workload(bench_name, rowptr, col, weight):
 
 @SETTINGS
 @given(graph=graphs_st(), policy=policies(),
-       device_loop=st.booleans(), frontier=st.booleans())
+       device_loop=st.booleans(), frontier=st.booleans(),
+       codec=st.sampled_from([{}, dict(weight_bits=4), dict(col_bits=24),
+                              dict(weight_bits=4, col_bits=24)]))
 def test_bfs_sssp_random_graphs_and_policies(graph, policy, device_loop,
-                                             frontier):
+                                             frontier, codec):
     rowptr, col, weight = graph
     dist, counts, levels = oracle.bfs(rowptr, col)
     bench, wl = _graph_workload("bfs", rowptr, col, weight)
@@ -150,7 +152,7 @@ def test_bfs_sssp_random_graphs_and_policies(graph, policy, device_loop,
     sdist, _ = oracle.sssp(rowptr, col, weight)
     bench, wl = _graph_workload("sssp", rowptr, col, weight)
     rep, _ = run_config(bench, wl, BenchConfig(
-        **policy, device_loop=device_loop, frontier=frontier))
+        **policy, device_loop=device_loop, frontier=frontier, **codec))
     np.testing.assert_array_equal(rep.arrays["dist"], sdist)
 
 
