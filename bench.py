@@ -80,7 +80,7 @@ BEST = {
 }
 
 
-def bt_stream_row(ncurves: int, quick: bool) -> dict:
+def bt_stream_row(ncurves: int, quick: bool, policy=None) -> dict:
     """BT at a streaming size on one GPU (the 25k config is
     launch-sized): device time of the tessellation (CUDA events inside
     libdynpar), algorithmic bytes 36 B/curve + 8 B/vertex against HBM."""
@@ -98,7 +98,8 @@ def bt_stream_row(ncurves: int, quick: bool) -> dict:
     offs = torch.empty(ncurves, dtype=torch.int64, device=dev)
     verts = torch.empty((cap, 2), dtype=torch.float32, device=dev)
     used = ctypes.c_int64()
-    cfg = _cfg(BEST["bt"])
+    policy = BEST["bt"] if policy is None else policy
+    cfg = _cfg(policy)
     ts = []
     for _ in range(7):
         st = _lib.DpStats()
@@ -115,7 +116,7 @@ def bt_stream_row(ncurves: int, quick: bool) -> dict:
     row = {"curves": ncurves, "ms": ms, "curves_per_s": ncurves / ms * 1e3,
            "vertices": nv, "gbps_alg": alg / (ms * 1e6),
            "frac_hbm": alg / (ms * 1e6) / peak, "peak_source": src,
-           "policy": BEST["bt"]}
+           "policy": policy}
     if not quick:
         from oracle import oracle
         want_nt, want_v = oracle.bt(cp_h, BT_MAX_TESS, BT_CURV_SCALE)
@@ -592,6 +593,10 @@ def extra_workloads(stream, quick: bool) -> dict:
     out["bt_25k"]["agg_only_matched_ms"] = matched
     out["bt_25k"]["vs_naive_cdp"] = naive.ns_device / 1e6 / ms
     out["bt_25k"]["vs_agg_only"] = min(agg_ms.values()) / ms
+    # the same kernel on device-resident buffers, calls back to back
+    # (dp_bt_dev): the host-buffer call above idles the GPU between runs
+    # and a ~30 us kernel then starts at lower clocks
+    out["bt_25k"]["ms_resident"] = bt_stream_row(25000, True)["ms"]
     out["bt_1m_streaming"] = bt_stream_row(1000000, quick)
     if quick:
         return out
