@@ -561,42 +561,39 @@ def extra_workloads(stream, quick: bool) -> dict:
                              "seconds": dt,
                              "sample": "full TC rmat-22, oracle/oracle.c"}})
     del rp, col
-    # BT 25k curves
+    # BT 25k curves.  Device time on device-resident buffers, calls back to
+    # back (dp_bt_dev), for every policy compared: the host-buffer call idles
+    # the GPU between runs and a ~30 us kernel then starts at lower clocks
+    # (45-63 vs 28 us for the same kernel, profiles/r02/bt25k_paths_r02.txt)
     bench, wl = load("bt", "curves:25000:seed1")
-    reps = []
-    for _ in range(6):
-        rep, _ = run_config(bench, wl, BenchConfig(**BEST["bt"]))
-        reps.append(rep)
-    ms = statistics.median(r.ns_device for r in reps[1:]) / 1e6
-    nv = int(reps[-1].arrays["ntess"].astype(np.int64).sum())
+    rep0 = run_config(bench, wl, BenchConfig(**BEST["bt"]))[0]
+    nv = int(rep0.arrays["ntess"].astype(np.int64).sum())
+
+    def bt_ms(p):
+        row = bt_stream_row(25000, True, p)
+        assert row["vertices"] == nv, (row["vertices"], nv)
+        return row["ms"]
+    ms = bt_ms(BEST["bt"])
     out["bt_25k"] = {"curves_per_s": 25000 / (ms * 1e-3), "ms": ms,
                      "vertices": nv, "gbps_alg": (36 * 25000 + 8 * nv) /
-                     (ms * 1e6), "policy": BEST["bt"]}
+                     (ms * 1e6), "policy": BEST["bt"],
+                     "ms_host_call": rep0.ns_device / 1e6}
     # BASELINE config 2 as written: coarsening + multi-block aggregation
     c2 = dict(threshold=64, cfactor=16, agg="multiblock", group_size=4,
               parent_block=256, child_block=32, serial="warp")
-    reps = [run_config(bench, wl, BenchConfig(**c2))[0] for _ in range(6)]
-    ms2 = statistics.median(r.ns_device for r in reps[1:]) / 1e6
-    naive = run_config(bench, wl, BenchConfig())[0]
+    ms2 = bt_ms(c2)
+    naive_ms = bt_ms({})
     out["config2_bt_25k_c_multiblock"] = {
         "curves_per_s": 25000 / (ms2 * 1e-3), "ms": ms2,
-        "device_launches": reps[-1].num_launches,
-        "vs_naive_cdp": naive.ns_device / 1e6 / ms2, "policy": c2}
-    agg_ms = {a: min(run_config(bench, wl, BenchConfig(agg=a))[0].ns_device
-                     for _ in range(3)) / 1e6
-              for a in ("warp", "block", "grid")}
-    matched = matched_agg_only(
-        BEST["bt"], lambda p: statistics.median(
-            run_config(bench, wl, BenchConfig(**p))[0].ns_device
-            for _ in range(5)) / 1e6)
+        "device_launches": run_config(bench, wl,
+                                      BenchConfig(**c2))[0].num_launches,
+        "vs_naive_cdp": naive_ms / ms2, "policy": c2}
+    agg_ms = {a: bt_ms(dict(agg=a)) for a in ("warp", "block", "grid")}
+    matched = matched_agg_only(BEST["bt"], bt_ms)
     out["bt_25k"]["vs_agg_only_matched"] = min(matched.values()) / ms
     out["bt_25k"]["agg_only_matched_ms"] = matched
-    out["bt_25k"]["vs_naive_cdp"] = naive.ns_device / 1e6 / ms
+    out["bt_25k"]["vs_naive_cdp"] = naive_ms / ms
     out["bt_25k"]["vs_agg_only"] = min(agg_ms.values()) / ms
-    # the same kernel on device-resident buffers, calls back to back
-    # (dp_bt_dev): the host-buffer call above idles the GPU between runs
-    # and a ~30 us kernel then starts at lower clocks
-    out["bt_25k"]["ms_resident"] = bt_stream_row(25000, True)["ms"]
     out["bt_1m_streaming"] = bt_stream_row(1000000, quick)
     if quick:
         return out
