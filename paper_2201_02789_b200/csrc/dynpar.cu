@@ -63,6 +63,7 @@ struct Workspace {
     DevState ds;
     unsigned seq;
     unsigned pad;
+    unsigned long long aux;  // d_scratch[1]: the lazy launcher count
   };
   Signal* h_sig = nullptr;  // host view (mapped pinned)
   Signal* d_sig = nullptr;  // device view of the same memory
@@ -154,6 +155,7 @@ Workspace* workspace(int* rc) {
                  std::string("workspace init: ") + cudaGetErrorString(e));
       return nullptr;
     }
+    std::memset((void*)w.h_sig, 0, sizeof(Workspace::Signal));
     w.ready = true;
   }
   return &w;
@@ -298,6 +300,51 @@ int count_launchers(Workspace* w, const dp_config* c, const int* data, int n,
   DP_CUDA(cudaStreamSynchronize(s));
   *out = (long long)w->h_ctr[1];
   return 0;
+}
+
+// count_launchers without the host round trip (BFS / SSSP level loops).
+// When a bound computed from m alone keeps the pool small, the count kernel
+// is queued into d_scratch[1] and its value rides on the first round's
+// readback (signal_kernel aux); *lazy_bound >= 0 then holds that pool bound
+// and *out an upper bound on the launchers.  Otherwise as count_launchers
+// (*lazy_bound = -1).  The stream synchronisation this saves left the GPU
+// idle between the count and the first parent grid of every call.
+int count_launchers_lazy(Workspace* w, const dp_config* c, const int* rowptr,
+                         int n, int64_t m, cudaStream_t s, long long* out,
+                         long long* lazy_bound) {
+  *lazy_bound = -1;
+  const long long thr = c->threshold;  // 0: every non-empty row launches
+  if (c->variant == DP_VARIANT_CDP && m >= 0 &&
+      launch_bound(c, n, n) > (1 << 16) && !std::getenv("DYNPAR_SYNC_COUNT")) {
+    // a launcher has >= max(T, 1) items
+    const long long L = std::min<long long>(n, m / std::max<long long>(thr, 1));
+    if (L == 0) {  // no row can reach the threshold: exact, nothing to count
+      *out = 0;
+      return 0;
+    }
+    // a row launched on its own under cf_wave has >= (cf_wave - 1) * cb + 1
+    long long solo = 0;
+    if (c->cf_wave > 0 && c->agg != DP_AGG_NONE)
+      solo = std::min<long long>(
+          L, m / ((long long)(c->cf_wave - 1) * c->child_block + 1));
+    const long long bound =
+        solo + launch_bound_agg(c, L, dp::ceil_div_ll(n, 32),
+                                dp::ceil_div_ll(n, c->parent_block));
+    if (bound <= (1 << 14)) {
+      DP_CUDA(cudaMemsetAsync(w->d_scratch + 1, 0, sizeof(unsigned long long),
+                              s));
+      if (n > 0) {
+        count_deg_ge_kernel<<<std::min(dp::ceil_div(n, 256), 148 * 8), 256, 0,
+                              s>>>(rowptr, n, effective_threshold(c),
+                                   w->d_scratch + 1);
+        DP_CUDA(cudaGetLastError());
+      }
+      *out = L;
+      *lazy_bound = bound;
+      return 0;
+    }
+  }
+  return count_launchers(w, c, rowptr, n, 0, s, out);
 }
 
 // Upper bound on device launches issued by ONE host launch of the parent
@@ -705,8 +752,10 @@ int check_published(Workspace* w) {
 }
 
 __global__ void signal_kernel(const DevState* ds, Workspace::Signal* sig,
-                              unsigned seq) {
+                              unsigned seq,
+                              const unsigned long long* __restrict__ aux) {
   sig->ds = *ds;
+  sig->aux = *aux;
   __threadfence_system();
   *(volatile unsigned*)&sig->seq = seq;
 }
@@ -714,27 +763,42 @@ __global__ void signal_kernel(const DevState* ds, Workspace::Signal* sig,
 // Same result as read_state, lower latency: a one-thread kernel queued after
 // the level's work publishes DevState into mapped host memory and the host
 // spins on the sequence number (no cudaMemcpyAsync + stream synchronise).
-int read_state_fast(Workspace* w, cudaStream_t s) {
+int post_signal(Workspace* w, cudaStream_t s, unsigned* seq_out) {
   const unsigned seq = ++w->seq;
-  signal_kernel<<<1, 1, 0, s>>>(w->ds, w->d_sig, seq);
+  signal_kernel<<<1, 1, 0, s>>>(w->ds, w->d_sig, seq, w->d_scratch + 1);
   DP_CUDA(cudaGetLastError());
+  *seq_out = seq;
+  return 0;
+}
+
+// wait until signal `seq` has landed; h_ds then holds the state after every
+// kernel queued before that signal
+int wait_signal(Workspace* w, cudaStream_t s, unsigned seq) {
   volatile unsigned* flag = &w->h_sig->seq;
-  for (unsigned spin = 1; *flag != seq; ++spin) {
+  auto landed = [&] { return *flag == seq; };
+  for (unsigned spin = 1; !landed(); ++spin) {
     if ((spin & 1023) == 0) {
       const cudaError_t e = cudaStreamQuery(s);
       if (e != cudaSuccess && e != cudaErrorNotReady)
         return fail(DP_ERR_CUDA, std::string("cuda-error: ") +
                                      cudaGetErrorString(e));
-      if (e == cudaSuccess && *flag != seq) break;  // drained: re-check below
+      if (e == cudaSuccess && !landed()) break;  // drained: re-check below
     }
   }
   __atomic_thread_fence(__ATOMIC_ACQUIRE);
-  if (w->h_sig->seq != seq) {  // stream drained without the signal: fall back
+  if (!landed()) {  // stream drained without the signal: fall back
     DP_CUDA(cudaStreamSynchronize(s));
   }
   std::memcpy((void*)w->h_ds, (const void*)&w->h_sig->ds, sizeof(DevState));
   if (w->h_ds->err) return map_device_error(w->h_ds->err);
   return check_published(w);
+}
+
+int read_state_fast(Workspace* w, cudaStream_t s) {
+  unsigned seq = 0;
+  int r;
+  if ((r = post_signal(w, s, &seq))) return r;
+  return wait_signal(w, s, seq);
 }
 
 int read_state(Workspace* w, cudaStream_t s) {
@@ -869,7 +933,7 @@ template <class MakeApp, class Finish = NoFinish, class Pick = AlwaysCdp>
 int iterate(Workspace* w, const dp_config* c, long long nparents,
             long long launchers, int max_iter, cudaStream_t s, MakeApp make,
             dp_stats* st, Arrival* arr = nullptr, Finish finish = Finish(),
-            Pick pick = Pick()) {
+            Pick pick = Pick(), long long lazy_bound = -1) {
   // a level in which no parent can reach the threshold runs the launch-free
   // parent variant: same serial arm, same outputs and counters, but without
   // the ~11 us a CDP-capable parent grid costs even when it launches nothing
@@ -878,15 +942,25 @@ int iterate(Workspace* w, const dp_config* c, long long nparents,
   c_flat.variant = DP_VARIANT_NOCDP;
   RunCounters rc;
   int r;
-  if ((r = ensure_pending_limit(w, c, launch_bound(c, nparents, launchers))))
+  // lazy_bound >= 0 (count_launchers_lazy): `launchers` is an upper bound,
+  // the pool bound is lazy_bound (one wave), and the exact count arrives
+  // with round 0's readback; until then round 0 keeps the launching variant
+  // (same outputs and counters either way)
+  long long exact = lazy_bound >= 0 ? -1 : launchers;
+  const long long wave_launchers = lazy_bound >= 0 ? 0 : launchers;
+  if ((r = ensure_pending_limit(w, c,
+                                lazy_bound >= 0
+                                    ? lazy_bound
+                                    : launch_bound(c, nparents, launchers))))
     return r;
   if ((r = begin_run(w, s))) return r;
   DP_CUDA(cudaEventRecord(w->ev0, s));
   int it = 0;
   bool converged = false;
+  bool fresh = false;  // h_ds holds the state after the last kernel
   if (c->device_loop && c->variant == DP_VARIANT_CDP && !arr &&
       c->agg != DP_AGG_GRID &&
-      wave_parents(c, nparents, launchers) == nparents) {
+      wave_parents(c, nparents, wave_launchers) == nparents) {
     if ((r = device_loop(w, c, nparents, max_iter, s, make(0, w->ds), &rc,
                          &it, &converged)))
       return r;
@@ -896,7 +970,7 @@ int iterate(Workspace* w, const dp_config* c, long long nparents,
     // no parent can ever reach the threshold (an exact launcher count of 0,
     // e.g. road graphs below T): every level runs launch-free
     const dp_config* cl = c->variant == DP_VARIANT_CDP &&
-                                  (launchers == 0 || !pick(it, w->h_ds))
+                                  (exact == 0 || !pick(it, w->h_ds))
                               ? &c_flat
                               : c;
     // chunks known to have landed before this round starts (it sees them)
@@ -910,8 +984,11 @@ int iterate(Workspace* w, const dp_config* c, long long nparents,
       if (cudaPeekAtLastError() == cudaErrorNotReady) (void)cudaGetLastError();
       break;
     }
-    if ((r = launch_parent(app, nparents, launchers, cl, w, s, &rc))) return r;
+    if ((r = launch_parent(app, nparents, wave_launchers, cl, w, s, &rc)))
+      return r;
     if ((r = read_state_fast(w, s))) return r;
+    fresh = true;
+    if (exact < 0) exact = (long long)w->h_sig->aux;
     if ((r = account_step(w, &rc))) return r;
     if (w->h_ds->flag[it & 1] == 0 &&
         (!arr || w->h_ds->skipped[it & 1] == 0)) {
@@ -946,7 +1023,9 @@ int iterate(Workspace* w, const dp_config* c, long long nparents,
   DP_CUDA(cudaEventSynchronize(w->ev1));
   float ms = 0.f;
   DP_CUDA(cudaEventElapsedTime(&ms, w->ev0, w->ev1));
-  if ((r = read_state(w, s))) return r;
+  // the epilogue kernels never touch DevState: the last round's readback
+  // is already the final state (saves a copy + synchronise per call)
+  if (!fresh && (r = read_state(w, s))) return r;
   if (rc.ms_kernel_sum == 0.0) {  // device loop: no per-level host events
     rc.ms_kernel_sum = ms;
     rc.ms_kernel_max = ms;
@@ -979,7 +1058,8 @@ __global__ void launch_bits_kernel(const int* __restrict__ rowptr, int n,
 
 int bfs_dev_impl(const int32_t* rowptr, const int32_t* col, int32_t n,
                  int32_t src, const dp_config* c, int32_t* dist,
-                 int32_t* counts, cudaStream_t s, dp_stats* st) {
+                 int32_t* counts, cudaStream_t s, dp_stats* st,
+                 int64_t m = -1) {
   int r;
   if ((r = validate(c))) return r;
   if (n < 1) return fail(DP_ERR_INVALID, "graph must have at least 1 vertex");
@@ -1002,9 +1082,9 @@ int bfs_dev_impl(const int32_t* rowptr, const int32_t* col, int32_t n,
   } else {
     DP_CUDA(cudaMemsetAsync(counts, 0, (size_t)n * sizeof(int), s));
   }
-  long long launchers = 0;
+  long long launchers = 0, lazy = -1;
   if (c->variant == DP_VARIANT_CDP &&
-      (r = count_launchers(w, c, rowptr, n, 0, s, &launchers)))
+      (r = count_launchers_lazy(w, c, rowptr, n, m, s, &launchers, &lazy)))
     return r;
   // launch bits: the host picks each level's parent variant from whether the
   // previous level discovered any vertex whose row would launch
@@ -1047,7 +1127,8 @@ int bfs_dev_impl(const int32_t* rowptr, const int32_t* col, int32_t n,
                  [&](int level, const DevState* h) {
                    // level 0 (the source alone) keeps the launching variant
                    return !per_level || level == 0 || h->big[level & 1] != 0;
-                 });
+                 },
+                 lazy);
 }
 
 // Pack int32 weights into nibbles (w - 1, 8 per word); *bad = 1 if any
@@ -1140,7 +1221,7 @@ int sssp_dev_impl(const int32_t* rowptr, const int32_t* col,
                   const int32_t* weight, int32_t n, int32_t src,
                   const dp_config* c, int32_t* dist, cudaStream_t s,
                   dp_stats* st, Arrival* arr = nullptr, int shift = 0,
-                  const unsigned* wpack = nullptr) {
+                  const unsigned* wpack = nullptr, int64_t m = -1) {
   int r;
   if ((r = validate(c))) return r;
   if (n < 1) return fail(DP_ERR_INVALID, "graph must have at least 1 vertex");
@@ -1155,13 +1236,14 @@ int sssp_dev_impl(const int32_t* rowptr, const int32_t* col,
     last = (int*)w->io[5];
     fill_kernel<int><<<dp::ceil_div(n, 256), 256, 0, s>>>(last, n, kUnreached);
   }
-  long long launchers = 0;
+  long long launchers = 0, lazy = -1;
   if (c->variant == DP_VARIANT_CDP &&
-      (r = count_launchers(w, c, rowptr, n, 0, s, &launchers)))
+      (r = count_launchers_lazy(w, c, rowptr, n, m, s, &launchers, &lazy)))
     return r;
   // bench/benchmarks.py:259-270: rounds until a full round changes nothing
   // (and, while edges are still landing, no parent was deferred)
   const int max_iter = n + (arr ? arr->nchunks + 1 : 0);
+
   auto run = [&](auto tag) {
     using App = decltype(tag);
     return iterate(w, c, n, launchers, max_iter, s,
@@ -1182,7 +1264,7 @@ int sssp_dev_impl(const int32_t* rowptr, const int32_t* col,
                      a.shift = shift;
                      return a;
                    },
-                   st, arr);
+                   st, arr, NoFinish(), AlwaysCdp(), lazy);
   };
   return wpack ? run(SsspPackedApp{}) : run(SsspApp{});
 }
@@ -2772,7 +2854,7 @@ int dp_bfs(const int32_t* rowptr, const int32_t* col, int32_t n, int64_t m,
   DP_TRY(stage(w_, 2, nullptr, (size_t)n * 4, s_, &h2d_));
   DP_TRY(stage(w_, 3, nullptr, (size_t)n * 4, s_, &h2d_));
   DP_TRY(bfs_dev_impl((int*)w_->io[0], (int*)w_->io[1], n, src, cfg,
-                      (int*)w_->io[2], (int*)w_->io[3], s_, stats));
+                      (int*)w_->io[2], (int*)w_->io[3], s_, stats, m));
   DP_TRY(unstage(w_, 2, dist, (size_t)n * 4, s_, &d2h_));
   DP_TRY(unstage(w_, 3, counts, (size_t)n * 4, s_, &d2h_));
   DP_HOST_CALL_END
@@ -2782,10 +2864,9 @@ int dp_bfs_dev(const int32_t* d_rowptr, const int32_t* d_col, int32_t n,
                int64_t m, int32_t src, const dp_config* cfg, int32_t* d_dist,
                int32_t* d_counts, void* stream, dp_stats* stats) {
   clear_stats(stats);
-  (void)m;
   const double t0 = now_ns();
   int r = bfs_dev_impl(d_rowptr, d_col, n, src, cfg, d_dist, d_counts,
-                       (cudaStream_t)stream, stats);
+                       (cudaStream_t)stream, stats, m);
   if (stats) stats->ns_host = now_ns() - t0;
   return r;
 }
@@ -2801,7 +2882,8 @@ int dp_sssp(const int32_t* rowptr, const int32_t* col, const int32_t* weight,
     DP_TRY(stage(w_, 1, col, (size_t)m * 4, s_, &h2d_));
     DP_TRY(stage(w_, 4, weight, (size_t)m * 4, s_, &h2d_));
     DP_TRY(sssp_dev_impl((int*)w_->io[0], (int*)w_->io[1], (int*)w_->io[4],
-                         n, src, cfg, (int*)w_->io[2], s_, stats));
+                         n, src, cfg, (int*)w_->io[2], s_, stats, nullptr, 0,
+                         nullptr, m));
   } else {
     // rounds start as soon as rowptr has landed; col / weight stream in
     // behind them in chunks and parents whose edges are still in flight
@@ -2833,7 +2915,7 @@ int dp_sssp(const int32_t* rowptr, const int32_t* col, const int32_t* weight,
     const int rs = sssp_dev_impl((int*)w_->io[0], (int*)w_->io[1],
                                  (int*)w_->io[4], n, src, cfg,
                                  (int*)w_->io[2], s_, stats, &arr, shift,
-                                 wpack);
+                                 wpack, m);
     DP_TRY(join_chunked(w_, s_, arr));
     if (rs) {
       cudaStreamSynchronize(s_);
@@ -2866,7 +2948,7 @@ int dp_sssp_dev(const int32_t* d_rowptr, const int32_t* d_col,
       return r;
   }
   r = sssp_dev_impl(d_rowptr, d_col, d_weight, n, src, cfg, d_dist,
-                    (cudaStream_t)stream, stats, nullptr, 0, wpack);
+                    (cudaStream_t)stream, stats, nullptr, 0, wpack, m);
   if (stats) stats->ns_host = now_ns() - t0;
   return r;
 }

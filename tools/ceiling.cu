@@ -285,6 +285,138 @@ __global__ void visit_spread(const int* __restrict__ col, long long m,
     *changed = 1;
 }
 
+// rank of v among the vertices with popcount(v) <= kmax (kmax <= 4, 22-bit
+// ids): 0 for v = 0, then the 1-bit ids, the 2-bit ids ... (combinatorial
+// number system); -1 when popcount(v) > kmax
+__device__ __forceinline__ int hub_rank(unsigned v, int kmax) {
+  const int k = __popc(v);
+  if (k > kmax) return -1;
+  // offsets: sum_{i<k} C(22, i) = 0, 1, 23, 254, 1794
+  int idx = k == 0 ? 0 : k == 1 ? 1 : k == 2 ? 23 : k == 3 ? 254 : 1794;
+  for (int j = 1; j <= k; ++j) {
+    const int p = __ffs(v) - 1;
+    v &= v - 1;
+    int c = p;  // C(p, j)
+    if (j >= 2) c = c * (p - 1) / 2;
+    if (j >= 3) c = c * (p - 2) / 3;
+    if (j >= 4) c = c * (p - 3) / 4;
+    idx += c;
+  }
+  return idx;
+}
+
+// visit_spread with the hub counters (popcount(v) <= kmax) replicated R ways
+// (replica picked by the global warp id, replicas 8 KB apart so they sit in
+// distinct lines / L2 slices)
+__global__ void visit_hubrep(const int* __restrict__ col, long long m,
+                             int* dist, int* counts, int* rep, int kmax,
+                             int rbits, int level, int* changed) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long nit = (m + stride * 2 - 1) / (stride * 2);
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = (int)((t >> 5) & ((1 << rbits) - 1));
+  int ch = 0;
+  for (long long it = 0; it < nit; ++it) {
+    int v[2], d[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const long long e = t + (it * 2 + j) * stride;
+      v[j] = e < m ? ld_stream(col + e) : -1;
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) d[j] = v[j] >= 0 ? __ldca(dist + v[j]) : 0;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const unsigned g = __match_any_sync(FULL, v[j]);
+      if (v[j] < 0) continue;
+      if ((threadIdx.x & 31) == __ffs(g) - 1) {
+        const int h = hub_rank((unsigned)v[j], kmax);
+        int* a = h >= 0 ? rep + (r << 11) + h
+                        : counts + spread_slot((uint32_t)v[j], 4095u);
+        atomicAdd(a, __popc(g));
+      }
+      if (d[j] == kUnreached &&
+          atomicCAS(dist + v[j], kUnreached, level + 1) == kUnreached)
+        ch = 1;
+    }
+  }
+  if (__any_sync(FULL, ch) && (threadIdx.x & 31) == 0 && __ldcg(changed) == 0)
+    *changed = 1;
+}
+
+// the visit without the counts (probe + CAS only): what counts cost
+__global__ void visit_nocount(const int* __restrict__ col, long long m,
+                              int* dist, int level, int* changed) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long nit = (m + stride * 2 - 1) / (stride * 2);
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  int ch = 0;
+  for (long long it = 0; it < nit; ++it) {
+    int v[2], d[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const long long e = t + (it * 2 + j) * stride;
+      v[j] = e < m ? ld_stream(col + e) : -1;
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) d[j] = v[j] >= 0 ? __ldca(dist + v[j]) : 0;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      if (v[j] < 0) continue;
+      if (d[j] == kUnreached &&
+          atomicCAS(dist + v[j], kUnreached, level + 1) == kUnreached)
+        ch = 1;
+    }
+  }
+  if (__any_sync(FULL, ch) && (threadIdx.x & 31) == 0 && __ldcg(changed) == 0)
+    *changed = 1;
+}
+
+__global__ void fill_hi(unsigned long long* w, long long n) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) w[i] = i == 0 ? 0ull : (unsigned long long)kUnreached << 32;
+}
+
+// counts and dist fused in one 64-bit word per vertex (hi = dist, lo =
+// count): the merged count's ATOM.ADD returns the old word, whose hi half
+// replaces the dist probe; the first discoverer CASes the hi half
+__global__ void visit_fused64(const int* __restrict__ col, long long m,
+                              unsigned long long* word, unsigned mask,
+                              int level, int* changed) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long nit = (m + stride * 2 - 1) / (stride * 2);
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  int ch = 0;
+  for (long long it = 0; it < nit; ++it) {
+    int v[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const long long e = t + (it * 2 + j) * stride;
+      v[j] = e < m ? ld_stream(col + e) : -1;
+    }
+    unsigned long long old[2];
+    bool lead[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const unsigned g = __match_any_sync(FULL, v[j]);
+      lead[j] = v[j] >= 0 && (threadIdx.x & 31) == __ffs(g) - 1;
+      old[j] = lead[j] ? atomicAdd(word + spread_slot((uint32_t)v[j], mask),
+                                   (unsigned long long)__popc(g))
+                       : 0ull;
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      if (lead[j] && (int)(old[j] >> 32) == kUnreached) {
+        int* hi = reinterpret_cast<int*>(
+                      word + spread_slot((uint32_t)v[j], mask)) + 1;
+        if (atomicCAS(hi, kUnreached, level + 1) == kUnreached) ch = 1;
+      }
+    }
+  }
+  if (__any_sync(FULL, ch) && (threadIdx.x & 31) == 0 && __ldcg(changed) == 0)
+    *changed = 1;
+}
+
 int ceil_run(int which, const int* col, const int* w, long long m, int* dist,
              int* counts, uint32_t nmask, int grid, int block, int* scratch,
              cudaStream_t s) {
@@ -308,6 +440,33 @@ int ceil_run(int which, const int* col, const int* w, long long m, int* dist,
     case 12: visit_spread<<<grid, block, 0, s>>>(col, m, dist, counts, 0,
                                                  scratch);
              break;
+    case 13: {
+      static int* rep = nullptr;
+      if (!rep && cudaMalloc(&rep, (32 << 11) * sizeof(int))) return -2;
+      cudaMemsetAsync(rep, 0, (32 << 11) * sizeof(int), s);
+      visit_hubrep<<<grid, block, 0, s>>>(col, m, dist, counts, rep,
+                                          (int)(nmask >> 8), (int)(nmask & 0xff),
+                                          0, scratch);
+      break;
+    }
+    case 14: visit_nocount<<<grid, block, 0, s>>>(col, m, dist, 0, scratch);
+             break;
+    case 15:
+    case 16: {
+      static unsigned long long* word = nullptr;
+      static long long have = 0;
+      const long long n = (long long)nmask + 1;
+      if (have < n) {
+        if (word) cudaFree(word);
+        if (cudaMalloc(&word, n * 8)) return -2;
+        have = n;
+      }
+      fill_hi<<<(int)((n + 255) / 256), 256, 0, s>>>(word, n);
+      visit_fused64<<<grid, block, 0, s>>>(col, m, word,
+                                           which == 16 ? 4095u : 0u, 0,
+                                           scratch);
+      break;
+    }
     default: return -1;
   }
   return (int)cudaGetLastError();

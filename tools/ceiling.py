@@ -34,7 +34,9 @@ def build():
 NAMES = {0: "stream_col", 1: "stream_col_int4", 2: "red_uniform",
          3: "red_targets", 4: "red_merged", 5: "probe_targets",
          6: "visit_flat", 7: "relax_flat", 8: "cas_uniform", 9: "red_hashed",
-         10: "red_single_address", 11: "red_one_line", 12: "visit_spread"}
+         10: "red_single_address", 11: "red_one_line", 12: "visit_spread",
+         13: "visit_hubrep", 14: "visit_nocount",
+         15: "visit_fused64", 16: "visit_fused64_spread"}
 
 
 def main():
@@ -56,6 +58,8 @@ def main():
     hbm = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] \
         if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
     out = {"scale": scale, "n": n, "m": m, "sms": sms, "hbm_gbs": hbm}
+    hubrep = [int(x) for x in __import__("os").environ.get(
+        "HUBREP", "3:4").split(":")]  # kmax : log2 replicas
     for which in only:
         best = None
         for blocks_per_sm, block in ((8, 256), (16, 128), (4, 512)):
@@ -63,7 +67,7 @@ def main():
             ts = []
             for it in range(6):
                 G.counts.zero_()
-                if which in (6, 12):
+                if which in (6, 12, 13, 14):
                     G.dist.fill_(1 << 30)
                     G.dist[0] = 0
                 elif which == 7:
@@ -74,7 +78,9 @@ def main():
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record(s)
                 rc = L.ceil_run(which, p(G.col), p(G.weight), m, p(G.dist),
-                                p(G.counts), nmask, grid, block, p(scratch), sp)
+                                p(G.counts),
+                                (hubrep[0] << 8 | hubrep[1]) if which == 13
+                                else nmask, grid, block, p(scratch), sp)
                 e1.record(s)
                 torch.cuda.synchronize()
                 assert rc == 0, rc
@@ -85,7 +91,8 @@ def main():
                 best = (t, grid, block)
         t, grid, block = best
         ops = m if which != 1 else m
-        r = {"kernel": NAMES[which], "ms": t, "grid": grid, "block": block,
+        r = {"kernel": NAMES[which] + (f" k<={hubrep[0]} R={1 << hubrep[1]}"
+                                       if which == 13 else ""), "ms": t, "grid": grid, "block": block,
              "g_ops_per_s": ops / t / 1e6}
         if which in (0, 1):
             r["gbps"] = 4 * m / t / 1e6
