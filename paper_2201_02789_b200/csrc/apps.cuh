@@ -44,6 +44,9 @@ namespace dp {
 #ifndef DP_SP_MINB
 #define DP_SP_MINB 1
 #endif
+#ifndef DP_SP_UNROLL
+#define DP_SP_UNROLL 1  // SP items in flight per thread (variable / ratio)
+#endif
 #ifndef DP_SP_RATIO_MINB
 #define DP_SP_RATIO_MINB 1
 #endif
@@ -1385,7 +1388,8 @@ struct MstVerifyApp {
 // synchronous sweep of the surveys eta (Braunstein, Mezard, Zecchina 2005):
 //   SpVarApp    parent = variable i, child item = occurrence e of i:
 //               P_s(i) *= (1 - eta[e]) for the occurrence's sign s, zero
-//               factors counted apart (so one factor can be divided out)
+//               factors counted apart (so one factor can be divided out);
+//               run once per L2 window of eta (below)
 //   SpRatioApp  parent = clause a, child item = edge e = (a, i):
 //               ratio[e] = Pu / (Pu + Ps + P0), S = P_s(i) / (1 - eta[e])
 //               (a excluded), U = P_-s(i), Pu = (1-U) S, Ps = (1-S) U, P0 = SU
@@ -1395,6 +1399,14 @@ struct MstVerifyApp {
 // Only the variable pass gathers (eta by occurrence): measured on 5-SAT,
 // a variable-major ratio pass costs 3.2 GB of DRAM per sweep (random eta
 // gathers + ratio scatters, ~64 B per 8 B access) against ~0.5 GB here.
+// The gather is windowed: the variable pass runs once per slice of the edge
+// (= eta) index space small enough to stay in L2, each parent taking only
+// its occurrences inside the slice (a variable's occurrence list is sorted
+// by edge, so a slice is a sub-range: seg_lo / seg_hi).  One pass over the
+// whole 160 MB eta of 5-SAT 200k read 1.92 GB of DRAM (L2 hit 32 %,
+// profiles/ncu_full_sp_ksat5_r01.json).  Scattering variable-major factors
+// from the clause pass instead was measured slower (5-SAT 20.9 vs 19.5 ms,
+// 3-SAT 14.8 vs 11.9 ms: partial-sector writes cost more than the gathers).
 // Arithmetic and storage in fp64 (explicit round-to-nearest ops, no FMA
 // contraction, as the CPU oracle does).  The product order of P_s depends on
 // the schedule, so results match the oracle within a tolerance, not
@@ -1403,9 +1415,11 @@ struct MstVerifyApp {
 // surveys by 0.08 after 10 sweeps), so fp32 rounding flips would not stay
 // within tolerance; fp64 order effects (~1e-16) do.
 // ---------------------------------------------------------------------------
-struct SpVarProd {
+// 32 B: the ratio pass fetches a variable's record with one 256-bit load
+struct alignas(16) SpVarProd {
   double p[2];  // product of the non-zero (1 - eta) factors, per sign
   int z[2];     // zero factors, per sign
+  int pad[2];
 };
 
 __device__ __forceinline__ void atomic_mul_f64(double* addr, double f) {
@@ -1419,8 +1433,9 @@ __device__ __forceinline__ void atomic_mul_f64(double* addr, double f) {
 }
 
 struct SpVarApp {
-  const int* __restrict__ occ_row;
-  const int* __restrict__ occs;  // e << 1 | negated
+  const int* __restrict__ seg_lo;  // variable i's occurrences in this
+  const int* __restrict__ seg_hi;  // window: occs[seg_lo[i], seg_hi[i])
+  const int* __restrict__ occs;    // sp_tile(e) << 1 | negated
   const double* __restrict__ eta;
   SpVarProd* prod;
   int nvars;
@@ -1444,8 +1459,8 @@ struct SpVarApp {
   __device__ void parent_prologue() const {}
   __device__ int expand(int i, bool valid, Args& a) const {
     if (!valid) return 0;
-    const int s = __ldg(occ_row + i);
-    const int d = __ldg(occ_row + i + 1) - s;
+    const int s = __ldg(seg_lo + i);
+    const int d = __ldg(seg_hi + i) - s;
     a = Args{s, d, i, 0};
     return d > 0 ? d : 0;
   }
@@ -1476,7 +1491,7 @@ struct SpVarApp {
     else
       acc.p[neg] = __dmul_rn(acc.p[neg], f);
   }
-  static constexpr int kUnroll = 1;
+  static constexpr int kUnroll = DP_SP_UNROLL;
   static constexpr bool kBlockMode = false;
   static constexpr bool kPureExpand = true;
   static constexpr int kMinBlocks = DP_SP_MINB;
@@ -1524,11 +1539,23 @@ __device__ __forceinline__ double sp_ratio(const double* p, const int* z,
   return den > 0.0 ? __ddiv_rn(pu, den) : 0.0;
 }
 
+// Clause-tiled edge layout of lit / eta / ratio on the device: literal j of
+// clause a at ((a >> 5) k + j) 32 + (a & 31).  With the serial arm in thread
+// mode a lane owns one clause, so the 32 lanes of a warp read literal j of
+// 32 consecutive clauses: one coalesced 128 B (int) / 256 B (double) access
+// instead of 32 accesses at a k-element stride (clause-major: L1 throughput
+// 89 % for 18 % DRAM in the ratio pass, profiles/r02/ncu_full_sp_window_r02.json).
+// The caller's clause-major eta is tiled on entry and untiled on exit.
+__host__ __device__ __forceinline__ long long sp_tile(long long a, int j,
+                                                      int k) {
+  return (((a >> 5) * k + j) << 5) + (a & 31);
+}
+
 struct SpRatioApp {
-  const int* __restrict__ lit;
-  const double* __restrict__ eta;
-  const SpVarProd* __restrict__ prod;  // L2-resident (24 B per variable)
-  double* ratio;                       // [edges], clause-major
+  const int* __restrict__ lit;         // clause-tiled (sp_tile)
+  const double* __restrict__ eta;      // clause-tiled
+  const SpVarProd* __restrict__ prod;  // L2-resident (32 B per variable)
+  double* __restrict__ ratio;          // clause-tiled
   int nclauses;
   int k;
 
@@ -1546,14 +1573,19 @@ struct SpRatioApp {
   }
   __device__ static int count(const Args& r) { return r.k; }
   __device__ void item(const Args& r, int t, Acc&) const {
-    const long long e = (long long)r.a * r.k + t;
+    const long long e = sp_tile(r.a, t, r.k);
     const int l = ld_stream(lit + e);
-    const SpVarProd* q = prod + (l >> 1);
-    const double p[2] = {__ldcg(&q->p[0]), __ldcg(&q->p[1])};
-    const int z[2] = {__ldcg(&q->z[0]), __ldcg(&q->z[1])};
+    // the variable's 32 B record in one 256-bit L2 load (sm_100)
+    unsigned long long q0, q1, q2, q3;
+    asm("ld.global.cg.v4.b64 {%0, %1, %2, %3}, [%4];"
+        : "=l"(q0), "=l"(q1), "=l"(q2), "=l"(q3)
+        : "l"(prod + (l >> 1)));
+    (void)q3;
+    const double p[2] = {__longlong_as_double(q0), __longlong_as_double(q1)};
+    const int z[2] = {(int)(unsigned)q2, (int)(unsigned)(q2 >> 32)};
     ratio[e] = sp_ratio(p, z, l & 1, __ldg(eta + e));
   }
-  static constexpr int kUnroll = 1;
+  static constexpr int kUnroll = DP_SP_UNROLL;
   static constexpr bool kBlockMode = false;
   static constexpr bool kPureExpand = true;
   static constexpr int kMinBlocks = DP_SP_RATIO_MINB;
@@ -1589,14 +1621,14 @@ struct SpClauseApp {
   }
   __device__ static int count(const Args& r) { return r.k; }
   __device__ void item(const Args& r, int t, Acc& acc) const {
-    const long long base = (long long)r.a * r.k;
+    const long long base = sp_tile(r.a, 0, r.k);  // literal j at base + 32 j
     double v = 1.0;
     for (int j = 0; j < r.k; ++j)  // fixed order: the oracle's
-      if (j != t) v = __dmul_rn(v, __ldg(ratio + base + j));
+      if (j != t) v = __dmul_rn(v, __ldg(ratio + base + 32 * j));
     const float d =
-        __double2float_ru(fabs(__dsub_rn(v, __ldg(eta + base + t))));
+        __double2float_ru(fabs(__dsub_rn(v, __ldg(eta + base + 32 * t))));
     acc.delta = fmaxf(acc.delta, d);
-    eta_next[base + t] = v;
+    eta_next[base + 32 * t] = v;
   }
   static constexpr int kUnroll = 1;
   static constexpr bool kBlockMode = false;

@@ -1589,19 +1589,73 @@ __global__ void sp_reset_kernel(int n, SpVarProd* prod) {
     SpVarProd q;
     q.p[0] = q.p[1] = 1.0;
     q.z[0] = q.z[1] = 0;
+    q.pad[0] = q.pad[1] = 0;
     prod[i] = q;
   }
 }
 
-// occs[t] = occ[t] << 1 | negated (the variable side reads signs in order)
-__global__ void sp_pack_kernel(long long ne, const int* __restrict__ occ,
+// occs[t] = sp_tile(occ[t]) << 1 | negated (the variable side reads signs
+// in order)
+__global__ void sp_pack_kernel(long long ne, int k,
+                               const int* __restrict__ occ,
                                const int* __restrict__ lits, int* occs) {
   for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < ne;
        t += (long long)gridDim.x * blockDim.x) {
     const int e = occ[t];
-    occs[t] = (e << 1) | (lits[e] & 1);
+    occs[t] = (int)(sp_tile(e / k, e % k, k) << 1) | (lits[e] & 1);
   }
 }
+
+// clause-major <-> clause-tiled (sp_tile) copies of lit and eta
+__global__ void sp_tile_kernel(long long ne, int k,
+                               const int* __restrict__ lits,
+                               const double* __restrict__ eta, int* lit_t,
+                               double* eta_t) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < ne;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long d = sp_tile(e / k, (int)(e % k), k);
+    lit_t[d] = lits[e];
+    eta_t[d] = eta[e];
+  }
+}
+
+__global__ void sp_untile_kernel(long long ne, int k,
+                                 const double* __restrict__ eta_t,
+                                 double* eta) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < ne;
+       e += (long long)gridDim.x * blockDim.x)
+    eta[e] = eta_t[sp_tile(e / k, (int)(e % k), k)];
+}
+
+// Interior window bounds of the variable pass: seg[(w-1) n + i] = first
+// occurrence of variable i whose edge is >= w * wsize (lists sorted by edge;
+// a list that is not sets *unsorted and the caller runs one window)
+__global__ void sp_window_kernel(int n, int nwin, long long wsize,
+                                 const int* __restrict__ occ_row,
+                                 const int* __restrict__ occ, int* seg,
+                                 int* unsorted) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int s = occ_row[i], e = occ_row[i + 1];
+    bool ok = true;
+    for (int t = s + 1; t < e; ++t) ok &= occ[t - 1] <= occ[t];
+    if (!ok) atomicOr(unsorted, 1);
+    int lo = s;
+    for (int w = 1; w < nwin; ++w) {
+      const long long b = (long long)w * wsize;
+      int hi = e;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (occ[mid] < b) lo = mid + 1; else hi = mid;
+      }
+      seg[(long long)(w - 1) * n + i] = lo;
+    }
+  }
+}
+
+#ifndef DP_SP_WINDOW_MB
+#define DP_SP_WINDOW_MB 96  // eta slice per variable pass (L2: 126 MB)
+#endif
 
 // W+ = Pi+ / (Pi+ + Pi- + Pi0), W- likewise, with P+ / P- the products of
 // (1 - eta) over the positive / negative occurrences:
@@ -1635,16 +1689,31 @@ int sp_dev_impl(const int32_t* lits, int32_t k, int32_t nclauses,
   if (!w) return r;
   const long long ne = (long long)nclauses * k;
   if (ne >= (1LL << 30)) return fail(DP_ERR_INVALID, "too many edges");
-  // prod[nvars] | eta scratch[ne] | ratio[ne] | occs[ne]
+  // L2 windows of the variable pass's eta gather
+  long long win_mb = DP_SP_WINDOW_MB;
+  if (const char* env = std::getenv("DYNPAR_SP_WINDOW_MB"))  // A/B; 0: off
+    win_mb = std::atoll(env);
+  int nwin = win_mb > 0 ? (int)std::min<long long>(
+                              16, std::max<long long>(
+                                      1, dp::ceil_div_ll(ne * 8, win_mb << 20)))
+                        : 1;
+  // prod[nvars] | eta_t x 2 [nt] | ratio[nt] | lit_t[nt] | occs[ne] |
+  // seg[nwin-1][nv]; nt = the clause-tiled size (clauses padded to 32)
   const size_t nv = (size_t)std::max(nvars, 1);
   const size_t nes = (size_t)std::max(ne, 1LL);
+  const size_t nt = (size_t)std::max(
+      dp::ceil_div_ll(std::max(nclauses, 1), 32) * 32 * k, 1LL);
   if ((r = grow(&w->io[5], &w->io_bytes[5],
-                nv * sizeof(SpVarProd) + nes * (8 + 8 + 4))))
+                nv * sizeof(SpVarProd) + nt * (8 + 8 + 8 + 4) + nes * 4 +
+                    (size_t)(nwin - 1) * nv * 4)))
     return r;
   SpVarProd* prod = (SpVarProd*)w->io[5];
-  double* eta_b = (double*)(prod + nv);
-  double* ratio = eta_b + nes;
-  int* occs = (int*)(ratio + nes);
+  double* eta_a = (double*)(prod + nv);
+  double* eta_b = eta_a + nt;
+  double* ratio = eta_b + nt;
+  int* lit_t = (int*)(ratio + nt);
+  int* occs = lit_t + nt;
+  int* seg = occs + nes;
   long long lv = 0;
   if (c->variant == DP_VARIANT_CDP &&
       (r = count_launchers(w, c, occ_row, nvars, 0, s, &lv)))
@@ -1660,14 +1729,30 @@ int sp_dev_impl(const int32_t* lits, int32_t k, int32_t nclauses,
                                       148 * 8));
   RunCounters rc;
   DP_CUDA(cudaEventRecord(w->ev0, s));
+  const int eb = (int)std::min<long long>(
+      dp::ceil_div_ll(std::max(ne, 1LL), 256), 148 * 8);
   if (ne) {
-    sp_pack_kernel<<<(int)std::min<long long>(dp::ceil_div_ll(ne, 256),
-                                              148 * 8),
-                     256, 0, s>>>(ne, occ, lits, occs);
+    sp_pack_kernel<<<eb, 256, 0, s>>>(ne, k, occ, lits, occs);
+    DP_CUDA(cudaGetLastError());
+    sp_tile_kernel<<<eb, 256, 0, s>>>(ne, k, lits, eta, lit_t, eta_a);
+    DP_CUDA(cudaGetLastError());
+    rc.kernel_launches += 2;
+  }
+  // window bounds on 32-clause tile boundaries: edge e < w * wsize exactly
+  // when its tiled index is below the window's tiled start
+  const long long wsize =
+      dp::ceil_div_ll(dp::ceil_div_ll(std::max(nclauses, 1), 32), nwin) * 32 *
+      k;
+  if (nwin > 1) {
+    DP_CUDA(cudaMemsetAsync(&w->ds->flag[1], 0, sizeof(int), s));
+    sp_window_kernel<<<vb, 256, 0, s>>>(nvars, nwin, wsize, occ_row, occ, seg,
+                                        &w->ds->flag[1]);
     DP_CUDA(cudaGetLastError());
     rc.kernel_launches += 1;
+    if ((r = read_state_fast(w, s))) return r;
+    if (w->h_ds->flag[1]) nwin = 1;  // caller's lists not sorted by edge
   }
-  double* cur = eta;
+  double* cur = eta_a;
   double* nxt = eta_b;
   int sweeps = 0;
   float delta = 0.f;
@@ -1675,19 +1760,24 @@ int sp_dev_impl(const int32_t* lits, int32_t k, int32_t nclauses,
     sp_reset_kernel<<<vb, 256, 0, s>>>(nvars, prod);
     DP_CUDA(cudaGetLastError());
     rc.kernel_launches += 1;
-    SpVarApp va;
-    va.occ_row = occ_row;
-    va.occs = occs;
-    va.eta = e;
-    va.prod = prod;
-    va.nvars = nvars;
-    va.pad = 0;
-    return launch_parent(va, nvars, lv, c, w, s, &rc);
+    for (int win = 0; win < nwin; ++win) {
+      SpVarApp va;
+      va.seg_lo = win == 0 ? occ_row : seg + (size_t)(win - 1) * nv;
+      va.seg_hi = win == nwin - 1 ? occ_row + 1 : seg + (size_t)win * nv;
+      va.occs = occs;
+      va.eta = e;
+      va.prod = prod;
+      va.nvars = nvars;
+      va.pad = 0;
+      const int r2 = launch_parent(va, nvars, lv, c, w, s, &rc);
+      if (r2) return r2;
+    }
+    return 0;
   };
   while (sweeps < max_sweeps) {
     if ((r = var_pass(cur))) return r;
     SpRatioApp ra;
-    ra.lit = lits;
+    ra.lit = lit_t;
     ra.eta = cur;
     ra.prod = prod;
     ra.ratio = ratio;
@@ -1714,9 +1804,11 @@ int sp_dev_impl(const int32_t* lits, int32_t k, int32_t nclauses,
   sp_bias_kernel<<<vb, 256, 0, s>>>(nvars, prod, wpos, wneg);
   DP_CUDA(cudaGetLastError());
   rc.kernel_launches += 1;
-  if (cur != eta && ne)
-    DP_CUDA(cudaMemcpyAsync(eta, cur, (size_t)ne * 8,
-                            cudaMemcpyDeviceToDevice, s));
+  if (ne) {
+    sp_untile_kernel<<<eb, 256, 0, s>>>(ne, k, cur, eta);
+    DP_CUDA(cudaGetLastError());
+    rc.kernel_launches += 1;
+  }
   DP_CUDA(cudaEventRecord(w->ev1, s));
   DP_CUDA(cudaEventSynchronize(w->ev1));
   float ms = 0.f;

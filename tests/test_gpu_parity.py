@@ -607,6 +607,28 @@ def test_sp_vs_oracle_fixed_sweeps(spec):
     _sp_close(run_reference(bench, wl).arrays, want)
 
 
+@pytest.mark.parametrize("shuffle", [False, True])
+def test_sp_windowed_variable_pass(shuffle, monkeypatch):
+    """The variable pass runs once per L2 window of eta (1 MB windows: three
+    passes here); occurrence lists that are not sorted by edge fall back to
+    one window.  Surveys and biases stay within tolerance either way."""
+    monkeypatch.setenv("DYNPAR_SP_WINDOW_MB", "1")
+    bench, wl = load("sp", "ksat3:30000:seed3")
+    b = dict(wl.buffers, max_sweeps=12, eps=0.0)
+    if shuffle:
+        occ, row = b["occ"].copy(), b["occ_row"]
+        rng = np.random.default_rng(5)
+        for i in range(0, len(row) - 1, 7):
+            rng.shuffle(occ[row[i]:row[i + 1]])
+        b["occ"] = occ
+    wl = Workload(wl.spec, b, wl.n, wl.payload)
+    want = oracle.sp(wl.payload, b["eta0"], 12, 0.0)
+    for policy in SP_POLICIES:
+        rep, _ = run_config(bench, wl, BenchConfig(**policy))
+        assert rep.iterations == 12
+        _sp_close(rep.arrays, want)
+
+
 def test_sp_converges_like_oracle():
     bench, wl = load("sp", "ksat3:20000:seed1")
     want = oracle.sp(wl.payload, wl.buffers["eta0"],
