@@ -47,6 +47,9 @@ namespace dp {
 #ifndef DP_SP_UNROLL
 #define DP_SP_UNROLL 1  // SP items in flight per thread (variable / ratio)
 #endif
+#ifndef DP_SP_OCC_L1
+#define DP_SP_OCC_L1 1  // variable pass: L1-cached occurrence loads
+#endif
 #ifndef DP_SP_RATIO_MINB
 #define DP_SP_RATIO_MINB 1
 #endif
@@ -1399,12 +1402,16 @@ struct MstVerifyApp {
 // Only the variable pass gathers (eta by occurrence): measured on 5-SAT,
 // a variable-major ratio pass costs 3.2 GB of DRAM per sweep (random eta
 // gathers + ratio scatters, ~64 B per 8 B access) against ~0.5 GB here.
-// The gather is windowed: the variable pass runs once per slice of the edge
-// (= eta) index space small enough to stay in L2, each parent taking only
-// its occurrences inside the slice (a variable's occurrence list is sorted
-// by edge, so a slice is a sub-range: seg_lo / seg_hi).  One pass over the
-// whole 160 MB eta of 5-SAT 200k read 1.92 GB of DRAM (L2 hit 32 %,
-// profiles/ncu_full_sp_ksat5_r01.json).  Scattering variable-major factors
+// The gather can be windowed (DYNPAR_SP_WINDOW_MB): the variable pass runs
+// once per slice of the edge (= eta) index space small enough to stay in L2,
+// each parent taking only its occurrences inside the slice (a variable's
+// occurrence list is sorted by edge, so a slice is a sub-range: seg_lo /
+// seg_hi).  One pass over the whole 160 MB eta of 5-SAT 200k read 1.92 GB
+// of DRAM (L2 hit 32 %, profiles/ncu_full_sp_ksat5_r01.json), four 48 MB
+// windows 4 x 145 MB; but once the occurrence lists are read through L1
+// (DP_SP_OCC_L1) one pass is faster (5-SAT 12.96 vs 13.29 ms at 96 MB,
+// 3-SAT 9.66 vs 10.36 ms: profiles/r02/ab_sp_win2_r02.txt), so it is off
+// by default.  Scattering variable-major factors
 // from the clause pass instead was measured slower (5-SAT 20.9 vs 19.5 ms,
 // 3-SAT 14.8 vs 11.9 ms: partial-sector writes cost more than the gathers).
 // Arithmetic and storage in fp64 (explicit round-to-nearest ops, no FMA
@@ -1473,7 +1480,13 @@ struct SpVarApp {
     }
   }
   __device__ void item(const Args& a, int t, Acc& acc) const {
+#if DP_SP_OCC_L1
+    // thread-mode serial arm: a lane walks its own variable's list, so the
+    // next occurrences sit in the sector just fetched -- keep it in L1
+    const int o = __ldg(occs + a.start + t);
+#else
     const int o = ld_stream(occs + a.start + t);
+#endif
     const int neg = o & 1;
     const double f = __dsub_rn(1.0, __ldg(eta + (o >> 1)));
     if (acc.has && acc.var != a.i) {

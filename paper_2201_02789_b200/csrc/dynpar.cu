@@ -1654,7 +1654,7 @@ __global__ void sp_window_kernel(int n, int nwin, long long wsize,
 }
 
 #ifndef DP_SP_WINDOW_MB
-#define DP_SP_WINDOW_MB 96  // eta slice per variable pass (L2: 126 MB)
+#define DP_SP_WINDOW_MB 0  // eta slice per variable pass (0: one pass; see apps.cuh)
 #endif
 
 // W+ = Pi+ / (Pi+ + Pi- + Pi0), W- likewise, with P+ / P- the products of
