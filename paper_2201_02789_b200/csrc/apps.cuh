@@ -47,6 +47,11 @@ namespace dp {
 #ifndef DP_SP_UNROLL
 #define DP_SP_UNROLL 1  // SP items in flight per thread (variable / ratio)
 #endif
+#ifndef DP_SP_VAR_UNROLL
+#define DP_SP_VAR_UNROLL 2  // variable pass: eta gathers in flight per lane
+                            // (1: 12.92, 2: 12.31, 4: 12.8, 8: 13.0 ms,
+                            // profiles/r02/ab_sp_varunroll_r02.txt)
+#endif
 #ifndef DP_SP_OCC_L1
 #define DP_SP_OCC_L1 1  // variable pass: L1-cached occurrence loads
 #endif
@@ -1479,7 +1484,7 @@ struct SpVarApp {
       if (z[s]) atomicAdd(&prod[var].z[s], z[s]);
     }
   }
-  __device__ void item(const Args& a, int t, Acc& acc) const {
+  __device__ double factor(const Args& a, int t, int& neg) const {
 #if DP_SP_OCC_L1
     // thread-mode serial arm: a lane walks its own variable's list, so the
     // next occurrences sit in the sector just fetched -- keep it in L1
@@ -1487,8 +1492,16 @@ struct SpVarApp {
 #else
     const int o = ld_stream(occs + a.start + t);
 #endif
-    const int neg = o & 1;
-    const double f = __dsub_rn(1.0, __ldg(eta + (o >> 1)));
+    neg = o & 1;
+    return __dsub_rn(1.0, __ldg(eta + (o >> 1)));
+  }
+  __device__ void item(const Args& a, int t, Acc& acc) const {
+    int neg;
+    const double f = factor(a, t, neg);
+    fold(a, f, neg, acc);
+  }
+  __device__ __forceinline__ void fold(const Args& a, double f, int neg,
+                                       Acc& acc) const {
     if (acc.has && acc.var != a.i) {
       commit(acc.var, acc.p, acc.z);
       acc.has = 0;
@@ -1504,14 +1517,24 @@ struct SpVarApp {
     else
       acc.p[neg] = __dmul_rn(acc.p[neg], f);
   }
-  static constexpr int kUnroll = DP_SP_UNROLL;
+  static constexpr int kUnroll = DP_SP_VAR_UNROLL;
   static constexpr bool kBlockMode = false;
   static constexpr bool kPureExpand = true;
   static constexpr int kMinBlocks = DP_SP_MINB;
+  // all U gathers first, then the folds in item order (same products):
+  // a fold may commit with atomics, which would otherwise keep the next
+  // item's loads from being issued ahead of it
   template <int U, class ArgsOf>
   __device__ __forceinline__ void items(ArgsOf args, const int* e,
                                         const bool* ok, Acc& acc) const {
-    items_loop<U>(*this, args, e, ok, acc);
+    double f[U];
+    int neg[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j)
+      f[j] = ok[j] ? factor(args(j), e[j], neg[j]) : (neg[j] = 0, 1.0);
+#pragma unroll
+    for (int j = 0; j < U; ++j)
+      if (ok[j]) fold(args(j), f[j], neg[j], acc);
   }
   __device__ void flush(Acc& acc) const {
     const int key = acc.has ? acc.var : -1;
