@@ -682,9 +682,29 @@ def extra_workloads(stream, quick: bool) -> dict:
     cpu = oracle.sp(wl.payload, wl.buffers["eta0"], 20, 0.0,
                     nthreads=threads)
     dt = time.perf_counter() - t0
+    from paper_2201_02789_b200.bench.benchmarks import sp_traffic
+    alg = sp_traffic(wl.payload.nvars, ne, wl.payload.k, rep.iterations)
+    try:  # DRAM bytes of one sweep's three passes, committed ncu capture
+        cap = json.loads((ROOT / "profiles" / "r02" /
+                          "ncu_full_sp_final_r02.json").read_text())
+        scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        dram = sum(float(l[m]) * scale[cap["units"][m]]
+                   for l in cap["launches"]
+                   for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+    except Exception:  # noqa: BLE001
+        dram = None
     out["sp_ksat5_200k"] = {
         "ms": ms, "sweeps": rep.iterations, "edges": ne,
         "edge_updates_per_s": ne * rep.iterations / (ms * 1e-3),
+        "gbps_alg": alg / (ms * 1e-3) / 1e9,
+        "frac_hbm": alg / (ms * 1e-3) / 1e9 / hbm_peak()[0],
+        "alg_bytes_per_sweep": sp_traffic(wl.payload.nvars, ne,
+                                          wl.payload.k, 1) -
+                               sp_traffic(wl.payload.nvars, ne,
+                                          wl.payload.k, 0),
+        "dram_bytes_per_sweep_ncu": dram,
+        "bound": "latency of the random fp64 eta / product gathers "
+                 "(profiles/r02/ncu_full_sp_final_r02.json)",
         "vs_agg_only_grid": grid_ms / ms,
         "vs_nocdp": ref.ns_device / 1e6 / ms, "policy": BEST["sp"],
         "parity": ("within 1e-5 of the oracle"

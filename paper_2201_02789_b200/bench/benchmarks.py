@@ -353,15 +353,17 @@ def _sp_run(wl: Workload, cfg: _lib.DpConfig):
 
 def sp_traffic(nvars: int, nedges: int, k: int, sweeps: int) -> int:
     """Per sweep (csrc/apps.cuh SpVarApp / SpRatioApp / SpClauseApp):
-    variable pass 32 B per variable (occ_row pair, product write) + 12 B per
-    occurrence (packed occurrence 4, eta 8); ratio pass 28 B per edge (lit,
-    eta, ratio write) + 24 B of products per variable; clause pass 24 B per
-    edge (its ratio, eta, eta' write).  The final bias pass adds one variable
-    pass and 8 B of biases per variable; packing the occurrences 12 B/edge."""
-    var = 32 * nvars + 12 * nedges
-    ratio = 24 * nvars + 28 * nedges
+    variable pass 40 B per variable (occ_row pair, 32 B product record) +
+    12 B per occurrence (packed occurrence 4, eta 8); ratio pass 28 B per
+    edge (lit, eta, ratio write) + 32 B of products per variable; clause
+    pass 24 B per edge (its ratio, eta, eta' write).  Once per call: the
+    final bias pass (one variable pass + 8 B of biases per variable),
+    packing the occurrences (12 B/edge) and tiling lit / eta in (24 B/edge)
+    and eta out (16 B/edge)."""
+    var = 40 * nvars + 12 * nedges
+    ratio = 32 * nvars + 28 * nedges
     clause = 24 * nedges
-    return sweeps * (var + ratio + clause) + var + 8 * nvars + 12 * nedges
+    return sweeps * (var + ratio + clause) + var + 8 * nvars + 52 * nedges
 
 
 def _sp_traffic(wl, out, st):
