@@ -56,7 +56,8 @@ namespace dp {
 #define DP_SP_OCC_L1 1  // variable pass: L1-cached occurrence loads
 #endif
 #ifndef DP_SP_RATIO_MINB
-#define DP_SP_RATIO_MINB 1
+#define DP_SP_RATIO_MINB 5  // 58 -> 48 registers: 5-SAT 12.29 -> 12.03 ms
+                            // (profiles/r02/ab_sp_rminb_r02.txt)
 #endif
 #ifndef DP_MST_MINB
 #define DP_MST_MINB 8  // <= 32 registers: MST 4.15 (56) -> 3.98 (48) -> 3.70 ms
