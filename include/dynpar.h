@@ -263,7 +263,11 @@ int dp_mst_dev(const int32_t* d_rowptr, const int32_t* d_col,
  * wpos/wneg[nvars] variable biases W+ / W-, *sweeps, *delta (last max
  * change).  fp64 arithmetic and surveys, fp32 biases; the per-variable
  * product order is schedule-dependent, so results equal the CPU oracle
- * within a tolerance. */
+ * within a tolerance.  Inside the call lit / eta live clause-tiled (32
+ * clauses per tile, literal-major within it); eta comes in and goes out
+ * clause-major as above.  Occurrence lists sorted by edge (as the
+ * reference-style generator builds them) also allow the L2-windowed
+ * variable pass (DYNPAR_SP_WINDOW_MB); unsorted lists run one pass. */
 int dp_sp(const int32_t* lits, int32_t k, int32_t nclauses,
           const int32_t* occ_row, const int32_t* occ, int32_t nvars,
           const double* eta0, int32_t max_sweeps, float eps,
