@@ -1873,11 +1873,31 @@ int manylaunch_dev_impl(const int32_t* sizes, int32_t n, const dp_config* c,
 // scan, scatter.  In-list order is the scatter's (irrelevant: in-lists are
 // only iterated, the probed / merged out-lists stay sorted).
 // ---------------------------------------------------------------------------
+// In-degrees of the oriented graph.  Edges point to the higher-ranked
+// (higher-degree) end, so the top ranks (the hubs) collect most of them and
+// their counters serialise at one L2 slice each (1.35 ms of RMAT-22's TC
+// for 63 M edges; merging equal heads within a warp did not help -- a row's
+// heads are distinct).  Each block counts heads in the top kTcHub ranks in
+// shared memory and adds them to the global counters once.
+constexpr int kTcHub = 4096;
+
 __global__ void tc_count_in_kernel(const int* __restrict__ col, long long lo,
-                                   long long hi, int* cnt) {
+                                   long long hi, int n, int* cnt) {
+  __shared__ int hist[kTcHub];
+  const int h0 = n > kTcHub ? n - kTcHub : 0;  // hub ranks [h0, n)
+  for (int i = threadIdx.x; i < kTcHub; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
   for (long long e = lo + (long long)blockIdx.x * blockDim.x + threadIdx.x;
-       e < hi; e += (long long)gridDim.x * blockDim.x)
-    atomicAdd(cnt + __ldg(col + e), 1);
+       e < hi; e += (long long)gridDim.x * blockDim.x) {
+    const int v = ld_stream(col + e);
+    if (v >= h0)
+      atomicAdd(hist + (v - h0), 1);
+    else
+      atomicAdd(cnt + v, 1);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kTcHub; i += blockDim.x)
+    if (hist[i]) atomicAdd(cnt + h0 + i, hist[i]);
 }
 
 // exclusive scan of x[0, n) into y[0, n] (y[n] = total), three passes
@@ -1964,6 +1984,11 @@ __global__ void scan_add_kernel(int* y, int* y2, long long n,
 // In-edge (u -> v) at slot i records the slots of N+(u) above v, [i + 1,
 // rowptr[u + 1]) (the rank-ordered CSR+ keeps rows ascending, so these are
 // exactly the w > v that can close a triangle at v)
+// One in-edge per lane of the row's warp, placed with an atomic cursor.
+// Measured alternatives (profiles/r02/ab_tc_transpose_r02.txt): privatising
+// the hub cursors in shared memory (2.01 vs 1.77 ms) and edge-balanced
+// warp-flattened rows (2.44 ms) were slower -- the kernel is bound by the
+// 8-byte scattered in_rng writes, not by the cursor atomics.
 __global__ void tc_scatter_in_kernel(const int* __restrict__ rowptr,
                                      const int* __restrict__ col, int n,
                                      long long lo, long long hi, int* cursor,
@@ -2009,7 +2034,7 @@ int tc_dev_impl(const int32_t* rowptr, const int32_t* col, int32_t n,
   const int gb = 148 * 8;
   DP_CUDA(cudaMemsetAsync(cursor, 0, (size_t)(n + 1) * 4, s));
   if (hi > lo)
-    tc_count_in_kernel<<<gb, 256, 0, s>>>(col, lo, hi, cursor);
+    tc_count_in_kernel<<<gb, 256, 0, s>>>(col, lo, hi, n, cursor);
   scan_tiles_kernel<<<(int)ntiles, 1024, 0, s>>>(cursor, n, in_rowptr,
                                                  tile_sum);
   scan_sums_kernel<<<1, 1024, 0, s>>>(tile_sum, (int)ntiles, in_rowptr, n);
