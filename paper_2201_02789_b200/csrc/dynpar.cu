@@ -1988,7 +1988,9 @@ __global__ void scan_add_kernel(int* y, int* y2, long long n,
 // Measured alternatives (profiles/r02/ab_tc_transpose_r02.txt): privatising
 // the hub cursors in shared memory (2.01 vs 1.77 ms) and edge-balanced
 // warp-flattened rows (2.44 ms) were slower -- the kernel is bound by the
-// 8-byte scattered in_rng writes, not by the cursor atomics.
+// 8-byte scattered in_rng writes, not by the cursor atomics -- and so was
+// placing the heads in L2-sized passes (15.5-21.8 vs 14.05 ms for the whole
+// TC, ab_tc_window_r02.txt: each pass re-reads col).
 __global__ void tc_scatter_in_kernel(const int* __restrict__ rowptr,
                                      const int* __restrict__ col, int n,
                                      long long lo, long long hi, int* cursor,
