@@ -515,8 +515,14 @@ def extra_workloads(stream, quick: bool) -> dict:
         from oracle import oracle
         threads = len(os.sched_getaffinity(0))
         t0 = time.perf_counter()
-        oracle.bfs(G.g.rowptr, G.g.col, nthreads=threads)
+        wd, wc, _ = oracle.bfs(G.g.rowptr, G.g.col, nthreads=threads)
         dt = time.perf_counter() - t0
+        # G holds the outputs of the last device run (every policy above
+        # computes the same dist / counts)
+        out["bfs_rmat22"]["parity"] = (
+            "bit-exact vs oracle (dist, counts)"
+            if np.array_equal(G.dist.cpu().numpy(), wd)
+            and np.array_equal(G.counts.cpu().numpy(), wc) else "MISMATCH")
         out["bfs_rmat22"]["cpu_baseline"] = {
             "value": e_t / dt / 1e9, "unit": "GTEPS", "cores": threads,
             "kind": "port", "seconds": dt,
